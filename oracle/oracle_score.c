@@ -1,0 +1,210 @@
+/*
+ * oracle_score.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, scalar CPU fp64 implementation of the per-pose quantity the CUDA path
+ * computes.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may load
+ * it.  It shares no source with paper_2510_26611_b200/csrc (no common headers, helpers
+ * or constants) and never links against the product library.
+ *
+ * Build (done by __graft_entry__.build()):
+ *   gcc -O2 -ffp-contract=off -fno-tree-vectorize -fopenmp -shared -fPIC \
+ *       -o oracle/liboracle.so oracle/oracle_score.c -lm
+ * -ffp-contract=off: no implicit a*b+c contraction; every fused multiply-add below is
+ * an explicit fma() call (correctly rounded), so each op sequence is exactly as written.
+ *
+ * What is computed, per pose p (paper notation: protein M = {x_m, z_m}, ligand
+ * L = {y_l, z_l}):
+ *   E_p = sum_l z_l * [ P^long_{M,R}(i_l) + sum_{m : |i_l - i_m|_2 <= n_sigma} z_m S(i_l - i_m) ]
+ *     -- Lemma 3.2 / Eq. (18) gives the long-range sum, Algorithm PLIE
+ *        steps 2-3 the <z_L, p_L> form; the RS entry formula of
+ *        PAPER.md:460-466 (Def. 2.1) adds the short-range replicas.
+ *   d_p = min_{l,m} |x'_l - x_m|  if below D_cap, else +inf
+ *     -- the constraint dist(M, F(L)) >= sigma of Eq. (22).
+ * The ligand atom positions are x'_l = R(q) y_l + t (F = R o T) and
+ * i_l is the cell of x'_l on the piecewise-constant grid.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---- O1: unit quaternion (w,x,y,z) -> rotation matrix, row-major R[3][3] ------------
+ * Rotation of the ligand about its geometric centre, parametrised by
+ * a quaternion (ledger A10).  s = 2/|q|^2 makes a non-unit q act as its normalisation.
+ * Returns 0 (invalid pose) when |q|^2 is zero or not finite. */
+int oracle_quat_to_rot(const double *q, double *R)
+{
+    double w = q[0], x = q[1], y = q[2], z = q[3];
+    double nn = ((w * w + x * x) + y * y) + z * z;
+    if (!(nn > 0.0) || !isfinite(nn)) return 0;
+    double s = 2.0 / nn;
+    double xs = x * s, ys = y * s, zs = z * s;
+    double wx = w * xs, wy = w * ys, wz = w * zs;
+    double xx = x * xs, xy = x * ys, xz = x * zs;
+    double yy = y * ys, yz = y * zs, zz = z * zs;
+    R[0] = 1.0 - (yy + zz); R[1] = xy - wz;          R[2] = xz + wy;
+    R[3] = xy + wz;         R[4] = 1.0 - (xx + zz);  R[5] = yz - wx;
+    R[6] = xz - wy;         R[7] = yz + wx;          R[8] = 1.0 - (xx + yy);
+    return 1;
+}
+
+/* ---- O2: rigid transform x' = R y + t ---- */
+void oracle_transform(const double *R, const double *y, const double *t, double *xp)
+{
+    for (int a = 0; a < 3; ++a)
+        xp[a] = ((R[3 * a + 0] * y[0] + R[3 * a + 1] * y[1]) + R[3 * a + 2] * y[2]) + t[a];
+}
+
+/* ---- O3: snap a coordinate to its grid cell (ledger A3/A4) ----
+ * Cells [-b + i h, -b + (i+1) h], i = 0..n-1, h = 2b/n.  u = (x + b) * inv_h with
+ * inv_h = n / (2b); i = ceil(u) - 1 clamped to [0, n-1]: an exact cell boundary (u an
+ * integer) goes to the lower cell ("ties toward the lower index").
+ * Returns -1 when x is outside [-b, b] (or NaN). */
+int oracle_snap(double x, double b, double inv_h, int n)
+{
+    if (!(x >= -b && x <= b)) return -1;
+    double u = (x + b) * inv_h;
+    double c = ceil(u) - 1.0;
+    if (c < 0.0) c = 0.0;
+    if (c > (double)(n - 1)) c = (double)(n - 1);
+    return (int)c;
+}
+
+/* ---- O6: double-double accumulation of exact products (Dekker TwoProduct, Knuth TwoSum) */
+typedef struct { double hi, lo; } dd_t;
+
+static void dd_add_product(dd_t *acc, double a, double b)
+{
+    double p = a * b;
+    double e = fma(a, b, -p);               /* a*b = p + e exactly */
+    double s = acc->hi + p;                 /* TwoSum(hi, p) */
+    double bb = s - acc->hi;
+    double err = (acc->hi - (s - bb)) + (p - bb);
+    acc->hi = s;
+    acc->lo = acc->lo + (err + e);
+}
+
+/* exposed for the O6 pin (tests compare with an exact rational sum) */
+double oracle_dd_sum_products(const double *a, const double *b, int64_t n)
+{
+    dd_t acc = {0.0, 0.0};
+    for (int64_t i = 0; i < n; ++i) dd_add_product(&acc, a[i], b[i]);
+    return acc.hi + acc.lo;
+}
+
+/* ---- O4: long-range CP value at cell i (Lemma 3.2 / Eq. (18); entry formula PAPER.md:463) */
+double oracle_long_value(const double *F1, const double *F2, const double *F3, int R,
+                         int i0, int i1, int i2)
+{
+    const double *a = F1 + (int64_t)i0 * R, *b = F2 + (int64_t)i1 * R, *c = F3 + (int64_t)i2 * R;
+    double phi = 0.0;
+    for (int k = 0; k < R; ++k) phi = phi + (a[k] * b[k]) * c[k];
+    return phi;
+}
+
+/* ---- O5: short-range reference value S(Delta) for |Delta|_2 <= n_sigma (Def. 2.1) ---- */
+double oracle_short_value(const double *S1, const double *S2, const double *S3, int Rs,
+                          int n_sigma, int d0, int d1, int d2)
+{
+    const double *a = S1 + (int64_t)(d0 + n_sigma) * Rs;
+    const double *b = S2 + (int64_t)(d1 + n_sigma) * Rs;
+    const double *c = S3 + (int64_t)(d2 + n_sigma) * Rs;
+    double s = 0.0;
+    for (int k = 0; k < Rs; ++k) s = s + (a[k] * b[k]) * c[k];
+    return s;
+}
+
+/*
+ * Score P poses.  All arrays host, row-major, fp64 unless stated:
+ *   F1,F2,F3 : n x R long-range CP factors (weights folded), exported by the library
+ *   S1,S2,S3 : (2 n_sigma + 1) x Rs short-range reference rows (a_k folded into S1)
+ *   X (M x 3), zM (M)      : protein atoms (continuous coordinates) and charges
+ *   Y (L x 3), zL (L)      : ligand body coordinates (centred) and charges
+ *   poses (P x 7)          : w,x,y,z,tx,ty,tz
+ *   long_only != 0         : skip O5 and O7 (Lemma 3.2's cost alone; CPU like-for-like rate)
+ * Outputs E (P), dmin (P).  Returns the number of invalid poses (O8: NaN outputs).
+ * Protein cells are recomputed here with oracle_snap (never taken from the library).
+ */
+int64_t oracle_score_poses(int n, double b, int R, const double *F1, const double *F2,
+                           const double *F3, int n_sigma, int Rs, const double *S1,
+                           const double *S2, const double *S3, int64_t M, const double *X,
+                           const double *zM, int64_t L, const double *Y, const double *zL,
+                           int64_t P, const double *poses, double dcap, int long_only,
+                           double *E, double *dmin)
+{
+    double inv_h = (double)n / (2.0 * b);
+    int *iM = (int *)malloc(sizeof(int) * 3 * (size_t)(M > 0 ? M : 1));
+    for (int64_t m = 0; m < M; ++m)
+        for (int a = 0; a < 3; ++a) iM[3 * m + a] = oracle_snap(X[3 * m + a], b, inv_h, n);
+    double dcap2 = dcap * dcap;
+    int64_t ns2 = (int64_t)n_sigma * n_sigma;
+    int64_t invalid = 0;
+
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : invalid)
+    for (int64_t p = 0; p < P; ++p) {
+        const double *pq = poses + 7 * p;
+        double Rm[9];
+        int ok = oracle_quat_to_rot(pq, Rm);
+        dd_t acc = {0.0, 0.0};
+        double best = INFINITY;
+        for (int64_t l = 0; l < L && ok; ++l) {
+            double xp[3];
+            int il[3];
+            oracle_transform(Rm, Y + 3 * l, pq + 4, xp);
+            for (int a = 0; a < 3; ++a) {
+                il[a] = oracle_snap(xp[a], b, inv_h, n);
+                if (il[a] < 0) ok = 0;
+            }
+            if (!ok) break;
+            /* O4 */
+            double phi = oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
+            dd_add_product(&acc, zL[l], phi);
+            if (long_only) continue;
+            for (int64_t m = 0; m < M; ++m) {
+                /* O7: distance between continuous coordinates */
+                double dx0 = xp[0] - X[3 * m + 0];
+                double dx1 = xp[1] - X[3 * m + 1];
+                double dx2 = xp[2] - X[3 * m + 2];
+                double d2 = (dx0 * dx0 + dx1 * dx1) + dx2 * dx2;
+                if (d2 < best) best = d2;
+                /* O5: short-range replica of protein atom m contains cell i_l */
+                int64_t e0 = il[0] - iM[3 * m + 0];
+                int64_t e1 = il[1] - iM[3 * m + 1];
+                int64_t e2 = il[2] - iM[3 * m + 2];
+                if (e0 * e0 + e1 * e1 + e2 * e2 <= ns2) {
+                    double s = oracle_short_value(S1, S2, S3, Rs, n_sigma, (int)e0, (int)e1,
+                                                  (int)e2);
+                    double w = zM[m] * s;
+                    dd_add_product(&acc, zL[l], w);
+                }
+            }
+        }
+        if (!ok) {
+            E[p] = NAN;
+            dmin[p] = NAN;
+            invalid += 1;
+        } else {
+            E[p] = acc.hi + acc.lo;
+            dmin[p] = (best < dcap2) ? sqrt(best) : INFINITY;
+        }
+    }
+    free(iM);
+    return invalid;
+}
+
+/* number of OpenMP threads the scorer uses (reported as cpu_baseline.cores) */
+int oracle_num_threads(void)
+{
+    int nt = 1;
+#ifdef _OPENMP
+#pragma omp parallel
+    {
+#pragma omp single
+        nt = omp_get_num_threads();
+    }
+#endif
+    return nt;
+}

@@ -1,0 +1,447 @@
+"""Pins for the oracle (oracle/): each test ties an oracle function to something other than
+itself -- a closed form, a worked example from the paper/SPEC, a library routine (scipy),
+exact rational arithmetic, or brute force -- chosen so a dropped term, wrong sign/index or
+transposed operand fails.  CPU only (-m "not gpu")."""
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import integrate
+from scipy.spatial.distance import cdist
+from scipy.spatial.transform import Rotation
+
+from synth import configs as syn
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    vals = {}
+    with open(os.path.join(GOLD, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                k, v = line.split()
+                vals[k] = float(v)
+    return vals
+
+
+# ---------------------------------------------------------------------------------- S1
+@pytest.mark.parametrize("b,n,eps", [(20.0, 256, 1e-4), (20.0, 256, 1e-6), (64.0, 4096, 1e-6)])
+def test_quadrature_approximates_newton_kernel(oracle, b, n, eps):
+    """Eq. (2): sum_k a_k exp(-t_k^2 r^2) ~ 1/r on [h/2, 2 sqrt3 b] within eps (relative),
+    checked on points the search never saw (random r, not the search's log grid)."""
+    h = 2 * b / n
+    Ls = 2 * math.sqrt(3) * b
+    s, K = oracle.choose_quadrature(eps, h / 2, Ls, Ls)
+    t, a = oracle.quadrature(s, K, Ls)
+    r = np.exp(np.random.default_rng(0).uniform(math.log(h / 2), math.log(Ls), 20000))
+    approx = (a[None, :] * np.exp(-(t[None, :] ** 2) * r[:, None] ** 2)).sum(axis=1)
+    assert np.max(np.abs(approx * r - 1)) <= 1.5 * eps
+    # the Laplace-Gauss integral itself by adaptive quadrature, one r
+    r0 = 1.7
+    val, _ = integrate.quad(lambda tt: math.exp(-r0 * r0 * tt * tt), 0, np.inf)
+    assert abs(2 / math.sqrt(math.pi) * val - 1 / r0) < 1e-12
+    # weights positive, nodes ascending, t_0 = 0 (constant term)
+    assert np.all(a > 0) and np.all(np.diff(t) > 0) and t[0] == 0.0
+
+
+def test_quadrature_table2_rank_trend(oracle):
+    """Table 2: the reference CP rank grows slowly with n (20 -> 32 for
+    n = 128 -> 16384).  Our rule at eps=1e-4 on the paper-like box grows monotonically and
+    stays within the same order."""
+    ranks = []
+    for n in (128, 1024, 16384):
+        b = 20.0
+        Ls = 2 * math.sqrt(3) * b
+        s, K = oracle.choose_quadrature(1e-4, (2 * b / n) / 2, Ls, Ls)
+        ranks.append(2 * K + 1)
+    assert ranks[0] <= ranks[1] <= ranks[2]
+    assert 15 <= ranks[0] and ranks[2] <= 80
+
+
+# ---------------------------------------------------------------------------------- S2
+def test_split_monotone_and_partition(oracle):
+    t, a = oracle.quadrature(0.32, 30, 69.28)
+    m2 = oracle.split_long(t, 2.0, 1e-6)
+    m4 = oracle.split_long(t, 4.0, 1e-6)
+    assert m2[0] and m4[0]                       # constant term always long
+    assert np.all(m2[m4])                        # raising sigma never moves short -> long
+    # long terms are wide: exp(-t^2 sigma^2) >= eps at sigma; short terms are narrow
+    assert np.all(np.exp(-(t[m2] * 2.0) ** 2) >= 1e-6 * (1 - 1e-12))
+    assert np.all(np.exp(-(t[~m2] * 2.0) ** 2) < 1e-6)
+
+
+# ---------------------------------------------------------------------------------- S3
+def test_cell_average_closed_form(oracle):
+    g = _golden("closed_forms.txt")
+    val = oracle.cell_average(1.0, 1.0, np.array([0.0]))[0]
+    assert abs(val - g["gauss_cell_t1_h1"]) < 1e-15
+
+
+def test_cell_average_vs_adaptive_quadrature(oracle):
+    rng = np.random.default_rng(3)
+    for _ in range(60):
+        t = float(np.exp(rng.uniform(-4, 3)))
+        h = float(np.exp(rng.uniform(-4, 0)))
+        d = int(rng.integers(-40, 41))
+        lo, hi = (d - 0.5) * h, (d + 0.5) * h
+        ref, _ = integrate.quad(lambda x: math.exp(-t * t * x * x), lo, hi, epsabs=0,
+                                epsrel=2e-14, limit=200)
+        ref /= h
+        val = oracle.cell_average(t, h, np.array([float(d)]))[0]
+        if ref > 1e-280:
+            assert abs(val - ref) <= 1e-12 * ref, (t, h, d, val, ref)
+    assert oracle.cell_average(0.0, 0.3, np.array([0.0, 7.0])).tolist() == [1.0, 1.0]
+
+
+def test_cell_average_even_bitwise(oracle):
+    d = np.arange(-300, 301, dtype=np.float64)
+    for t in (0.05, 0.7, 3.0, 20.0):
+        g = oracle.cell_average(t, 0.03125, d)
+        assert np.array_equal(g, g[::-1])
+
+
+# ---------------------------------------------------------------------------------- O3
+def test_snap_spec_examples(oracle):
+    with open(os.path.join(GOLD, "spec_snap.txt")) as f:
+        rows = [l.split() for l in f if l.strip() and not l.startswith("#")]
+    for r in rows:
+        b, n = float(r[0]), int(r[1])
+        xyz = [float(v) for v in r[2:5]]
+        want = [int(v) for v in r[5:8]]
+        got = [oracle.snap(x, b, n) for x in xyz]
+        assert got == want, (r, got)
+
+
+def test_snap_ties_go_low_and_cells_contain_point(oracle):
+    b, n = 2.0, 64                        # h = 1/16 exactly representable
+    h = 2 * b / n
+    for j in range(n + 1):
+        x = -b + j * h                    # an exact cell boundary
+        assert oracle.snap(x, b, n) == max(j - 1, 0)
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-b, b, 5000)
+    i = oracle.snap_np(x, b, n)
+    assert np.all((-b + i * h <= x) & (x <= -b + (i + 1) * h))
+    assert oracle.snap(b + 1e-12, b, n) == -1 and oracle.snap(float("nan"), b, n) == -1
+    assert [oracle.snap(v, b, n) for v in x[:200]] == i[:200].tolist()
+
+
+# ---------------------------------------------------------------------------------- O1/O2
+def test_quaternion_rotation_vs_scipy(oracle):
+    rng = np.random.default_rng(1)
+    q = syn.shoemake_quaternions(rng, 2000)
+    ref = Rotation.from_quat(q[:, [1, 2, 3, 0]]).as_matrix()     # scipy is scalar-last
+    for k in range(q.shape[0]):
+        R = oracle.quat_to_rot(q[k])
+        assert np.max(np.abs(R - ref[k])) < 2e-15
+        assert np.array_equal(R, oracle.quat_to_rot(-q[k]))       # R(q) = R(-q) bitwise
+        assert np.max(np.abs(R - oracle.quat_to_rot(3.0 * q[k]))) < 1e-15   # implicit norm
+    assert np.array_equal(oracle.quat_to_rot([1, 0, 0, 0]), np.eye(3))
+    assert np.array_equal(oracle.quat_to_rot([0, 1, 0, 0]), np.diag([1.0, -1, -1]))
+    assert np.array_equal(oracle.quat_to_rot([0, 0, 0, 1]), np.diag([-1.0, -1, 1]))
+    assert oracle.quat_to_rot([0, 0, 0, 0]) is None
+
+
+def test_transform_identity_bitwise_and_isometry(oracle):
+    rng = np.random.default_rng(2)
+    Y = rng.normal(size=(30, 3)) * 3
+    I = oracle.quat_to_rot([1, 0, 0, 0])
+    for y in Y:
+        assert np.array_equal(oracle.transform(I, y, np.zeros(3)), y)
+    R = oracle.quat_to_rot(syn.shoemake_quaternions(rng, 1)[0])
+    t = rng.normal(size=3) * 10
+    Xp = np.stack([oracle.transform(R, y, t) for y in Y])
+    assert np.max(np.abs(cdist(Xp, Xp) - cdist(Y, Y))) < 1e-12
+    assert np.max(np.abs(Xp - (Y @ R.T + t))) < 1e-13
+
+
+# ---------------------------------------------------------------------------------- O6
+def test_dd_sum_matches_exact_rational(oracle):
+    rng = np.random.default_rng(4)
+    exact_hits, n_cases = 0, 300
+    for c in range(n_cases):
+        n = int(rng.integers(1, 200))
+        a = rng.normal(size=n) * np.exp(rng.uniform(-20, 20, n))
+        b = rng.normal(size=n)
+        if c % 2:     # adversarial: heavy cancellation
+            b[n // 2:] = -b[: n - n // 2] * (a[: n - n // 2] / a[n // 2:])[: n - n // 2]
+        got = oracle.dd_sum_products(a, b)
+        ex = oracle.exact_sum_products(a, b)
+        if got == ex:
+            exact_hits += (c % 2 == 0)
+        else:
+            # double-double bound: one final rounding + n * 2^-104 * sum |a_i b_i|
+            bound = np.spacing(abs(ex)) + n * 2.0 ** -104 * float(np.sum(np.abs(a * b)))
+            assert abs(got - ex) <= bound, (got, ex, bound)
+    assert exact_hits >= (n_cases // 2) * 0.98   # well-conditioned sums: correctly rounded
+
+
+# ---------------------------------------------------------------------------------- O4
+def _tables(F, S=None, n_sigma=0, n=None, b=1.0):
+    F1, F2, F3 = F
+    if S is None:
+        S = (np.zeros((2 * n_sigma + 1, 1)),) * 3
+    return dict(n=n if n is not None else F1.shape[0], b=b, R=F1.shape[1], F1=F1, F2=F2, F3=F3,
+                n_sigma=n_sigma, S1=S[0], S2=S[1], S3=S[2])
+
+
+def test_long_value_rank1_ones_and_one_hot(oracle):
+    n = 8
+    ones = np.ones((n, 1))
+    assert oracle.lib().oracle_long_value(*(oracle._p(np.ascontiguousarray(ones)),) * 3, 1, 3, 4, 5) == 1.0
+    # rank-2, e1 x e1 x e1 (xi=3) and e2 x e2 x e2 (xi=5)
+    F = np.zeros((n, 2))
+    F[0, 0] = 1
+    F[1, 1] = 1
+    F1 = F * np.array([3.0, 5.0])
+    lv = lambda i: oracle.lib().oracle_long_value(oracle._p(np.ascontiguousarray(F1)),
+                                                  oracle._p(F), oracle._p(F), 2, i, i, i)
+    assert lv(0) == 3.0 and lv(1) == 5.0 and lv(2) == 0.0
+
+
+def test_scorer_long_range_equals_dense_materialisation(oracle):
+    """O2-O4+O6 vs numpy: dense tensor T = einsum(F1,F2,F3) indexed at the snapped cells of
+    the transformed atoms, summed with weights z (SPEC.md:67 dense materialisation, n<=16)."""
+    rng = np.random.default_rng(5)
+    n, b, R = 16, 4.0, 5
+    F = [rng.normal(size=(n, R)) for _ in range(3)]
+    T = np.einsum("ik,jk,lk->ijl", *F)
+    Y = rng.normal(size=(6, 3))
+    Y -= Y.mean(0)
+    z = rng.uniform(-1, 1, 6)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, 40), rng.uniform(-1, 1, (40, 3))], 1)
+    E, d, inv = oracle.score_poses(_tables(F, b=b), np.zeros((0, 3)), np.zeros(0), Y, z, poses,
+                                   1.0, long_only=True)
+    assert inv == 0
+    for p in range(40):
+        R_ = Rotation.from_quat(poses[p, [1, 2, 3, 0]]).as_matrix()
+        Xp = Y @ R_.T + poses[p, 4:]
+        idx = oracle.snap_np(Xp, b, n)
+        ref = math.fsum(z[l] * T[tuple(idx[l])] for l in range(6))
+        assert abs(E[p] - ref) <= 1e-13 * (np.abs(z) @ np.abs(T[tuple(idx.T)]) + 1e-300)
+    # bitwise linearity in the ligand charges (power-of-two scaling; north_star invariant)
+    E2, _, _ = oracle.score_poses(_tables(F, b=b), np.zeros((0, 3)), np.zeros(0), Y, 4.0 * z,
+                                  poses, 1.0, long_only=True)
+    assert np.array_equal(E2, 4.0 * E)
+
+
+# ---------------------------------------------------------------------------------- O7/O8
+def test_scorer_min_distance_vs_cdist_and_invalid(oracle):
+    rng = np.random.default_rng(6)
+    n, b = 32, 8.0
+    F = [np.zeros((n, 1))] * 3
+    X = rng.uniform(-3, 3, (40, 3))
+    q = rng.uniform(-1, 1, 40)
+    Y = rng.normal(size=(5, 3))
+    Y -= Y.mean(0)
+    z = rng.uniform(-1, 1, 5)
+    P = 200
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), rng.uniform(-5, 5, (P, 3))], 1)
+    poses[7, :4] = 0.0                       # zero quaternion -> invalid
+    poses[9, 4] = 7.9                        # atoms leave the box -> invalid
+    cap = 2.5
+    E, d, inv = oracle.score_poses(_tables(F, b=b), X, q, Y, z, poses, cap)
+    for p in range(P):
+        if p in (7, 9):
+            assert math.isnan(E[p]) and math.isnan(d[p])
+            continue
+        R_ = Rotation.from_quat(poses[p, [1, 2, 3, 0]]).as_matrix()
+        m = cdist(Y @ R_.T + poses[p, 4:], X).min()
+        if m < cap - 1e-12:
+            assert abs(d[p] - m) < 1e-13
+        elif m > cap + 1e-12:
+            assert d[p] == np.inf
+    assert inv == 2
+
+
+def test_vdw_threshold_boundary(oracle):
+    """SPEC.md:480-481 / Eq. (22) 'dist >= sigma': exactly sigma is feasible, sigma - 1e-9 is a
+    clash.  Distances reported exactly below the cap."""
+    F = [np.zeros((16, 1))] * 3
+    X = np.array([[0.0, 0.0, 0.0]])
+    Y = np.array([[0.0, 0.0, 0.0]])
+    for dist, clash in ((2.5, False), (2.5 - 1e-9, True)):
+        poses = np.array([[1.0, 0, 0, 0, dist, 0, 0]])
+        E, d, inv = oracle.score_poses(_tables(F, b=4.0), X, np.ones(1), Y, np.ones(1), poses, 3.0)
+        assert d[0] == dist and (d[0] < 2.5) == clash
+
+
+# ---------------------------------------------------------------------------------- physics chain
+def _newton_self_cell_numeric():
+    """h*K_h(0) = (1/h^2) int_cube 1/|x| = 0.75 * int_{[-1,1]^2} (1+u^2+v^2)^(-1/2) du dv
+    (six pyramids, one per face, each rescaled to the reference face)."""
+    I, _ = integrate.dblquad(lambda v, u: 1.0 / math.sqrt(1 + u * u + v * v), -1, 1, -1, 1,
+                             epsabs=1e-14, epsrel=2e-14)
+    return 0.75 * I
+
+
+def test_newton_self_cell_closed_form(oracle):
+    g = _golden("closed_forms.txt")
+    assert abs(oracle.K_H0 - g["newton_self_cell"]) < 1e-12
+    assert abs(_newton_self_cell_numeric() - oracle.K_H0) < 1e-12
+
+
+def test_K_h_cubature_vs_point_kernel(oracle):
+    # far cells: cell average -> 1/r with an O(h^2/r^2) midpoint correction
+    h = 0.1
+    for dl in [(5, 0, 0), (3, 4, 1), (10, 2, 7)]:
+        r = h * math.sqrt(sum(v * v for v in dl))
+        kh = oracle.K_h(dl, h)
+        assert abs(kh * r - 1) < 0.01 * (h / r) ** 2 * 10
+    # adjacent cell vs scipy tplquad
+    ref, _ = integrate.tplquad(lambda z, y, x: 1 / math.sqrt(x * x + y * y + z * z),
+                               0.5, 1.5, -0.5, 0.5, -0.5, 0.5, epsabs=1e-12, epsrel=1e-12)
+    assert abs(oracle.K_h((1, 0, 0), 1.0, order=24) - ref) < 1e-10
+
+
+def _rs_setup(oracle, b, n, eps_q, sigma_s, eps_split=1e-6):
+    h = 2 * b / n
+    Ls = 2 * math.sqrt(3) * b
+    s, K = oracle.choose_quadrature(eps_q, h / 4, Ls, Ls)
+    t, a = oracle.quadrature(s, K, Ls)
+    lm = oracle.split_long(t, sigma_s, eps_split)
+    n_sigma = int(math.ceil(sigma_s / h))
+    return h, t, a, lm, n_sigma
+
+
+def test_K_RS_vs_cell_averaged_newton_kernel(oracle):
+    """SURVEY §8(c) C2 vs C1: |K_RS - K_h| / K_h <= ~eps_q off the singular cell; the singular
+    cell against the closed form with a looser bound (quadrature weakest there)."""
+    b, n = 8.0, 128
+    h, t, a, lm, ns = _rs_setup(oracle, b, n, 1e-8, 1.0)
+    for dl in [(1, 0, 0), (2, 1, 0), (5, 3, 1), (16, 0, 0), (30, 20, 10)]:
+        krs = oracle.K_RS(dl, t, a, lm, h, ns)
+        kh = oracle.K_h(dl, h, order=16)
+        assert abs(krs - kh) / kh < 2e-7, dl
+    k0 = oracle.K_RS((0, 0, 0), t, a, lm, h, ns)
+    assert abs(k0 - oracle.K_H0 / h) / (oracle.K_H0 / h) < 1e-2
+    # the short part vanishes outside the ball, so K_RS there equals the long-range part
+    dl = (ns + 1, 0, 0)
+    long_only = sum(a[k] * np.prod(oracle.cell_average(float(t[k]), h, np.array(dl, float)))
+                    for k in range(len(t)) if lm[k])
+    assert oracle.K_RS(dl, t, a, lm, h, ns) == pytest.approx(long_only, rel=1e-15)
+
+
+def _chain_case(oracle, seed=0):
+    rng = np.random.default_rng(seed)
+    b, n = 10.0, 128
+    h, t, a, lm, ns = _rs_setup(oracle, b, n, 1e-8, 1.0)
+    X = syn.packed_ball(rng, 30, 4.0, 1.2)
+    qM = rng.uniform(-1, 1, 30)
+    Y = syn.packed_ball(rng, 6, 1.8, 1.2)
+    Y -= Y.mean(0)
+    zL = rng.uniform(-1, 1, 6)
+    iM = oracle.snap_np(X, b, n)
+    F = oracle.uncompressed_long_factors(iM, qM, t, a, lm, n, h)
+    S = oracle.short_tables(t, a, lm, h, ns)
+    tables = dict(n=n, b=b, R=F[0].shape[1], F1=F[0], F2=F[1], F3=F[2], n_sigma=ns,
+                  S1=S[0], S2=S[1], S3=S[2])
+    return b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng
+
+
+def test_scorer_equals_pairwise_K_RS_sum(oracle):
+    """Scorer with uncompressed factors == sum_l sum_m z_l z_m K_RS(i_l - i_m) (double loop):
+    pins the shift-and-window factors (Eq. (6)), the short-range ball (Def. 2.1) and the
+    scorer's bookkeeping against an independent pairwise evaluation."""
+    b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng = _chain_case(oracle)
+    P = 12
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), rng.uniform(-4, 4, (P, 3))], 1)
+    E, d, inv = oracle.score_poses(tables, X, qM, Y, zL, poses, 2.5)
+    assert inv == 0
+    for p in range(P):
+        R_ = oracle.quat_to_rot(poses[p, :4])
+        Xp = np.stack([oracle.transform(R_, y, poses[p, 4:]) for y in Y])
+        iL = oracle.snap_np(Xp, b, n)
+        ref, scale = [], 0.0
+        for l in range(len(zL)):
+            for m in range(len(qM)):
+                k = oracle.K_RS(iL[l] - iM[m], t, a, lm, h, ns)
+                ref.append(zL[l] * qM[m] * k)
+        ref_sum = math.fsum(ref)
+        scale = math.fsum(abs(v) for v in ref)
+        assert abs(E[p] - ref_sum) <= 1e-12 * scale
+
+
+def test_rs_energy_vs_brute_force_coulomb(oracle):
+    """Whole-oracle pin (north_star): RS energy (uncompressed) vs the brute-force Coulomb sum
+    of Eq. (13), normalised by S = sum |z z|/r (SURVEY §8(c) measured-magnitudes table):
+    non-clashing poses within the O(h/r) snapping bound, and E_RS vs point Coulomb at the
+    snapped cell centres within the O(h^2/r^2) + eps_q bound."""
+    b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng = _chain_case(oracle, seed=1)
+    P = 40
+    u = syn.unit_vectors(rng, P)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), u * rng.uniform(7.5, 8.0, (P, 1))], 1)
+    E, d, inv = oracle.score_poses(tables, X, qM, Y, zL, poses, 2.5)
+    assert inv == 0
+    centres = lambda i: -b + (i + 0.5) * h
+    for p in range(P):
+        R_ = oracle.quat_to_rot(poses[p, :4])
+        Xp = np.stack([oracle.transform(R_, y, poses[p, 4:]) for y in Y])
+        S = oracle.coulomb_scale(X, qM, Xp, zL)
+        e_cont = oracle.coulomb_binding(X, qM, Xp, zL)
+        e_snap = oracle.coulomb_binding(centres(iM), qM, centres(oracle.snap_np(Xp, b, n)), zL)
+        assert abs(E[p] - e_snap) <= 1e-6 * S
+        assert abs(E[p] - e_cont) <= 2e-2 * S
+
+
+def test_swap_symmetry(oracle):
+    """Eq. (15): sum_l z_l P_M(x_l) = sum_m z_m P_L(x_m).  With K_RS even
+    (g[-d] == g[d]) the uncompressed RS energies agree to roundoff."""
+    b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng = _chain_case(oracle, seed=2)
+    tvec = np.array([3.0, -1.0, 2.0])
+    Xl = Y + tvec                                   # ligand placed by a pure translation
+    ident = np.array([[1.0, 0, 0, 0, *tvec]])
+    E_ml, _, _ = oracle.score_poses(tables, X, qM, Y, zL, ident, 2.5)
+    iL = oracle.snap_np(Xl, b, n)
+    F = oracle.uncompressed_long_factors(iL, zL, t, a, lm, n, h)
+    tab2 = dict(tables, F1=F[0], F2=F[1], F3=F[2], R=F[0].shape[1])
+    E_lm, _, _ = oracle.score_poses(tab2, Xl, zL, X, qM, np.array([[1.0, 0, 0, 0, 0, 0, 0]]), 2.5)
+    S = oracle.coulomb_scale(X, qM, Xl, zL)
+    assert abs(E_ml[0] - E_lm[0]) <= 1e-13 * S
+
+
+def test_decomposition_identity_brute_force(oracle):
+    """E_N(M u L) = E_M + E_L + E_N(M, L), all by Eq. (10)/(13)."""
+    rng = np.random.default_rng(7)
+    X = rng.normal(size=(20, 3)) * 3
+    Y = rng.normal(size=(5, 3)) * 3 + 10
+    q, z = rng.uniform(-1, 1, 20), rng.uniform(-1, 1, 5)
+
+    def total(P, c):
+        r = cdist(P, P)
+        np.fill_diagonal(r, np.inf)
+        return 0.5 * math.fsum((c[:, None] * c[None, :] / r).ravel())
+    lhs = total(np.vstack([X, Y]), np.concatenate([q, z]))
+    rhs = total(X, q) + total(Y, z) + oracle.coulomb_binding(X, q, Y, z)
+    assert abs(lhs - rhs) < 1e-12 * (abs(lhs) + 1)
+
+
+def test_table2_first_order_grid_convergence(oracle):
+    """Table 2: two opposite charges ~1.5 A apart; the tensor energy error
+    halves per grid doubling (first order: error * n ~ const).  Averaged over placements."""
+    rng = np.random.default_rng(8)
+    b = 4.0
+    sep = 1.5875
+    errs = []
+    for n in (32, 64, 128, 256):
+        h, t, a, lm, ns = _rs_setup(oracle, b, n, 1e-8, 0.3)
+        e = []
+        for _ in range(24):
+            c = rng.uniform(-1, 1, 3)
+            u = syn.unit_vectors(rng, 1)[0]
+            Xm = (c - 0.5 * sep * u)[None, :]
+            Y = np.zeros((1, 3))
+            iM = oracle.snap_np(Xm, b, n)
+            F = oracle.uncompressed_long_factors(iM, np.array([1.0]), t, a, lm, n, h)
+            S = oracle.short_tables(t, a, lm, h, ns)
+            tab = dict(n=n, b=b, R=F[0].shape[1], F1=F[0], F2=F[1], F3=F[2], n_sigma=ns,
+                       S1=S[0], S2=S[1], S3=S[2])
+            pose = np.array([[1.0, 0, 0, 0, *(c + 0.5 * sep * u)]])
+            E, _, _ = oracle.score_poses(tab, Xm, np.array([1.0]), Y, np.array([-1.0]), pose, 1.0)
+            e.append(abs(E[0] - (-1.0 / sep)))
+        errs.append(np.mean(e))
+    ratios = [errs[i] / errs[i + 1] for i in range(3)]
+    assert all(1.4 < r < 2.9 for r in ratios), (errs, ratios)
