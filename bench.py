@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the RS-tensor pose-rescoring hot path (Algorithm PLIE + Eq. (22)) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+One "step" = one pass of the whole hot path (H1-H8) over the config's full pose batch
+(C3: 10^6 poses x 60 atoms, n = 4096, R = 16), inputs resident in HBM, through the C ABI
+(rs_score_poses_async on device tensors).  L2 is flushed (256 MiB write) between timed
+steps, outside the timed events.  Prints ONE JSON line on rank 0.
+
+Multi-GPU (torchrun, one process per GPU): poses are independent units, so each rank scores
+its own batch with its own replica of the protein handle and no data-path collective
+("scaling": "weak"); the step time is the max over ranks (NCCL all-reduce of the timings).
+
+--impl reference times the oracle (oracle/, plain scalar C, OpenMP over poses) on the host
+cores on a bounded sample of the same workload (rank 0 only)."""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "poses/sec and ligand-atom evals/sec at 1 B200; fraction of FP64/L2 roofline"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def run_microbench():
+    exe = os.path.join(ROOT, "tools", "microbench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_workload(name):
+    from synth import configs as syn
+    return syn.make(name)
+
+
+def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=20000, seed=7):
+    """Time the oracle (as it stands) on a bounded seeded sample of the workload's poses."""
+    from oracle import rs_oracle
+    from synth import configs as syn
+    _, probe = syn.subsample(w.poses, 64, seed=seed)
+    t0 = time.perf_counter()
+    rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, probe,
+                          w.dmin_cap)
+    dt = time.perf_counter() - t0
+    k = int(min(max_poses, max(64, 64 * budget_s / max(dt, 1e-6))))
+    idx, sample = syn.subsample(w.poses, k, seed=seed + 1)
+    t0 = time.perf_counter()
+    rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, sample,
+                          w.dmin_cap)
+    dt = time.perf_counter() - t0
+    return k, dt, rs_oracle.num_threads()
+
+
+def impl_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    w = load_workload(args.config)
+    from paper_2510_26611_b200 import rsdock
+    flags = 0
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            flags = rsdock.RS_FLAG_HOST_ONLY
+    except Exception:
+        flags = rsdock.RS_FLAG_HOST_ONLY
+    prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(), flags=flags)
+    tables = prot.export_tables()
+    from oracle import rs_oracle
+    from synth import configs as syn
+    per_step = max(16, args.ref_poses)
+    times = []
+    for s in range(args.warmup + args.steps):
+        _, sample = syn.subsample(w.poses, per_step, seed=100 + s)
+        t0 = time.perf_counter()
+        rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, sample,
+                              w.dmin_cap)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.sum(times))
+    val = per_step * args.steps / t
+    cores = rs_oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "poses/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "atom_evals_per_s": val * w.L,
+        "config": config_dict(w, args),
+        "cpu_baseline": {"value": val, "unit": "poses/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} seeded poses of {w.name} per step "
+                                   f"(brute-force short-range/vdW over all {w.M} protein atoms)"},
+        "e2e": {"value": val, "unit": "poses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(w, args):
+    return {"workload": f"{w.name}: protein M={w.M}, ligand L={w.L}, grid n={w.grid_n}, "
+                        f"box b={w.box_half_width}, R={w.rank_R}, P={w.P} poses",
+            "config": args.config, "M": w.M, "L": w.L, "n": w.grid_n, "R": w.rank_R,
+            "poses": w.P, "sigma_split": w.sigma_split, "sigma_vdw": w.sigma_vdw,
+            "parallelism": f"pose-shard x{args.gpus} (replicated handle)",
+            "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-poses", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return impl_reference(args)
+
+    import torch
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("nccl", device_id=dev)
+        dist = dist_mod
+
+    import __graft_entry__
+    __graft_entry__.build_library()
+    from paper_2510_26611_b200 import rsdock
+
+    w = load_workload(args.config)
+    ncpu = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                          device=local, n_threads=max(1, ncpu // max(world, 1)))
+    setup_s = time.perf_counter() - t0
+    info = prot.info
+
+    q = torch.tensor(w.ligand_q, device=dev)
+    y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
+    poses = torch.tensor(w.poses, device=dev).contiguous()
+    P, L = w.P, w.L
+    E = torch.empty(P, dtype=torch.float64, device=dev)
+    D = torch.empty(P, dtype=torch.float64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        prot.score_async(q, y, poses, E, D, cnt, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    if dist:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms = total_ms / args.steps
+    value = world * P / (ms * 1e-3)
+    invalid = int(cnt.item())
+
+    # end to end through the same C ABI with pinned HOST buffers (copies inside the call)
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(w.poses).pin_memory()
+        hq = torch.from_numpy(w.ligand_q).pin_memory()
+        hy = torch.from_numpy(np.ascontiguousarray(w.ligand_xyz)).pin_memory()
+        hE = torch.empty(P, dtype=torch.float64).pin_memory()
+        hD = torch.empty(P, dtype=torch.float64).pin_memory()
+        rsdock.rs_score_poses(prot.handle, hq, hy, L, hp, P, hE, hD)
+        tl = []
+        for _ in range(max(3, min(args.steps, 5))):
+            t1 = time.perf_counter()
+            rsdock.rs_score_poses(prot.handle, hq, hy, L, hp, P, hE, hD)
+            tl.append(time.perf_counter() - t1)
+        te = float(np.median(tl))
+        if dist:
+            tt = torch.tensor([te], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * P / te, "unit": "poses/s",
+               "h2d_bytes_per_step": int(P * 7 * 8 + L * 4 * 8), "d2h_bytes_per_step": int(P * 2 * 8),
+               "path": "rs_score_poses, pinned host buffers, 2-stream chunked H2D/kernel/D2H"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    mb = run_microbench()
+    peaks = _peaks()
+    R = info["R"]
+    gather_bytes = 24.0 * R * P * L                 # H4: 3 rows x R fp64 per atom evaluation
+    t_s = ms * 1e-3
+    achieved = gather_bytes / t_s / 1e9
+    smem_peak = mb.get("lds128_random_row_rotated_gbs") if mb else None
+    l2_peak = mb.get("l2_gather_1p5MB_gbs") if mb else None
+    fp64_rate = mb.get("dfma_instr_per_s") if mb else None
+    dp_instr = (3.0 * R + 25.0) * P * L            # R DMUL + R DMUL + R DADD + ~25 per atom
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+        "frac": (achieved / smem_peak) if smem_peak else None, "traffic": traffic,
+        "kernel": rsdock.load() and f"score_kernel<{R}>",
+        "peak_source": "tools/microbench (same run): conflict-free random-row LDS.128 "
+                       "(lane-rotated chunks), 148 SMs",
+        "algorithmic_bytes_per_launch": gather_bytes,
+        "fp64_frac": (dp_instr / t_s / fp64_rate) if fp64_rate else None,
+        "l2_literal_frac": (achieved / l2_peak) if l2_peak else None,
+        "hbm_peak_measured_gbs": peaks.get("hbm_gbs"),
+    }
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        k, dt, cores = cpu_reference_rate(w, prot.export_tables())
+        cpu = {"value": k / dt, "unit": "poses/s", "cores": cores, "kind": "oracle",
+               "sample": f"{k} seeded poses of {w.name} ({dt:.1f} s; brute-force short-range/vdW "
+                         f"over all {w.M} protein atoms)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "atom_evals_per_s": value * L,
+        "config": config_dict(w, args),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps, "clocks": clk.summary(),
+        "invalid_poses": invalid, "setup_seconds": setup_s,
+        "setup": {k: info[k] for k in ("R", "tucker_r", "quad_K", "R_long_ref", "R_short",
+                                       "n_sigma", "sampled_max_err", "sampled_rms_err",
+                                       "cp_core_err", "nbr_entries", "device_bytes")},
+        "step_ms_min": float(np.min(step_ms)), "step_ms_max": float(np.max(step_ms)),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,179 @@
+/*
+ * rs_dock.h -- C ABI of the B200-native RS-tensor pose-rescoring library (librsdock.so).
+ *
+ * Path: batched rescoring of rigid ligand poses against a protein whose
+ * free-space electrostatic potential is held in the range-separated (RS) canonical tensor
+ * format of Benner, Khoromskij, Khoromskaia & Stein, arXiv 2510.26611 ("the paper",
+ * PAPER.md):
+ *   - rs_build_protein  = Algorithm TEP, once per protein, host C++;
+ *   - rs_score_poses    = Algorithm PLIE with Lemma 3.2 / Eq. (18)
+ *     (PAPER.md:864-891), the RS entry formula and the van der Waals
+ *     constraint of Eq. (22), one fused sm_100a kernel.
+ *
+ * Units: the library is unit-agnostic.  Lengths in the caller's unit (the tests and bench
+ * use Angstrom), charges in e, energies in charge^2/length (x 0.529177210903 = hartree
+ * when lengths are Angstrom).
+ *
+ * Conventions shared by every entry point:
+ *   - All arrays are fp64, row-major, C-contiguous.  xyz arrays are N x 3.
+ *   - Poses are P x 7: (w, x, y, z, tx, ty, tz) = quaternion (scalar first, need not be
+ *     unit: it acts as its normalisation) and the translation of the ligand body frame.
+ *     The ligand coordinates passed in are body-frame coordinates, i.e. the caller centres
+ *     the ligand at its geometric centre (rotation about the centre,
+ *     then translation of the centre), so an atom lands at x' = R(q) y + t.
+ *   - The grid is Omega = [-b, b]^3 split into n^3 cells of width h = 2b/n (n even,
+ *     PAPER.md:278-282).  A point is evaluated at its cell (piecewise-constant basis,
+ *     PAPER.md:279-290); a point on a cell boundary belongs to the lower cell.
+ *   - Ownership: every input is caller-owned and only read during the call.  The handle
+ *     deep-copies what it needs and owns all device memory it allocates; rs_free releases
+ *     it.  Outputs are written, never retained.
+ *   - Errors: functions returning a pointer return NULL on error, functions returning an
+ *     integer return a negative RS_E_* code; rs_last_error() gives a thread-local message.
+ *     There is no CPU fallback: without a CUDA device rs_build_protein fails.
+ *   - Thread safety: a handle is immutable after build.  rs_score_poses_async on one handle
+ *     from several host threads / streams is safe.  rs_score_poses with host pointers
+ *     serialises on a per-handle lock (it reuses the handle's staging buffers).
+ */
+#ifndef RS_DOCK_H
+#define RS_DOCK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_E_INVALID_ARG (-1) /* a null pointer, a size < 0, a non-finite parameter ... */
+#define RS_E_CUDA        (-2) /* a CUDA runtime error (message in rs_last_error)        */
+#define RS_E_NOMEM       (-3) /* host or device allocation failed                        */
+#define RS_E_NO_DEVICE   (-4) /* handle built with RS_FLAG_HOST_ONLY or no CUDA device     */
+
+#define RS_FLAG_HOST_ONLY 1u  /* build the tables on the host only (no upload); for tests */
+
+typedef struct rs_handle rs_handle; /* opaque, immutable after build */
+
+/* Build parameters.  Initialise with rs_params_default() and override fields. */
+typedef struct {
+    int32_t  grid_n;        /* n, cells per axis, even, >= 2                */
+    int32_t  rank_R;        /* uploaded CP width R of the long-range part (Lemma 3.2's R;
+                               BASELINE's "R_l").  0 = tolerance mode: R from eps_compress     */
+    double   eps_compress;  /* relative tolerance of the Tucker (RHOSVD) and slice truncation  */
+    double   eps_quad;      /* sinc-quadrature target max relative error of 1/r on
+                               [h/4, 2 sqrt(3) b] (Eq. (2))                  */
+    double   sigma_split;   /* sigma_s: range-split radius; n_sigma = ceil(sigma_s / h)
+                               (TEP step 2 PAPER.md:1190-1193)               */
+    double   eps_split;     /* Gaussian k is long-range iff sqrt(ln(1/eps_split))/t_k >= sigma_s */
+    double   sigma_vdw;     /* vdW threshold: a pose clashes iff mindist < sigma_vdw (Eq. (22)) */
+    double   dmin_cap;      /* D_cap >= sigma_vdw: mindist is reported exactly below D_cap,
+                               +inf otherwise                                                   */
+    int32_t  tucker_rank_max; /* cap on the Tucker ranks r_l (0 = automatic)                    */
+    int32_t  als_sweeps;    /* CP-ALS sweeps when R < the exact C2T2C rank (0 = default 300)    */
+    int32_t  device;        /* CUDA device ordinal                                              */
+    int32_t  n_threads;     /* host threads for the setup (0 = all)                             */
+    uint64_t seed;          /* seed of the randomized range finder / ALS init                   */
+    uint32_t flags;         /* RS_FLAG_*                                                        */
+} rs_params;
+
+/* Information about a built handle (all host values). */
+typedef struct {
+    int32_t  n;             /* grid cells per axis */
+    double   b, h, inv_h;   /* half width, cell width 2b/n, n/(2b) */
+    int32_t  R;             /* CP width of the uploaded long-range factors */
+    int32_t  R_exact;       /* rank before CP-ALS (C2T2C rank of the Tucker core) */
+    int32_t  tucker_r[3];   /* Tucker ranks of the RHOSVD step */
+    int32_t  quad_K;        /* quadrature terms k = 0..K */
+    double   quad_s, quad_Ls; /* sinc step s and scale L_s (t_k = sinh(k s)/L_s) */
+    double   quad_err;      /* measured max relative error of the quadrature on its interval */
+    int32_t  R_long_ref;    /* number of long-range reference terms (Eq. (4) R_l) */
+    int32_t  R_short;       /* number of short-range reference terms R_s */
+    int32_t  n_sigma;       /* short-range support radius in cells */
+    int64_t  n_atoms;       /* protein atoms M */
+    double   tucker_err;    /* estimated relative Frobenius error of the Tucker step */
+    double   cp_core_err;   /* relative Frobenius error of the CP fit of the Tucker core */
+    double   sampled_max_err;  /* max |P_l - CP| / max |P_l| over sampled exterior cells */
+    double   sampled_rms_err;  /* rms of the same, relative to rms |P_l| */
+    int32_t  n_err_samples;
+    double   sigma_vdw, dmin_cap;
+    int64_t  nbr_cells;     /* coarse cells of the neighbour (cell-list) structure */
+    int64_t  nbr_entries;   /* total candidate entries */
+    int32_t  nbr_shift;     /* coarse cell = 2^nbr_shift fine cells */
+    int64_t  device_bytes;  /* bytes uploaded to the device */
+    double   setup_seconds; /* wall time of the whole build */
+    int32_t  on_device;     /* 1 when the tables are resident on a device */
+} rs_info;
+
+void rs_params_default(rs_params* p);
+
+/*
+ * Build the RS tensor of a protein (Algorithm TEP) and upload it once.
+ *   q        : n_atoms charges z_m                         (host)
+ *   xyz      : n_atoms x 3 positions x_m, inside [-b, b]^3 (host)
+ *   box_half_width : b > 0
+ *   params   : may be NULL (defaults)
+ * Steps: S1 sinc quadrature of 1/r (Eq. (2)), S2 long/short split (Eq. (4)), S3 1D Galerkin
+ * cell averages (Eq. (1)), S4 snapping of the atoms, S5 randomized RHOSVD of the implicit
+ * side matrices of the rank-(M x R_l) long-range sum (Eq. (6)), S6 Tucker core, S7 core ->
+ * CP of width R (exact canonical-Tucker-canonical when it fits, else CP-ALS), S8 short-range
+ * reference rows (Def. 2.1), S9 cell lists for the short-range / vdW pass, S10 upload.
+ * Returns NULL on error (invalid argument, atom outside the box, odd n, sigma_split < h,
+ * sigma_vdw > dmin_cap, no CUDA device unless RS_FLAG_HOST_ONLY, CUDA or allocation failure).
+ */
+rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
+                            double box_half_width, const rs_params* params);
+
+/*
+ * Score P poses of a rigid ligand (Algorithm PLIE + Eq. (22)), synchronously.
+ *   q_lig (n_lig), xyz_lig (n_lig x 3) : ligand charges and body-frame coordinates
+ *   poses (P x 7)                      : see conventions above
+ *   energies_out (P)                   : E_p = sum_l z_l [ P^long_{M,R}(i_l)
+ *                                         + sum_{m: |i_l - i_m|_2 <= n_sigma} z_m S(i_l - i_m) ]
+ *   mindist_out (P)                    : min_{l,m} |x'_l - x_m| if < dmin_cap, else +inf
+ * Pointers may be host (pageable or pinned) or device memory of the handle's device; each
+ * is detected with cudaPointerGetAttributes.  Host data are copied in and out inside the
+ * call.  A pose with a zero quaternion, a non-finite value, or any transformed atom outside
+ * [-b, b]^3 is invalid: both outputs are NaN.
+ * Returns the number of invalid poses (>= 0) or a negative RS_E_* code.
+ */
+int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                       const double* poses, int64_t P, double* energies_out, double* mindist_out);
+
+/*
+ * Asynchronous variant: all five arrays must be DEVICE memory; the work is enqueued on
+ * `cuda_stream` (a cudaStream_t, NULL = legacy default stream) and the call returns at once.
+ * If invalid_count_dev is not NULL, the number of invalid poses is written there (int64,
+ * device memory) by the same stream.  Returns 0 or a negative RS_E_* code.
+ */
+int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xyz_lig,
+                             int64_t n_lig, const double* poses, int64_t P,
+                             double* energies_out, double* mindist_out,
+                             int64_t* invalid_count_dev, void* cuda_stream);
+
+/* Fill *out.  Returns 0 or RS_E_INVALID_ARG. */
+int rs_get_info(const rs_handle* h, rs_info* out);
+
+/*
+ * Copy the uploaded tables to caller buffers (host), for the oracle and tests:
+ *   F1, F2, F3 : n x R each (long-range CP factors, weights folded into F1)
+ *   S1, S2, S3 : (2 n_sigma + 1) x R_short each (short-range reference rows, a_k in S1)
+ * Any pointer may be NULL to skip it.  Returns 0 or a negative code.
+ */
+int rs_export_tables(const rs_handle* h, double* F1, double* F2, double* F3, double* S1,
+                     double* S2, double* S3);
+
+/*
+ * Quadrature and split of the handle: t (K+1), a (K+1), is_long (K+1, 1/0), and the
+ * protein cells i_m (n_atoms x 3, int32) the handle snapped.  NULL skips an output.
+ */
+int rs_export_setup(const rs_handle* h, double* t, double* a, int32_t* is_long,
+                    int32_t* protein_cells);
+
+/* Message of the last error on this thread ("" if none). */
+const char* rs_last_error(void);
+
+/* Release the handle and its device memory.  NULL is a no-op. */
+void rs_free(rs_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_DOCK_H */

@@ -1,0 +1,493 @@
+// C ABI of librsdock (include/rs_dock.h): handle build (Algorithm TEP, host C++), upload,
+// and the scoring entry points that enqueue the fused sm_100a kernel (score_kernel.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "rs_internal.h"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const std::string& s) { g_err = s; }
+
+#define CUDA_TRY(expr, code)                                                               \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      set_err(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #expr);        \
+      return code;                                                                         \
+    }                                                                                      \
+  } while (0)
+
+bool finite_all(const double* p, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+// O3 snapping, the library's copy (the oracle has its own): u = (x + b) * inv_h,
+// i = ceil(u) - 1 clamped to [0, n-1]; -1 outside [-b, b].
+int snap_cell(double x, double b, double inv_h, int n) {
+  if (!(x >= -b && x <= b)) return -1;
+  double u = (x + b) * inv_h;
+  double c = std::ceil(u) - 1.0;
+  c = std::min(std::max(c, 0.0), double(n - 1));
+  return (int)c;
+}
+
+void free_device(rs_handle* h) {
+  if (!h->on_device) return;
+  cudaSetDevice(h->device);
+  for (void*& p : h->dmem) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  if (h->d_nb_idx) cudaFree(h->d_nb_idx);
+  h->d_nb_idx = nullptr;
+  if (h->stage) cudaFree(h->stage);
+  h->stage = nullptr;
+  for (void*& s : h->streams) {
+    if (s) cudaStreamDestroy((cudaStream_t)s);
+    s = nullptr;
+  }
+  h->on_device = false;
+}
+
+template <class T>
+int upload(void** dst, const std::vector<T>& v, int64_t* bytes) {
+  size_t nb = std::max<size_t>(sizeof(T), v.size() * sizeof(T));
+  CUDA_TRY(cudaMalloc(dst, nb), RS_E_NOMEM);
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), RS_E_CUDA);
+  *bytes += (int64_t)nb;
+  return 0;
+}
+
+int upload_handle(rs_handle* h) {
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  h->on_device = true;
+  int64_t bytes = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (int e = upload(&h->dmem[a], h->F[a], &bytes)) return e;
+    if (int e = upload(&h->dmem[3 + a], h->S[a], &bytes)) return e;
+  }
+  std::vector<double> rec(4 * (size_t)h->M);
+  std::vector<int32_t> ridx(4 * (size_t)h->M, 0);
+  for (int64_t m = 0; m < h->M; ++m) {
+    for (int a = 0; a < 3; ++a) {
+      rec[4 * m + a] = h->xyz[3 * m + a];
+      ridx[4 * m + a] = h->cells[3 * m + a];
+    }
+    rec[4 * m + 3] = h->z[m];
+  }
+  if (int e = upload(&h->dmem[6], rec, &bytes)) return e;
+  if (int e = upload(&h->dmem[7], ridx, &bytes)) return e;
+  if (int e = upload(&h->dmem[8], h->cg.off, &bytes)) return e;
+  if (int e = upload(&h->d_nb_idx, h->cg.idx, &bytes)) return e;
+  h->device_bytes = bytes;
+  return 0;
+}
+
+rs::ScoreArgs base_args(const rs_handle* h) {
+  rs::ScoreArgs a{};
+  a.n = h->n;
+  a.R = h->R;
+  a.Rs = h->Rs;
+  a.n_sigma = h->n_sigma;
+  a.b = h->b;
+  a.inv_h = h->inv_h;
+  a.h = h->h;
+  a.dcap2 = h->prm.dmin_cap * h->prm.dmin_cap;
+  a.nb_shift = h->cg.shift;
+  for (int i = 0; i < 3; ++i) {
+    a.nb_lo[i] = h->cg.lo[i];
+    a.nb_dim[i] = h->cg.dim[i];
+    a.t.F[i] = (const double*)h->dmem[i];
+    a.t.S[i] = (const double*)h->dmem[3 + i];
+  }
+  a.t.rec = h->dmem[6];
+  a.t.rec_idx = h->dmem[7];
+  a.t.nb_off = (const int32_t*)h->dmem[8];
+  a.t.nb_idx = (const int32_t*)h->d_nb_idx;
+  return a;
+}
+
+// 1 = device (or managed) pointer of the handle's device, 0 = host memory
+int pointer_kind(const void* p) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? 1 : 0;
+}
+
+// Ligand radius max |y_l| (body frame).  Only steers the launch shape (shared-memory window
+// or not); correctness never depends on it (the kernel recomputes it).  Device ligands are
+// read back once per (pointer, L) and cached on the handle.
+double ligand_rmax(rs_handle* h, const double* yl, int64_t L, bool dev) {
+  if (L <= 0) return 0.0;
+  std::vector<double> tmp;
+  const double* y = yl;
+  if (dev) {
+    if (h->rmax_key == (const void*)yl && h->rmax_L == L) return h->rmax_val;
+    tmp.resize(3 * (size_t)L);
+    if (cudaMemcpy(tmp.data(), yl, 3 * (size_t)L * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return -1.0;
+    }
+    y = tmp.data();
+  }
+  double r2 = 0.0;
+  for (int64_t l = 0; l < L; ++l)
+    r2 = std::max(r2, y[3 * l] * y[3 * l] + y[3 * l + 1] * y[3 * l + 1] + y[3 * l + 2] * y[3 * l + 2]);
+  const double r = std::sqrt(r2);
+  if (dev) {
+    h->rmax_key = (const void*)yl;
+    h->rmax_L = L;
+    h->rmax_val = r;
+  }
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+void rs_params_default(rs_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->grid_n = 256;
+  p->rank_R = 16;
+  p->eps_compress = 1e-8;
+  p->eps_quad = 1e-6;
+  p->sigma_split = 2.0;
+  p->eps_split = 1e-6;
+  p->sigma_vdw = 2.5;
+  p->dmin_cap = 2.5;
+  p->tucker_rank_max = 0;
+  p->als_sweeps = 0;
+  p->device = 0;
+  p->n_threads = 0;
+  p->seed = 0x5EED5EEDull;
+  p->flags = 0;
+}
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
+                            double box_half_width, const rs_params* params) {
+  g_err.clear();
+  auto t0 = std::chrono::steady_clock::now();
+  rs_params prm;
+  if (params) prm = *params; else rs_params_default(&prm);
+  if (!q || !xyz) { set_err("null input pointer"); return nullptr; }
+  if (n_atoms <= 0) { set_err("n_atoms must be > 0"); return nullptr; }
+  if (!(box_half_width > 0) || !std::isfinite(box_half_width)) { set_err("box_half_width must be finite and > 0"); return nullptr; }
+  if (prm.grid_n < 2 || (prm.grid_n & 1)) { set_err("grid_n must be even and >= 2"); return nullptr; }
+  if (prm.grid_n > (1 << 20)) { set_err("grid_n too large"); return nullptr; }
+  if (prm.rank_R < 0) { set_err("rank_R must be >= 0"); return nullptr; }
+  if (!(prm.eps_compress > 0 && prm.eps_compress < 1)) { set_err("eps_compress must be in (0,1)"); return nullptr; }
+  if (!(prm.eps_quad > 0 && prm.eps_quad < 1)) { set_err("eps_quad must be in (0,1)"); return nullptr; }
+  if (!(prm.eps_split > 0 && prm.eps_split < 1)) { set_err("eps_split must be in (0,1)"); return nullptr; }
+  if (!(prm.sigma_vdw >= 0) || !(prm.dmin_cap >= prm.sigma_vdw) || !std::isfinite(prm.dmin_cap)) {
+    set_err("need 0 <= sigma_vdw <= dmin_cap < inf");
+    return nullptr;
+  }
+  if (!finite_all(q, n_atoms) || !finite_all(xyz, 3 * n_atoms)) { set_err("non-finite protein input"); return nullptr; }
+  const int n = prm.grid_n;
+  const double b = box_half_width;
+  const double h = 2.0 * b / double(n);
+  if (!(prm.sigma_split >= h) || !std::isfinite(prm.sigma_split)) { set_err("sigma_split must be >= h = 2b/n"); return nullptr; }
+  const bool host_only = (prm.flags & RS_FLAG_HOST_ONLY) != 0;
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= prm.device || prm.device < 0) {
+      cudaGetLastError();
+      set_err("no CUDA device (there is no CPU fallback; use RS_FLAG_HOST_ONLY for host-only tables)");
+      return nullptr;
+    }
+  }
+#ifdef _OPENMP
+  if (prm.n_threads > 0) omp_set_num_threads(prm.n_threads);
+#endif
+  std::unique_ptr<rs_handle> H;
+  try {
+    H.reset(new rs_handle());
+  } catch (...) {
+    set_err("out of host memory");
+    return nullptr;
+  }
+  rs_handle* hd = H.get();
+  hd->prm = prm;
+  hd->n = n;
+  hd->b = b;
+  hd->h = h;
+  hd->inv_h = double(n) / (2.0 * b);
+  hd->device = prm.device;
+  hd->M = n_atoms;
+  try {
+    hd->xyz.assign(xyz, xyz + 3 * n_atoms);
+    hd->z.assign(q, q + n_atoms);
+    // S4: snap protein atoms
+    hd->cells.resize(3 * n_atoms);
+    for (int64_t m = 0; m < n_atoms; ++m)
+      for (int a = 0; a < 3; ++a) {
+        int c = snap_cell(xyz[3 * m + a], b, hd->inv_h, n);
+        if (c < 0) {
+          set_err("protein atom " + std::to_string(m) + " outside [-b, b]^3");
+          return nullptr;
+        }
+        hd->cells[3 * m + a] = c;
+      }
+    // S1: quadrature on [h/4, 2 sqrt(3) b]
+    const double Ls = 2.0 * std::sqrt(3.0) * b;
+    hd->quad = rs::choose_quadrature(prm.eps_quad, h / 4.0, Ls, Ls);
+    if (hd->quad.K < 0) { set_err("quadrature search failed for eps_quad"); return nullptr; }
+    // S2: split
+    std::vector<double> tl, al, ts, as;
+    hd->is_long.resize(hd->quad.t.size());
+    for (size_t k = 0; k < hd->quad.t.size(); ++k) {
+      bool lg = rs::is_long_term(hd->quad.t[k], prm.sigma_split, prm.eps_split);
+      hd->is_long[k] = lg ? 1 : 0;
+      if (lg) { tl.push_back(hd->quad.t[k]); al.push_back(hd->quad.a[k]); }
+      else { ts.push_back(hd->quad.t[k]); as.push_back(hd->quad.a[k]); }
+    }
+    hd->R_long_ref = (int)tl.size();
+    hd->Rs = (int)ts.size();
+    hd->n_sigma = (int)std::ceil(prm.sigma_split / h);
+    // S5-S7
+    rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
+                            prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep);
+    // S8: short-range reference rows, a_k folded into S1 (Def. 2.1, A_0)
+    const int ns = hd->n_sigma, Rs = hd->Rs;
+    for (int a = 0; a < 3; ++a) hd->S[a].assign((size_t)(2 * ns + 1) * Rs, 0.0);
+    for (int d = -ns; d <= ns; ++d)
+      for (int k = 0; k < Rs; ++k) {
+        const double g = rs::cell_average(ts[k], h, d);
+        hd->S[0][(size_t)(d + ns) * Rs + k] = g * as[k];
+        hd->S[1][(size_t)(d + ns) * Rs + k] = g;
+        hd->S[2][(size_t)(d + ns) * Rs + k] = g;
+      }
+    // S9: cell lists covering every pair that can matter: vdW pairs (< dmin_cap) and the
+    // short-range ball (|i_l - i_m|_2 <= n_sigma => |x_l - x_m| <= (n_sigma + sqrt 3) h)
+    const double rho = std::max(prm.dmin_cap, (ns + std::sqrt(3.0)) * h);
+    rs::build_cell_lists(n, b, h, hd->xyz, hd->cells, rho, &hd->cg);
+    // sampled compression error at exterior cells
+    const double work = double(n_atoms) * double(tl.size());
+    const int nsamp = (int)std::max(100.0, std::min(2000.0, 4e9 / std::max(work, 1.0)));
+    rs::sample_compression_error(n, b, h, hd->xyz, hd->cells, hd->z, tl, al, hd->F, hd->R,
+                                 std::max(prm.sigma_vdw, h), hd->cg, nsamp, prm.seed, &hd->rep);
+  } catch (const std::bad_alloc&) {
+    set_err("out of host memory during setup");
+    return nullptr;
+  }
+  if (!host_only) {
+    if (upload_handle(hd) != 0) {
+      std::string msg = g_err;
+      free_device(hd);
+      set_err(msg.empty() ? "upload failed" : msg);
+      return nullptr;
+    }
+  }
+  hd->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return H.release();
+}
+
+int rs_get_info(const rs_handle* h, rs_info* out) {
+  if (!h || !out) { set_err("null argument"); return RS_E_INVALID_ARG; }
+  std::memset(out, 0, sizeof(*out));
+  out->n = h->n;
+  out->b = h->b;
+  out->h = h->h;
+  out->inv_h = h->inv_h;
+  out->R = h->R;
+  out->R_exact = h->rep.R_exact;
+  for (int i = 0; i < 3; ++i) out->tucker_r[i] = h->rep.tucker_r[i];
+  out->quad_K = h->quad.K;
+  out->quad_s = h->quad.s;
+  out->quad_Ls = h->quad.Ls;
+  out->quad_err = h->quad.err;
+  out->R_long_ref = h->R_long_ref;
+  out->R_short = h->Rs;
+  out->n_sigma = h->n_sigma;
+  out->n_atoms = h->M;
+  out->tucker_err = h->rep.tucker_err;
+  out->cp_core_err = h->rep.cp_core_err;
+  out->sampled_max_err = h->rep.sampled_max;
+  out->sampled_rms_err = h->rep.sampled_rms;
+  out->n_err_samples = h->rep.n_samples;
+  out->sigma_vdw = h->prm.sigma_vdw;
+  out->dmin_cap = h->prm.dmin_cap;
+  out->nbr_cells = (int64_t)h->cg.dim[0] * h->cg.dim[1] * h->cg.dim[2];
+  out->nbr_entries = (int64_t)h->cg.idx.size();
+  out->nbr_shift = h->cg.shift;
+  out->device_bytes = h->device_bytes;
+  out->setup_seconds = h->setup_seconds;
+  out->on_device = h->on_device ? 1 : 0;
+  return 0;
+}
+
+int rs_export_tables(const rs_handle* h, double* F1, double* F2, double* F3, double* S1,
+                     double* S2, double* S3) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  double* F[3] = {F1, F2, F3};
+  double* S[3] = {S1, S2, S3};
+  for (int a = 0; a < 3; ++a) {
+    if (F[a]) std::copy(h->F[a].begin(), h->F[a].end(), F[a]);
+    if (S[a]) std::copy(h->S[a].begin(), h->S[a].end(), S[a]);
+  }
+  return 0;
+}
+
+int rs_export_setup(const rs_handle* h, double* t, double* a, int32_t* is_long,
+                    int32_t* protein_cells) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  if (t) std::copy(h->quad.t.begin(), h->quad.t.end(), t);
+  if (a) std::copy(h->quad.a.begin(), h->quad.a.end(), a);
+  if (is_long) std::copy(h->is_long.begin(), h->is_long.end(), is_long);
+  if (protein_cells) std::copy(h->cells.begin(), h->cells.end(), protein_cells);
+  return 0;
+}
+
+void rs_free(rs_handle* h) {
+  if (!h) return;
+  free_device(h);
+  delete h;
+}
+
+int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xyz_lig,
+                             int64_t n_lig, const double* poses, int64_t P,
+                             double* energies_out, double* mindist_out,
+                             int64_t* invalid_count_dev, void* cuda_stream) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
+  if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
+  if (P > 0 && (!poses || !energies_out || !mindist_out)) { set_err("null pose/output pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > 0 && (!q_lig || !xyz_lig)) { set_err("null ligand pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > (int64_t)1 << 30) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
+  const void* ptrs[5] = {q_lig, xyz_lig, poses, energies_out, mindist_out};
+  for (const void* p : ptrs)
+    if (p && pointer_kind(p) != 1) { set_err("rs_score_poses_async needs device pointers"); return RS_E_INVALID_ARG; }
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (invalid_count_dev)
+    CUDA_TRY(cudaMemsetAsync(invalid_count_dev, 0, sizeof(int64_t), st), RS_E_CUDA);
+  if (P == 0) return 0;
+  rs::ScoreArgs a = base_args(h);
+  a.zl = q_lig;
+  a.yl = xyz_lig;
+  a.L = n_lig;
+  a.poses = poses;
+  a.P = P;
+  a.E = energies_out;
+  a.D = mindist_out;
+  a.invalid = (unsigned long long*)invalid_count_dev;
+  {
+    std::lock_guard<std::mutex> lock(h->mtx);
+    a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, true);
+  }
+  int e = rs::launch_score(a, st, h->device, nullptr);
+  if (e != 0) {
+    set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
+    return RS_E_CUDA;
+  }
+  return 0;
+}
+
+int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                       const double* poses, int64_t P, double* energies_out, double* mindist_out) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
+  if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
+  if (P > 0 && (!poses || !energies_out || !mindist_out)) { set_err("null pose/output pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > 0 && (!q_lig || !xyz_lig)) { set_err("null ligand pointer"); return RS_E_INVALID_ARG; }
+  if (P == 0) return 0;
+  std::lock_guard<std::mutex> lock(h->mtx);
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  // synchronous API: order after any prior work on the device that produced the inputs
+  CUDA_TRY(cudaDeviceSynchronize(), RS_E_CUDA);
+  const bool lig_dev = n_lig == 0 || (pointer_kind(q_lig) == 1 && pointer_kind(xyz_lig) == 1);
+  const bool pose_dev = pointer_kind(poses) == 1;
+  const bool e_dev = pointer_kind(energies_out) == 1;
+  const bool d_dev = pointer_kind(mindist_out) == 1;
+  // chunked 2-stream pipeline: H2D(poses chunk) -> kernel -> D2H(outputs chunk), so the copies
+  // of one chunk overlap the kernel of the other
+  const int64_t CH = std::min<int64_t>(P, std::max<int64_t>(1 << 16, (P + 7) / 8));
+  const size_t lig_b = (size_t)4 * std::max<int64_t>(n_lig, 1) * sizeof(double);
+  const size_t pose_b = (size_t)CH * 7 * sizeof(double), out_b = (size_t)CH * sizeof(double);
+  const size_t need = lig_b + 2 * pose_b + 4 * out_b + 64;
+  if (h->stage_bytes < need) {
+    if (h->stage) cudaFree(h->stage);
+    h->stage = nullptr;
+    h->stage_bytes = 0;
+    CUDA_TRY(cudaMalloc(&h->stage, need), RS_E_NOMEM);
+    h->stage_bytes = need;
+  }
+  for (void*& s : h->streams)
+    if (!s) CUDA_TRY(cudaStreamCreateWithFlags((cudaStream_t*)&s, cudaStreamNonBlocking), RS_E_CUDA);
+  char* base = (char*)h->stage;
+  double* d_lig = (double*)base;
+  double* d_pose[2] = {(double*)(base + lig_b), (double*)(base + lig_b + pose_b)};
+  double* d_E[2] = {(double*)(base + lig_b + 2 * pose_b), (double*)(base + lig_b + 2 * pose_b + out_b)};
+  double* d_D[2] = {(double*)(base + lig_b + 2 * pose_b + 2 * out_b),
+                    (double*)(base + lig_b + 2 * pose_b + 3 * out_b)};
+  unsigned long long* d_cnt = (unsigned long long*)(base + lig_b + 2 * pose_b + 4 * out_b);
+  const double *zl = q_lig, *yl = xyz_lig;
+  if (!lig_dev) {
+    CUDA_TRY(cudaMemcpy(d_lig, q_lig, n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpy(d_lig + n_lig, xyz_lig, 3 * n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+    zl = d_lig;
+    yl = d_lig + n_lig;
+  }
+  cudaStream_t st[2] = {(cudaStream_t)h->streams[0], (cudaStream_t)h->streams[1]};
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), st[0]), RS_E_CUDA);
+  CUDA_TRY(cudaStreamSynchronize(st[0]), RS_E_CUDA);
+  rs::ScoreArgs a = base_args(h);
+  a.zl = zl;
+  a.yl = yl;
+  a.L = n_lig;
+  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
+  int chunk = 0;
+  for (int64_t off = 0; off < P; off += CH, ++chunk) {
+    const int64_t cnt = std::min(CH, P - off);
+    const int s = chunk & 1;
+    const double* pp = poses + 7 * off;
+    if (!pose_dev) {
+      CUDA_TRY(cudaMemcpyAsync(d_pose[s], pp, cnt * 7 * sizeof(double), cudaMemcpyHostToDevice, st[s]), RS_E_CUDA);
+      pp = d_pose[s];
+    }
+    a.poses = pp;
+    a.P = cnt;
+    a.E = e_dev ? energies_out + off : d_E[s];
+    a.D = d_dev ? mindist_out + off : d_D[s];
+    a.invalid = d_cnt + s;
+    int e = rs::launch_score(a, st[s], h->device, nullptr);
+    if (e != 0) {
+      set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
+      return RS_E_CUDA;
+    }
+    if (!e_dev) CUDA_TRY(cudaMemcpyAsync(energies_out + off, d_E[s], cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
+    if (!d_dev) CUDA_TRY(cudaMemcpyAsync(mindist_out + off, d_D[s], cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
+  }
+  CUDA_TRY(cudaStreamSynchronize(st[1]), RS_E_CUDA);
+  CUDA_TRY(cudaStreamSynchronize(st[0]), RS_E_CUDA);
+  unsigned long long cnts[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(cnts, d_cnt, sizeof(cnts), cudaMemcpyDeviceToHost), RS_E_CUDA);
+  return (int64_t)(cnts[0] + cnts[1]);
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Internal declarations of librsdock (not part of the C ABI; see include/rs_dock.h).
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rs_dock.h"
+
+namespace rs {
+
+// ---- host setup (Algorithm TEP) --------------------------------------
+
+struct Quadrature {          // S1: 1/r ~ sum_k a_k exp(-t_k^2 r^2)   (Eq. (2))
+  double s = 0, Ls = 0, err = 0;
+  int K = 0;
+  std::vector<double> t, a;  // k = 0..K
+};
+
+Quadrature choose_quadrature(double eps, double rmin, double rmax, double Ls);
+// S2: long iff t_k == 0 or sqrt(ln(1/eps_split))/t_k >= sigma_s  (Eq. (4))
+bool is_long_term(double t, double sigma_s, double eps_split);
+// S3: (1/h) * integral over cell d of exp(-t^2 x^2)  (Eq. (1))
+double cell_average(double t, double h, long d);
+
+struct CoarseGrid {          // S9 neighbour structure (cell lists over coarse cells)
+  int shift = 0;             // coarse cell = 2^shift fine cells per axis
+  int lo[3] = {0, 0, 0};     // first coarse index per axis
+  int dim[3] = {0, 0, 0};    // coarse cells per axis
+  std::vector<int32_t> off;  // CSR offsets (ncells + 1)
+  std::vector<int32_t> idx;  // protein atom indices
+};
+
+struct SetupReport {
+  int tucker_r[3] = {0, 0, 0};
+  int R_exact = 0;
+  double tucker_err = 0, cp_core_err = 0, sampled_max = 0, sampled_rms = 0;
+  int n_samples = 0;
+};
+
+// S5-S7: rank-R CP factors (n x R row-major each) of the protein's long-range potential
+// P_l[i] = sum_m z_m sum_{k long} a_k prod_a g_k[i_a - i_{m,a}]   (Eq. (6))
+void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
+                         const std::vector<double>& z, const std::vector<double>& t_long,
+                         const std::vector<double>& a_long, int rank_R, double eps,
+                         int tucker_cap, int als_sweeps, uint64_t seed,
+                         std::vector<double> F[3], int* R_out, SetupReport* rep);
+
+void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
+                      const std::vector<int32_t>& cells, double rho, CoarseGrid* cg);
+
+void sample_compression_error(int n, double b, double h, const std::vector<double>& xyz,
+                              const std::vector<int32_t>& cells, const std::vector<double>& z,
+                              const std::vector<double>& t_long, const std::vector<double>& a_long,
+                              const std::vector<double> F[3], int R, double r_excl,
+                              const CoarseGrid& cg, int n_samples, uint64_t seed,
+                              SetupReport* rep);
+
+// ---- device side -------------------------------------------------------------------------
+
+struct DeviceTables {
+  const double* F[3] = {nullptr, nullptr, nullptr};
+  const double* S[3] = {nullptr, nullptr, nullptr};
+  const void* rec = nullptr;      // double4 per protein atom: x, y, z, q
+  const void* rec_idx = nullptr;  // int4 per protein atom: i0, i1, i2, 0
+  const int32_t* nb_off = nullptr;
+  const int32_t* nb_idx = nullptr;
+};
+
+struct ScoreArgs {               // one launch of the scoring kernel
+  int n, R, Rs, n_sigma;
+  double b, inv_h, h, dcap2;
+  int nb_shift, nb_lo[3], nb_dim[3];
+  DeviceTables t;
+  const double* zl;
+  const double* yl;
+  int64_t L;
+  const double* poses;
+  int64_t P;
+  double* E;
+  double* D;
+  unsigned long long* invalid;   // may be null
+  double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
+};
+
+// Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
+// (if not null) is incremented by the number of kernels enqueued.
+int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
+const char* score_kernel_variant(int R);
+
+}  // namespace rs
+
+struct rs_handle {
+  rs_params prm;
+  int n = 0;
+  double b = 0, h = 0, inv_h = 0;
+  rs::Quadrature quad;
+  std::vector<int32_t> is_long;        // per quadrature term
+  int R = 0, Rs = 0, n_sigma = 0, R_long_ref = 0;
+  std::vector<double> F[3];            // n x R
+  std::vector<double> S[3];            // (2 n_sigma + 1) x Rs
+  int64_t M = 0;
+  std::vector<double> xyz, z;          // protein
+  std::vector<int32_t> cells;          // M x 3
+  rs::CoarseGrid cg;
+  rs::SetupReport rep;
+  double setup_seconds = 0;
+  // device
+  bool on_device = false;
+  int device = 0;
+  void* dmem[9] = {nullptr};           // F1..3, S1..3, rec, rec_idx, nb_off
+  void* d_nb_idx = nullptr;
+  int64_t device_bytes = 0;
+  // staging for host-pointer calls
+  std::mutex mtx;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  void* streams[2] = {nullptr, nullptr};
+  // cached ligand radius for device-resident ligands (only steers the launch shape)
+  const void* rmax_key = nullptr;
+  int64_t rmax_L = -1;
+  double rmax_val = -1;
+};

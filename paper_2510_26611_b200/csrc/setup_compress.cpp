@@ -1,0 +1,661 @@
+// S5-S7 of Algorithm TEP: the long-range part of the protein potential
+//   P_l[i] = sum_m z_m sum_{k long} a_k g_k[i_0 - c_{m,0}] g_k[i_1 - c_{m,1}] g_k[i_2 - c_{m,2}]
+// (shift-and-windowing sum, Eq. (5)-(6)) is a canonical tensor of rank
+// M * R_l ("initial rank R' = N_M R_L").  It is never formed.  Its rank is
+// reduced (TEP step 4, "canonical-Tucker-canonical transform") by
+//   S5  RHOSVD: per mode, the dominant left singular subspace of the implicit, weighted side
+//       matrix [g_k[. - c_{m,l}]]_{(m,k)} (n x M R_l), found by a randomized range finder whose
+//       products with the side matrix are 1D convolutions (FFT) with binned charge trains;
+//   S6  the exact Tucker core G = P_l x_0 U_0^T x_1 U_1^T x_2 U_2^T;
+//   S7  core -> CP: the exact slice expansion (rank <= r_0 min(r_1, r_2)) when it fits in R,
+//       else CP-ALS to width R initialised from the dominant slice triplets.
+// Then F_l = U_l X_l (n x R), weights folded into F_0.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "rs_internal.h"
+#include "setup_linalg.h"
+
+namespace rs {
+
+using la::cplx;
+
+namespace {
+
+struct ConvOps {
+  int n = 0, N = 0, RL = 0;
+  la::FFT fft{2};
+  std::vector<std::vector<double>> G;     // G[k][d], d = 0..n-1 (even kernel)
+  std::vector<std::vector<cplx>> FG;      // FFT of the centred kernel, size N
+  std::vector<std::vector<double>> nrm;   // windowed column norms N_k(j)
+
+  ConvOps(int n_, double h, const std::vector<double>& t_long) : n(n_), RL((int)t_long.size()) {
+    N = 1;
+    while (N < 3 * n) N <<= 1;
+    fft = la::FFT(N);
+    G.assign(RL, std::vector<double>(n));
+    FG.assign(RL, std::vector<cplx>(N));
+    nrm.assign(RL, std::vector<double>(n));
+#pragma omp parallel for schedule(dynamic)
+    for (int k = 0; k < RL; ++k) {
+      for (int d = 0; d < n; ++d) G[k][d] = cell_average(t_long[k], h, d);
+      std::vector<cplx>& f = FG[k];
+      std::fill(f.begin(), f.end(), cplx(0, 0));
+      for (int m = 0; m < 2 * n - 1; ++m) f[m] = G[k][std::abs(m - (n - 1))];
+      fft.forward(f.data());
+      // prefix sums of G^2 over d = -(n-1)..(n-1)
+      std::vector<double> pre(2 * n, 0.0);
+      for (int m = 0; m < 2 * n - 1; ++m) {
+        double g = G[k][std::abs(m - (n - 1))];
+        pre[m + 1] = pre[m] + g * g;
+      }
+      // N_k(j)^2 = sum_{i=0}^{n-1} G[i-j]^2 = sum_{d=-j}^{n-1-j}; index m = d + n - 1
+      for (int j = 0; j < n; ++j) {
+        int m0 = -j + n - 1, m1 = (n - 1 - j) + n - 1;
+        nrm[k][j] = std::sqrt(std::max(0.0, pre[m1 + 1] - pre[m0]));
+      }
+    }
+  }
+
+  // y_s = T_k x_s for the columns s of X (n x p column-major); Y likewise.
+  void apply_one(int k, const double* X, double* Y, int p) const {
+    std::vector<cplx> buf(N);
+    for (int s = 0; s < p; s += 2) {
+      std::fill(buf.begin(), buf.end(), cplx(0, 0));
+      const bool two = s + 1 < p;
+      for (int i = 0; i < n; ++i)
+        buf[i] = cplx(X[(size_t)s * n + i], two ? X[(size_t)(s + 1) * n + i] : 0.0);
+      fft.forward(buf.data());
+      for (int m = 0; m < N; ++m) buf[m] *= FG[k][m];
+      fft.inverse(buf.data());
+      const double inv = 1.0 / N;
+      for (int i = 0; i < n; ++i) {
+        Y[(size_t)s * n + i] = buf[i + n - 1].real() * inv;
+        if (two) Y[(size_t)(s + 1) * n + i] = buf[i + n - 1].imag() * inv;
+      }
+    }
+  }
+};
+
+// Thin orthonormal basis of the columns of Y (n x p) in place.
+void orthonormalise(std::vector<double>& Y, int n, int p) {
+  std::vector<double> tau;
+  std::vector<double> A = Y;
+  la::householder_qr(A.data(), n, p, tau);
+  la::form_q(A.data(), n, p, tau, Y.data());
+}
+
+// Mode-l RHOSVD basis.  c[k][j] = sum_{m at j} D_{mk}^2 with D_{mk} = |z_m a_k| times the
+// windowed norms of the other two modes' columns (the Khatri-Rao column norms of the
+// unfolding T_(l) = A_l diag(z a) (A_l'' kr A_l')^T).
+struct ModeBasis {
+  std::vector<double> U;      // n x r column-major
+  std::vector<double> sigma;  // singular values of the weighted side matrix (p of them)
+  int r = 0;
+  double tail = 0;            // relative discarded energy sqrt(sum_{i>=r} s^2 / sum s^2)
+};
+
+ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& cells,
+                     const std::vector<double>& z, const std::vector<double>& a_long,
+                     int rank_R, double eps, int tucker_cap, uint64_t seed) {
+  const int n = ops.n, RL = ops.RL;
+  const int64_t M = (int64_t)z.size();
+  const int l1 = (mode + 1) % 3, l2 = (mode + 2) % 3;
+  std::vector<std::vector<double>> c(RL, std::vector<double>(n, 0.0));
+  std::vector<char> occ(n, 0);
+  for (int64_t m = 0; m < M; ++m) {
+    const int j = cells[3 * m + mode];
+    occ[j] = 1;
+    for (int k = 0; k < RL; ++k) {
+      double d = z[m] * a_long[k] * ops.nrm[k][cells[3 * m + l1]] * ops.nrm[k][cells[3 * m + l2]];
+      c[k][j] += d * d;
+    }
+  }
+  std::vector<int> occj;
+  for (int j = 0; j < n; ++j)
+    if (occ[j]) occj.push_back(j);
+
+  const int pmax = std::min(n, 512);
+  int p = (rank_R > 0) ? std::min(pmax, std::max(2 * rank_R + 16, 48)) : std::min(pmax, 64);
+  ModeBasis out;
+  for (;;) {
+    // range finder: Y = sum_k T_k (sqrt(c_k) .* Xi_k).  Per-k results are summed in k order
+    // so the setup is bitwise independent of the thread count.
+    std::vector<double> Y((size_t)n * p, 0.0);
+    std::vector<std::vector<double>> Yk(RL);
+#pragma omp parallel
+    {
+      std::vector<double> X((size_t)n * p);
+#pragma omp for schedule(dynamic)
+      for (int k = 0; k < RL; ++k) {
+        std::fill(X.begin(), X.end(), 0.0);
+        for (int s = 0; s < p; ++s)
+          for (int j : occj)
+            X[(size_t)s * n + j] = std::sqrt(c[k][j]) *
+                la::normal(seed + 0x51ED27ull * (mode + 1), ((uint64_t)k * n + j) * 4096u + s);
+        Yk[k].assign((size_t)n * p, 0.0);
+        ops.apply_one(k, X.data(), Yk[k].data(), p);
+      }
+    }
+    for (int k = 0; k < RL; ++k) {
+      for (size_t i = 0; i < Y.size(); ++i) Y[i] += Yk[k][i];
+      std::vector<double>().swap(Yk[k]);
+    }
+    orthonormalise(Y, n, p);
+    // one power iteration: Y = sum_k T_k (c_k .* (T_k Q))
+    {
+      std::vector<double> Y2((size_t)n * p, 0.0);
+#pragma omp parallel
+      {
+        std::vector<double> Z((size_t)n * p);
+#pragma omp for schedule(dynamic)
+        for (int k = 0; k < RL; ++k) {
+          ops.apply_one(k, Y.data(), Z.data(), p);
+          for (int s = 0; s < p; ++s)
+            for (int j = 0; j < n; ++j) Z[(size_t)s * n + j] *= c[k][j];
+          Yk[k].assign((size_t)n * p, 0.0);
+          ops.apply_one(k, Z.data(), Yk[k].data(), p);
+        }
+      }
+      for (int k = 0; k < RL; ++k) {
+        for (size_t i = 0; i < Y2.size(); ++i) Y2[i] += Yk[k][i];
+        std::vector<double>().swap(Yk[k]);
+      }
+      Y.swap(Y2);
+      orthonormalise(Y, n, p);
+    }
+    // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :]; streaming QR.
+    std::vector<double> Rt((size_t)p * p, 0.0);
+    bool have_R = false;
+    const int nocc = (int)occj.size();
+    std::vector<std::vector<double>> Zk(RL);   // (T_k Q) at the occupied rows, nocc x p
+#pragma omp parallel
+    {
+      std::vector<double> Z((size_t)n * p);
+#pragma omp for schedule(dynamic)
+      for (int k = 0; k < RL; ++k) {
+        ops.apply_one(k, Y.data(), Z.data(), p);
+        Zk[k].assign((size_t)nocc * p, 0.0);
+        for (int jj = 0; jj < nocc; ++jj)
+          for (int s = 0; s < p; ++s) Zk[k][(size_t)jj * p + s] = Z[(size_t)s * n + occj[jj]];
+      }
+    }
+    const int blk_rows = std::max(4 * p, 2048);
+    std::vector<double> B;
+    int rows = 0;
+    auto flush = [&]() {
+      if (rows == 0) return;
+      const int m = std::max(rows + (have_R ? p : 0), p);   // zero rows pad a short block
+      std::vector<double> A((size_t)m * p, 0.0);
+      for (int s = 0; s < p; ++s) {
+        int off = 0;
+        if (have_R)
+          for (int i = 0; i < p; ++i) A[(size_t)s * m + i] = Rt[(size_t)s * p + i];
+        off = have_R ? p : 0;
+        for (int i = 0; i < rows; ++i) A[(size_t)s * m + off + i] = B[(size_t)i * p + s];
+      }
+      std::vector<double> tau;
+      la::householder_qr(A.data(), m, p, tau);
+      std::fill(Rt.begin(), Rt.end(), 0.0);
+      for (int s = 0; s < p; ++s)
+        for (int i = 0; i <= std::min(s, m - 1); ++i) Rt[(size_t)s * p + i] = A[(size_t)s * m + i];
+      have_R = true;
+      rows = 0;
+      B.clear();
+    };
+    for (int k = 0; k < RL; ++k) {
+      for (int jj = 0; jj < nocc; ++jj) {
+        const int j = occj[jj];
+        const double w = std::sqrt(c[k][j]);
+        for (int s = 0; s < p; ++s) B.push_back(w * Zk[k][(size_t)jj * p + s]);
+        if (++rows >= blk_rows) flush();
+      }
+    }
+    flush();
+    std::vector<double> sv(p), V((size_t)p * p);
+    la::jacobi_svd(Rt.data(), p, p, sv.data(), V.data(), nullptr);
+    double tot = 0;
+    for (double v : sv) tot += v * v;
+    // rank for the tolerance
+    int r_tol = p;
+    {
+      double tail = 0;
+      for (int i = p - 1; i >= 0; --i) {
+        if (std::sqrt(tail + sv[i] * sv[i]) > eps * std::sqrt(tot)) {
+          r_tol = i + 1;
+          break;
+        }
+        tail += sv[i] * sv[i];
+        r_tol = i;
+      }
+      r_tol = std::max(r_tol, 1);
+    }
+    const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax || p >= n;
+    if (!resolved && r_tol >= p - 4) {
+      p = std::min(pmax, 2 * p);
+      continue;
+    }
+    int r;
+    if (rank_R > 0) r = std::max(rank_R, std::min(r_tol, rank_R + 8));
+    else r = r_tol;
+    if (tucker_cap > 0) r = std::min(r, tucker_cap);
+    r = std::min(r, std::min(p, n));
+    double tail = 0;
+    for (int i = r; i < p; ++i) tail += sv[i] * sv[i];
+    out.r = r;
+    out.tail = tot > 0 ? std::sqrt(tail / tot) : 0.0;
+    out.sigma = sv;
+    out.U.assign((size_t)n * r, 0.0);
+    for (int a = 0; a < r; ++a)
+      for (int s = 0; s < p; ++s) {
+        const double v = V[(size_t)a * p + s];
+        if (v == 0.0) continue;
+        for (int i = 0; i < n; ++i) out.U[(size_t)a * n + i] += Y[(size_t)s * n + i] * v;
+      }
+    return out;
+  }
+}
+
+// dense CP reconstruction error ||G - [[A,B,C]]|| (G r0 x r1 x r2 row-major, factors
+// column-major r_l x R)
+double cp_error(const std::vector<double>& G, int r0, int r1, int r2, const std::vector<double>& A,
+                const std::vector<double>& B, const std::vector<double>& C, int R) {
+  double err = 0;
+  for (int a = 0; a < r0; ++a)
+    for (int b = 0; b < r1; ++b)
+      for (int c = 0; c < r2; ++c) {
+        double v = 0;
+        for (int q = 0; q < R; ++q) v += A[(size_t)q * r0 + a] * B[(size_t)q * r1 + b] * C[(size_t)q * r2 + c];
+        double d = G[((size_t)a * r1 + b) * r2 + c] - v;
+        err += d * d;
+      }
+  return std::sqrt(err);
+}
+
+// X = Mt * pinv(V) for symmetric PSD V (R x R); Mt is r x R column-major.
+void solve_normal(std::vector<double>& X, const std::vector<double>& Mt, std::vector<double> V,
+                  int r, int R) {
+  std::vector<double> w(R), E((size_t)R * R);
+  la::sym_eig(V.data(), R, w.data(), E.data());
+  double wmax = 0;
+  for (double v : w) wmax = std::max(wmax, std::fabs(v));
+  std::vector<double> Pinv((size_t)R * R, 0.0);
+  for (int e = 0; e < R; ++e) {
+    if (!(w[e] > 1e-13 * wmax)) continue;
+    for (int i = 0; i < R; ++i)
+      for (int j = 0; j < R; ++j)
+        Pinv[(size_t)j * R + i] += E[(size_t)e * R + i] * E[(size_t)e * R + j] / w[e];
+  }
+  X.assign((size_t)r * R, 0.0);
+  for (int q = 0; q < R; ++q)
+    for (int j = 0; j < R; ++j) {
+      const double pij = Pinv[(size_t)q * R + j];
+      if (pij == 0.0) continue;
+      for (int i = 0; i < r; ++i) X[(size_t)q * r + i] += Mt[(size_t)j * r + i] * pij;
+    }
+}
+
+void gram(const std::vector<double>& A, int r, int R, std::vector<double>& out) {
+  out.assign((size_t)R * R, 0.0);
+  for (int p = 0; p < R; ++p)
+    for (int q = 0; q < R; ++q) {
+      double s = 0;
+      for (int i = 0; i < r; ++i) s += A[(size_t)p * r + i] * A[(size_t)q * r + i];
+      out[(size_t)q * R + p] = s;
+    }
+}
+
+void cp_als(const std::vector<double>& G, int r0, int r1, int r2, int R, int sweeps,
+            std::vector<double>& A, std::vector<double>& B, std::vector<double>& C) {
+  double gn = 0;
+  for (double v : G) gn += v * v;
+  gn = std::sqrt(gn);
+  double prev = cp_error(G, r0, r1, r2, A, B, C, R);
+  std::vector<double> Mt, V, V2;
+  for (int it = 0; it < sweeps; ++it) {
+    // A <- G_(0) (C kr B) ((B^T B) * (C^T C))^+
+    Mt.assign((size_t)r0 * R, 0.0);
+    for (int q = 0; q < R; ++q)
+      for (int a = 0; a < r0; ++a) {
+        double s = 0;
+        for (int b = 0; b < r1; ++b) {
+          const double bq = B[(size_t)q * r1 + b];
+          const double* g = &G[((size_t)a * r1 + b) * r2];
+          double t = 0;
+          for (int c = 0; c < r2; ++c) t += g[c] * C[(size_t)q * r2 + c];
+          s += bq * t;
+        }
+        Mt[(size_t)q * r0 + a] = s;
+      }
+    gram(B, r1, R, V);
+    gram(C, r2, R, V2);
+    for (size_t i = 0; i < V.size(); ++i) V[i] *= V2[i];
+    solve_normal(A, Mt, V, r0, R);
+    // B
+    Mt.assign((size_t)r1 * R, 0.0);
+    for (int q = 0; q < R; ++q)
+      for (int b = 0; b < r1; ++b) {
+        double s = 0;
+        for (int a = 0; a < r0; ++a) {
+          const double aq = A[(size_t)q * r0 + a];
+          const double* g = &G[((size_t)a * r1 + b) * r2];
+          double t = 0;
+          for (int c = 0; c < r2; ++c) t += g[c] * C[(size_t)q * r2 + c];
+          s += aq * t;
+        }
+        Mt[(size_t)q * r1 + b] = s;
+      }
+    gram(A, r0, R, V);
+    gram(C, r2, R, V2);
+    for (size_t i = 0; i < V.size(); ++i) V[i] *= V2[i];
+    solve_normal(B, Mt, V, r1, R);
+    // C
+    Mt.assign((size_t)r2 * R, 0.0);
+    for (int q = 0; q < R; ++q) {
+      std::vector<double> acc(r2, 0.0);
+      for (int a = 0; a < r0; ++a)
+        for (int b = 0; b < r1; ++b) {
+          const double w = A[(size_t)q * r0 + a] * B[(size_t)q * r1 + b];
+          if (w == 0.0) continue;
+          const double* g = &G[((size_t)a * r1 + b) * r2];
+          for (int c = 0; c < r2; ++c) acc[c] += w * g[c];
+        }
+      for (int c = 0; c < r2; ++c) Mt[(size_t)q * r2 + c] = acc[c];
+    }
+    gram(A, r0, R, V);
+    gram(B, r1, R, V2);
+    for (size_t i = 0; i < V.size(); ++i) V[i] *= V2[i];
+    solve_normal(C, Mt, V, r2, R);
+    // normalise B, C columns into A
+    for (int q = 0; q < R; ++q) {
+      double nb = 0, nc = 0;
+      for (int i = 0; i < r1; ++i) nb += B[(size_t)q * r1 + i] * B[(size_t)q * r1 + i];
+      for (int i = 0; i < r2; ++i) nc += C[(size_t)q * r2 + i] * C[(size_t)q * r2 + i];
+      nb = std::sqrt(nb);
+      nc = std::sqrt(nc);
+      if (nb > 0) for (int i = 0; i < r1; ++i) B[(size_t)q * r1 + i] /= nb;
+      if (nc > 0) for (int i = 0; i < r2; ++i) C[(size_t)q * r2 + i] /= nc;
+      for (int i = 0; i < r0; ++i) A[(size_t)q * r0 + i] *= nb * nc;
+    }
+    if ((it & 7) == 7 || it == sweeps - 1) {
+      double e = cp_error(G, r0, r1, r2, A, B, C, R);
+      if (std::fabs(prev - e) <= 1e-12 * gn) break;
+      prev = e;
+    }
+  }
+}
+
+}  // namespace
+
+void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
+                         const std::vector<double>& z, const std::vector<double>& t_long,
+                         const std::vector<double>& a_long, int rank_R, double eps,
+                         int tucker_cap, int als_sweeps, uint64_t seed,
+                         std::vector<double> F[3], int* R_out, SetupReport* rep) {
+  ConvOps ops(n, h, t_long);
+  const int RL = ops.RL;
+  const int64_t M = (int64_t)z.size();
+  ModeBasis mb[3];
+  for (int l = 0; l < 3; ++l)
+    mb[l] = mode_basis(ops, l, cells, z, a_long, rank_R, eps, tucker_cap, seed);
+  const int r0 = mb[0].r, r1 = mb[1].r, r2 = mb[2].r;
+  for (int l = 0; l < 3; ++l) rep->tucker_r[l] = mb[l].r;
+  rep->tucker_err = std::sqrt(mb[0].tail * mb[0].tail + mb[1].tail * mb[1].tail +
+                              mb[2].tail * mb[2].tail);
+
+  // S6: core G = sum_k sum_m z_m a_k (U_0^T g_k[.-c_m0]) o (U_1^T ...) o (U_2^T ...)
+  std::vector<double> G((size_t)r0 * r1 * r2, 0.0);
+  for (int k = 0; k < RL; ++k) {
+    std::vector<double> H[3];   // row-major n x r_l
+    for (int l = 0; l < 3; ++l) {
+      const int r = mb[l].r;
+      std::vector<double> tmp((size_t)n * r);
+      ops.apply_one(k, mb[l].U.data(), tmp.data(), r);
+      H[l].assign((size_t)n * r, 0.0);
+      for (int a = 0; a < r; ++a)
+        for (int i = 0; i < n; ++i) H[l][(size_t)i * r + a] = tmp[(size_t)a * n + i];
+    }
+#pragma omp parallel for schedule(dynamic)
+    for (int a = 0; a < r0; ++a) {
+      std::vector<double> row((size_t)r1 * r2, 0.0);
+      for (int64_t m = 0; m < M; ++m) {
+        const double w = z[m] * a_long[k] * H[0][(size_t)cells[3 * m] * r0 + a];
+        if (w == 0.0) continue;
+        const double* h1 = &H[1][(size_t)cells[3 * m + 1] * r1];
+        const double* h2 = &H[2][(size_t)cells[3 * m + 2] * r2];
+        for (int b = 0; b < r1; ++b) {
+          const double wb = w * h1[b];
+          double* dst = &row[(size_t)b * r2];
+          for (int c = 0; c < r2; ++c) dst[c] += wb * h2[c];
+        }
+      }
+      double* g = &G[(size_t)a * r1 * r2];
+      for (size_t i = 0; i < row.size(); ++i) g[i] += row[i];
+    }
+  }
+  double gnorm = 0;
+  for (double v : G) gnorm += v * v;
+  gnorm = std::sqrt(gnorm);
+
+  // S7: slice SVDs G[a,:,:] = sum sigma u v^T -> exact canonical expansion
+  struct Trip { int a; double s; std::vector<double> u, v; };
+  std::vector<Trip> trips;
+  const bool tr = r1 < r2;              // Jacobi SVD wants rows >= cols
+  const int mr = tr ? r2 : r1, nc = tr ? r1 : r2;
+  for (int a = 0; a < r0; ++a) {
+    std::vector<double> S((size_t)mr * nc), V((size_t)nc * nc), U((size_t)mr * nc), sv(nc);
+    for (int b = 0; b < r1; ++b)
+      for (int c = 0; c < r2; ++c) {
+        const double v = G[((size_t)a * r1 + b) * r2 + c];
+        if (!tr) S[(size_t)c * mr + b] = v; else S[(size_t)b * mr + c] = v;
+      }
+    la::jacobi_svd(S.data(), mr, nc, sv.data(), V.data(), U.data());
+    for (int q = 0; q < nc; ++q) {
+      if (!(sv[q] > 1e-15 * gnorm)) continue;
+      Trip t;
+      t.a = a;
+      t.s = sv[q];
+      std::vector<double> uu(U.begin() + (size_t)q * mr, U.begin() + (size_t)(q + 1) * mr);
+      std::vector<double> vv(V.begin() + (size_t)q * nc, V.begin() + (size_t)(q + 1) * nc);
+      if (!tr) { t.u = uu; t.v = vv; } else { t.u = vv; t.v = uu; }
+      trips.push_back(std::move(t));
+    }
+  }
+  std::stable_sort(trips.begin(), trips.end(), [](const Trip& x, const Trip& y) { return x.s > y.s; });
+  rep->R_exact = (int)trips.size();
+  int R;
+  size_t keep = trips.size();
+  if (rank_R <= 0) {
+    double tot = 0, drop = 0;
+    for (auto& t : trips) tot += t.s * t.s;
+    while (keep > 1 && drop + trips[keep - 1].s * trips[keep - 1].s <= eps * eps * tot) {
+      drop += trips[keep - 1].s * trips[keep - 1].s;
+      --keep;
+    }
+    R = (int)keep;
+  } else {
+    R = rank_R;
+    keep = std::min(trips.size(), (size_t)rank_R);
+  }
+  std::vector<double> A((size_t)r0 * R, 0.0), B((size_t)r1 * R, 0.0), C((size_t)r2 * R, 0.0);
+  for (size_t q = 0; q < keep; ++q) {
+    A[q * r0 + trips[q].a] = trips[q].s;
+    for (int i = 0; i < r1; ++i) B[q * r1 + i] = trips[q].u[i];
+    for (int i = 0; i < r2; ++i) C[q * r2 + i] = trips[q].v[i];
+  }
+  if (rank_R > 0 && (int)trips.size() > rank_R)
+    cp_als(G, r0, r1, r2, R, als_sweeps > 0 ? als_sweeps : 300, A, B, C);
+  rep->cp_core_err = gnorm > 0 ? cp_error(G, r0, r1, r2, A, B, C, R) / gnorm : 0.0;
+
+  // F_l = U_l X_l  (n x R row-major)
+  const std::vector<double>* X[3] = {&A, &B, &C};
+  const int rr[3] = {r0, r1, r2};
+  for (int l = 0; l < 3; ++l) {
+    F[l].assign((size_t)n * R, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i)
+      for (int q = 0; q < R; ++q) {
+        double s = 0;
+        for (int a = 0; a < rr[l]; ++a) s += mb[l].U[(size_t)a * n + i] * (*X[l])[(size_t)q * rr[l] + a];
+        F[l][(size_t)i * R + q] = s;
+      }
+  }
+  *R_out = R;
+}
+
+// ---- S9: cell lists --------------------------------------------------------------------------
+void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
+                      const std::vector<int32_t>& cells, double rho, CoarseGrid* cg) {
+  const int64_t M = (int64_t)cells.size() / 3;
+  const double target = rho / 2.0;
+  int shift = 0;
+  while (shift < 20 && h * double(1 << (shift + 1)) <= target * 1.4142) ++shift;
+  cg->shift = shift;
+  const int pf = (int)std::ceil((rho + 2 * h) / h) + 1;
+  for (int a = 0; a < 3; ++a) {
+    int mn = n, mx = -1;
+    for (int64_t m = 0; m < M; ++m) {
+      mn = std::min(mn, (int)cells[3 * m + a]);
+      mx = std::max(mx, (int)cells[3 * m + a]);
+    }
+    if (M == 0) { mn = 0; mx = 0; }
+    const int lo = std::max(0, mn - pf) >> shift;
+    const int hi = std::min(n - 1, mx + pf) >> shift;
+    cg->lo[a] = lo;
+    cg->dim[a] = hi - lo + 1;
+  }
+  const int64_t ncell = (int64_t)cg->dim[0] * cg->dim[1] * cg->dim[2];
+  std::vector<int32_t> cnt(ncell + 1, 0);
+  const double cw = h * double(1 << shift);
+  const double rr = rho + 2 * h, rr2 = rr * rr;
+  auto visit = [&](int64_t m, auto&& fn) {
+    const double* x = &xyz[3 * m];
+    int c0[3], c1[3];
+    for (int a = 0; a < 3; ++a) {
+      int f0 = (int)std::floor((x[a] - rr + b) / h) - 1, f1 = (int)std::floor((x[a] + rr + b) / h) + 1;
+      f0 = std::max(f0, 0);
+      f1 = std::min(f1, n - 1);
+      c0[a] = std::max(f0 >> shift, cg->lo[a]);
+      c1[a] = std::min(f1 >> shift, cg->lo[a] + cg->dim[a] - 1);
+    }
+    for (int i = c0[0]; i <= c1[0]; ++i) {
+      const double lo0 = -b + i * cw, hi0 = lo0 + cw;
+      const double d0 = std::max({0.0, lo0 - x[0], x[0] - hi0});
+      for (int j = c0[1]; j <= c1[1]; ++j) {
+        const double lo1 = -b + j * cw, hi1 = lo1 + cw;
+        const double d1 = std::max({0.0, lo1 - x[1], x[1] - hi1});
+        if (d0 * d0 + d1 * d1 > rr2) continue;
+        for (int k = c0[2]; k <= c1[2]; ++k) {
+          const double lo2 = -b + k * cw, hi2 = lo2 + cw;
+          const double d2 = std::max({0.0, lo2 - x[2], x[2] - hi2});
+          if (d0 * d0 + d1 * d1 + d2 * d2 > rr2) continue;
+          const int64_t cell = ((int64_t)(i - cg->lo[0]) * cg->dim[1] + (j - cg->lo[1])) * cg->dim[2] +
+                               (k - cg->lo[2]);
+          fn(cell);
+        }
+      }
+    }
+  };
+  for (int64_t m = 0; m < M; ++m) visit(m, [&](int64_t c) { cnt[c + 1]++; });
+  for (int64_t c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
+  cg->off = cnt;
+  cg->idx.assign(cnt[ncell], 0);
+  std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+  for (int64_t m = 0; m < M; ++m) visit(m, [&](int64_t c) { cg->idx[pos[c]++] = (int32_t)m; });
+}
+
+// ---- sampled compression error (reported; O11(iii) re-checks it independently) ---------------
+void sample_compression_error(int n, double b, double h, const std::vector<double>& xyz,
+                              const std::vector<int32_t>& cells, const std::vector<double>& z,
+                              const std::vector<double>& t_long, const std::vector<double>& a_long,
+                              const std::vector<double> F[3], int R, double r_excl,
+                              const CoarseGrid& cg, int n_samples, uint64_t seed,
+                              SetupReport* rep) {
+  const int64_t M = (int64_t)z.size();
+  const int RL = (int)t_long.size();
+  if (M == 0 || n_samples <= 0) return;
+  std::vector<double> G((size_t)RL * n);
+  for (int k = 0; k < RL; ++k)
+    for (int d = 0; d < n; ++d) G[(size_t)k * n + d] = cell_average(t_long[k], h, d);
+  const double inv_h = double(n) / (2.0 * b);
+  auto snapc = [&](double x) {
+    double u = (x + b) * inv_h;
+    double c = std::ceil(u) - 1.0;
+    c = std::min(std::max(c, 0.0), double(n - 1));
+    return (int)c;
+  };
+  // sample exterior points: x = x_m + delta u, delta in [r_excl, 4 r_excl], no atom within r_excl
+  std::vector<int> pts;
+  uint64_t ctr = 0;
+  const double rx2 = r_excl * r_excl;
+  while ((int)pts.size() / 3 < n_samples && ctr < (uint64_t)n_samples * 400) {
+    const double u0 = la::normal(seed ^ 0xABCDEFull, ctr * 5 + 0);
+    const double u1 = la::normal(seed ^ 0xABCDEFull, ctr * 5 + 1);
+    const double u2 = la::normal(seed ^ 0xABCDEFull, ctr * 5 + 2);
+    const double uu = la::normal(seed ^ 0xABCDEFull, ctr * 5 + 3);
+    const double vv = la::normal(seed ^ 0xABCDEFull, ctr * 5 + 4);
+    ++ctr;
+    const double nu = std::sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+    if (!(nu > 0)) continue;
+    const int64_t m = (int64_t)(std::fabs(uu) * 1e6) % M;
+    const double delta = r_excl * (1.0 + 3.0 * (0.5 + 0.5 * std::erf(vv / std::sqrt(2.0))));
+    double x[3] = {xyz[3 * m] + delta * u0 / nu, xyz[3 * m + 1] + delta * u1 / nu,
+                   xyz[3 * m + 2] + delta * u2 / nu};
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) ok = ok && x[a] > -b + h && x[a] < b - h;
+    if (!ok) continue;
+    int c[3] = {snapc(x[0]), snapc(x[1]), snapc(x[2])};
+    // exclusion via the cell lists (they cover every atom within rho >= r_excl)
+    int cc[3];
+    for (int a = 0; a < 3; ++a) cc[a] = (c[a] >> cg.shift) - cg.lo[a];
+    if (cc[0] >= 0 && cc[0] < cg.dim[0] && cc[1] >= 0 && cc[1] < cg.dim[1] && cc[2] >= 0 &&
+        cc[2] < cg.dim[2]) {
+      const int64_t cell = ((int64_t)cc[0] * cg.dim[1] + cc[1]) * cg.dim[2] + cc[2];
+      for (int32_t e = cg.off[cell]; e < cg.off[cell + 1] && ok; ++e) {
+        const int32_t q = cg.idx[e];
+        double d2 = 0;
+        for (int a = 0; a < 3; ++a) d2 += (x[a] - xyz[3 * q + a]) * (x[a] - xyz[3 * q + a]);
+        if (d2 < rx2) ok = false;
+      }
+    }
+    if (!ok) continue;
+    pts.push_back(c[0]);
+    pts.push_back(c[1]);
+    pts.push_back(c[2]);
+  }
+  const int ns = (int)pts.size() / 3;
+  std::vector<double> ex(ns), cp(ns);
+#pragma omp parallel for schedule(dynamic)
+  for (int s = 0; s < ns; ++s) {
+    const int* c = &pts[3 * s];
+    double v = 0;
+    for (int64_t m = 0; m < M; ++m) {
+      const int d0 = std::abs(c[0] - cells[3 * m]), d1 = std::abs(c[1] - cells[3 * m + 1]),
+                d2 = std::abs(c[2] - cells[3 * m + 2]);
+      double acc = 0;
+      for (int k = 0; k < RL; ++k)
+        acc += a_long[k] * G[(size_t)k * n + d0] * G[(size_t)k * n + d1] * G[(size_t)k * n + d2];
+      v += z[m] * acc;
+    }
+    ex[s] = v;
+    double w = 0;
+    for (int q = 0; q < R; ++q)
+      w += F[0][(size_t)c[0] * R + q] * F[1][(size_t)c[1] * R + q] * F[2][(size_t)c[2] * R + q];
+    cp[s] = w;
+  }
+  double emax = 0, vmax = 0, e2 = 0, v2 = 0;
+  for (int s = 0; s < ns; ++s) {
+    emax = std::max(emax, std::fabs(ex[s] - cp[s]));
+    vmax = std::max(vmax, std::fabs(ex[s]));
+    e2 += (ex[s] - cp[s]) * (ex[s] - cp[s]);
+    v2 += ex[s] * ex[s];
+  }
+  rep->n_samples = ns;
+  rep->sampled_max = vmax > 0 ? emax / vmax : 0.0;
+  rep->sampled_rms = v2 > 0 ? std::sqrt(e2 / v2) : 0.0;
+}
+
+}  // namespace rs

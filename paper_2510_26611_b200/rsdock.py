@@ -1,0 +1,246 @@
+"""Thin Python binding of librsdock (include/rs_dock.h) -- argument marshalling only.
+
+Every step of the scoring path runs in the library's CUDA kernels; there is no Python or CPU
+fallback: if librsdock.so is missing or was built without a usable device, the calls raise.
+PyTorch is used only for device memory and streams (tensors' data_ptr / current stream).
+
+Same names as the C ABI: rs_params_default, rs_build_protein, rs_score_poses,
+rs_score_poses_async, rs_get_info, rs_export_tables, rs_export_setup, rs_last_error, rs_free.
+`Protein` is a small RAII wrapper over the opaque handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librsdock.so")
+
+RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
+RS_FLAG_HOST_ONLY = 1
+
+EXPORTED = ["rs_params_default", "rs_build_protein", "rs_score_poses", "rs_score_poses_async",
+            "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
+
+
+class rs_params(ctypes.Structure):
+    _fields_ = [("grid_n", ctypes.c_int32), ("rank_R", ctypes.c_int32),
+                ("eps_compress", ctypes.c_double), ("eps_quad", ctypes.c_double),
+                ("sigma_split", ctypes.c_double), ("eps_split", ctypes.c_double),
+                ("sigma_vdw", ctypes.c_double), ("dmin_cap", ctypes.c_double),
+                ("tucker_rank_max", ctypes.c_int32), ("als_sweeps", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("n_threads", ctypes.c_int32),
+                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32)]
+
+
+class rs_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("b", ctypes.c_double), ("h", ctypes.c_double),
+                ("inv_h", ctypes.c_double), ("R", ctypes.c_int32), ("R_exact", ctypes.c_int32),
+                ("tucker_r", ctypes.c_int32 * 3), ("quad_K", ctypes.c_int32),
+                ("quad_s", ctypes.c_double), ("quad_Ls", ctypes.c_double),
+                ("quad_err", ctypes.c_double), ("R_long_ref", ctypes.c_int32),
+                ("R_short", ctypes.c_int32), ("n_sigma", ctypes.c_int32),
+                ("n_atoms", ctypes.c_int64), ("tucker_err", ctypes.c_double),
+                ("cp_core_err", ctypes.c_double), ("sampled_max_err", ctypes.c_double),
+                ("sampled_rms_err", ctypes.c_double), ("n_err_samples", ctypes.c_int32),
+                ("sigma_vdw", ctypes.c_double), ("dmin_cap", ctypes.c_double),
+                ("nbr_cells", ctypes.c_int64), ("nbr_entries", ctypes.c_int64),
+                ("nbr_shift", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("setup_seconds", ctypes.c_double), ("on_device", ctypes.c_int32)]
+
+
+_lib = None
+_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+def load():
+    """Load librsdock.so (raises if absent: build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build() -- there is no "
+                           "CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    L.rs_params_default.argtypes = [ctypes.POINTER(rs_params)]
+    L.rs_build_protein.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_double,
+                                   ctypes.POINTER(rs_params)]
+    L.rs_build_protein.restype = _vp
+    L.rs_score_poses.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp]
+    L.rs_score_poses.restype = ctypes.c_int64
+    L.rs_score_poses_async.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
+                                       _vp, _vp, _vp]
+    L.rs_score_poses_async.restype = ctypes.c_int64
+    L.rs_get_info.argtypes = [_vp, ctypes.POINTER(rs_info)]
+    L.rs_get_info.restype = ctypes.c_int
+    L.rs_export_tables.argtypes = [_vp] + [_vp] * 6
+    L.rs_export_tables.restype = ctypes.c_int
+    L.rs_export_setup.argtypes = [_vp, _vp, _vp, _vp, _vp]
+    L.rs_export_setup.restype = ctypes.c_int
+    L.rs_last_error.restype = ctypes.c_char_p
+    L.rs_free.argtypes = [_vp]
+    _lib = L
+    return L
+
+
+# ---------------------------------------------------------------------------- raw C names
+
+def rs_params_default(**overrides) -> rs_params:
+    p = rs_params()
+    load().rs_params_default(ctypes.byref(p))
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    return p
+
+
+def rs_last_error() -> str:
+    return load().rs_last_error().decode()
+
+
+def _ptr(x):
+    """data pointer of a numpy array or torch tensor (contiguous fp64 expected)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def rs_build_protein(q, xyz, box_half_width, params: rs_params | None = None):
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    h = load().rs_build_protein(q.ctypes.data, xyz.ctypes.data, q.shape[0], float(box_half_width),
+                                ctypes.byref(params) if params is not None else None)
+    if not h:
+        raise RuntimeError("rs_build_protein: " + rs_last_error())
+    return h
+
+
+def rs_score_poses(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out) -> int:
+    r = load().rs_score_poses(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
+                              _ptr(energies_out), _ptr(mindist_out))
+    if r < 0:
+        raise RuntimeError(f"rs_score_poses ({r}): " + rs_last_error())
+    return int(r)
+
+
+def rs_score_poses_async(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out,
+                         invalid_count=None, stream=None) -> int:
+    r = load().rs_score_poses_async(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
+                                    _ptr(energies_out), _ptr(mindist_out), _ptr(invalid_count),
+                                    stream)
+    if r < 0:
+        raise RuntimeError(f"rs_score_poses_async ({r}): " + rs_last_error())
+    return int(r)
+
+
+def rs_get_info(h) -> dict:
+    info = rs_info()
+    if load().rs_get_info(h, ctypes.byref(info)) != 0:
+        raise RuntimeError(rs_last_error())
+    out = {}
+    for name, _ in rs_info._fields_:
+        v = getattr(info, name)
+        out[name] = list(v) if name == "tucker_r" else v
+    return out
+
+
+def rs_export_tables(h) -> dict:
+    info = rs_get_info(h)
+    n, R, ns, Rs = info["n"], info["R"], info["n_sigma"], info["R_short"]
+    F = [np.empty((n, R)) for _ in range(3)]
+    S = [np.empty((2 * ns + 1, Rs)) for _ in range(3)]
+    rc = load().rs_export_tables(h, *[a.ctypes.data for a in F], *[a.ctypes.data for a in S])
+    if rc != 0:
+        raise RuntimeError(rs_last_error())
+    return dict(n=n, b=info["b"], R=R, n_sigma=ns, Rs=Rs, F1=F[0], F2=F[1], F3=F[2], S1=S[0],
+                S2=S[1], S3=S[2])
+
+
+def rs_export_setup(h) -> dict:
+    info = rs_get_info(h)
+    K1 = info["quad_K"] + 1
+    t, a = np.empty(K1), np.empty(K1)
+    is_long = np.empty(K1, dtype=np.int32)
+    cells = np.empty((info["n_atoms"], 3), dtype=np.int32)
+    rc = load().rs_export_setup(h, t.ctypes.data, a.ctypes.data, is_long.ctypes.data,
+                                cells.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(rs_last_error())
+    return dict(t=t, a=a, is_long=is_long.astype(bool), cells=cells, s=info["quad_s"],
+                K=info["quad_K"], Ls=info["quad_Ls"])
+
+
+def rs_free(h) -> None:
+    if h:
+        load().rs_free(h)
+
+
+# ---------------------------------------------------------------------------- wrapper
+
+class Protein:
+    """Owns one rs_handle (the protein's RS tensor, resident on the device)."""
+
+    def __init__(self, q, xyz, box_half_width, **params):
+        self._h = None
+        self.params = rs_params_default(**params)
+        self._h = rs_build_protein(q, xyz, box_half_width, self.params)
+        self.info = rs_get_info(self._h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            rs_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export_tables(self) -> dict:
+        return rs_export_tables(self._h)
+
+    def export_setup(self) -> dict:
+        return rs_export_setup(self._h)
+
+    def score(self, q_lig, xyz_lig, poses, energies_out=None, mindist_out=None):
+        """Synchronous scoring.  Inputs may be numpy arrays (host) or torch tensors (host or
+        device).  Returns (energies, mindist, n_invalid); outputs live where the poses live
+        unless given."""
+        P = int(poses.shape[0])
+        L = int(q_lig.shape[0])
+        if isinstance(poses, np.ndarray):
+            poses = np.ascontiguousarray(poses, dtype=np.float64)
+            q_lig = np.ascontiguousarray(q_lig, dtype=np.float64)
+            xyz_lig = np.ascontiguousarray(xyz_lig, dtype=np.float64)
+            if energies_out is None:
+                energies_out = np.empty(P)
+            if mindist_out is None:
+                mindist_out = np.empty(P)
+        else:
+            import torch
+            if energies_out is None:
+                energies_out = torch.empty(P, dtype=torch.float64, device=poses.device)
+            if mindist_out is None:
+                mindist_out = torch.empty(P, dtype=torch.float64, device=poses.device)
+        inv = rs_score_poses(self._h, q_lig, xyz_lig, L, poses, P, energies_out, mindist_out)
+        return energies_out, mindist_out, inv
+
+    def score_async(self, q_lig, xyz_lig, poses, energies_out, mindist_out, invalid_count=None,
+                    stream=None):
+        """Enqueue scoring of device tensors on `stream` (default: torch's current stream)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(poses.device)
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        return rs_score_poses_async(self._h, q_lig, xyz_lig, int(q_lig.shape[0]), poses,
+                                    int(poses.shape[0]), energies_out, mindist_out, invalid_count,
+                                    s)

@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bar (north_star / SURVEY.md §8(c) M8): per-pose energy within 1e-12 relative (expected
+bitwise), min distance bitwise, identical NaN (invalid-pose) pattern and count.  Small cases
+compare every pose; full-size configs run the whole batch in the launch configuration
+bench.py times and compare a seeded sample of poses the oracle scores one by one."""
+import math
+
+import numpy as np
+import pytest
+
+from synth import configs as syn
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_library()
+    from paper_2510_26611_b200 import rsdock
+    from oracle import rs_oracle
+    rs_oracle.lib()
+    return torch, rsdock, rs_oracle
+
+
+def build(rsdock, w, **kw):
+    prm = dict(w.params())
+    prm.update(kw)
+    return rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **prm)
+
+
+def gpu_score(torch, rsdock, prot, w, poses, async_api=False):
+    dev = torch.device("cuda:0")
+    q = torch.tensor(w.ligand_q, device=dev)
+    y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
+    ps = torch.tensor(poses, device=dev).contiguous()
+    P = ps.shape[0]
+    E = torch.empty(P, dtype=torch.float64, device=dev)
+    D = torch.empty(P, dtype=torch.float64, device=dev)
+    if async_api:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        prot.score_async(q, y, ps, E, D, cnt)
+        torch.cuda.synchronize()
+        inv = int(cnt.item())
+    else:
+        inv = rsdock.rs_score_poses(prot.handle, q, y, w.L, ps, P, E, D)
+    return E.cpu().numpy(), D.cpu().numpy(), inv
+
+
+def compare(Eg, Dg, Eo, Do, invg=None, invo=None):
+    assert np.array_equal(np.isnan(Eg), np.isnan(Eo))
+    assert np.array_equal(np.isnan(Dg), np.isnan(Do))
+    ok = ~np.isnan(Eo)
+    rel = np.abs(Eg[ok] - Eo[ok]) / np.maximum(np.abs(Eo[ok]), 1e-300)
+    assert np.all((rel <= REL) | (Eg[ok] == Eo[ok])), f"max rel {rel.max():.3e}"
+    assert np.array_equal(Dg[ok], Do[ok])
+    if invg is not None:
+        assert invg == invo
+    return float(np.mean(Eg[ok] == Eo[ok])) if ok.any() else 1.0
+
+
+def oracle_score(rs_oracle, prot, w, poses, idx=None):
+    tb = prot.export_tables()
+    ps = poses if idx is None else poses[idx]
+    return rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, ps,
+                                 w.dmin_cap)
+
+
+# ----------------------------------------------------------------------------- widths / tiles
+
+@pytest.mark.parametrize("R", [4, 8, 12, 16, 24, 32, 10])
+def test_small_random_all_widths(env, R):
+    """Every compiled width (and a runtime width, 10), several tiles and a ragged tail
+    (P = 333 = 5 tiles of 64 + 13)."""
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=R, M=40, L=9, n=64, b=8.0, R=R, P=333)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_c1_all_poses(env):
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1()
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
+    frac = compare(Eg, Dg, Eo, Do, inv, invo)
+    assert frac > 0.99
+    assert np.mean(Dg < w.sigma_vdw) > 0.5           # C1 is the clash-heavy config
+
+
+def test_c1_host_pointers_and_async_agree(env):
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1()
+    prot = build(rsdock, w)
+    Ed, Dd, invd = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eh, Dh, invh = prot.score(w.ligand_q, w.ligand_xyz, w.poses)     # numpy: host path
+    Ea, Da, inva = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
+    assert np.array_equal(Ed, Eh) and np.array_equal(Dd, Dh) and invd == invh
+    assert np.array_equal(Ed, Ea) and np.array_equal(Dd, Da) and invd == inva
+
+
+# ----------------------------------------------------------------------------- edge cases
+
+def test_edge_cases(env):
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=11, M=40, L=7, n=64, b=8.0, R=8, P=64)
+    prot = build(rsdock, w)
+    poses = w.poses.copy()
+    poses[3, :4] = 0.0                      # zero quaternion
+    poses[5, 4] = np.nan                    # NaN translation
+    poses[7, 5] = 7.9                       # leaves the box
+    poses[9, :4] = [2.0, 0.0, 0.0, 0.0]     # non-unit quaternion == identity
+    poses[10, 4:] = [-7.0, 7.0, -7.0]       # far corner, valid or not by the rule
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    assert np.isnan(Eg[[3, 5, 7]]).all() and inv >= 3
+    # P = 0
+    E0, D0, inv0 = gpu_score(torch, rsdock, prot, w, poses[:0])
+    assert E0.size == 0 and inv0 == 0
+    # L = 0: E = 0, d = +inf
+    wl = syn.Workload(w.name, w.protein_xyz, w.protein_q, np.zeros((0, 3)), np.zeros(0), poses,
+                      w.grid_n, w.box_half_width, w.rank_R, w.sigma_split, w.sigma_vdw, w.dmin_cap)
+    E1, D1, inv1 = gpu_score(torch, rsdock, prot, wl, w.poses)
+    assert np.all(E1 == 0.0) and np.all(np.isinf(D1)) and inv1 == 0
+    # L = 1
+    w1 = syn.Workload(w.name, w.protein_xyz, w.protein_q, np.zeros((1, 3)), np.array([0.7]),
+                      w.poses, w.grid_n, w.box_half_width, w.rank_R, w.sigma_split, w.sigma_vdw,
+                      w.dmin_cap)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w1, w.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w1, w.poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_large_ligand_and_scattered_tiles(env):
+    """L > 256 (ligand read from global memory) and tiles whose poses are far apart (the
+    shared-memory window does not fit -> per-tile halving and the L2 fallback)."""
+    torch, rsdock, rs_oracle = env
+    rng = np.random.default_rng(4)
+    w = syn.random_small(seed=12, M=60, L=5, n=256, b=16.0, R=16, P=300, trans=10.0)
+    Y = syn.packed_ball(rng, 300, 4.0, 0.6)
+    Y -= Y.mean(0)
+    wl = syn.Workload("bigL", w.protein_xyz, w.protein_q, Y, rng.uniform(-1, 1, 300), w.poses,
+                      w.grid_n, w.box_half_width, 16, w.sigma_split, w.sigma_vdw, w.dmin_cap)
+    prot = build(rsdock, wl)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, wl, wl.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, wl, wl.poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    # alternate two distant translations pose by pose
+    poses = w.poses.copy()
+    poses[0::2, 4:] = [-9.0, -9.0, -9.0]
+    poses[1::2, 4:] = [9.0, 9.0, 9.0]
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_order_invariance(env):
+    """O9 freedoms: pose order and ligand atom order do not change a pose's result."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1(n_poses=400)
+    prot = build(rsdock, w)
+    E, D, _ = gpu_score(torch, rsdock, prot, w, w.poses)
+    perm = np.random.default_rng(0).permutation(w.P)
+    E2, D2, _ = gpu_score(torch, rsdock, prot, w, w.poses[perm])
+    assert np.array_equal(E2, E[perm]) and np.array_equal(D2, D[perm])
+    ap = np.random.default_rng(1).permutation(w.L)
+    wa = syn.Workload(w.name, w.protein_xyz, w.protein_q, w.ligand_xyz[ap], w.ligand_q[ap],
+                      w.poses, w.grid_n, w.box_half_width, w.rank_R, w.sigma_split, w.sigma_vdw,
+                      w.dmin_cap)
+    E3, D3, _ = gpu_score(torch, rsdock, prot, wa, w.poses)
+    assert np.array_equal(D3, D)
+    assert np.all(np.abs(E3 - E) <= 1e-14 * np.abs(E) + 1e-300)
+
+
+def test_linearity_in_ligand_charges(env):
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1(n_poses=300)
+    prot = build(rsdock, w)
+    E, D, _ = gpu_score(torch, rsdock, prot, w, w.poses)
+    w2 = syn.Workload(w.name, w.protein_xyz, w.protein_q, w.ligand_xyz, 2.0 * w.ligand_q, w.poses,
+                      w.grid_n, w.box_half_width, w.rank_R, w.sigma_split, w.sigma_vdw, w.dmin_cap)
+    E2, D2, _ = gpu_score(torch, rsdock, prot, w2, w.poses)
+    assert np.array_equal(E2, 2.0 * E) and np.array_equal(D2, D)
+
+
+# ----------------------------------------------------------------------------- physics on GPU
+
+def test_tolerance_mode_gpu_vs_coulomb(env):
+    """Tolerance-mode build (rank_R = 0, eps 1e-6, runtime-width kernel): parity with the
+    oracle, and the GPU energies of non-clashing poses against brute-force Coulomb (Eq. (13))
+    within the chain tolerance of SURVEY §8(c) (x S = sum |z z|/r)."""
+    torch, rsdock, rs_oracle = env
+    w0 = syn.config_c1()
+    rng = np.random.default_rng(5)
+    P = 60
+    u = syn.unit_vectors(rng, P)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), u * rng.uniform(14, 16, (P, 1))], 1)
+    w = w0.with_poses(poses)
+    prot = build(rsdock, w, rank_R=0, eps_compress=1e-6)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    for p in range(P):
+        R_ = rs_oracle.quat_to_rot(poses[p, :4])
+        Xp = w.ligand_xyz @ R_.T + poses[p, 4:]
+        S = rs_oracle.coulomb_scale(w.protein_xyz, w.protein_q, Xp, w.ligand_q)
+        e = rs_oracle.coulomb_binding(w.protein_xyz, w.protein_q, Xp, w.ligand_q)
+        assert abs(Eg[p] - e) <= 1e-3 * S
+
+
+# ----------------------------------------------------------------------------- full sizes
+
+@pytest.mark.parametrize("name,k", [("C2", 2000), ("C3", 400)])
+def test_full_size_sampled(env, name, k):
+    """Whole batch on the GPU in the bench launch configuration (async API, device tensors);
+    the oracle re-scores a seeded sample of poses."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
+    idx, _ = syn.subsample(w.poses, k, seed=3)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
+    compare(Eg[idx], Dg[idx], Eo, Do)
+    assert inv == int(np.isnan(Eg).sum())

@@ -1,0 +1,192 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/rs_dock.h declares,
+validates its arguments, refuses to run without a device (no CPU fallback), and its host
+setup (Algorithm TEP, built with RS_FLAG_HOST_ONLY -- no compute call goes to a GPU)
+agrees with the oracle's independent re-implementation of S1-S4 and the uncompressed
+long-range potential."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from synth import configs as syn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def rsd():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    from paper_2510_26611_b200 import rsdock
+    rsdock.load()
+    return rsdock
+
+
+def test_exports_every_declared_symbol(rsd):
+    hdr = open(os.path.join(ROOT, "include", "rs_dock.h")).read()
+    declared = set(re.findall(r"\b(rs_[a-z_]+)\s*\(", hdr))
+    declared -= {"rs_handle"}
+    assert declared == set(rsd.EXPORTED), declared
+    lib = ctypes.CDLL(rsd.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_struct_layouts_match_header(rsd):
+    # rs_params: 2 int32, 6 double, 4 int32, uint64, uint32 (+pad) -> 88 bytes
+    assert ctypes.sizeof(rsd.rs_params) == 88
+    p = rsd.rs_params_default()
+    assert p.grid_n == 256 and p.rank_R == 16 and p.sigma_vdw == 2.5 and p.flags == 0
+
+
+def _small():
+    return syn.random_small(seed=3, M=40, L=6, n=64, b=8.0, R=8)
+
+
+def test_argument_validation(rsd):
+    w = _small()
+    ok = dict(grid_n=w.grid_n, rank_R=8, sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    bad_cases = [
+        (dict(ok, grid_n=63), "even"),
+        (dict(ok, sigma_split=0.01), "sigma_split"),
+        (dict(ok, dmin_cap=0.5, sigma_vdw=1.0), "dmin_cap"),
+        (dict(ok, rank_R=-1), "rank_R"),
+    ]
+    for prm, msg in bad_cases:
+        with pytest.raises(RuntimeError, match=msg):
+            rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **prm)
+    X = w.protein_xyz.copy()
+    X[3, 0] = 9.0
+    with pytest.raises(RuntimeError, match="outside"):
+        rsd.Protein(w.protein_q, X, w.box_half_width, **ok)
+    q = w.protein_q.copy()
+    q[0] = np.nan
+    with pytest.raises(RuntimeError, match="non-finite"):
+        rsd.Protein(q, w.protein_xyz, w.box_half_width, **ok)
+
+
+@pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) != "" and
+                    __import__("torch").cuda.is_available(), reason="a GPU is present")
+def test_no_cpu_fallback(rsd):
+    w = _small()
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=64, rank_R=8,
+                    sigma_split=1.0)
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=64, rank_R=8,
+                    sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    with pytest.raises(RuntimeError, match="no device tables"):
+        p.score(w.ligand_q, w.ligand_xyz, w.poses)
+
+
+@pytest.fixture(scope="module")
+def c1_host(rsd):
+    w = syn.config_c1()
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=w.grid_n,
+                    rank_R=w.rank_R, sigma_split=w.sigma_split, eps_quad=w.eps_quad,
+                    eps_split=w.eps_split, flags=rsd.RS_FLAG_HOST_ONLY)
+    return w, p
+
+
+def test_setup_S1_S4_match_oracle(oracle, c1_host):
+    """O11 (i)-(ii): the oracle rebuilds the quadrature from the exported (s, K, L_s), the
+    split, the short-range rows and the protein cells with its own code."""
+    w, p = c1_host
+    st = p.export_setup()
+    tb = p.export_tables()
+    t, a = oracle.quadrature(st["s"], st["K"], st["Ls"])
+    assert np.allclose(t, st["t"], rtol=2e-15, atol=0) and np.allclose(a, st["a"], rtol=2e-15, atol=0)
+    h = 2 * w.box_half_width / w.grid_n
+    assert oracle.quadrature_rel_error(t, a, h / 4, st["Ls"], 4000) <= 1.05 * w.eps_quad
+    lm = oracle.split_long(t, w.sigma_split, w.eps_split)
+    assert np.array_equal(lm, st["is_long"])
+    ns = int(math.ceil(w.sigma_split / h))
+    assert tb["n_sigma"] == ns
+    S = oracle.short_tables(t, a, lm, h, ns)
+    for k in range(3):
+        ref = S[k]
+        got = tb[f"S{k + 1}"]
+        assert got.shape == ref.shape
+        # libm erfc (library) vs Cephes erfc (scipy) differ by up to ~3e-13 relative in the far tail (values ~1e-235)
+        assert np.all(np.abs(got - ref) <= 1e-12 * np.abs(ref) + 1e-300)
+    assert np.array_equal(st["cells"], oracle.snap_np(w.protein_xyz, w.box_half_width, w.grid_n))
+
+
+def _uncompressed_long(oracle, w, st, cells, pts):
+    t, a = st["t"], st["a"]
+    lm = st["is_long"]
+    h = 2 * w.box_half_width / w.grid_n
+    ks = np.nonzero(lm)[0]
+    vals = []
+    for c in pts:
+        d = (c[None, :] - cells).astype(np.float64)          # (M, 3)
+        acc = np.zeros(len(cells))
+        for k in ks:
+            g = oracle.cell_average(float(t[k]), h, d.ravel()).reshape(d.shape)
+            acc += a[k] * g[:, 0] * g[:, 1] * g[:, 2]
+        vals.append(math.fsum(w.protein_q * acc))
+    return np.array(vals)
+
+
+def _exterior_cells(oracle, w, k, seed, dmin=2.5, dmax=10.0):
+    rng = np.random.default_rng(seed)
+    pts = []
+    while len(pts) < k:
+        m = rng.integers(w.M)
+        u = syn.unit_vectors(rng, 1)[0]
+        x = w.protein_xyz[m] + rng.uniform(dmin, dmax) * u
+        if np.min(np.linalg.norm(w.protein_xyz - x, axis=1)) < dmin:
+            continue
+        if np.any(np.abs(x) >= w.box_half_width):
+            continue
+        pts.append(oracle.snap_np(x, w.box_half_width, w.grid_n))
+    return np.array(pts)
+
+
+def test_setup_F_within_reported_error(oracle, c1_host):
+    """O11 (iii): the CP value of the exported F at exterior cells agrees with the oracle's own
+    uncompressed long-range sum within the build's reported (sampled) compression error."""
+    w, p = c1_host
+    st = p.export_setup()
+    tb = p.export_tables()
+    pts = _exterior_cells(oracle, w, 150, seed=11)
+    ref = _uncompressed_long(oracle, w, st, st["cells"], pts)
+    cp = np.einsum("pk,pk,pk->p", tb["F1"][pts[:, 0]], tb["F2"][pts[:, 1]], tb["F3"][pts[:, 2]])
+    rel_max = np.max(np.abs(cp - ref)) / np.max(np.abs(ref))
+    assert rel_max <= 2.0 * p.info["sampled_max_err"] + 1e-12, (rel_max, p.info["sampled_max_err"])
+
+
+def test_tolerance_mode_reaches_eps(oracle, rsd):
+    """Tolerance mode (rank_R = 0): RHOSVD + exact canonical-Tucker-canonical at eps=1e-7."""
+    w = syn.random_small(seed=5, M=60, L=5, n=64, b=8.0)
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=64, rank_R=0,
+                    eps_compress=1e-7, sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    st = p.export_setup()
+    tb = p.export_tables()
+    pts = _exterior_cells(oracle, w, 80, seed=12, dmin=1.0, dmax=4.0)
+    ref = _uncompressed_long(oracle, w, st, st["cells"], pts)
+    cp = np.einsum("pk,pk,pk->p", tb["F1"][pts[:, 0]], tb["F2"][pts[:, 1]], tb["F3"][pts[:, 2]])
+    assert np.max(np.abs(cp - ref)) / np.max(np.abs(ref)) < 1e-5
+    assert p.info["R"] == tb["F1"].shape[1] > 0
+
+
+def test_cell_lists_cover_all_relevant_pairs(oracle, c1_host):
+    """S9: every protein atom within max(D_cap, (n_sigma + sqrt 3) h) of a ligand point is a
+    candidate of the coarse cell containing the point's grid cell -- checked by the oracle's
+    brute force through the C scorer's result equality later; here via the neighbour counts
+    reported by the handle being non-trivial and consistent."""
+    w, p = c1_host
+    info = p.info
+    assert info["nbr_entries"] >= w.M
+    assert info["nbr_cells"] > 0 and info["nbr_shift"] >= 0
+
+
+def test_setup_deterministic(rsd):
+    w = syn.random_small(seed=6, M=50, L=5, n=64, b=8.0)
+    kw = dict(grid_n=64, rank_R=8, sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    a = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, n_threads=1, **kw).export_tables()
+    b = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, n_threads=4, **kw).export_tables()
+    for k in ("F1", "F2", "F3", "S1"):
+        assert np.array_equal(a[k], b[k])
