@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--ref-poses", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return impl_reference(args)
@@ -297,7 +298,7 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    mb = run_microbench()
+    mb = None if args.no_microbench else run_microbench()
     peaks = _peaks()
     R = info["R"]
     gather_bytes = 24.0 * R * P * L                 # H4: 3 rows x R fp64 per atom evaluation

@@ -55,8 +55,10 @@ void free_device(rs_handle* h) {
     if (p) cudaFree(p);
     p = nullptr;
   }
-  if (h->d_nb_idx) cudaFree(h->d_nb_idx);
-  h->d_nb_idx = nullptr;
+  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_memo}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
   if (h->stage) cudaFree(h->stage);
   h->stage = nullptr;
   for (void*& s : h->streams) {
@@ -96,6 +98,22 @@ int upload_handle(rs_handle* h) {
   if (int e = upload(&h->dmem[7], ridx, &bytes)) return e;
   if (int e = upload(&h->dmem[8], h->cg.off, &bytes)) return e;
   if (int e = upload(&h->d_nb_idx, h->cg.idx, &bytes)) return e;
+  std::vector<int16_t> cell16(4 * h->cg.idx.size(), 0);
+  for (size_t j = 0; j < h->cg.idx.size(); ++j)
+    for (int a = 0; a < 3; ++a) cell16[4 * j + a] = (int16_t)h->cells[3 * (size_t)h->cg.idx[j] + a];
+  if (int e = upload(&h->d_nb_cell, cell16, &bytes)) return e;
+  // dense memo of the short-range chain over |D_a| <= n_sigma (filled on the device by the same
+  // O5 op sequence), when it is small enough to stay L2-resident
+  const double memo_b = 8.0 * std::pow(double(h->n_sigma + 1), 3.0);
+  if (h->Rs > 0 && memo_b <= 64.0 * (1 << 20)) {
+    CUDA_TRY(cudaMalloc(&h->d_memo, (size_t)memo_b), RS_E_NOMEM);
+    bytes += (int64_t)memo_b;
+    int e = rs::launch_fill_short_memo((const double*)h->dmem[3], (const double*)h->dmem[4],
+                                       (const double*)h->dmem[5], h->Rs, h->n_sigma,
+                                       (double*)h->d_memo, nullptr);
+    if (e != 0) { set_err("short-range memo fill failed"); return RS_E_CUDA; }
+    CUDA_TRY(cudaDeviceSynchronize(), RS_E_CUDA);
+  }
   h->device_bytes = bytes;
   return 0;
 }
@@ -121,6 +139,14 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.t.rec_idx = h->dmem[7];
   a.t.nb_off = (const int32_t*)h->dmem[8];
   a.t.nb_idx = (const int32_t*)h->d_nb_idx;
+  a.t.nb_cell = (const int16_t*)h->d_nb_cell;
+  a.t.short_memo = (const double*)h->d_memo;
+  {
+    // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
+    const double t = h->prm.dmin_cap / h->h + std::sqrt(3.0) + 2.0;
+    a.vdw_cells2 = (int64_t)std::ceil(t * t);
+  }
+  a.rmax_hint = -1.0;
   return a;
 }
 
@@ -198,7 +224,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
   if (n_atoms <= 0) { set_err("n_atoms must be > 0"); return nullptr; }
   if (!(box_half_width > 0) || !std::isfinite(box_half_width)) { set_err("box_half_width must be finite and > 0"); return nullptr; }
   if (prm.grid_n < 2 || (prm.grid_n & 1)) { set_err("grid_n must be even and >= 2"); return nullptr; }
-  if (prm.grid_n > (1 << 20)) { set_err("grid_n too large"); return nullptr; }
+  if (prm.grid_n > 32768) { set_err("grid_n too large (max 32768)"); return nullptr; }
   if (prm.rank_R < 0) { set_err("rank_R must be >= 0"); return nullptr; }
   if (!(prm.eps_compress > 0 && prm.eps_compress < 1)) { set_err("eps_compress must be in (0,1)"); return nullptr; }
   if (!(prm.eps_quad > 0 && prm.eps_quad < 1)) { set_err("eps_quad must be in (0,1)"); return nullptr; }

@@ -66,6 +66,8 @@ struct DeviceTables {
   const void* rec_idx = nullptr;  // int4 per protein atom: i0, i1, i2, 0
   const int32_t* nb_off = nullptr;
   const int32_t* nb_idx = nullptr;
+  const int16_t* nb_cell = nullptr;   // per list entry: the atom's cell (i0, i1, i2, 0) as int16
+  const double* short_memo = nullptr; // s(|D0|,|D1|,|D2|) for |D_a| <= n_sigma, or null
 };
 
 struct ScoreArgs {               // one launch of the scoring kernel
@@ -82,7 +84,12 @@ struct ScoreArgs {               // one launch of the scoring kernel
   double* D;
   unsigned long long* invalid;   // may be null
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
+  int64_t vdw_cells2;            // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
 };
+
+// Fill the dense short-range memo table s(d0,d1,d2), d_a = 0..n_sigma, with the O5 chain.
+int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
+                           int n_sigma, double* out, void* stream);
 
 // Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
 // (if not null) is incremented by the number of kernels enqueued.
@@ -111,6 +118,8 @@ struct rs_handle {
   int device = 0;
   void* dmem[9] = {nullptr};           // F1..3, S1..3, rec, rec_idx, nb_off
   void* d_nb_idx = nullptr;
+  void* d_nb_cell = nullptr;
+  void* d_memo = nullptr;
   int64_t device_bytes = 0;
   // staging for host-pointer calls
   std::mutex mtx;

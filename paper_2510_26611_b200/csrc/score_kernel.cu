@@ -34,7 +34,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 4 * kWarps;        // poses per tile (upper bound)
+constexpr int kTile = 8 * kWarps;        // poses per tile (upper bound)
 constexpr int kLigSmem = 256;            // ligand atoms staged in shared memory
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -161,11 +161,45 @@ struct Window {
   int lo[3], hi[3], base[3];   // staged rows [lo, hi] per axis, first smem row of each axis
 };
 
+// Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
+struct PairStage {
+  double x[3][32];   // transformed coordinates x'
+  double z[32];      // charges
+  int4 cell[32];     // i0, i1, i2, list begin
+  int off[32];       // exclusive prefix of the candidate counts
+};
+
+// L2 path of O4 for compile-time R, kept out of line (it is the rare path in window mode)
+template <int RT>
+__device__ __noinline__ double long_phi_global(const double* F0, const double* F1, const double* F2,
+                                               int i0, int i1, int i2, int rho) {
+  return long_phi<RT, false>((const double2*)(F0 + (size_t)i0 * RT),
+                             (const double2*)(F1 + (size_t)i1 * RT),
+                             (const double2*)(F2 + (size_t)i2 * RT), rho);
+}
+
+// O5 value s(D): from the dense memo (filled by the same chain) or the chain itself
+__device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2) {
+  if (a.t.short_memo) {
+    const int d = a.n_sigma + 1;
+    const int u0 = e0 < 0 ? -e0 : e0, u1 = e1 < 0 ? -e1 : e1, u2 = e2 < 0 ? -e2 : e2;
+    return __ldg(a.t.short_memo + ((size_t)u0 * d + u1) * d + u2);
+  }
+  const double* s0 = a.t.S[0] + (size_t)(e0 + a.n_sigma) * a.Rs;
+  const double* s1 = a.t.S[1] + (size_t)(e1 + a.n_sigma) * a.Rs;
+  const double* s2 = a.t.S[2] + (size_t)(e2 + a.n_sigma) * a.Rs;
+  double s = 0.0;
+  for (int k = 0; k < a.Rs; ++k)
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(__ldg(s0 + k), __ldg(s1 + k)), __ldg(s2 + k)));
+  return s;
+}
+
 // Score one pose with one warp.  RT > 0: compile-time width with an optional smem window.
 template <int RT>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool use_win,
                                            const Window& W, const double2* win,
-                                           const double4* s_lig, bool lig_smem, int lane) {
+                                           const double4* s_lig, bool lig_smem, int lane,
+                                           PairStage& ps) {
   const double* pq = a.poses + 7 * p;
   double qv[7];
 #pragma unroll
@@ -177,10 +211,13 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
   const int rho = lane & 7;
   const int64_t ns2 = (int64_t)a.n_sigma * a.n_sigma;
   const double2* rec2 = (const double2*)a.t.rec;
-  const int4* ridx = (const int4*)a.t.rec_idx;
-  if (ok) {
-    for (int64_t l = lane; l < a.L; l += 32) {
-      double y0, y1, y2, z;
+  const int64_t npass = ok ? (a.L + 31) / 32 : 0;
+  for (int64_t pass = 0; pass < npass; ++pass) {
+    const int64_t l = pass * 32 + lane;
+    int cnt = 0, beg = 0, i0 = 0, i1 = 0, i2 = 0;
+    double xp[3] = {0.0, 0.0, 0.0}, z = 0.0;
+    if (l < a.L) {
+      double y0, y1, y2;
       if (lig_smem) {
         const double4 v = s_lig[l];
         y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
@@ -191,73 +228,105 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
         z = __ldg(a.zl + l);
       }
       // H2 (O2)
-      double xp[3];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
         xp[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3 * r], y0), __dmul_rn(Rm[3 * r + 1], y1)),
                                     __dmul_rn(Rm[3 * r + 2], y2)),
                           qv[4 + r]);
       // H3 (O3)
-      const int i0 = snap_dev(xp[0], a.b, a.inv_h, a.n);
-      const int i1 = snap_dev(xp[1], a.b, a.inv_h, a.n);
-      const int i2 = snap_dev(xp[2], a.b, a.inv_h, a.n);
+      i0 = snap_dev(xp[0], a.b, a.inv_h, a.n);
+      i1 = snap_dev(xp[1], a.b, a.inv_h, a.n);
+      i2 = snap_dev(xp[2], a.b, a.inv_h, a.n);
       if ((i0 | i1 | i2) < 0) {
         bad = true;
-        continue;
-      }
-      // H4 (O4)
-      double phi;
-      if constexpr (RT > 0) {
-        using G = Geo<RT>;
-        const bool inwin = use_win && i0 >= W.lo[0] && i0 <= W.hi[0] && i1 >= W.lo[1] &&
-                           i1 <= W.hi[1] && i2 >= W.lo[2] && i2 <= W.hi[2];
-        if (inwin) {
-          phi = long_phi<RT, true>(win + (size_t)(W.base[0] + i0 - W.lo[0]) * G::CHP,
-                                   win + (size_t)(W.base[1] + i1 - W.lo[1]) * G::CHP,
-                                   win + (size_t)(W.base[2] + i2 - W.lo[2]) * G::CHP, rho);
-        } else {
-          phi = long_phi<RT, false>((const double2*)(a.t.F[0] + (size_t)i0 * RT),
-                                    (const double2*)(a.t.F[1] + (size_t)i1 * RT),
-                                    (const double2*)(a.t.F[2] + (size_t)i2 * RT), rho);
-        }
       } else {
-        phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
-                          a.t.F[2] + (size_t)i2 * a.R, a.R);
+        // H4 (O4)
+        double phi;
+        if constexpr (RT > 0) {
+          using G = Geo<RT>;
+          const bool inwin = use_win && i0 >= W.lo[0] && i0 <= W.hi[0] && i1 >= W.lo[1] &&
+                             i1 <= W.hi[1] && i2 >= W.lo[2] && i2 <= W.hi[2];
+          if (inwin) {
+            phi = long_phi<RT, true>(win + (size_t)(W.base[0] + i0 - W.lo[0]) * G::CHP,
+                                     win + (size_t)(W.base[1] + i1 - W.lo[1]) * G::CHP,
+                                     win + (size_t)(W.base[2] + i2 - W.lo[2]) * G::CHP, rho);
+          } else {
+            phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2, rho);
+          }
+        } else {
+          phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
+                            a.t.F[2] + (size_t)i2 * a.R, a.R);
+        }
+        dd_add_prod(hi, lo, z, phi);
+        // candidate range of the coarse cell containing i (cell lists cover every protein atom
+        // within max(D_cap, (n_sigma + sqrt 3) h) of any point of the cell)
+        const int cx = (i0 >> a.nb_shift) - a.nb_lo[0];
+        const int cy = (i1 >> a.nb_shift) - a.nb_lo[1];
+        const int cz = (i2 >> a.nb_shift) - a.nb_lo[2];
+        if (cx >= 0 && cx < a.nb_dim[0] && cy >= 0 && cy < a.nb_dim[1] && cz >= 0 &&
+            cz < a.nb_dim[2]) {
+          const int64_t cell = ((int64_t)cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz;
+          beg = __ldg(a.t.nb_off + cell);
+          cnt = __ldg(a.t.nb_off + cell + 1) - beg;
+        }
       }
-      dd_add_prod(hi, lo, z, phi);
-      // H5 + H6: candidates of the coarse cell containing i (cell lists cover every protein
-      // atom within max(D_cap, (n_sigma + sqrt 3) h) of any point of the cell)
-      const int cx = (i0 >> a.nb_shift) - a.nb_lo[0];
-      const int cy = (i1 >> a.nb_shift) - a.nb_lo[1];
-      const int cz = (i2 >> a.nb_shift) - a.nb_lo[2];
-      if (cx >= 0 && cx < a.nb_dim[0] && cy >= 0 && cy < a.nb_dim[1] && cz >= 0 && cz < a.nb_dim[2]) {
-        const int64_t cell = ((int64_t)cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz;
-        const int beg = __ldg(a.t.nb_off + cell), end = __ldg(a.t.nb_off + cell + 1);
-        for (int j = beg; j < end; ++j) {
+    }
+    if (__any_sync(kFull, bad)) {
+      bad = true;
+      break;                      // the pose is invalid: NaN outputs, skip the rest
+    }
+    // H5 + H6 over the pass's (atom, candidate) pairs, flattened across the warp so every lane
+    // works on some pair in every round (the pose sums are order-free, O6/O7)
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const int total = __shfl_sync(kFull, inc, 31);
+    if (total == 0) continue;
+    ps.x[0][lane] = xp[0];
+    ps.x[1][lane] = xp[1];
+    ps.x[2][lane] = xp[2];
+    ps.z[lane] = z;
+    ps.cell[lane] = make_int4(i0, i1, i2, beg);
+    ps.off[lane] = inc - cnt;
+    __syncwarp();
+    for (int base = 0; base < total; base += 32) {
+      const int k = base + lane;
+      if (k < total) {
+        int ow = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (ow + step < 32 && ps.off[ow + step] <= k) ow += step;
+        const int4 oc = ps.cell[ow];
+        const int j = oc.w + (k - ps.off[ow]);
+        const short4 mc = __ldg(reinterpret_cast<const short4*>(a.t.nb_cell) + j);
+        const int e0 = oc.x - mc.x, e1 = oc.y - mc.y, e2 = oc.z - mc.z;
+        const int64_t dd = (int64_t)e0 * e0 + (int64_t)e1 * e1 + (int64_t)e2 * e2;
+        const bool h5 = dd <= ns2, h6 = dd < a.vdw_cells2;
+        if (h5 || h6) {
           const int m = __ldg(a.t.nb_idx + j);
-          const double2 xy = ldg2(rec2 + 2 * m);
           const double2 zq = ldg2(rec2 + 2 * m + 1);
-          // O7
-          const double dx0 = __dsub_rn(xp[0], xy.x);
-          const double dx1 = __dsub_rn(xp[1], xy.y);
-          const double dx2 = __dsub_rn(xp[2], zq.x);
-          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
-          best = fmin(best, d2);
-          // O5
-          const int4 im = __ldg(ridx + m);
-          const int64_t e0 = i0 - im.x, e1 = i1 - im.y, e2 = i2 - im.z;
-          if (e0 * e0 + e1 * e1 + e2 * e2 <= ns2) {
-            const double* s0 = a.t.S[0] + (size_t)(e0 + a.n_sigma) * a.Rs;
-            const double* s1 = a.t.S[1] + (size_t)(e1 + a.n_sigma) * a.Rs;
-            const double* s2 = a.t.S[2] + (size_t)(e2 + a.n_sigma) * a.Rs;
-            double s = 0.0;
-            for (int k = 0; k < a.Rs; ++k)
-              s = __dadd_rn(s, __dmul_rn(__dmul_rn(__ldg(s0 + k), __ldg(s1 + k)), __ldg(s2 + k)));
-            dd_add_prod(hi, lo, z, __dmul_rn(zq.y, s));
+          if (h6) {
+            // O7
+            const double2 xy = ldg2(rec2 + 2 * m);
+            const double dx0 = __dsub_rn(ps.x[0][ow], xy.x);
+            const double dx1 = __dsub_rn(ps.x[1][ow], xy.y);
+            const double dx2 = __dsub_rn(ps.x[2][ow], zq.x);
+            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)),
+                                        __dmul_rn(dx2, dx2));
+            best = fmin(best, d2);
+          }
+          if (h5) {
+            // O5: z_l * fl(z_m * s(D))
+            const double sv = short_value(a, e0, e1, e2);
+            dd_add_prod(hi, lo, ps.z[ow], __dmul_rn(zq.y, sv));
           }
         }
       }
     }
+    __syncwarp();
   }
   // H7
   bad = __any_sync(kFull, bad);
@@ -295,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   __shared__ int s_win[7];       // lo[3], hi[3], fits
   __shared__ Window s_cur;
   __shared__ double s_rmax2;
+  __shared__ PairStage s_ps[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool lig_smem = a.L <= kLigSmem;
@@ -329,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     // no shared-memory window: rows come from L2 (through L1)
     Window W{};
     for (int64_t p = p_begin + warp; p < p_end; p += kWarps)
-      score_pose<RT>(a, p, false, W, win, s_lig, lig_smem, lane);
+      score_pose<RT>(a, p, false, W, win, s_lig, lig_smem, lane, s_ps[warp]);
     return;
   }
   if constexpr (RT > 0) {
@@ -436,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       __syncthreads();
       Window W = s_cur;
       for (int64_t pp = p + warp; pp < p + T; pp += kWarps)
-        score_pose<RT>(a, pp, fits, W, win, s_lig, lig_smem, lane);
+        score_pose<RT>(a, pp, fits, W, win, s_lig, lig_smem, lane, s_ps[warp]);
       __syncthreads();
       p += T;
     }
@@ -471,6 +541,12 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   if (RT > 0 && window_mode) {
     const size_t avail = (size_t)dc.max_dyn[slot] > lig_b ? (size_t)dc.max_dyn[slot] - lig_b : 0;
     cap_rows = (int)(avail / (16 * kChp));
+    if (a.rmax_hint >= 0) {
+      // leave the rest of the 228 KB to L1 (cell lists, memo, records): ~1.3x what one
+      // translation's window needs
+      const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
+      cap_rows = std::min(cap_rows, (int)std::max(64.0, 1.3 * need));
+    }
     dyn = lig_b + (size_t)cap_rows * 16 * kChp;
   }
   const int64_t tiles = (a.P + kTile - 1) / kTile;
@@ -480,7 +556,28 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   return (int)cudaGetLastError();
 }
 
+__global__ void fill_short_memo_kernel(const double* __restrict__ S0, const double* __restrict__ S1,
+                                       const double* __restrict__ S2, int Rs, int ns, double* out) {
+  const int64_t d = ns + 1, tot = d * d * d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int e0 = (int)(t / (d * d)), e1 = (int)((t / d) % d), e2 = (int)(t % d);
+    const double* s0 = S0 + (size_t)(e0 + ns) * Rs;
+    const double* s1 = S1 + (size_t)(e1 + ns) * Rs;
+    const double* s2 = S2 + (size_t)(e2 + ns) * Rs;
+    double s = 0.0;                    // the O5 chain, ascending k
+    for (int k = 0; k < Rs; ++k) s = __dadd_rn(s, __dmul_rn(__dmul_rn(s0[k], s1[k]), s2[k]));
+    out[t] = s;
+  }
+}
+
 }  // namespace
+
+int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
+                           int n_sigma, double* out, void* stream) {
+  fill_short_memo_kernel<<<1024, 256, 0, (cudaStream_t)stream>>>(S0, S1, S2, Rs, n_sigma, out);
+  return (int)cudaGetLastError();
+}
 
 const char* score_kernel_variant(int R) {
   switch (R) {

@@ -188,10 +188,18 @@ def product_poses(quats, trans):
     return poses
 
 
+_POSE_STREAM = 0
+
+
 def _streams(seed):
     ss = np.random.SeedSequence(seed).spawn(6)
     # fixed order: protein xyz, protein q, ligand xyz, ligand q, rotations, translations
-    return [np.random.default_rng(s) for s in ss]
+    g = [np.random.default_rng(s) for s in ss]
+    if _POSE_STREAM:
+        # an independent pose batch (weak-scaling shard) for the same protein and ligand
+        r = np.random.SeedSequence([seed, _POSE_STREAM]).spawn(2)
+        g[4], g[5] = np.random.default_rng(r[0]), np.random.default_rng(r[1])
+    return g
 
 
 # --------------------------------------------------------------------------------------
@@ -302,8 +310,14 @@ def config_c5(seed=0, rank_R=16, sigma_mult=1, n_poses=100_000) -> Workload:
 CONFIGS = {"C1": config_c1, "C2": config_c2, "C3": config_c3, "C4": config_c4, "C5": config_c5}
 
 
-def make(name: str, **kw) -> Workload:
-    return CONFIGS[name](**kw)
+def make(name: str, pose_stream: int = 0, **kw) -> Workload:
+    """Config `name`; pose_stream > 0 draws an independent pose batch (same protein/ligand)."""
+    global _POSE_STREAM
+    _POSE_STREAM = int(pose_stream)
+    try:
+        return CONFIGS[name](**kw)
+    finally:
+        _POSE_STREAM = 0
 
 
 def subsample(poses: np.ndarray, k: int, seed: int = 1) -> tuple[np.ndarray, np.ndarray]:

@@ -1,0 +1,70 @@
+"""World-size-2 gloo tests of the multi-GPU host logic (pose sharding + gather), on CPU: the
+per-rank scorer is the oracle, so the test exercises exactly the sharding/gather code the GPU
+path uses, without a GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_26611_b200.shard import score_sharded, shard_bounds
+from synth import configs as syn
+
+
+def test_shard_bounds_partition():
+    for P in (0, 1, 7, 64, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            got = [shard_bounds(P, world, r) for r in range(world)]
+            assert got[0][0] == 0 and got[-1][1] == P
+            assert all(got[i][1] == got[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in got]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import rs_oracle
+    w = syn.random_small(seed=21, M=30, L=6, n=32, b=8.0, R=4, P=101)
+    rng = np.random.default_rng(0)
+    tb = dict(n=32, b=8.0, R=4, F1=rng.normal(size=(32, 4)), F2=rng.normal(size=(32, 4)),
+              F3=rng.normal(size=(32, 4)), n_sigma=2, S1=rng.normal(size=(5, 3)),
+              S2=rng.normal(size=(5, 3)), S3=rng.normal(size=(5, 3)))
+    poses = w.poses.copy()
+    poses[5, :4] = 0.0                      # one invalid pose (in rank 0's shard)
+    poses[77, 4] = 50.0                     # one invalid pose (in rank 1's shard)
+
+    def score(ps):
+        return rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q,
+                                     np.ascontiguousarray(ps), 1.5)
+
+    E, D, inv, rng_ = score_sharded(score, poses, gather=True)
+    E1, D1, inv1 = score(poses)
+    ok = (np.array_equal(E.numpy(), E1, equal_nan=True) and
+          np.array_equal(D.numpy(), D1, equal_nan=True) and inv == inv1 == 2)
+    El, Dl, invl, (lo, hi) = score_sharded(score, poses, gather=False)
+    ok = ok and np.array_equal(El.numpy(), E1[lo:hi], equal_nan=True) and invl == 2
+    out[rank] = bool(ok)
+    dist.destroy_process_group()
+
+
+def test_sharded_scoring_gloo_world2():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] and out[1]

@@ -25,7 +25,7 @@ __global__ void k_dfma(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[blockIdx.x] = s;
 }
 
-// mode 0: conflict-free (lane reads chunk lane&7 of row (lane>>3)+k)
+// mode 0: 4 rows per warp (one per quarter-warp), lane-rotated chunks (conflict-free)
 // mode 1: random row per lane, chunk c same for all lanes (unrotated)
 // mode 2: random row per lane, chunk (c + lane) & 7 (rotated)
 template <int MODE>
@@ -42,7 +42,7 @@ __global__ void k_lds(unsigned long long* out, int iters, int nrows) {
     int row = (MODE == 0) ? (((lane >> 3) + it * 4) % nrows) : (int)((st >> 8) % (uint32_t)nrows);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      int ch = (MODE == 0) ? (lane & 7) : (MODE == 1 ? c : ((c + lane) & 7));
+      int ch = (MODE == 1) ? c : ((c + lane) & 7);
       double2 v = sm[row * 8 + ch];
       acc0 += v.x; acc1 += v.y;
     }
