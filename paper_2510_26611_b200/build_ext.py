@@ -27,10 +27,13 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile every csrc/ source and link librsdock.so (or `out`, with extra -D defines)."""
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" + ("_" + os.path.basename(lib) if out else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -39,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+                   *[f"-D{d}" for d in defines],
                    "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-c", src, "-o", obj]
         else:
             cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler",
@@ -50,9 +54,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         out, _ = p.communicate()
         if p.returncode != 0:
             raise RuntimeError("build failed: " + " ".join(cmd) + "\n" + out.decode())
-    link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
+    link = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
     subprocess.check_call(link)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -55,7 +55,7 @@ void free_device(rs_handle* h) {
     if (p) cudaFree(p);
     p = nullptr;
   }
-  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_memo}) {
+  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_nb_rec, &h->d_memo}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -102,6 +102,16 @@ int upload_handle(rs_handle* h) {
   for (size_t j = 0; j < h->cg.idx.size(); ++j)
     for (int a = 0; a < 3; ++a) cell16[4 * j + a] = (int16_t)h->cells[3 * (size_t)h->cg.idx[j] + a];
   if (int e = upload(&h->d_nb_cell, cell16, &bytes)) return e;
+  {
+    // candidate records inline in list order (no index indirection on the device)
+    std::vector<double> nrec(4 * h->cg.idx.size());
+    for (size_t j = 0; j < h->cg.idx.size(); ++j) {
+      const size_t m = (size_t)h->cg.idx[j];
+      for (int a = 0; a < 3; ++a) nrec[4 * j + a] = h->xyz[3 * m + a];
+      nrec[4 * j + 3] = h->z[m];
+    }
+    if (int e = upload(&h->d_nb_rec, nrec, &bytes)) return e;
+  }
   // dense memo of the short-range chain over |D_a| <= n_sigma (filled on the device by the same
   // O5 op sequence), when it is small enough to stay L2-resident
   const double memo_b = 8.0 * std::pow(double(h->n_sigma + 1), 3.0);
@@ -140,6 +150,7 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.t.nb_off = (const int32_t*)h->dmem[8];
   a.t.nb_idx = (const int32_t*)h->d_nb_idx;
   a.t.nb_cell = (const int16_t*)h->d_nb_cell;
+  a.t.nb_rec = (const double*)h->d_nb_rec;
   a.t.short_memo = (const double*)h->d_memo;
   {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding

@@ -67,6 +67,7 @@ struct DeviceTables {
   const int32_t* nb_off = nullptr;
   const int32_t* nb_idx = nullptr;
   const int16_t* nb_cell = nullptr;   // per list entry: the atom's cell (i0, i1, i2, 0) as int16
+  const double* nb_rec = nullptr;     // per list entry: the atom's (x, y, z, q)
   const double* short_memo = nullptr; // s(|D0|,|D1|,|D2|) for |D_a| <= n_sigma, or null
 };
 
@@ -119,6 +120,7 @@ struct rs_handle {
   void* dmem[9] = {nullptr};           // F1..3, S1..3, rec, rec_idx, nb_off
   void* d_nb_idx = nullptr;
   void* d_nb_cell = nullptr;
+  void* d_nb_rec = nullptr;
   void* d_memo = nullptr;
   int64_t device_bytes = 0;
   // staging for host-pointer calls

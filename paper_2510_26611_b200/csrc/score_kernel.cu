@@ -32,7 +32,10 @@
 namespace rs {
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef RS_THREADS
+#define RS_THREADS 640
+#endif
+constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = 8 * kWarps;        // poses per tile (upper bound)
 constexpr int kLigSmem = 256;            // ligand atoms staged in shared memory
@@ -161,12 +164,20 @@ struct Window {
   int lo[3], hi[3], base[3];   // staged rows [lo, hi] per axis, first smem row of each axis
 };
 
+// A tile's poses, decoded once by one thread each (H1): rotation, translation, validity.
+struct __align__(16) PoseStage {
+  double R[kTile][9];
+  double t[kTile][3];
+  int ok[kTile];
+};
+
 // Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
-struct PairStage {
+struct __align__(16) PairStage {
   double x[3][32];   // transformed coordinates x'
   double z[32];      // charges
   int4 cell[32];     // i0, i1, i2, list begin
   int off[32];       // exclusive prefix of the candidate counts
+  int map[64];       // two rounds: candidate slot where an atom's segment starts -> atom lane
 };
 
 // L2 path of O4 for compile-time R, kept out of line (it is the rare path in window mode)
@@ -194,26 +205,41 @@ __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1
   return s;
 }
 
+// One candidate pair (atom `ow` of the pass, list entry j): O7 distance and O5 replica term.
+__device__ __forceinline__ void pair_term(const ScoreArgs& a, const PairStage& ps, int ow,
+                                          int4 oc, short4 mc, double2 xy, double2 zq,
+                                          int64_t ns2, double& hi, double& lo, double& best) {
+  const int e0 = oc.x - mc.x, e1 = oc.y - mc.y, e2 = oc.z - mc.z;
+  const int64_t dd = (int64_t)e0 * e0 + (int64_t)e1 * e1 + (int64_t)e2 * e2;
+  if (dd < a.vdw_cells2) {
+    const double dx0 = __dsub_rn(ps.x[0][ow], xy.x);
+    const double dx1 = __dsub_rn(ps.x[1][ow], xy.y);
+    const double dx2 = __dsub_rn(ps.x[2][ow], zq.x);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
+    best = fmin(best, d2);
+  }
+  if (dd <= ns2) {
+    const double sv = short_value(a, e0, e1, e2);
+    dd_add_prod(hi, lo, ps.z[ow], __dmul_rn(zq.y, sv));
+  }
+}
+
 // Score one pose with one warp.  RT > 0: compile-time width with an optional smem window.
 template <int RT>
-__device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool use_win,
+__device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const double* Rm,
+                                           const double* tv, bool ok, bool use_win,
                                            const Window& W, const double2* win,
                                            const double4* s_lig, bool lig_smem, int lane,
                                            PairStage& ps) {
-  const double* pq = a.poses + 7 * p;
-  double qv[7];
-#pragma unroll
-  for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
-  double Rm[9];
-  const bool ok = quat_rot_dev(qv, Rm);
   double hi = 0.0, lo = 0.0, best = INFINITY;
   bool bad = !ok;
   const int rho = lane & 7;
   const int64_t ns2 = (int64_t)a.n_sigma * a.n_sigma;
-  const double2* rec2 = (const double2*)a.t.rec;
-  const int64_t npass = ok ? (a.L + 31) / 32 : 0;
-  for (int64_t pass = 0; pass < npass; ++pass) {
-    const int64_t l = pass * 32 + lane;
+  const int npass = ok ? (int)((a.L + 31) / 32) : 0;
+  const double2* nrec = (const double2*)a.t.nb_rec;
+  const short4* ncell = reinterpret_cast<const short4*>(a.t.nb_cell);
+  for (int pass = 0; pass < npass; ++pass) {
+    const int64_t l = (int64_t)pass * 32 + lane;
     int cnt = 0, beg = 0, i0 = 0, i1 = 0, i2 = 0;
     double xp[3] = {0.0, 0.0, 0.0}, z = 0.0;
     if (l < a.L) {
@@ -232,7 +258,7 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
       for (int r = 0; r < 3; ++r)
         xp[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3 * r], y0), __dmul_rn(Rm[3 * r + 1], y1)),
                                     __dmul_rn(Rm[3 * r + 2], y2)),
-                          qv[4 + r]);
+                          tv[r]);
       // H3 (O3)
       i0 = snap_dev(xp[0], a.b, a.inv_h, a.n);
       i1 = snap_dev(xp[1], a.b, a.inv_h, a.n);
@@ -240,12 +266,31 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
       if ((i0 | i1 | i2) < 0) {
         bad = true;
       } else {
+#if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
+        // candidate range of the coarse cell containing i (cell lists cover every protein atom
+        // within max(D_cap, (n_sigma + sqrt 3) h) of any point of the cell); loads issued
+        // before H4 so their latency hides behind the gathers
+        const int cx = (i0 >> a.nb_shift) - a.nb_lo[0];
+        const int cy = (i1 >> a.nb_shift) - a.nb_lo[1];
+        const int cz = (i2 >> a.nb_shift) - a.nb_lo[2];
+        if (cx >= 0 && cx < a.nb_dim[0] && cy >= 0 && cy < a.nb_dim[1] && cz >= 0 &&
+            cz < a.nb_dim[2]) {
+          const int64_t cell = ((int64_t)cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz;
+          beg = __ldg(a.t.nb_off + cell);
+          cnt = __ldg(a.t.nb_off + cell + 1) - beg;
+        }
+#endif
         // H4 (O4)
         double phi;
         if constexpr (RT > 0) {
           using G = Geo<RT>;
           const bool inwin = use_win && i0 >= W.lo[0] && i0 <= W.hi[0] && i1 >= W.lo[1] &&
                              i1 <= W.hi[1] && i2 >= W.lo[2] && i2 <= W.hi[2];
+#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
+          if (inwin) {
+            phi = z;
+          } else
+#endif
           if (inwin) {
             phi = long_phi<RT, true>(win + (size_t)(W.base[0] + i0 - W.lo[0]) * G::CHP,
                                      win + (size_t)(W.base[1] + i1 - W.lo[1]) * G::CHP,
@@ -258,17 +303,6 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
                             a.t.F[2] + (size_t)i2 * a.R, a.R);
         }
         dd_add_prod(hi, lo, z, phi);
-        // candidate range of the coarse cell containing i (cell lists cover every protein atom
-        // within max(D_cap, (n_sigma + sqrt 3) h) of any point of the cell)
-        const int cx = (i0 >> a.nb_shift) - a.nb_lo[0];
-        const int cy = (i1 >> a.nb_shift) - a.nb_lo[1];
-        const int cz = (i2 >> a.nb_shift) - a.nb_lo[2];
-        if (cx >= 0 && cx < a.nb_dim[0] && cy >= 0 && cy < a.nb_dim[1] && cz >= 0 &&
-            cz < a.nb_dim[2]) {
-          const int64_t cell = ((int64_t)cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz;
-          beg = __ldg(a.t.nb_off + cell);
-          cnt = __ldg(a.t.nb_off + cell + 1) - beg;
-        }
       }
     }
     if (__any_sync(kFull, bad)) {
@@ -276,7 +310,8 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
       break;                      // the pose is invalid: NaN outputs, skip the rest
     }
     // H5 + H6 over the pass's (atom, candidate) pairs, flattened across the warp so every lane
-    // works on some pair in every round (the pose sums are order-free, O6/O7)
+    // works on some pair in every round (the pose sums are order-free, O6/O7); two rounds per
+    // iteration keep two independent sets of loads in flight
     int inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -285,46 +320,48 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
     }
     const int total = __shfl_sync(kFull, inc, 31);
     if (total == 0) continue;
+    const int myoff = inc - cnt;
     ps.x[0][lane] = xp[0];
     ps.x[1][lane] = xp[1];
     ps.x[2][lane] = xp[2];
     ps.z[lane] = z;
     ps.cell[lane] = make_int4(i0, i1, i2, beg);
-    ps.off[lane] = inc - cnt;
-    __syncwarp();
-    for (int base = 0; base < total; base += 32) {
-      const int k = base + lane;
-      if (k < total) {
-        int ow = 0;
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
-          if (ow + step < 32 && ps.off[ow + step] <= k) ow += step;
-        const int4 oc = ps.cell[ow];
-        const int j = oc.w + (k - ps.off[ow]);
-        const short4 mc = __ldg(reinterpret_cast<const short4*>(a.t.nb_cell) + j);
-        const int e0 = oc.x - mc.x, e1 = oc.y - mc.y, e2 = oc.z - mc.z;
-        const int64_t dd = (int64_t)e0 * e0 + (int64_t)e1 * e1 + (int64_t)e2 * e2;
-        const bool h5 = dd <= ns2, h6 = dd < a.vdw_cells2;
-        if (h5 || h6) {
-          const int m = __ldg(a.t.nb_idx + j);
-          const double2 zq = ldg2(rec2 + 2 * m + 1);
-          if (h6) {
-            // O7
-            const double2 xy = ldg2(rec2 + 2 * m);
-            const double dx0 = __dsub_rn(ps.x[0][ow], xy.x);
-            const double dx1 = __dsub_rn(ps.x[1][ow], xy.y);
-            const double dx2 = __dsub_rn(ps.x[2][ow], zq.x);
-            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)),
-                                        __dmul_rn(dx2, dx2));
-            best = fmin(best, d2);
-          }
-          if (h5) {
-            // O5: z_l * fl(z_m * s(D))
-            const double sv = short_value(a, e0, e1, e2);
-            dd_add_prod(hi, lo, ps.z[ow], __dmul_rn(zq.y, sv));
-          }
-        }
+    ps.off[lane] = myoff;
+    int carry = 0;
+    for (int base = 0; base < total; base += 64) {
+      const int rel = myoff - base;
+      const bool starts = cnt > 0 && rel >= 0 && rel < 64;
+      __syncwarp();
+      if (starts) ps.map[rel] = lane;
+      const unsigned m0 = __reduce_or_sync(kFull, (starts && rel < 32) ? (1u << rel) : 0u);
+      const unsigned m1 = __reduce_or_sync(kFull, (starts && rel >= 32) ? (1u << (rel - 32)) : 0u);
+      __syncwarp();
+      const unsigned long long m64 = ((unsigned long long)m1 << 32) | m0;
+      const unsigned long long below0 = m64 & (0xffffffffull >> (31 - lane));
+      const unsigned long long below1 = m64 & (0xffffffffffffffffull >> (31 - lane));
+      const int ow0 = below0 ? ps.map[63 - __clzll(below0)] : carry;
+      const int ow1 = below1 ? ps.map[63 - __clzll(below1)] : carry;
+      carry = __shfl_sync(kFull, ow1, 31);
+      const int k0 = base + lane, k1 = base + 32 + lane;
+      int4 oc0 = make_int4(0, 0, 0, 0), oc1 = oc0;
+      short4 mc0 = make_short4(0, 0, 0, 0), mc1 = mc0;
+      double2 xy0 = make_double2(0.0, 0.0), zq0 = xy0, xy1 = xy0, zq1 = xy0;
+      if (k0 < total) {
+        oc0 = ps.cell[ow0];
+        const int j = oc0.w + (k0 - ps.off[ow0]);
+        mc0 = __ldg(ncell + j);
+        xy0 = ldg2(nrec + 2 * (size_t)j);
+        zq0 = ldg2(nrec + 2 * (size_t)j + 1);
       }
+      if (k1 < total) {
+        oc1 = ps.cell[ow1];
+        const int j = oc1.w + (k1 - ps.off[ow1]);
+        mc1 = __ldg(ncell + j);
+        xy1 = ldg2(nrec + 2 * (size_t)j);
+        zq1 = ldg2(nrec + 2 * (size_t)j + 1);
+      }
+      if (k0 < total) pair_term(a, ps, ow0, oc0, mc0, xy0, zq0, ns2, hi, lo, best);
+      if (k1 < total) pair_term(a, ps, ow1, oc1, mc1, xy1, zq1, ns2, hi, lo, best);
     }
     __syncwarp();
   }
@@ -355,19 +392,22 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, bool u
 }
 
 template <int RT>
-__global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows) {
+__global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
+                                                            int lig_smem_n) {
+  // dynamic shared memory: [PairStage x warps][PoseStage][ligand][factor-row window]
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double4* s_lig = reinterpret_cast<double4*>(smem_raw);
-  double2* win = reinterpret_cast<double2*>(smem_raw + kLigSmem * sizeof(double4));
+  PairStage* s_ps = reinterpret_cast<PairStage*>(smem_raw);
+  PoseStage& s_pose = *reinterpret_cast<PoseStage*>(s_ps + kWarps);
+  double4* s_lig = reinterpret_cast<double4*>(&s_pose + 1);
+  double2* win = reinterpret_cast<double2*>(s_lig + lig_smem_n);
   __shared__ double s_red[kWarps][6];
   __shared__ int s_bad[kWarps];
   __shared__ int s_win[7];       // lo[3], hi[3], fits
   __shared__ Window s_cur;
   __shared__ double s_rmax2;
-  __shared__ PairStage s_ps[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool lig_smem = a.L <= kLigSmem;
+  const bool lig_smem = a.L <= lig_smem_n;
   // ligand radius (body frame) and staging
   double r2 = 0.0;
   for (int64_t l = tid; l < a.L; l += kThreads) {
@@ -391,31 +431,38 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   __syncthreads();
   // slack: |R y| <= |y| (1 + 1e-15) plus two cells for the snap rounding and the clamp
   const double rb = sqrt(s_rmax2) * (1.0 + 1e-12) + 2.0 * a.h;
+  const bool window_mode = RT > 0 && cap_rows > 0;
 
   const int64_t p_begin = a.P * (int64_t)blockIdx.x / gridDim.x;
   const int64_t p_end = a.P * (int64_t)(blockIdx.x + 1) / gridDim.x;
-
-  if (RT == 0 || cap_rows == 0) {
-    // no shared-memory window: rows come from L2 (through L1)
-    Window W{};
-    for (int64_t p = p_begin + warp; p < p_end; p += kWarps)
-      score_pose<RT>(a, p, false, W, win, s_lig, lig_smem, lane, s_ps[warp]);
-    return;
-  }
-  if constexpr (RT > 0) {
-    using G = Geo<RT>;
-    int64_t p = p_begin;
-    while (p < p_end) {
-      int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
+  int64_t p = p_begin;
+  while (p < p_end) {
+    int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
+    // H1 for the tile: one thread per pose
+    if (tid < T) {
+      const double* pq = a.poses + 7 * (p + tid);
+      double qv[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
+      double Rm[9];
+      const bool ok = quat_rot_dev(qv, Rm);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_pose.R[tid][i] = Rm[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_pose.t[tid][i] = qv[4 + i];
+      s_pose.ok[tid] = ok ? 1 : 0;
+    }
+    bool fits = false;
+    if (window_mode) {
       for (;;) {
-        // block min/max of the tile's translations
+        // block min/max of the tile's translations (staged above)
+        __syncthreads();
         double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
         int badt = 0;
         if (tid < T) {
-          const double* pq = a.poses + 7 * (p + tid);
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
-            const double t = __ldg(pq + 4 + r);
+            const double t = s_pose.t[tid][r];
             if (!isfinite(t)) badt = 1;
             mn[r] = t;
             mx[r] = t;
@@ -454,27 +501,24 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             hi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
             rows += hi[r] - lo[r] + 1;
           }
-          const int fits = (!bad && rows <= cap_rows) ? 1 : 0;
+          const int fts = (!bad && rows <= cap_rows) ? 1 : 0;
           for (int r = 0; r < 3; ++r) {
             s_win[r] = lo[r];
             s_win[3 + r] = hi[r];
           }
-          s_win[6] = fits;
+          s_win[6] = fts;
         }
         __syncthreads();
-        const bool fits = s_win[6] != 0;
+        fits = s_win[6] != 0;
         if (fits || T == 1) break;
-        T = (T + 1) / 2;
-        __syncthreads();
+        T = (T + 1) / 2;           // the staged poses [0, T) stay valid
       }
-      const bool fits = s_win[6] != 0;
       if (fits) {
         bool contained = true;
 #pragma unroll
         for (int r = 0; r < 3; ++r)
           contained = contained && s_cur.lo[r] <= s_win[r] && s_win[3 + r] <= s_cur.hi[r];
         if (!contained) {
-          __syncthreads();
           if (tid == 0) {
             int rows = 0;
             for (int r = 0; r < 3; ++r) rows += s_win[3 + r] - s_win[r] + 1;
@@ -490,26 +534,36 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             }
           }
           __syncthreads();
-          const int rows0 = s_cur.hi[0] - s_cur.lo[0] + 1, rows1 = s_cur.hi[1] - s_cur.lo[1] + 1;
-          const int total = s_cur.base[2] + s_cur.hi[2] - s_cur.lo[2] + 1;
-          for (int idx = tid; idx < total * G::CHP; idx += kThreads) {
-            const int row = idx / G::CHP, ph = idx - row * G::CHP;
-            const int ax = row < rows0 ? 0 : (row < rows0 + rows1 ? 1 : 2);
-            const int grow = s_cur.lo[ax] + row - s_cur.base[ax];
-            double2 v = make_double2(0.0, 0.0);
-            const int src = G::REP ? (ph & (G::CH - 1)) : ph;
-            if (G::REP || ph < G::CH) v = ldg2((const double2*)(a.t.F[ax] + (size_t)grow * RT) + src);
-            win[idx] = v;
+          if constexpr (RT > 0) {
+            using G = Geo<RT>;
+            const int rows0 = s_cur.hi[0] - s_cur.lo[0] + 1, rows1 = s_cur.hi[1] - s_cur.lo[1] + 1;
+            const int total = s_cur.base[2] + s_cur.hi[2] - s_cur.lo[2] + 1;
+            for (int idx = tid; idx < total * G::CHP; idx += kThreads) {
+              const int row = idx / G::CHP, ph = idx - row * G::CHP;
+              const int ax = row < rows0 ? 0 : (row < rows0 + rows1 ? 1 : 2);
+              const int grow = s_cur.lo[ax] + row - s_cur.base[ax];
+              double2 v = make_double2(0.0, 0.0);
+              const int src = G::REP ? (ph & (G::CH - 1)) : ph;
+              if (G::REP || ph < G::CH) v = ldg2((const double2*)(a.t.F[ax] + (size_t)grow * RT) + src);
+              win[idx] = v;
+            }
           }
         }
       }
-      __syncthreads();
-      Window W = s_cur;
-      for (int64_t pp = p + warp; pp < p + T; pp += kWarps)
-        score_pose<RT>(a, pp, fits, W, win, s_lig, lig_smem, lane, s_ps[warp]);
-      __syncthreads();
-      p += T;
     }
+    __syncthreads();
+    const Window W = s_cur;
+    for (int s = warp; s < T; s += kWarps) {
+      double Rm[9], tv[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Rm[i] = s_pose.R[s][i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tv[i] = s_pose.t[s][i];
+      score_pose<RT>(a, p + s, Rm, tv, s_pose.ok[s] != 0, fits, W, win, s_lig, lig_smem, lane,
+                     s_ps[warp]);
+    }
+    __syncthreads();
+    p += T;
   }
 }
 
@@ -535,24 +589,25 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
     dc.attr_set[slot] = true;
   }
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  const size_t lig_b = kLigSmem * sizeof(double4);
+  const int lig_n = (int)std::min<int64_t>(a.L, kLigSmem);
+  const size_t lig_b = (size_t)lig_n * sizeof(double4) + sizeof(PairStage) * kWarps + sizeof(PoseStage);
   size_t dyn = lig_b;
   int cap_rows = 0;
   if (RT > 0 && window_mode) {
     const size_t avail = (size_t)dc.max_dyn[slot] > lig_b ? (size_t)dc.max_dyn[slot] - lig_b : 0;
     cap_rows = (int)(avail / (16 * kChp));
     if (a.rmax_hint >= 0) {
-      // leave the rest of the 228 KB to L1 (cell lists, memo, records): ~1.3x what one
+      // leave the rest of the 228 KB to L1 (cell lists, records, memo): ~1.15x what one
       // translation's window needs
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
-      cap_rows = std::min(cap_rows, (int)std::max(64.0, 1.3 * need));
+      cap_rows = std::min(cap_rows, (int)std::max(64.0, 1.15 * need));
     }
     dyn = lig_b + (size_t)cap_rows * 16 * kChp;
   }
   const int64_t tiles = (a.P + kTile - 1) / kTile;
-  int grid = (int)std::min<int64_t>(tiles, (int64_t)dc.sms * (cap_rows > 0 ? 1 : 2));
+  int grid = (int)std::min<int64_t>(tiles, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
-  score_kernel<RT><<<grid, kThreads, dyn, st>>>(a, cap_rows);
+  score_kernel<RT><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
   return (int)cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librsdock.so")
+LIB_PATH = os.environ.get("RSDOCK_LIB") or os.path.join(_PKG, "librsdock.so")
 
 RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
 RS_FLAG_HOST_ONLY = 1

@@ -232,3 +232,31 @@ def test_full_size_sampled(env, name, k):
     Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
     compare(Eg[idx], Dg[idx], Eo, Do)
     assert inv == int(np.isnan(Eg).sum())
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled(env):
+    """C4: n = 16384, 50,000 atoms, R = 24 (L2 path: the ligand spans more rows than fit in
+    shared memory), 10^7 poses on the GPU, 64 sampled poses re-scored by the oracle."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make("C4")
+    prot = build(rsdock, w)
+    assert prot.info["R"] == 24
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
+    idx, _ = syn.subsample(w.poses, 64, seed=4)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
+    compare(Eg[idx], Dg[idx], Eo, Do)
+    assert inv == int(np.isnan(Eg).sum())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("R,mult", [(16, 1), (32, 3)])
+def test_c5_full_size_sampled(env, R, mult):
+    """C5 protein-protein: 5000-atom rigid partner (ligand from global memory), n = 8192."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c5(rank_R=R, sigma_mult=mult)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
+    idx, _ = syn.subsample(w.poses, 24, seed=5)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
+    compare(Eg[idx], Dg[idx], Eo, Do)
