@@ -95,14 +95,31 @@ double oracle_dd_sum_products(const double *a, const double *b, int64_t n)
     return acc.hi + acc.lo;
 }
 
-/* ---- O4: long-range CP value at cell i (Lemma 3.2 / Eq. (18); entry formula PAPER.md:463) */
+/* ---- O4: long-range CP value at cell i (Lemma 3.2 / Eq. (18); entry formula PAPER.md:463)
+ * phi = sum_{k<R} F1[i0][k] F2[i1][k] F3[i2][k].  The paper fixes no summation order; the
+ * contract (reading A20) is:
+ *   q_k = (F1[i0][k] * F2[i1][k]) * F3[i2][k]      for k < R,   q_k = 0 for R <= k < 2C,
+ *   C   = smallest power of two >= ceil(R/2)       (number of rank pairs "chunks"),
+ *   s_c = q_{2c} + q_{2c+1}                        for c < C,
+ *   for m = C/2, C/4, ..., 1:  s_c = s_c + s_{c+m}  for c < m,
+ *   phi = s_0.
+ * (A pairwise halving tree over rank pairs.) */
 double oracle_long_value(const double *F1, const double *F2, const double *F3, int R,
                          int i0, int i1, int i2)
 {
     const double *a = F1 + (int64_t)i0 * R, *b = F2 + (int64_t)i1 * R, *c = F3 + (int64_t)i2 * R;
-    double phi = 0.0;
-    for (int k = 0; k < R; ++k) phi = phi + (a[k] * b[k]) * c[k];
-    return phi;
+    int C = 1;
+    while (2 * C < R) C *= 2;
+    double s[C];
+    for (int j = 0; j < C; ++j) {
+        double q0 = 0.0, q1 = 0.0;
+        if (2 * j < R) q0 = (a[2 * j] * b[2 * j]) * c[2 * j];
+        if (2 * j + 1 < R) q1 = (a[2 * j + 1] * b[2 * j + 1]) * c[2 * j + 1];
+        s[j] = q0 + q1;
+    }
+    for (int m = C / 2; m >= 1; m /= 2)
+        for (int j = 0; j < m; ++j) s[j] = s[j] + s[j + m];
+    return s[0];
 }
 
 /* ---- O5: short-range reference value S(Delta) for |Delta|_2 <= n_sigma (Def. 2.1) ---- */

@@ -4,6 +4,7 @@ exact rational arithmetic, or brute force -- chosen so a dropped term, wrong sig
 transposed operand fails.  CPU only (-m "not gpu")."""
 import math
 import os
+from fractions import Fraction
 
 import numpy as np
 import pytest
@@ -200,6 +201,56 @@ def test_long_value_rank1_ones_and_one_hot(oracle):
     lv = lambda i: oracle.lib().oracle_long_value(oracle._p(np.ascontiguousarray(F1)),
                                                   oracle._p(F), oracle._p(F), 2, i, i, i)
     assert lv(0) == 3.0 and lv(1) == 5.0 and lv(2) == 0.0
+
+
+def _lv(oracle, F1, F2, F3, i=(0, 0, 0)):
+    c = lambda x: oracle._p(np.ascontiguousarray(x, dtype=np.float64))
+    return oracle.lib().oracle_long_value(c(F1), c(F2), c(F3), F1.shape[1], *i)
+
+
+def test_long_value_summation_order_worked_example(oracle):
+    """O4 order contract (reading A20), worked by hand with q = (1e16, 1, 2, -1e16, 3)
+    (R = 5, so C = 4 rank pairs, the last two padded with zeros):
+      s = (1e16 + 1, 2 - 1e16, 3 + 0, 0) = (1e16, -1e16 + 2, 3, 0)      [1e16 + 1 ties to even]
+      m = 2: s0 = 1e16 + 3 = 1e16 + 4 (tie to even), s1 = -1e16 + 2
+      m = 1: phi = (1e16 + 4) + (-1e16 + 2) = 6.
+    The exact sum is 7 and the ascending sequential chain gives 5, so this pins the tree."""
+    q = np.array([[1e16, 1.0, 2.0, -1e16, 3.0]])
+    ones = np.ones_like(q)
+    assert _lv(oracle, q, ones, ones) == 6.0
+    # R = 4 (C = 2): (1e16 + 1) + (-1e16 + 1) = 1e16 - 1e16 = 0, sequential would give 1
+    q4 = np.array([[1e16, 1.0, -1e16, 1.0]])
+    assert _lv(oracle, q4, np.ones_like(q4), np.ones_like(q4)) == 0.0
+    # the triple product is rounded as (F1 F2) F3: 3 * (1/3) * 3 with 1/3 rounded
+    t = np.array([[1.0 / 3.0]])
+    assert _lv(oracle, np.array([[3.0]]), t, np.array([[3.0]])) == (3.0 * (1.0 / 3.0)) * 3.0
+
+
+@pytest.mark.parametrize("R", [4, 8, 12, 16, 24, 32])
+def test_long_value_cyclic_pair_rotation_invariance(oracle, R):
+    """The halving tree is invariant, bitwise, under any cyclic rotation of the C rank pairs
+    (pair c is combined with c + C/2 first, i.e. c XOR C/2, which commutes with rotation mod C);
+    the kernel relies on this to read chunks in a lane-rotated order.  Also within the
+    classical bound |phi - exact| <= gamma_{log2(C) + 3} sum |a b c|."""
+    rng = np.random.default_rng(R)
+    C = 1
+    while 2 * C < R:
+        C *= 2
+    for trial in range(50):
+        F = [rng.normal(size=(1, 2 * C)) * np.exp(rng.normal(0, 3, size=(1, 2 * C))) for _ in range(3)]
+        for f in F:
+            f[:, R:] = 0.0
+        base = _lv(oracle, *[f[:, :R] for f in F])
+        for rot in range(1, C):
+            perm = np.concatenate([np.arange(2 * ((c + rot) % C), 2 * ((c + rot) % C) + 2) for c in range(C)])
+            Fr = [f[:, perm] for f in F]        # width 2C: the padding zeros move with their pair
+            assert _lv(oracle, *Fr) == base
+        ex = sum(Fraction(float(F[0][0, k])) * Fraction(float(F[1][0, k])) * Fraction(float(F[2][0, k]))
+                 for k in range(R))
+        mag = float(np.sum(np.abs(F[0][0, :R] * F[1][0, :R] * F[2][0, :R])))
+        k = int(np.log2(C)) + 3
+        u = 2.0 ** -53
+        assert abs(float(Fraction(base) - ex)) <= k * u / (1 - k * u) * mag * (1 + 1e-12)
 
 
 def test_scorer_long_range_equals_dense_materialisation(oracle):
