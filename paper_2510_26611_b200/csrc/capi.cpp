@@ -309,6 +309,10 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     // S5-S7
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
                             prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep);
+    if (hd->R > (1 << 20)) {
+      set_err("compressed CP width " + std::to_string(hd->R) + " exceeds 2^20 (raise eps_compress or fix rank_R)");
+      return nullptr;
+    }
     // S8: short-range reference rows, a_k folded into S1 (Def. 2.1, A_0)
     const int ns = hd->n_sigma, Rs = hd->Rs;
     for (int a = 0; a < 3; ++a) hd->S[a].assign((size_t)(2 * ns + 1) * Rs, 0.0);

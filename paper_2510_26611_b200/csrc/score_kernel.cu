@@ -10,7 +10,8 @@
 // Arithmetic contract (mirrored by oracle/oracle_score.c):
 // every floating-point op of H1-H5 and H7 is an explicit round-to-nearest intrinsic (no FMA
 // contraction; the file is also compiled with -fmad=false), in the same order as the oracle:
-//   phi = 0; for k ascending: phi = phi + (F0[i0][k] * F1[i1][k]) * F2[i2][k]
+//   q_k = (F0[i0][k] * F1[i1][k]) * F2[i2][k]; rank pairs s_c = q_2c + q_2c+1 summed by a
+//   pairwise halving tree (reading A20)
 // Per-pose sums are double-double (Dekker TwoProduct + Knuth TwoSum), so the order in which
 // lanes accumulate and the reduction tree are free.
 //
@@ -20,7 +21,7 @@
 // chunks, padded or replicated to whole 128-byte bank lines.  Lane l of a warp reads the
 // chunks of its own row in the rotated order (c + (l & 7)) mod CHP, so the 8 lanes of every
 // quarter-warp hit 8 distinct bank groups whatever rows they gather (conflict-free LDS.128);
-// the products are then rotated back in registers (3 select stages) and summed in rank order.
+// the halving tree over rank pairs is invariant under that rotation, so no rotate-back is needed.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -128,36 +129,42 @@ __device__ __forceinline__ double long_phi(const double2* r0, const double2* r1,
     q[2 * c] = __dmul_rn(__dmul_rn(a.x, b.x), cc.x);
     q[2 * c + 1] = __dmul_rn(__dmul_rn(a.y, b.y), cc.y);
   }
-  // slot c holds chunk (c + rot) mod NS: rotate back so q[2L], q[2L+1] are ranks 2L, 2L+1
-  const int rot = G::REP ? (rho & (G::CH - 1)) : rho;
+  // O4 (A20): s_c = q_2c + q_2c+1, then the pairwise halving tree
+  // s_c = s_c + s_{c+m}, m = NS/2 .. 1.  Slot c holds pair (c + rot) mod NS; the tree pairs
+  // c with c + m (mod NS) at every level, so it is bitwise invariant under that rotation and
+  // the slots are summed as they were loaded.
+  double s[G::NS];
 #pragma unroll
-  for (int bit = 0; bit < 3; ++bit) {
-    if ((1 << bit) >= G::NS) break;
-    const bool sel = (rot >> bit) & 1;
-    const int sh = 1 << bit;
-    double t[2 * G::NS];
+  for (int c = 0; c < G::NS; ++c) s[c] = __dadd_rn(q[2 * c], q[2 * c + 1]);
 #pragma unroll
-    for (int i = 0; i < G::NS; ++i) {
-      const int j = (i - sh + G::NS) % G::NS;
-      t[2 * i] = sel ? q[2 * j] : q[2 * i];
-      t[2 * i + 1] = sel ? q[2 * j + 1] : q[2 * i + 1];
-    }
+  for (int m = G::NS / 2; m >= 1; m /= 2) {
 #pragma unroll
-    for (int i = 0; i < 2 * G::NS; ++i) q[i] = t[i];
+    for (int c = 0; c < m; ++c) s[c] = __dadd_rn(s[c], s[c + m]);
   }
-  double phi = 0.0;
-#pragma unroll
-  for (int i = 0; i < 2 * G::CH; ++i) phi = __dadd_rn(phi, q[i]);
-  return phi;
+  return s[0];
 }
 
-// O4 with a runtime R (generic widths, e.g. tolerance-mode builds): rows from L2
+// O4 with a runtime R (generic widths, e.g. tolerance-mode builds): rows from L2, the same
+// pairwise halving tree over rank pairs.  The tree is walked depth-first: its leaves in order
+// are the pairs c = bitrev(j), j = 0..C-1, merged with a binary-counter stack (depth log2 C).
 __device__ __forceinline__ double long_phi_rt(const double* r0, const double* r1, const double* r2,
                                               int R) {
-  double phi = 0.0;
-  for (int k = 0; k < R; ++k)
-    phi = __dadd_rn(phi, __dmul_rn(__dmul_rn(__ldg(r0 + k), __ldg(r1 + k)), __ldg(r2 + k)));
-  return phi;
+  int lg = 0;
+  while ((2 << lg) < R) ++lg;            // C = 2^lg pairs
+  const int C = 1 << lg;
+  double st[24];
+  int top = 0;
+  for (int j = 0; j < C; ++j) {
+    const int c = lg ? (int)(__brev((unsigned)j) >> (32 - lg)) : 0;
+    double q0 = 0.0, q1 = 0.0;
+    if (2 * c < R) q0 = __dmul_rn(__dmul_rn(__ldg(r0 + 2 * c), __ldg(r1 + 2 * c)), __ldg(r2 + 2 * c));
+    if (2 * c + 1 < R)
+      q1 = __dmul_rn(__dmul_rn(__ldg(r0 + 2 * c + 1), __ldg(r1 + 2 * c + 1)), __ldg(r2 + 2 * c + 1));
+    double v = __dadd_rn(q0, q1);
+    for (int t = j; t & 1; t >>= 1) v = __dadd_rn(st[--top], v);
+    st[top++] = v;
+  }
+  return st[0];
 }
 
 struct Window {
