@@ -55,7 +55,8 @@ void free_device(rs_handle* h) {
     if (p) cudaFree(p);
     p = nullptr;
   }
-  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_nb_rec, &h->d_memo}) {
+  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_nb_rec, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1],
+                   &h->d_Fw[2], &h->d_nb_range}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -97,6 +98,24 @@ int upload_handle(rs_handle* h) {
   if (int e = upload(&h->dmem[6], rec, &bytes)) return e;
   if (int e = upload(&h->dmem[7], ridx, &bytes)) return e;
   if (int e = upload(&h->dmem[8], h->cg.off, &bytes)) return e;
+  {
+    // per coarse cell (begin, count): one 8-byte load per ligand atom
+    const size_t nc = h->cg.off.size() - 1;
+    std::vector<int32_t> rng(2 * nc);
+    for (size_t c = 0; c < nc; ++c) {
+      rng[2 * c] = h->cg.off[c];
+      rng[2 * c + 1] = h->cg.off[c + 1] - h->cg.off[c];
+    }
+    if (int e = upload(&h->d_nb_range, rng, &bytes)) return e;
+  }
+  if (rs::window_row_chunks(h->R) > 0) {
+    // row-padded copy of the factors: the shared-memory window is staged by 1-D bulk copies
+    std::vector<double> packed;
+    for (int a = 0; a < 3; ++a) {
+      rs::pack_window_rows(h->F[a], h->n, h->R, packed);
+      if (int e = upload(&h->d_Fw[a], packed, &bytes)) return e;
+    }
+  }
   if (int e = upload(&h->d_nb_idx, h->cg.idx, &bytes)) return e;
   std::vector<int16_t> cell16(4 * h->cg.idx.size(), 0);
   for (size_t j = 0; j < h->cg.idx.size(); ++j)
@@ -143,6 +162,7 @@ rs::ScoreArgs base_args(const rs_handle* h) {
     a.nb_lo[i] = h->cg.lo[i];
     a.nb_dim[i] = h->cg.dim[i];
     a.t.F[i] = (const double*)h->dmem[i];
+    a.t.Fw[i] = (const double2*)h->d_Fw[i];
     a.t.S[i] = (const double*)h->dmem[3 + i];
   }
   a.t.rec = h->dmem[6];
@@ -152,10 +172,12 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.t.nb_cell = (const int16_t*)h->d_nb_cell;
   a.t.nb_rec = (const double*)h->d_nb_rec;
   a.t.short_memo = (const double*)h->d_memo;
+  a.t.nb_range = (const int2*)h->d_nb_range;
+  a.ns2 = (unsigned)((int64_t)h->n_sigma * h->n_sigma);
   {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
     const double t = h->prm.dmin_cap / h->h + std::sqrt(3.0) + 2.0;
-    a.vdw_cells2 = (int64_t)std::ceil(t * t);
+    a.vdw_cells2 = (unsigned)std::min(std::ceil(t * t), 4294967295.0);
   }
   a.rmax_hint = -1.0;
   return a;

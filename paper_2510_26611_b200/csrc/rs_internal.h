@@ -1,6 +1,8 @@
 // Internal declarations of librsdock (not part of the C ABI; see include/rs_dock.h).
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -61,6 +63,8 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
 
 struct DeviceTables {
   const double* F[3] = {nullptr, nullptr, nullptr};
+  const double2* Fw[3] = {nullptr, nullptr, nullptr};  // rows padded/replicated to CHP chunks
+  const int2* nb_range = nullptr;     // per coarse cell: (list begin, count)
   const double* S[3] = {nullptr, nullptr, nullptr};
   const void* rec = nullptr;      // double4 per protein atom: x, y, z, q
   const void* rec_idx = nullptr;  // int4 per protein atom: i0, i1, i2, 0
@@ -85,7 +89,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
   double* D;
   unsigned long long* invalid;   // may be null
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
-  int64_t vdw_cells2;            // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
+  unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
+  unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
 };
 
 // Fill the dense short-range memo table s(d0,d1,d2), d_a = 0..n_sigma, with the O5 chain.
@@ -96,6 +101,10 @@ int launch_fill_short_memo(const double* S0, const double* S1, const double* S2,
 // (if not null) is incremented by the number of kernels enqueued.
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
 const char* score_kernel_variant(int R);
+// Chunks (16 B) per row of the window copy of the factors for compiled width R (0: none), and
+// the host packing of that copy (rows padded with zeros or replicated to CHP chunks).
+int window_row_chunks(int R);
+void pack_window_rows(const std::vector<double>& F, int n, int R, std::vector<double>& out);
 
 }  // namespace rs
 
@@ -122,6 +131,8 @@ struct rs_handle {
   void* d_nb_cell = nullptr;
   void* d_nb_rec = nullptr;
   void* d_memo = nullptr;
+  void* d_Fw[3] = {nullptr, nullptr, nullptr};
+  void* d_nb_range = nullptr;
   int64_t device_bytes = 0;
   // staging for host-pointer calls
   std::mutex mtx;

@@ -2,7 +2,7 @@
 // Eq. (18), the RS entry formula and the vdW constraint
 // of Eq. (22).  Rows H1-H8 of SURVEY.md §8(a), in one pass:
 //   H1 quaternion -> rotation      H2 x' = R y + t           H3 snap to the cell grid
-//   H4 long-range CP gather + rank chain (rows of F_0, F_1, F_2 from a shared-memory window
+//   H4 long-range CP gather + rank sum (rows of F_0, F_1, F_2 from a shared-memory window
 //      or from L2)                  H5 short-range replicas of nearby protein atoms
 //   H6 vdW min distance over the same cell-list candidates
 //   H7 warp double-double reduction H8 one energy + one min distance per pose
@@ -13,20 +13,26 @@
 //   q_k = (F0[i0][k] * F1[i1][k]) * F2[i2][k]; rank pairs s_c = q_2c + q_2c+1 summed by a
 //   pairwise halving tree (reading A20)
 // Per-pose sums are double-double (Dekker TwoProduct + Knuth TwoSum), so the order in which
-// lanes accumulate and the reduction tree are free.
+// lanes accumulate and the reduction tree are free.  The snap (O3) is finished in integers
+// after the two fp64 ops that define it (ceil of a value in [0, n+1) is exact).
 //
-// Layout of the shared-memory window (design notes): a CTA scores a tile
-// of poses whose atoms fall inside per-axis row ranges [lo_a, hi_a]; those rows of the three
-// factor matrices are staged once per tile (reused across tiles when contained) as 16-byte
-// chunks, padded or replicated to whole 128-byte bank lines.  Lane l of a warp reads the
-// chunks of its own row in the rotated order (c + (l & 7)) mod CHP, so the 8 lanes of every
-// quarter-warp hit 8 distinct bank groups whatever rows they gather (conflict-free LDS.128);
-// the halving tree over rank pairs is invariant under that rotation, so no rotate-back is needed.
+// Work layout: persistent CTAs (one per SM) own contiguous pose ranges; a warp
+// scores one pose at a time (lanes over ligand atoms), taking poses from a per-tile queue.
+// A tile is the longest run of poses whose rows fit the shared-memory window (a block scan of
+// per-pose row bounds); the window's rows of the three factor matrices arrive by TMA bulk
+// copies (cp.async.bulk, mbarrier completion) from a row-padded device copy, with slack so that
+// the following tiles usually reuse them.  Rows are 16-byte chunks padded (R=12, 24) or
+// replicated (R=4, 8) to whole 128-byte lines; lane l reads the chunks of its own row in the
+// rotated order (c + (l & 7)) mod CHP, so the 8 lanes of every quarter-warp hit 8 distinct bank
+// groups whatever rows they gather (conflict-free LDS.128); the halving tree over rank pairs is
+// invariant under that rotation, so no rotate-back is needed.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdint>
+#include <vector>
 
 #include "rs_internal.h"
 
@@ -34,12 +40,15 @@ namespace rs {
 namespace {
 
 #ifndef RS_THREADS
-#define RS_THREADS 640
+#define RS_THREADS 512
+#endif
+#ifndef RS_TILE
+#define RS_TILE RS_THREADS
 #endif
 constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 8 * kWarps;        // poses per tile (upper bound)
-constexpr int kLigSmem = 256;            // ligand atoms staged in shared memory
+constexpr int kTile = RS_TILE;           // poses per tile (upper bound)
+static_assert(kTile <= kThreads, "one thread per pose of a tile");
 constexpr unsigned kFull = 0xffffffffu;
 
 template <int R>
@@ -58,14 +67,18 @@ __device__ __forceinline__ double2 ld2(const double2* p) {
   else return __ldg(p);
 }
 
-// O3: cell of coordinate x; -1 outside [-b, b]
-__device__ __forceinline__ int snap_dev(double x, double b, double inv_h, int n) {
-  if (!(x >= -b && x <= b)) return -1;
+// O3 validity: -b <= x <= b  <=>  |x| <= b (b > 0 finite), as an integer compare of the
+// magnitude bits (false for NaN and +-inf)
+__device__ __forceinline__ bool in_box(double x, unsigned long long bbits) {
+  return ((unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull) <= bbits;
+}
+
+// O3 cell of a valid coordinate: u = (x + b) * inv_h in [0, n(1+eps)]; i = clamp(ceil(u)-1)
+__device__ __forceinline__ int snap_dev(double x, double b, double inv_h, int nm1) {
   const double u = __dmul_rn(__dadd_rn(x, b), inv_h);
-  double c = __dsub_rn(ceil(u), 1.0);
-  c = fmax(c, 0.0);
-  c = fmin(c, (double)(n - 1));
-  return (int)c;
+  int c;
+  asm("cvt.rpi.s32.f64 %0, %1;" : "=r"(c) : "d"(u));
+  return min(max(c - 1, 0), nm1);
 }
 
 // O1: quaternion (w,x,y,z) -> R (row-major); false if |q|^2 is 0 or not finite
@@ -107,7 +120,7 @@ template <int R, bool SMEM>
 __device__ __forceinline__ double long_phi(const double2* r0, const double2* r1, const double2* r2,
                                            int rho) {
   using G = Geo<R>;
-  double q[2 * G::NS];
+  double s[G::NS];
 #pragma unroll
   for (int c = 0; c < G::NS; ++c) {
     const int ph = (c + rho) & (G::CHP - 1);
@@ -126,16 +139,10 @@ __device__ __forceinline__ double long_phi(const double2* r0, const double2* r1,
       b = ld2<SMEM>(r1 + src);
       cc = ld2<SMEM>(r2 + src);
     }
-    q[2 * c] = __dmul_rn(__dmul_rn(a.x, b.x), cc.x);
-    q[2 * c + 1] = __dmul_rn(__dmul_rn(a.y, b.y), cc.y);
+    s[c] = __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), cc.x), __dmul_rn(__dmul_rn(a.y, b.y), cc.y));
   }
-  // O4 (A20): s_c = q_2c + q_2c+1, then the pairwise halving tree
-  // s_c = s_c + s_{c+m}, m = NS/2 .. 1.  Slot c holds pair (c + rot) mod NS; the tree pairs
-  // c with c + m (mod NS) at every level, so it is bitwise invariant under that rotation and
-  // the slots are summed as they were loaded.
-  double s[G::NS];
-#pragma unroll
-  for (int c = 0; c < G::NS; ++c) s[c] = __dadd_rn(q[2 * c], q[2 * c + 1]);
+  // O4 (A20): slot c holds pair (c + rot) mod NS; the halving tree pairs c with
+  // c + m (mod NS) at every level, so it is bitwise invariant under that rotation.
 #pragma unroll
   for (int m = G::NS / 2; m >= 1; m /= 2) {
 #pragma unroll
@@ -167,26 +174,6 @@ __device__ __forceinline__ double long_phi_rt(const double* r0, const double* r1
   return st[0];
 }
 
-struct Window {
-  int lo[3], hi[3], base[3];   // staged rows [lo, hi] per axis, first smem row of each axis
-};
-
-// A tile's poses, decoded once by one thread each (H1): rotation, translation, validity.
-struct __align__(16) PoseStage {
-  double R[kTile][9];
-  double t[kTile][3];
-  int ok[kTile];
-};
-
-// Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
-struct __align__(16) PairStage {
-  double x[3][32];   // transformed coordinates x'
-  double z[32];      // charges
-  int4 cell[32];     // i0, i1, i2, list begin
-  int off[32];       // exclusive prefix of the candidate counts
-  int map[64];       // two rounds: candidate slot where an atom's segment starts -> atom lane
-};
-
 // L2 path of O4 for compile-time R, kept out of line (it is the rare path in window mode)
 template <int RT>
 __device__ __noinline__ double long_phi_global(const double* F0, const double* F1, const double* F2,
@@ -196,12 +183,55 @@ __device__ __noinline__ double long_phi_global(const double* F0, const double* F
                              (const double2*)(F2 + (size_t)i2 * RT), rho);
 }
 
+struct Window {
+  int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
+};
+
+struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
+  double m[12];
+};
+
+// Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
+struct __align__(16) PairStage {
+  double4 xz[32];    // transformed coordinates x' and charge
+  int4 cb[32];       // i0, i1, i2, (list begin - exclusive prefix of the counts)
+  int map[64];       // two rounds: candidate slot where an atom's segment starts -> atom lane
+};
+
+// ---- TMA bulk copy + mbarrier (window staging) ---------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // O5 value s(D): from the dense memo (filled by the same chain) or the chain itself
 __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2) {
   if (a.t.short_memo) {
     const int d = a.n_sigma + 1;
-    const int u0 = e0 < 0 ? -e0 : e0, u1 = e1 < 0 ? -e1 : e1, u2 = e2 < 0 ? -e2 : e2;
-    return __ldg(a.t.short_memo + ((size_t)u0 * d + u1) * d + u2);
+    return __ldg(a.t.short_memo + (abs(e0) * d + abs(e1)) * d + abs(e2));
   }
   const double* s0 = a.t.S[0] + (size_t)(e0 + a.n_sigma) * a.Rs;
   const double* s1 = a.t.S[1] + (size_t)(e1 + a.n_sigma) * a.Rs;
@@ -212,96 +242,107 @@ __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1
   return s;
 }
 
-// One candidate pair (atom `ow` of the pass, list entry j): O7 distance and O5 replica term.
-__device__ __forceinline__ void pair_term(const ScoreArgs& a, const PairStage& ps, int ow,
-                                          int4 oc, short4 mc, double2 xy, double2 zq,
-                                          int64_t ns2, double& hi, double& lo, double& best) {
+// One candidate pair (an atom of the pass with cell oc and coordinates/charge ox, list entry
+// with cell mc and record xy, zq): O7 distance and O5 replica term.  Cells are < 2^15, so the
+// squared integer offsets sum exactly in 32 unsigned bits.
+__device__ __forceinline__ void pair_term(const ScoreArgs& a, const int4 oc, const double4 ox,
+                                          short4 mc, double2 xy, double2 zq, double& hi,
+                                          double& lo, double& best) {
   const int e0 = oc.x - mc.x, e1 = oc.y - mc.y, e2 = oc.z - mc.z;
-  const int64_t dd = (int64_t)e0 * e0 + (int64_t)e1 * e1 + (int64_t)e2 * e2;
+  const unsigned dd = (unsigned)(e0 * e0) + (unsigned)(e1 * e1) + (unsigned)(e2 * e2);
   if (dd < a.vdw_cells2) {
-    const double dx0 = __dsub_rn(ps.x[0][ow], xy.x);
-    const double dx1 = __dsub_rn(ps.x[1][ow], xy.y);
-    const double dx2 = __dsub_rn(ps.x[2][ow], zq.x);
+    const double dx0 = __dsub_rn(ox.x, xy.x);
+    const double dx1 = __dsub_rn(ox.y, xy.y);
+    const double dx2 = __dsub_rn(ox.z, zq.x);
     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
     best = fmin(best, d2);
   }
-  if (dd <= ns2) {
+  if (dd <= a.ns2) {
     const double sv = short_value(a, e0, e1, e2);
-    dd_add_prod(hi, lo, ps.z[ow], __dmul_rn(zq.y, sv));
+    dd_add_prod(hi, lo, ox.w, __dmul_rn(zq.y, sv));
   }
 }
 
 // Score one pose with one warp.  RT > 0: compile-time width with an optional smem window.
 template <int RT>
-__device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const double* Rm,
-                                           const double* tv, bool ok, bool use_win,
-                                           const Window& W, const double2* win,
-                                           const double4* s_lig, bool lig_smem, int lane,
-                                           PairStage& ps) {
+__device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
+                                           bool ok, bool use_win, const Window& W,
+                                           const double2* win, const double4* s_lig, int lig_smem_n,
+                                           int lane, PairStage& ps) {
+  double Rm[9], tv[3];
+  {
+    const double2* m2 = reinterpret_cast<const double2*>(pr.m);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const double2 v = m2[i];
+      const int k0 = 2 * i, k1 = 2 * i + 1;
+      if (k0 < 9) Rm[k0] = v.x; else tv[k0 - 9] = v.x;
+      if (k1 < 9) Rm[k1] = v.y; else tv[k1 - 9] = v.y;
+    }
+  }
   double hi = 0.0, lo = 0.0, best = INFINITY;
   bool bad = !ok;
   const int rho = lane & 7;
-  const int64_t ns2 = (int64_t)a.n_sigma * a.n_sigma;
-  const int npass = ok ? (int)((a.L + 31) / 32) : 0;
+  const unsigned long long bbits = (unsigned long long)__double_as_longlong(a.b);
+  const int nm1 = a.n - 1;
+  const int npass = ok ? (a.L + 31) >> 5 : 0;
   const double2* nrec = (const double2*)a.t.nb_rec;
   const short4* ncell = reinterpret_cast<const short4*>(a.t.nb_cell);
+  const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   for (int pass = 0; pass < npass; ++pass) {
-    const int64_t l = (int64_t)pass * 32 + lane;
+    const int l = pass * 32 + lane;
     int cnt = 0, beg = 0, i0 = 0, i1 = 0, i2 = 0;
-    double xp[3] = {0.0, 0.0, 0.0}, z = 0.0;
+    double xp0 = 0.0, xp1 = 0.0, xp2 = 0.0, z = 0.0;
     if (l < a.L) {
       double y0, y1, y2;
-      if (lig_smem) {
+      if (l < lig_smem_n) {
         const double4 v = s_lig[l];
         y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
       } else {
-        y0 = __ldg(a.yl + 3 * l);
-        y1 = __ldg(a.yl + 3 * l + 1);
-        y2 = __ldg(a.yl + 3 * l + 2);
+        y0 = __ldg(a.yl + 3 * (int64_t)l);
+        y1 = __ldg(a.yl + 3 * (int64_t)l + 1);
+        y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
         z = __ldg(a.zl + l);
       }
       // H2 (O2)
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-        xp[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3 * r], y0), __dmul_rn(Rm[3 * r + 1], y1)),
-                                    __dmul_rn(Rm[3 * r + 2], y2)),
-                          tv[r]);
+      xp0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
+      xp1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
+      xp2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
       // H3 (O3)
-      i0 = snap_dev(xp[0], a.b, a.inv_h, a.n);
-      i1 = snap_dev(xp[1], a.b, a.inv_h, a.n);
-      i2 = snap_dev(xp[2], a.b, a.inv_h, a.n);
-      if ((i0 | i1 | i2) < 0) {
+      if (!(in_box(xp0, bbits) && in_box(xp1, bbits) && in_box(xp2, bbits))) {
         bad = true;
       } else {
+        i0 = snap_dev(xp0, a.b, a.inv_h, nm1);
+        i1 = snap_dev(xp1, a.b, a.inv_h, nm1);
+        i2 = snap_dev(xp2, a.b, a.inv_h, nm1);
 #if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
         // candidate range of the coarse cell containing i (cell lists cover every protein atom
-        // within max(D_cap, (n_sigma + sqrt 3) h) of any point of the cell); loads issued
-        // before H4 so their latency hides behind the gathers
-        const int cx = (i0 >> a.nb_shift) - a.nb_lo[0];
-        const int cy = (i1 >> a.nb_shift) - a.nb_lo[1];
-        const int cz = (i2 >> a.nb_shift) - a.nb_lo[2];
-        if (cx >= 0 && cx < a.nb_dim[0] && cy >= 0 && cy < a.nb_dim[1] && cz >= 0 &&
-            cz < a.nb_dim[2]) {
-          const int64_t cell = ((int64_t)cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz;
-          beg = __ldg(a.t.nb_off + cell);
-          cnt = __ldg(a.t.nb_off + cell + 1) - beg;
+        // that can matter to H5/H6 for any point of the cell); loaded before H4 so its latency
+        // hides behind the gathers
+        const unsigned cx = (unsigned)((i0 >> a.nb_shift) - a.nb_lo[0]);
+        const unsigned cy = (unsigned)((i1 >> a.nb_shift) - a.nb_lo[1]);
+        const unsigned cz = (unsigned)((i2 >> a.nb_shift) - a.nb_lo[2]);
+        if (cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
+          const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
+          beg = bc.x;
+          cnt = bc.y;
         }
 #endif
         // H4 (O4)
         double phi;
         if constexpr (RT > 0) {
           using G = Geo<RT>;
-          const bool inwin = use_win && i0 >= W.lo[0] && i0 <= W.hi[0] && i1 >= W.lo[1] &&
-                             i1 <= W.hi[1] && i2 >= W.lo[2] && i2 <= W.hi[2];
+          const bool inwin = use_win && (unsigned)(i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
+                             (unsigned)(i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
+                             (unsigned)(i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
 #if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
           if (inwin) {
             phi = z;
           } else
 #endif
           if (inwin) {
-            phi = long_phi<RT, true>(win + (size_t)(W.base[0] + i0 - W.lo[0]) * G::CHP,
-                                     win + (size_t)(W.base[1] + i1 - W.lo[1]) * G::CHP,
-                                     win + (size_t)(W.base[2] + i2 - W.lo[2]) * G::CHP, rho);
+            phi = long_phi<RT, true>(win + (i0 + W.off[0]) * G::CHP, win + (i1 + W.off[1]) * G::CHP,
+                                     win + (i2 + W.off[2]) * G::CHP, rho);
           } else {
             phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2, rho);
           }
@@ -317,8 +358,8 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       break;                      // the pose is invalid: NaN outputs, skip the rest
     }
     // H5 + H6 over the pass's (atom, candidate) pairs, flattened across the warp so every lane
-    // works on some pair in every round (the pose sums are order-free, O6/O7); two rounds per
-    // iteration keep two independent sets of loads in flight
+    // works on some pair in every round (the pose sums are order-free, O6/O7); two slots per
+    // lane and round keep two independent sets of loads in flight
     int inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -328,12 +369,8 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
     const int total = __shfl_sync(kFull, inc, 31);
     if (total == 0) continue;
     const int myoff = inc - cnt;
-    ps.x[0][lane] = xp[0];
-    ps.x[1][lane] = xp[1];
-    ps.x[2][lane] = xp[2];
-    ps.z[lane] = z;
-    ps.cell[lane] = make_int4(i0, i1, i2, beg);
-    ps.off[lane] = myoff;
+    ps.xz[lane] = make_double4(xp0, xp1, xp2, z);
+    ps.cb[lane] = make_int4(i0, i1, i2, beg - myoff);
     int carry = 0;
     for (int base = 0; base < total; base += 64) {
       const int rel = myoff - base;
@@ -343,37 +380,45 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       const unsigned m0 = __reduce_or_sync(kFull, (starts && rel < 32) ? (1u << rel) : 0u);
       const unsigned m1 = __reduce_or_sync(kFull, (starts && rel >= 32) ? (1u << (rel - 32)) : 0u);
       __syncwarp();
-      const unsigned long long m64 = ((unsigned long long)m1 << 32) | m0;
-      const unsigned long long below0 = m64 & (0xffffffffull >> (31 - lane));
-      const unsigned long long below1 = m64 & (0xffffffffffffffffull >> (31 - lane));
-      const int ow0 = below0 ? ps.map[63 - __clzll(below0)] : carry;
-      const int ow1 = below1 ? ps.map[63 - __clzll(below1)] : carry;
+      // owner of slot base + lane (+ 32): the last segment starting at or before it
+      const unsigned b0 = m0 & lanemask_le, b1 = m1 & lanemask_le;
+      const int ow0 = b0 ? ps.map[31 - __clz(b0)] : carry;
+      const int ow1 = b1 ? ps.map[63 - __clz(b1)] : (m0 ? ps.map[31 - __clz(m0)] : carry);
       carry = __shfl_sync(kFull, ow1, 31);
       const int k0 = base + lane, k1 = base + 32 + lane;
       int4 oc0 = make_int4(0, 0, 0, 0), oc1 = oc0;
       short4 mc0 = make_short4(0, 0, 0, 0), mc1 = mc0;
       double2 xy0 = make_double2(0.0, 0.0), zq0 = xy0, xy1 = xy0, zq1 = xy0;
       if (k0 < total) {
-        oc0 = ps.cell[ow0];
-        const int j = oc0.w + (k0 - ps.off[ow0]);
+        oc0 = ps.cb[ow0];
+        const int j = oc0.w + k0;
         mc0 = __ldg(ncell + j);
-        xy0 = ldg2(nrec + 2 * (size_t)j);
-        zq0 = ldg2(nrec + 2 * (size_t)j + 1);
+        xy0 = ldg2(nrec + 2 * j);
+        zq0 = ldg2(nrec + 2 * j + 1);
       }
       if (k1 < total) {
-        oc1 = ps.cell[ow1];
-        const int j = oc1.w + (k1 - ps.off[ow1]);
+        oc1 = ps.cb[ow1];
+        const int j = oc1.w + k1;
         mc1 = __ldg(ncell + j);
-        xy1 = ldg2(nrec + 2 * (size_t)j);
-        zq1 = ldg2(nrec + 2 * (size_t)j + 1);
+        xy1 = ldg2(nrec + 2 * j);
+        zq1 = ldg2(nrec + 2 * j + 1);
       }
-      if (k0 < total) pair_term(a, ps, ow0, oc0, mc0, xy0, zq0, ns2, hi, lo, best);
-      if (k1 < total) pair_term(a, ps, ow1, oc1, mc1, xy1, zq1, ns2, hi, lo, best);
+      if (k0 < total) pair_term(a, oc0, ps.xz[ow0], mc0, xy0, zq0, hi, lo, best);
+      if (k1 < total) pair_term(a, oc1, ps.xz[ow1], mc1, xy1, zq1, hi, lo, best);
     }
     __syncwarp();
   }
-  // H7
+  // H7: double-double butterfly (TwoSum is exact, so all lanes agree); min of d^2 >= +0 by its
+  // bit pattern (non-negative doubles order like their unsigned bits)
   bad = __any_sync(kFull, bad);
+  if (bad) {
+    if (lane == 0) {
+      a.E[p] = NAN;
+      a.D[p] = NAN;
+      if (a.invalid) atomicAdd(a.invalid, 1ull);
+    }
+    return;
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const double h2 = __shfl_xor_sync(kFull, hi, off);
@@ -383,69 +428,71 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
     const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
     hi = s;
     lo = __dadd_rn(__dadd_rn(lo, l2), e);
-    best = fmin(best, __shfl_xor_sync(kFull, best, off));
   }
+  const unsigned long long bb = (unsigned long long)__double_as_longlong(best);
+  const unsigned bhi = (unsigned)(bb >> 32);
+  const unsigned mhi = __reduce_min_sync(kFull, bhi);
+  const unsigned mlo = __reduce_min_sync(kFull, bhi == mhi ? (unsigned)bb : 0xffffffffu);
   // H8
   if (lane == 0) {
-    if (bad) {
-      a.E[p] = NAN;
-      a.D[p] = NAN;
-      if (a.invalid) atomicAdd(a.invalid, 1ull);
-    } else {
-      a.E[p] = __dadd_rn(hi, lo);
-      a.D[p] = best < a.dcap2 ? __dsqrt_rn(best) : INFINITY;
-    }
+    const double m = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+    a.E[p] = __dadd_rn(hi, lo);
+    a.D[p] = m < a.dcap2 ? __dsqrt_rn(m) : INFINITY;
   }
 }
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
                                                             int lig_smem_n) {
-  // dynamic shared memory: [PairStage x warps][PoseStage][ligand][factor-row window]
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairStage* s_ps = reinterpret_cast<PairStage*>(smem_raw);
-  PoseStage& s_pose = *reinterpret_cast<PoseStage*>(s_ps + kWarps);
-  double4* s_lig = reinterpret_cast<double4*>(&s_pose + 1);
-  double2* win = reinterpret_cast<double2*>(s_lig + lig_smem_n);
-  __shared__ double s_red[kWarps][6];
-  __shared__ int s_bad[kWarps];
-  __shared__ int s_win[7];       // lo[3], hi[3], fits
+  // dynamic shared memory: [factor-row window (128-B aligned)][PoseRec x kTile]
+  //                        [PairStage x warps][ligand double4 x lig_smem_n]
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
+  unsigned char* base = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+  double2* win = reinterpret_cast<double2*>(base);
+  PoseRec* s_pose = reinterpret_cast<PoseRec*>(base + (size_t)cap_rows * kChp * 16);
+  PairStage* s_ps = reinterpret_cast<PairStage*>(s_pose + kTile);
+  double4* s_lig = reinterpret_cast<double4*>(s_ps + kWarps);
+  __shared__ int s_ok[kTile];
+  __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
-  __shared__ double s_rmax2;
+  __shared__ int s_next, s_restaged;
+  __shared__ double s_rmax2[kWarps];
+  __shared__ __align__(8) uint64_t s_bar;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool lig_smem = a.L <= lig_smem_n;
   // ligand radius (body frame) and staging
   double r2 = 0.0;
-  for (int64_t l = tid; l < a.L; l += kThreads) {
-    const double y0 = __ldg(a.yl + 3 * l), y1 = __ldg(a.yl + 3 * l + 1), y2 = __ldg(a.yl + 3 * l + 2);
+  for (int l = tid; l < a.L; l += kThreads) {
+    const double y0 = __ldg(a.yl + 3 * (int64_t)l), y1 = __ldg(a.yl + 3 * (int64_t)l + 1),
+                 y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
     r2 = fmax(r2, y0 * y0 + y1 * y1 + y2 * y2);
-    if (lig_smem) s_lig[l] = make_double4(y0, y1, y2, __ldg(a.zl + l));
+    if (l < lig_smem_n) s_lig[l] = make_double4(y0, y1, y2, __ldg(a.zl + l));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) r2 = fmax(r2, __shfl_xor_sync(kFull, r2, off));
-  if (lane == 0) s_red[warp][0] = r2;
+  if (lane == 0) s_rmax2[warp] = r2;
   if (tid == 0) {
     s_cur.lo[0] = s_cur.lo[1] = s_cur.lo[2] = 1;
     s_cur.hi[0] = s_cur.hi[1] = s_cur.hi[2] = 0;   // empty
+    s_cur.off[0] = s_cur.off[1] = s_cur.off[2] = 0;
+    mbar_init(&s_bar);
   }
   __syncthreads();
-  if (tid == 0) {
-    double m = 0.0;
-    for (int w = 0; w < kWarps; ++w) m = fmax(m, s_red[w][0]);
-    s_rmax2 = m;
-  }
-  __syncthreads();
+  double rmax2 = 0.0;
+  for (int w = 0; w < kWarps; ++w) rmax2 = fmax(rmax2, s_rmax2[w]);
   // slack: |R y| <= |y| (1 + 1e-15) plus two cells for the snap rounding and the clamp
-  const double rb = sqrt(s_rmax2) * (1.0 + 1e-12) + 2.0 * a.h;
+  const double rb = sqrt(rmax2) * (1.0 + 1e-12) + 2.0 * a.h;
   const bool window_mode = RT > 0 && cap_rows > 0;
+  unsigned phase = 0;
 
   const int64_t p_begin = a.P * (int64_t)blockIdx.x / gridDim.x;
   const int64_t p_end = a.P * (int64_t)(blockIdx.x + 1) / gridDim.x;
   int64_t p = p_begin;
   while (p < p_end) {
     int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
-    // H1 for the tile: one thread per pose
+    // H1 for the tile: one thread per pose; per-pose window row bounds
+    int wlo[3] = {INT_MAX, INT_MAX, INT_MAX}, whi[3] = {INT_MIN, INT_MIN, INT_MIN}, wbad = 0;
     if (tid < T) {
       const double* pq = a.poses + 7 * (p + tid);
       double qv[7];
@@ -453,120 +500,123 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
       double Rm[9];
       const bool ok = quat_rot_dev(qv, Rm);
+      PoseRec& pr = s_pose[tid];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) s_pose.R[tid][i] = Rm[i];
+      for (int i = 0; i < 9; ++i) pr.m[i] = Rm[i];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) s_pose.t[tid][i] = qv[4 + i];
-      s_pose.ok[tid] = ok ? 1 : 0;
+      for (int i = 0; i < 3; ++i) pr.m[9 + i] = qv[4 + i];
+      s_ok[tid] = ok ? 1 : 0;
+      if (window_mode) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double t = qv[4 + r];
+          if (!isfinite(t)) wbad = 1;
+          const double f0 = floor((t - rb + a.b) * a.inv_h) - 1.0;
+          const double f1 = floor((t + rb + a.b) * a.inv_h) + 1.0;
+          wlo[r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
+          whi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
+        }
+      }
     }
     bool fits = false;
     if (window_mode) {
-      for (;;) {
-        // block min/max of the tile's translations (staged above)
-        __syncthreads();
-        double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-        int badt = 0;
-        if (tid < T) {
+      // inclusive block scan of the row bounds over the tile's poses: the tile becomes the
+      // longest prefix whose cumulative window fits cap_rows
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int v[7];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          v[r] = __shfl_up_sync(kFull, wlo[r], o);
+          v[3 + r] = __shfl_up_sync(kFull, whi[r], o);
+        }
+        v[6] = __shfl_up_sync(kFull, wbad, o);
+        if (lane >= o) {
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
-            const double t = s_pose.t[tid][r];
-            if (!isfinite(t)) badt = 1;
-            mn[r] = t;
-            mx[r] = t;
+            wlo[r] = min(wlo[r], v[r]);
+            whi[r] = max(whi[r], v[3 + r]);
           }
+          wbad |= v[6];
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            mn[r] = fmin(mn[r], __shfl_xor_sync(kFull, mn[r], off));
-            mx[r] = fmax(mx[r], __shfl_xor_sync(kFull, mx[r], off));
-          }
-        }
-        badt = __any_sync(kFull, badt);
-        if (lane == 0) {
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            s_red[warp][r] = mn[r];
-            s_red[warp][3 + r] = mx[r];
-          }
-          s_bad[warp] = badt;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          int bad = 0, rows = 0, lo[3], hi[3];
-          for (int r = 0; r < 3; ++r) {
-            double m0 = INFINITY, m1 = -INFINITY;
-            for (int w = 0; w < kWarps; ++w) {
-              m0 = fmin(m0, s_red[w][r]);
-              m1 = fmax(m1, s_red[w][3 + r]);
-              bad |= s_bad[w];
-            }
-            const double f0 = floor((m0 - rb + a.b) * a.inv_h) - 1.0;
-            const double f1 = floor((m1 + rb + a.b) * a.inv_h) + 1.0;
-            lo[r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
-            hi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
-            rows += hi[r] - lo[r] + 1;
-          }
-          const int fts = (!bad && rows <= cap_rows) ? 1 : 0;
-          for (int r = 0; r < 3; ++r) {
-            s_win[r] = lo[r];
-            s_win[3 + r] = hi[r];
-          }
-          s_win[6] = fts;
-        }
-        __syncthreads();
-        fits = s_win[6] != 0;
-        if (fits || T == 1) break;
-        T = (T + 1) / 2;           // the staged poses [0, T) stay valid
       }
-      if (fits) {
+      if (lane == 31) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          s_wred[warp][r] = wlo[r];
+          s_wred[warp][3 + r] = whi[r];
+        }
+        s_wred[warp][6] = wbad;
+      }
+      __syncthreads();
+      for (int w = 0; w < warp; ++w) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          wlo[r] = min(wlo[r], s_wred[w][r]);
+          whi[r] = max(whi[r], s_wred[w][3 + r]);
+        }
+        wbad |= s_wred[w][6];
+      }
+      int rows = 0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) rows += whi[r] - wlo[r] + 1;
+      const bool fit_me = tid < T && !wbad && rows <= cap_rows;
+      // fit_me is monotone in tid (cumulative bounds), so the first Tfit poses form the tile
+      const int Tfit = __syncthreads_count(fit_me);
+      fits = Tfit > 0;
+      T = fits ? Tfit : 1;         // a single pose whose rows do not fit takes the L2 path
+      // the tile's last thread owns the tile's bounds: it restages the window if needed
+      if (tid == T - 1) {
+        int rs = 0;
         bool contained = true;
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
-          contained = contained && s_cur.lo[r] <= s_win[r] && s_win[3 + r] <= s_cur.hi[r];
-        if (!contained) {
-          if (tid == 0) {
-            int rows = 0;
-            for (int r = 0; r < 3; ++r) rows += s_win[3 + r] - s_win[r] + 1;
-            const int extra = (cap_rows - rows) / 3;
-            int base = 0;
-            for (int r = 0; r < 3; ++r) {
-              int lo = max(0, s_win[r] - extra / 2);
-              int hi = min(a.n - 1, s_win[3 + r] + (extra - extra / 2));
-              s_cur.lo[r] = lo;
-              s_cur.hi[r] = hi;
-              s_cur.base[r] = base;
-              base += hi - lo + 1;
-            }
+        for (int r = 0; r < 3; ++r) contained = contained && s_cur.lo[r] <= wlo[r] && whi[r] <= s_cur.hi[r];
+        if (fits && !contained) {
+          const int extra = (cap_rows - rows) / 3;
+          int row0 = 0;
+          unsigned bytes = 0;
+          int lo_[3], hi_[3];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            lo_[r] = max(0, wlo[r] - extra / 2);
+            hi_[r] = min(a.n - 1, whi[r] + (extra - extra / 2));
+            bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16;
           }
-          __syncthreads();
-          if constexpr (RT > 0) {
-            using G = Geo<RT>;
-            const int rows0 = s_cur.hi[0] - s_cur.lo[0] + 1, rows1 = s_cur.hi[1] - s_cur.lo[1] + 1;
-            const int total = s_cur.base[2] + s_cur.hi[2] - s_cur.lo[2] + 1;
-            for (int idx = tid; idx < total * G::CHP; idx += kThreads) {
-              const int row = idx / G::CHP, ph = idx - row * G::CHP;
-              const int ax = row < rows0 ? 0 : (row < rows0 + rows1 ? 1 : 2);
-              const int grow = s_cur.lo[ax] + row - s_cur.base[ax];
-              double2 v = make_double2(0.0, 0.0);
-              const int src = G::REP ? (ph & (G::CH - 1)) : ph;
-              if (G::REP || ph < G::CH) v = ldg2((const double2*)(a.t.F[ax] + (size_t)grow * RT) + src);
-              win[idx] = v;
-            }
+          // the window was last read through the generic proxy, before the previous barrier
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&s_bar, bytes);
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            s_cur.lo[r] = lo_[r];
+            s_cur.hi[r] = hi_[r];
+            s_cur.off[r] = row0 - lo_[r];
+            tma_load_1d(win + (size_t)row0 * kChp, a.t.Fw[r] + (size_t)lo_[r] * kChp,
+                        (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
+            row0 += hi_[r] - lo_[r] + 1;
           }
+          rs = 1;
         }
+        s_restaged = rs;
+        s_next = 0;
+      }
+    } else {
+      if (tid == 0) {
+        s_restaged = 0;
+        s_next = 0;
       }
     }
     __syncthreads();
+    if (s_restaged) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1;
+    }
     const Window W = s_cur;
-    for (int s = warp; s < T; s += kWarps) {
-      double Rm[9], tv[3];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Rm[i] = s_pose.R[s][i];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) tv[i] = s_pose.t[s][i];
-      score_pose<RT>(a, p + s, Rm, tv, s_pose.ok[s] != 0, fits, W, win, s_lig, lig_smem, lane,
+    for (;;) {
+      int s = 0;
+      if (lane == 0) s = atomicAdd(&s_next, 1);
+      s = __shfl_sync(kFull, s, 0);
+      if (s >= T) break;
+      score_pose<RT>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, win, s_lig, lig_smem_n, lane,
                      s_ps[warp]);
     }
     __syncthreads();
@@ -596,21 +646,23 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
     dc.attr_set[slot] = true;
   }
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  const int lig_n = (int)std::min<int64_t>(a.L, kLigSmem);
-  const size_t lig_b = (size_t)lig_n * sizeof(double4) + sizeof(PairStage) * kWarps + sizeof(PoseStage);
-  size_t dyn = lig_b;
+  const size_t fixed = 128 + sizeof(PoseRec) * kTile + sizeof(PairStage) * kWarps;
+  const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
+  const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
   int cap_rows = 0;
-  if (RT > 0 && window_mode) {
-    const size_t avail = (size_t)dc.max_dyn[slot] > lig_b ? (size_t)dc.max_dyn[slot] - lig_b : 0;
-    cap_rows = (int)(avail / (16 * kChp));
+  if (RT > 0 && window_mode && a.t.Fw[0]) {
+    cap_rows = (int)std::min<size_t>((avail - lig_res) / (16 * kChp), (1u << 20) / (16 * kChp) - 1);
     if (a.rmax_hint >= 0) {
       // leave the rest of the 228 KB to L1 (cell lists, records, memo): ~1.15x what one
       // translation's window needs
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
       cap_rows = std::min(cap_rows, (int)std::max(64.0, 1.15 * need));
     }
-    dyn = lig_b + (size_t)cap_rows * 16 * kChp;
   }
+  const size_t win_b = (size_t)cap_rows * 16 * kChp;
+  const int64_t lig_fit = (int64_t)((avail - std::min(avail, win_b)) / sizeof(double4));
+  const int lig_n = (int)std::min<int64_t>(a.L, cap_rows > 0 ? std::min<int64_t>(lig_fit, 256) : lig_fit);
+  const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
   const int64_t tiles = (a.P + kTile - 1) / kTile;
   int grid = (int)std::min<int64_t>(tiles, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
@@ -653,6 +705,33 @@ const char* score_kernel_variant(int R) {
   }
 }
 
+int window_row_chunks(int R) {
+  switch (R) {
+    case 4: return Geo<4>::CHP;
+    case 8: return Geo<8>::CHP;
+    case 12: return Geo<12>::CHP;
+    case 16: return Geo<16>::CHP;
+    case 24: return Geo<24>::CHP;
+    case 32: return Geo<32>::CHP;
+    default: return 0;
+  }
+}
+
+void pack_window_rows(const std::vector<double>& F, int n, int R, std::vector<double>& out) {
+  const int chp = window_row_chunks(R);
+  out.assign((size_t)n * chp * 2, 0.0);
+  if (chp == 0) return;
+  const int ch = R / 2;
+  const bool rep = (ch == 1 || ch == 2 || ch == 4);   // replicated widths repeat the row
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < chp; ++c) {
+      const int src = rep ? (c % ch) : c;
+      if (src >= ch) continue;                           // padded widths: zero chunks
+      out[((size_t)i * chp + c) * 2] = F[(size_t)i * R + 2 * src];
+      out[((size_t)i * chp + c) * 2 + 1] = F[(size_t)i * R + 2 * src + 1];
+    }
+}
+
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   if (a.P <= 0) return 0;
   DevCache& dc = g_dev[device & 63];
@@ -666,7 +745,7 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   if (a.rmax_hint >= 0) {
     const double rows = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 4.0);
     const double row_b = 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
-    window_mode = rows * row_b <= 0.9 * double(dc.smem_optin);
+    window_mode = rows * row_b <= 0.75 * double(dc.smem_optin);
   }
   int e;
   switch (a.R) {
