@@ -55,8 +55,10 @@ void free_device(rs_handle* h) {
     if (p) cudaFree(p);
     p = nullptr;
   }
-  for (void** p : {&h->d_nb_idx, &h->d_nb_cell, &h->d_nb_rec, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1],
-                   &h->d_Fw[2], &h->d_nb_range}) {
+  if (h->d_work) cudaFree(h->d_work);
+  h->d_work = nullptr;
+  for (void** p : {&h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
+                   &h->d_nb_range}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -86,20 +88,39 @@ int upload_handle(rs_handle* h) {
     if (int e = upload(&h->dmem[a], h->F[a], &bytes)) return e;
     if (int e = upload(&h->dmem[3 + a], h->S[a], &bytes)) return e;
   }
-  std::vector<double> rec(4 * (size_t)h->M);
-  std::vector<int32_t> ridx(4 * (size_t)h->M, 0);
-  for (int64_t m = 0; m < h->M; ++m) {
-    for (int a = 0; a < 3; ++a) {
-      rec[4 * m + a] = h->xyz[3 * m + a];
-      ridx[4 * m + a] = h->cells[3 * m + a];
-    }
-    rec[4 * m + 3] = h->z[m];
-  }
-  if (int e = upload(&h->dmem[6], rec, &bytes)) return e;
-  if (int e = upload(&h->dmem[7], ridx, &bytes)) return e;
-  if (int e = upload(&h->dmem[8], h->cg.off, &bytes)) return e;
   {
-    // per coarse cell (begin, count): one 8-byte load per ligand atom
+    // S9 on the device.  Protein atoms are renumbered in coarse-cell order (spatially sorted,
+    // so the few atoms near one pose tile share cache lines); each list entry carries the
+    // atom's fine cell (for the integer prefilter) and its sorted index:
+    //   nb_range[c] = (first entry, count)       int2 per coarse cell
+    //   nb_ent[j]   = (i0 | i1 << 16, i2, k, 0)  int4 per list entry
+    //   prec[k]     = (x, y, z, q)               double4 per protein atom
+    const int64_t M = h->M;
+    std::vector<int64_t> key(M);
+    std::vector<int32_t> order(M), rank(M);
+    for (int64_t m = 0; m < M; ++m) {
+      int64_t k = 0;
+      for (int a = 0; a < 3; ++a) k = k * 65536 + (h->cells[3 * m + a] >> h->cg.shift);
+      key[m] = k;
+      order[m] = (int32_t)m;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+    for (int64_t k = 0; k < M; ++k) rank[order[k]] = (int32_t)k;
+    std::vector<double> prec(4 * (size_t)M);
+    for (int64_t k = 0; k < M; ++k) {
+      const size_t m = (size_t)order[k];
+      for (int a = 0; a < 3; ++a) prec[4 * k + a] = h->xyz[3 * m + a];
+      prec[4 * k + 3] = h->z[m];
+    }
+    if (int e = upload(&h->d_prec, prec, &bytes)) return e;
+    std::vector<int32_t> ent(4 * h->cg.idx.size(), 0);
+    for (size_t j = 0; j < h->cg.idx.size(); ++j) {
+      const size_t m = (size_t)h->cg.idx[j];
+      ent[4 * j] = (int32_t)((uint32_t)h->cells[3 * m] | ((uint32_t)h->cells[3 * m + 1] << 16));
+      ent[4 * j + 1] = h->cells[3 * m + 2];
+      ent[4 * j + 2] = rank[m];
+    }
+    if (int e = upload(&h->d_nb_ent, ent, &bytes)) return e;
     const size_t nc = h->cg.off.size() - 1;
     std::vector<int32_t> rng(2 * nc);
     for (size_t c = 0; c < nc; ++c) {
@@ -116,21 +137,8 @@ int upload_handle(rs_handle* h) {
       if (int e = upload(&h->d_Fw[a], packed, &bytes)) return e;
     }
   }
-  if (int e = upload(&h->d_nb_idx, h->cg.idx, &bytes)) return e;
-  std::vector<int16_t> cell16(4 * h->cg.idx.size(), 0);
-  for (size_t j = 0; j < h->cg.idx.size(); ++j)
-    for (int a = 0; a < 3; ++a) cell16[4 * j + a] = (int16_t)h->cells[3 * (size_t)h->cg.idx[j] + a];
-  if (int e = upload(&h->d_nb_cell, cell16, &bytes)) return e;
-  {
-    // candidate records inline in list order (no index indirection on the device)
-    std::vector<double> nrec(4 * h->cg.idx.size());
-    for (size_t j = 0; j < h->cg.idx.size(); ++j) {
-      const size_t m = (size_t)h->cg.idx[j];
-      for (int a = 0; a < 3; ++a) nrec[4 * j + a] = h->xyz[3 * m + a];
-      nrec[4 * j + 3] = h->z[m];
-    }
-    if (int e = upload(&h->d_nb_rec, nrec, &bytes)) return e;
-  }
+  CUDA_TRY(cudaMalloc(&h->d_work, rs::kWorkSlots * sizeof(int)), RS_E_NOMEM);
+  CUDA_TRY(cudaMemset(h->d_work, 0, rs::kWorkSlots * sizeof(int)), RS_E_CUDA);
   // dense memo of the short-range chain over |D_a| <= n_sigma (filled on the device by the same
   // O5 op sequence), when it is small enough to stay L2-resident
   const double memo_b = 8.0 * std::pow(double(h->n_sigma + 1), 3.0);
@@ -165,12 +173,8 @@ rs::ScoreArgs base_args(const rs_handle* h) {
     a.t.Fw[i] = (const double2*)h->d_Fw[i];
     a.t.S[i] = (const double*)h->dmem[3 + i];
   }
-  a.t.rec = h->dmem[6];
-  a.t.rec_idx = h->dmem[7];
-  a.t.nb_off = (const int32_t*)h->dmem[8];
-  a.t.nb_idx = (const int32_t*)h->d_nb_idx;
-  a.t.nb_cell = (const int16_t*)h->d_nb_cell;
-  a.t.nb_rec = (const double*)h->d_nb_rec;
+  a.t.nb_ent = (const int4*)h->d_nb_ent;
+  a.t.prec = (const double4*)h->d_prec;
   a.t.short_memo = (const double*)h->d_memo;
   a.t.nb_range = (const int2*)h->d_nb_range;
   a.ns2 = (unsigned)((int64_t)h->n_sigma * h->n_sigma);
@@ -463,6 +467,8 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
     std::lock_guard<std::mutex> lock(h->mtx);
     a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, true);
   }
+  a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
+  CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st), RS_E_CUDA);
   int e = rs::launch_score(a, st, h->device, nullptr);
   if (e != 0) {
     set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
@@ -538,6 +544,8 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     a.E = e_dev ? energies_out + off : d_E[s];
     a.D = d_dev ? mindist_out + off : d_D[s];
     a.invalid = d_cnt + s;
+    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
+    CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st[s]), RS_E_CUDA);
     int e = rs::launch_score(a, st[s], h->device, nullptr);
     if (e != 0) {
       set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -66,12 +67,8 @@ struct DeviceTables {
   const double2* Fw[3] = {nullptr, nullptr, nullptr};  // rows padded/replicated to CHP chunks
   const int2* nb_range = nullptr;     // per coarse cell: (list begin, count)
   const double* S[3] = {nullptr, nullptr, nullptr};
-  const void* rec = nullptr;      // double4 per protein atom: x, y, z, q
-  const void* rec_idx = nullptr;  // int4 per protein atom: i0, i1, i2, 0
-  const int32_t* nb_off = nullptr;
-  const int32_t* nb_idx = nullptr;
-  const int16_t* nb_cell = nullptr;   // per list entry: the atom's cell (i0, i1, i2, 0) as int16
-  const double* nb_rec = nullptr;     // per list entry: the atom's (x, y, z, q)
+  const int4* nb_ent = nullptr;       // per list entry: (i0 | i1 << 16, i2, sorted atom, 0)
+  const double4* prec = nullptr;      // per sorted protein atom: (x, y, z, q)
   const double* short_memo = nullptr; // s(|D0|,|D1|,|D2|) for |D_a| <= n_sigma, or null
 };
 
@@ -88,6 +85,7 @@ struct ScoreArgs {               // one launch of the scoring kernel
   double* E;
   double* D;
   unsigned long long* invalid;   // may be null
+  int* work;                     // zeroed work counter (dynamic pose chunks), stream-ordered
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
@@ -96,6 +94,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
 // Fill the dense short-range memo table s(d0,d1,d2), d_a = 0..n_sigma, with the O5 chain.
 int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
                            int n_sigma, double* out, void* stream);
+
+constexpr int kWorkSlots = 64;   // concurrent launches per handle with distinct work counters
 
 // Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
 // (if not null) is incremented by the number of kernels enqueued.
@@ -126,13 +126,14 @@ struct rs_handle {
   // device
   bool on_device = false;
   int device = 0;
-  void* dmem[9] = {nullptr};           // F1..3, S1..3, rec, rec_idx, nb_off
-  void* d_nb_idx = nullptr;
-  void* d_nb_cell = nullptr;
-  void* d_nb_rec = nullptr;
+  void* dmem[6] = {nullptr};           // F1..3, S1..3
+  void* d_nb_ent = nullptr;
+  void* d_prec = nullptr;
   void* d_memo = nullptr;
   void* d_Fw[3] = {nullptr, nullptr, nullptr};
   void* d_nb_range = nullptr;
+  int* d_work = nullptr;               // kWorkSlots zeroed-per-launch work counters
+  std::atomic<unsigned> work_slot{0};
   int64_t device_bytes = 0;
   // staging for host-pointer calls
   std::mutex mtx;

@@ -22,10 +22,10 @@
 // per-pose row bounds); the window's rows of the three factor matrices arrive by TMA bulk
 // copies (cp.async.bulk, mbarrier completion) from a row-padded device copy, with slack so that
 // the following tiles usually reuse them.  Rows are 16-byte chunks padded (R=12, 24) or
-// replicated (R=4, 8) to whole 128-byte lines; lane l reads the chunks of its own row in the
-// rotated order (c + (l & 7)) mod CHP, so the 8 lanes of every quarter-warp hit 8 distinct bank
-// groups whatever rows they gather (conflict-free LDS.128); the halving tree over rank pairs is
-// invariant under that rotation, so no rotate-back is needed.
+// replicated (R=4, 8) to whole 128-byte lines; lane l reads chunk c ^ (l & 7) of its own row in
+// slot c, so the 8 lanes of every quarter-warp hit 8 distinct bank groups whatever rows they
+// gather (conflict-free LDS.128); the halving tree over rank pairs is invariant under that
+// relabelling, so no un-permute is needed.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,11 +43,18 @@ namespace {
 #define RS_THREADS 512
 #endif
 #ifndef RS_TILE
-#define RS_TILE RS_THREADS
+#define RS_TILE 128
+#endif
+#ifndef RS_CHUNK
+#define RS_CHUNK 256
+#endif
+#ifndef RS_WIN_SLACK
+#define RS_WIN_SLACK 1.03
 #endif
 constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = RS_TILE;           // poses per tile (upper bound)
+constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 static_assert(kTile <= kThreads, "one thread per pose of a tile");
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -60,12 +67,6 @@ struct Geo {
 };
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
-
-template <bool SMEM>
-__device__ __forceinline__ double2 ld2(const double2* p) {
-  if constexpr (SMEM) return *p;
-  else return __ldg(p);
-}
 
 // O3 validity: -b <= x <= b  <=>  |x| <= b (b > 0 finite), as an integer compare of the
 // magnitude bits (false for NaN and +-inf)
@@ -115,40 +116,62 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
   lo = __dadd_rn(lo, __dadd_rn(err, e));
 }
 
-// O4 with compile-time R, rows given as 16-byte chunk pointers (smem window or global rows)
-template <int R, bool SMEM>
-__device__ __forceinline__ double long_phi(const double2* r0, const double2* r1, const double2* r2,
-                                           int rho) {
-  using G = Geo<R>;
-  double s[G::NS];
+__device__ __forceinline__ double2 lds2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+// One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
+__device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
+  return __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), c.x), __dmul_rn(__dmul_rn(a.y, b.y), c.y));
+}
+
+// O4 halving tree over NS pair sums (A20): s_c = s_c + s_{c+m}, m = NS/2 .. 1
+template <int NS>
+__device__ __forceinline__ double halving_tree(double* s) {
 #pragma unroll
-  for (int c = 0; c < G::NS; ++c) {
-    const int ph = (c + rho) & (G::CHP - 1);
-    int src;
-    bool valid;
-    if constexpr (G::REP) {
-      src = SMEM ? ph : (ph & (G::CH - 1));
-      valid = true;
-    } else {
-      src = ph;
-      valid = ph < G::CH;
-    }
-    double2 a = make_double2(0.0, 0.0), b = a, cc = a;
-    if (valid) {
-      a = ld2<SMEM>(r0 + src);
-      b = ld2<SMEM>(r1 + src);
-      cc = ld2<SMEM>(r2 + src);
-    }
-    s[c] = __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), cc.x), __dmul_rn(__dmul_rn(a.y, b.y), cc.y));
-  }
-  // O4 (A20): slot c holds pair (c + rot) mod NS; the halving tree pairs c with
-  // c + m (mod NS) at every level, so it is bitwise invariant under that rotation.
-#pragma unroll
-  for (int m = G::NS / 2; m >= 1; m /= 2) {
+  for (int m = NS / 2; m >= 1; m /= 2) {
 #pragma unroll
     for (int c = 0; c < m; ++c) s[c] = __dadd_rn(s[c], s[c + m]);
   }
   return s[0];
+}
+
+// O4 with compile-time R from the shared-memory window.  rK = byte address of row K (aligned
+// to the row size).  Slot c reads physical chunk c ^ rho (rho = lane & 7): the 8 lanes of a
+// quarter-warp hit 8 distinct 16-byte bank groups whatever rows they read.  Physical chunk p
+// holds pair p (padded widths: zero beyond CH; replicated widths: pair p mod CH), so slot c
+// holds pair (c ^ rho) mod NS, and the halving tree, which combines c with c ^ m at every
+// level, is bitwise invariant under that relabelling.
+template <int R>
+__device__ __forceinline__ double long_phi_smem(unsigned r0, unsigned r1, unsigned r2, int rho) {
+  using G = Geo<R>;
+  const unsigned x = (unsigned)rho << 4;
+  r0 |= x;
+  r1 |= x;
+  r2 |= x;
+  double s[G::NS];
+#pragma unroll
+  for (int c = 0; c < G::NS; ++c) {
+    const unsigned o = (unsigned)c << 4;
+    s[c] = pair_prod(lds2(r0 ^ o), lds2(r1 ^ o), lds2(r2 ^ o));
+  }
+  return halving_tree<G::NS>(s);
+}
+
+// O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
+template <int R>
+__device__ __forceinline__ double long_phi_l2(const double2* r0, const double2* r1, const double2* r2) {
+  using G = Geo<R>;
+  constexpr int C = G::REP ? G::CH : G::CHP;
+  double s[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    if (c < G::CH) s[c] = pair_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
+    else s[c] = 0.0;
+  }
+  return halving_tree<C>(s);
 }
 
 // O4 with a runtime R (generic widths, e.g. tolerance-mode builds): rows from L2, the same
@@ -177,10 +200,9 @@ __device__ __forceinline__ double long_phi_rt(const double* r0, const double* r1
 // L2 path of O4 for compile-time R, kept out of line (it is the rare path in window mode)
 template <int RT>
 __device__ __noinline__ double long_phi_global(const double* F0, const double* F1, const double* F2,
-                                               int i0, int i1, int i2, int rho) {
-  return long_phi<RT, false>((const double2*)(F0 + (size_t)i0 * RT),
-                             (const double2*)(F1 + (size_t)i1 * RT),
-                             (const double2*)(F2 + (size_t)i2 * RT), rho);
+                                               int i0, int i1, int i2) {
+  return long_phi_l2<RT>((const double2*)(F0 + (size_t)i0 * RT), (const double2*)(F1 + (size_t)i1 * RT),
+                         (const double2*)(F2 + (size_t)i2 * RT));
 }
 
 struct Window {
@@ -192,10 +214,11 @@ struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
 };
 
 // Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
+template <int NA>
 struct __align__(16) PairStage {
-  double4 xz[32];    // transformed coordinates x' and charge
-  int4 cb[32];       // i0, i1, i2, (list begin - exclusive prefix of the counts)
-  int map[64];       // two rounds: candidate slot where an atom's segment starts -> atom lane
+  double4 xz[32 * NA];  // transformed coordinates x' and charge (slot 32 u + lane)
+  int4 cb[32 * NA];     // i0, i1, i2, (list begin - start of the atom's candidate segment)
+  int map[64];          // two rounds: candidate slot where an atom's segment starts -> atom slot
 };
 
 // ---- TMA bulk copy + mbarrier (window staging) ---------------------------------------------
@@ -242,14 +265,17 @@ __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1
   return s;
 }
 
-// One candidate pair (an atom of the pass with cell oc and coordinates/charge ox, list entry
-// with cell mc and record xy, zq): O7 distance and O5 replica term.  Cells are < 2^15, so the
-// squared integer offsets sum exactly in 32 unsigned bits.
-__device__ __forceinline__ void pair_term(const ScoreArgs& a, const int4 oc, const double4 ox,
-                                          short4 mc, double2 xy, double2 zq, double& hi,
-                                          double& lo, double& best) {
-  const int e0 = oc.x - mc.x, e1 = oc.y - mc.y, e2 = oc.z - mc.z;
-  const unsigned dd = (unsigned)(e0 * e0) + (unsigned)(e1 * e1) + (unsigned)(e2 * e2);
+// One candidate pair: an atom of the pass (cell oc, coordinates and charge ox) and a list entry
+// en = (i0 | i1 << 16, i2, sorted atom k).  O7 distance when the integer prefilter admits it,
+// O5 replica term inside the n_sigma ball.  Cells are < 2^15, so the squared integer offsets sum
+// exactly in 32 unsigned bits.
+__device__ __forceinline__ unsigned pair_dd(const int4 oc, const int4 en) {
+  const int e0 = oc.x - (en.x & 0xffff), e1 = oc.y - (int)((unsigned)en.x >> 16), e2 = oc.z - en.y;
+  return (unsigned)(e0 * e0) + (unsigned)(e1 * e1) + (unsigned)(e2 * e2);
+}
+__device__ __forceinline__ void pair_term(const ScoreArgs& a, const double4 ox, unsigned dd,
+                                          double sv, double2 xy, double2 zq, double& hi, double& lo,
+                                          double& best) {
   if (dd < a.vdw_cells2) {
     const double dx0 = __dsub_rn(ox.x, xy.x);
     const double dx1 = __dsub_rn(ox.y, xy.y);
@@ -257,18 +283,118 @@ __device__ __forceinline__ void pair_term(const ScoreArgs& a, const int4 oc, con
     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
     best = fmin(best, d2);
   }
-  if (dd <= a.ns2) {
-    const double sv = short_value(a, e0, e1, e2);
-    dd_add_prod(hi, lo, ox.w, __dmul_rn(zq.y, sv));
-  }
+  if (dd <= a.ns2) dd_add_prod(hi, lo, ox.w, __dmul_rn(zq.y, sv));
 }
 
-// Score one pose with one warp.  RT > 0: compile-time width with an optional smem window.
+// O5 value for a pair inside the n_sigma ball (issued as soon as the offset is known)
+__device__ __forceinline__ double pair_short(const ScoreArgs& a, const int4 oc, const int4 en) {
+#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 8)
+  return 1.0;
+#else
+  return short_value(a, oc.x - (en.x & 0xffff), oc.y - (int)((unsigned)en.x >> 16), oc.z - en.y);
+#endif
+}
+
+// Per-atom state of one pass slot (H2/H3 output and the atom's candidate-list range)
+struct AtomState {
+  double x0, x1, x2, z;
+  int i0, i1, i2, beg, cnt;
+};
+
+// H2-H4 for ligand atom l of one pose: transform, snap, candidate range, long-range value
+// (accumulated into (hi, lo)).  bad is set if the atom leaves the box (O8).
 template <int RT>
+__device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
+                                           const double* tv, bool use_win, const Window& W,
+                                           unsigned win_u32, const double4* s_lig, int lig_smem_n,
+                                           int rho, unsigned long long bbits, AtomState& st,
+                                           double& hi, double& lo, bool& bad) {
+  st.x0 = st.x1 = st.x2 = st.z = 0.0;
+  st.i0 = st.i1 = st.i2 = st.beg = st.cnt = 0;
+  if (l >= a.L) return;
+  double y0, y1, y2;
+  if (l < lig_smem_n) {
+    const double4 v = s_lig[l];
+    y0 = v.x; y1 = v.y; y2 = v.z; st.z = v.w;
+  } else {
+    y0 = __ldg(a.yl + 3 * (int64_t)l);
+    y1 = __ldg(a.yl + 3 * (int64_t)l + 1);
+    y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
+    st.z = __ldg(a.zl + l);
+  }
+  // H2 (O2)
+  st.x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
+  st.x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
+  st.x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
+  // H3 (O3)
+  if (!(in_box(st.x0, bbits) && in_box(st.x1, bbits) && in_box(st.x2, bbits))) {
+    bad = true;
+    return;
+  }
+  const int nm1 = a.n - 1;
+  const int i0 = snap_dev(st.x0, a.b, a.inv_h, nm1);
+  const int i1 = snap_dev(st.x1, a.b, a.inv_h, nm1);
+  const int i2 = snap_dev(st.x2, a.b, a.inv_h, nm1);
+  st.i0 = i0;
+  st.i1 = i1;
+  st.i2 = i2;
+#if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
+  // candidate range of the coarse cell containing i (cell lists cover every protein atom that can
+  // matter to H5/H6 for any point of the cell); loaded before H4 so its latency hides behind it
+  {
+    const unsigned cx = (unsigned)((i0 >> a.nb_shift) - a.nb_lo[0]);
+    const unsigned cy = (unsigned)((i1 >> a.nb_shift) - a.nb_lo[1]);
+    const unsigned cz = (unsigned)((i2 >> a.nb_shift) - a.nb_lo[2]);
+    if (cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
+      const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
+      st.beg = bc.x;
+      st.cnt = bc.y;
+    }
+  }
+#endif
+  // H4 (O4)
+  double phi;
+  if constexpr (RT > 0) {
+    using G = Geo<RT>;
+    const bool inwin = use_win && (unsigned)(i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
+                       (unsigned)(i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
+                       (unsigned)(i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
+#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
+    if (inwin) {
+      phi = st.z;
+    } else
+#endif
+    if (inwin) {
+      constexpr unsigned kRow = 16u * G::CHP;
+      phi = long_phi_smem<RT>(win_u32 + (unsigned)(i0 + W.off[0]) * kRow,
+                              win_u32 + (unsigned)(i1 + W.off[1]) * kRow,
+                              win_u32 + (unsigned)(i2 + W.off[2]) * kRow, rho);
+    } else {
+      phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2);
+    }
+  } else {
+    phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
+                      a.t.F[2] + (size_t)i2 * a.R, a.R);
+  }
+  dd_add_prod(hi, lo, st.z, phi);
+}
+
+// (hi, lo) += (h2, l2) exactly up to the final lo rounding (TwoSum on the high parts)
+__device__ __forceinline__ void dd_merge(double& hi, double& lo, double h2, double l2) {
+  const double s = __dadd_rn(hi, h2);
+  const double bb = __dsub_rn(s, hi);
+  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
+  hi = s;
+  lo = __dadd_rn(__dadd_rn(lo, l2), e);
+}
+
+// Score one pose with one warp: lanes over ligand atoms, NA atoms per lane and pass (NA = 2
+// gives every lane two independent dependency chains and halves the per-pass overheads).
+template <int RT, int NA>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
-                                           const double2* win, const double4* s_lig, int lig_smem_n,
-                                           int lane, PairStage& ps) {
+                                           unsigned win_u32, const double4* s_lig, int lig_smem_n,
+                                           int lane, PairStage<NA>& ps) {
   double Rm[9], tv[3];
   {
     const double2* m2 = reinterpret_cast<const double2*>(pr.m);
@@ -280,79 +406,21 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       if (k1 < 9) Rm[k1] = v.y; else tv[k1 - 9] = v.y;
     }
   }
-  double hi = 0.0, lo = 0.0, best = INFINITY;
+  double hi[NA], lo[NA], best = INFINITY;
+#pragma unroll
+  for (int u = 0; u < NA; ++u) hi[u] = lo[u] = 0.0;
   bool bad = !ok;
   const int rho = lane & 7;
   const unsigned long long bbits = (unsigned long long)__double_as_longlong(a.b);
-  const int nm1 = a.n - 1;
-  const int npass = ok ? (a.L + 31) >> 5 : 0;
-  const double2* nrec = (const double2*)a.t.nb_rec;
-  const short4* ncell = reinterpret_cast<const short4*>(a.t.nb_cell);
+  const int L = ok ? a.L : 0;
+  const double2* prec = reinterpret_cast<const double2*>(a.t.prec);
   const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
-  for (int pass = 0; pass < npass; ++pass) {
-    const int l = pass * 32 + lane;
-    int cnt = 0, beg = 0, i0 = 0, i1 = 0, i2 = 0;
-    double xp0 = 0.0, xp1 = 0.0, xp2 = 0.0, z = 0.0;
-    if (l < a.L) {
-      double y0, y1, y2;
-      if (l < lig_smem_n) {
-        const double4 v = s_lig[l];
-        y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
-      } else {
-        y0 = __ldg(a.yl + 3 * (int64_t)l);
-        y1 = __ldg(a.yl + 3 * (int64_t)l + 1);
-        y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
-        z = __ldg(a.zl + l);
-      }
-      // H2 (O2)
-      xp0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
-      xp1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
-      xp2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
-      // H3 (O3)
-      if (!(in_box(xp0, bbits) && in_box(xp1, bbits) && in_box(xp2, bbits))) {
-        bad = true;
-      } else {
-        i0 = snap_dev(xp0, a.b, a.inv_h, nm1);
-        i1 = snap_dev(xp1, a.b, a.inv_h, nm1);
-        i2 = snap_dev(xp2, a.b, a.inv_h, nm1);
-#if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
-        // candidate range of the coarse cell containing i (cell lists cover every protein atom
-        // that can matter to H5/H6 for any point of the cell); loaded before H4 so its latency
-        // hides behind the gathers
-        const unsigned cx = (unsigned)((i0 >> a.nb_shift) - a.nb_lo[0]);
-        const unsigned cy = (unsigned)((i1 >> a.nb_shift) - a.nb_lo[1]);
-        const unsigned cz = (unsigned)((i2 >> a.nb_shift) - a.nb_lo[2]);
-        if (cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
-          const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
-          beg = bc.x;
-          cnt = bc.y;
-        }
-#endif
-        // H4 (O4)
-        double phi;
-        if constexpr (RT > 0) {
-          using G = Geo<RT>;
-          const bool inwin = use_win && (unsigned)(i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
-                             (unsigned)(i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
-                             (unsigned)(i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
-#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
-          if (inwin) {
-            phi = z;
-          } else
-#endif
-          if (inwin) {
-            phi = long_phi<RT, true>(win + (i0 + W.off[0]) * G::CHP, win + (i1 + W.off[1]) * G::CHP,
-                                     win + (i2 + W.off[2]) * G::CHP, rho);
-          } else {
-            phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2, rho);
-          }
-        } else {
-          phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
-                            a.t.F[2] + (size_t)i2 * a.R, a.R);
-        }
-        dd_add_prod(hi, lo, z, phi);
-      }
-    }
+  for (int l0 = 0; l0 < L; l0 += 32 * NA) {
+    AtomState st[NA];
+#pragma unroll
+    for (int u = 0; u < NA; ++u)
+      atom_stage<RT>(a, l0 + 32 * u + lane, Rm, tv, use_win, W, win_u32, s_lig, lig_smem_n, rho,
+                     bbits, st[u], hi[u], lo[u], bad);
     if (__any_sync(kFull, bad)) {
       bad = true;
       break;                      // the pose is invalid: NaN outputs, skip the rest
@@ -360,25 +428,43 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
     // H5 + H6 over the pass's (atom, candidate) pairs, flattened across the warp so every lane
     // works on some pair in every round (the pose sums are order-free, O6/O7); two slots per
     // lane and round keep two independent sets of loads in flight
-    int inc = cnt;
+    int cl = 0;
+#pragma unroll
+    for (int u = 0; u < NA; ++u) cl += st[u].cnt;
+    if (__ballot_sync(kFull, cl > 0) == 0) continue;
+    int inc = cl;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(kFull, inc, o);
       if (lane >= o) inc += v;
     }
     const int total = __shfl_sync(kFull, inc, 31);
-    if (total == 0) continue;
-    const int myoff = inc - cnt;
-    ps.xz[lane] = make_double4(xp0, xp1, xp2, z);
-    ps.cb[lane] = make_int4(i0, i1, i2, beg - myoff);
+    int seg[NA];
+    {
+      int s0 = inc - cl;
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        seg[u] = s0;
+        ps.xz[32 * u + lane] = make_double4(st[u].x0, st[u].x1, st[u].x2, st[u].z);
+        ps.cb[32 * u + lane] = make_int4(st[u].i0, st[u].i1, st[u].i2, st[u].beg - s0);
+        s0 += st[u].cnt;
+      }
+    }
     int carry = 0;
     for (int base = 0; base < total; base += 64) {
-      const int rel = myoff - base;
-      const bool starts = cnt > 0 && rel >= 0 && rel < 64;
+      unsigned m0 = 0, m1 = 0;
       __syncwarp();
-      if (starts) ps.map[rel] = lane;
-      const unsigned m0 = __reduce_or_sync(kFull, (starts && rel < 32) ? (1u << rel) : 0u);
-      const unsigned m1 = __reduce_or_sync(kFull, (starts && rel >= 32) ? (1u << (rel - 32)) : 0u);
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        const int rel = seg[u] - base;
+        if (st[u].cnt > 0 && rel >= 0 && rel < 64) {
+          ps.map[rel] = 32 * u + lane;
+          if (rel < 32) m0 |= 1u << rel;
+          else m1 |= 1u << (rel - 32);
+        }
+      }
+      m0 = __reduce_or_sync(kFull, m0);
+      m1 = __reduce_or_sync(kFull, m1);
       __syncwarp();
       // owner of slot base + lane (+ 32): the last segment starting at or before it
       const unsigned b0 = m0 & lanemask_le, b1 = m1 & lanemask_le;
@@ -386,25 +472,33 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       const int ow1 = b1 ? ps.map[63 - __clz(b1)] : (m0 ? ps.map[31 - __clz(m0)] : carry);
       carry = __shfl_sync(kFull, ow1, 31);
       const int k0 = base + lane, k1 = base + 32 + lane;
-      int4 oc0 = make_int4(0, 0, 0, 0), oc1 = oc0;
-      short4 mc0 = make_short4(0, 0, 0, 0), mc1 = mc0;
-      double2 xy0 = make_double2(0.0, 0.0), zq0 = xy0, xy1 = xy0, zq1 = xy0;
+      int4 oc0 = make_int4(0, 0, 0, 0), oc1 = oc0, en0 = oc0, en1 = oc0;
       if (k0 < total) {
         oc0 = ps.cb[ow0];
-        const int j = oc0.w + k0;
-        mc0 = __ldg(ncell + j);
-        xy0 = ldg2(nrec + 2 * j);
-        zq0 = ldg2(nrec + 2 * j + 1);
+        en0 = __ldg(a.t.nb_ent + oc0.w + k0);
       }
       if (k1 < total) {
         oc1 = ps.cb[ow1];
-        const int j = oc1.w + k1;
-        mc1 = __ldg(ncell + j);
-        xy1 = ldg2(nrec + 2 * j);
-        zq1 = ldg2(nrec + 2 * j + 1);
+        en1 = __ldg(a.t.nb_ent + oc1.w + k1);
       }
-      if (k0 < total) pair_term(a, oc0, ps.xz[ow0], mc0, xy0, zq0, hi, lo, best);
-      if (k1 < total) pair_term(a, oc1, ps.xz[ow1], mc1, xy1, zq1, hi, lo, best);
+      const unsigned dd0 = k0 < total ? pair_dd(oc0, en0) : 0xffffffffu;
+      const unsigned dd1 = k1 < total ? pair_dd(oc1, en1) : 0xffffffffu;
+      const bool s0 = dd0 <= a.ns2, s1 = dd1 <= a.ns2;
+      const bool n0 = s0 || dd0 < a.vdw_cells2, n1 = s1 || dd1 < a.vdw_cells2;
+      // loads of this round, all independent: memo values, then records
+      const double sv0 = s0 ? pair_short(a, oc0, en0) : 0.0;
+      const double sv1 = s1 ? pair_short(a, oc1, en1) : 0.0;
+      double2 xy0 = make_double2(0.0, 0.0), zq0 = xy0, xy1 = xy0, zq1 = xy0;
+      if (n0) {
+        xy0 = ldg2(prec + 2 * en0.z);
+        zq0 = ldg2(prec + 2 * en0.z + 1);
+      }
+      if (n1) {
+        xy1 = ldg2(prec + 2 * en1.z);
+        zq1 = ldg2(prec + 2 * en1.z + 1);
+      }
+      if (n0) pair_term(a, ps.xz[ow0], dd0, sv0, xy0, zq0, hi[0], lo[0], best);
+      if (n1) pair_term(a, ps.xz[ow1], dd1, sv1, xy1, zq1, hi[NA - 1], lo[NA - 1], best);
     }
     __syncwarp();
   }
@@ -419,15 +513,14 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
     }
     return;
   }
+  double H = hi[0], Lo = lo[0];
+#pragma unroll
+  for (int u = 1; u < NA; ++u) dd_merge(H, Lo, hi[u], lo[u]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    const double h2 = __shfl_xor_sync(kFull, hi, off);
-    const double l2 = __shfl_xor_sync(kFull, lo, off);
-    const double s = __dadd_rn(hi, h2);
-    const double bb = __dsub_rn(s, hi);
-    const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
-    hi = s;
-    lo = __dadd_rn(__dadd_rn(lo, l2), e);
+    const double h2 = __shfl_xor_sync(kFull, H, off);
+    const double l2 = __shfl_xor_sync(kFull, Lo, off);
+    dd_merge(H, Lo, h2, l2);
   }
   const unsigned long long bb = (unsigned long long)__double_as_longlong(best);
   const unsigned bhi = (unsigned)(bb >> 32);
@@ -436,27 +529,27 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   // H8
   if (lane == 0) {
     const double m = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-    a.E[p] = __dadd_rn(hi, lo);
+    a.E[p] = __dadd_rn(H, Lo);
     a.D[p] = m < a.dcap2 ? __dsqrt_rn(m) : INFINITY;
   }
 }
 
-template <int RT>
+template <int RT, int NA>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
                                                             int lig_smem_n) {
-  // dynamic shared memory: [factor-row window (128-B aligned)][PoseRec x kTile]
+  // dynamic shared memory: [factor-row window (256-B aligned)][PoseRec x kTile]
   //                        [PairStage x warps][ligand double4 x lig_smem_n]
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  unsigned char* base = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+  unsigned char* base = smem_raw + ((256 - (smem_u32(smem_raw) & 255)) & 255);
   double2* win = reinterpret_cast<double2*>(base);
   PoseRec* s_pose = reinterpret_cast<PoseRec*>(base + (size_t)cap_rows * kChp * 16);
-  PairStage* s_ps = reinterpret_cast<PairStage*>(s_pose + kTile);
+  PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(s_pose + kTile);
   double4* s_lig = reinterpret_cast<double4*>(s_ps + kWarps);
   __shared__ int s_ok[kTile];
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
-  __shared__ int s_next, s_restaged;
+  __shared__ int s_next, s_restaged, s_chunk;
   __shared__ double s_rmax2[kWarps];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -486,187 +579,195 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   const bool window_mode = RT > 0 && cap_rows > 0;
   unsigned phase = 0;
 
-  const int64_t p_begin = a.P * (int64_t)blockIdx.x / gridDim.x;
-  const int64_t p_end = a.P * (int64_t)(blockIdx.x + 1) / gridDim.x;
-  int64_t p = p_begin;
-  while (p < p_end) {
-    int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
-    // H1 for the tile: one thread per pose; per-pose window row bounds
-    int wlo[3] = {INT_MAX, INT_MAX, INT_MAX}, whi[3] = {INT_MIN, INT_MIN, INT_MIN}, wbad = 0;
-    if (tid < T) {
-      const double* pq = a.poses + 7 * (p + tid);
-      double qv[7];
+  // dynamic chunks of kChunk consecutive poses (a global work counter): the neighbour work per
+  // pose varies by an order of magnitude between translations, so static ranges leave the
+  // busiest SM 2-3x behind the mean
+  for (;;) {
+    if (tid == 0) s_chunk = atomicAdd(a.work, 1);
+    __syncthreads();
+    const int64_t c0 = (int64_t)s_chunk * kChunk;
+    if (c0 >= a.P) break;
+    const int64_t p_end = c0 + kChunk < a.P ? c0 + kChunk : a.P;
+    int64_t p = c0;
+    while (p < p_end) {
+      int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
+      // H1 for the tile: one thread per pose; per-pose window row bounds
+      int wlo[3] = {INT_MAX, INT_MAX, INT_MAX}, whi[3] = {INT_MIN, INT_MIN, INT_MIN}, wbad = 0;
+      if (tid < T) {
+        const double* pq = a.poses + 7 * (p + tid);
+        double qv[7];
 #pragma unroll
-      for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
-      double Rm[9];
-      const bool ok = quat_rot_dev(qv, Rm);
-      PoseRec& pr = s_pose[tid];
+        for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
+        double Rm[9];
+        const bool ok = quat_rot_dev(qv, Rm);
+        PoseRec& pr = s_pose[tid];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) pr.m[i] = Rm[i];
+        for (int i = 0; i < 9; ++i) pr.m[i] = Rm[i];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) pr.m[9 + i] = qv[4 + i];
-      s_ok[tid] = ok ? 1 : 0;
-      if (window_mode) {
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const double t = qv[4 + r];
-          if (!isfinite(t)) wbad = 1;
-          const double f0 = floor((t - rb + a.b) * a.inv_h) - 1.0;
-          const double f1 = floor((t + rb + a.b) * a.inv_h) + 1.0;
-          wlo[r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
-          whi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
-        }
-      }
-    }
-    bool fits = false;
-    if (window_mode) {
-      // inclusive block scan of the row bounds over the tile's poses: the tile becomes the
-      // longest prefix whose cumulative window fits cap_rows
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int v[7];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          v[r] = __shfl_up_sync(kFull, wlo[r], o);
-          v[3 + r] = __shfl_up_sync(kFull, whi[r], o);
-        }
-        v[6] = __shfl_up_sync(kFull, wbad, o);
-        if (lane >= o) {
+        for (int i = 0; i < 3; ++i) pr.m[9 + i] = qv[4 + i];
+        s_ok[tid] = ok ? 1 : 0;
+        if (window_mode) {
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
-            wlo[r] = min(wlo[r], v[r]);
-            whi[r] = max(whi[r], v[3 + r]);
+            const double t = qv[4 + r];
+            if (!isfinite(t)) wbad = 1;
+            const double f0 = floor((t - rb + a.b) * a.inv_h) - 1.0;
+            const double f1 = floor((t + rb + a.b) * a.inv_h) + 1.0;
+            wlo[r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
+            whi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
           }
-          wbad |= v[6];
         }
       }
-      if (lane == 31) {
+      bool fits = false;
+      if (window_mode) {
+        // inclusive block scan of the row bounds over the tile's poses: the tile becomes the
+        // longest prefix whose cumulative window fits cap_rows
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          s_wred[warp][r] = wlo[r];
-          s_wred[warp][3 + r] = whi[r];
+        for (int o = 1; o < 32; o <<= 1) {
+          int v[7];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            v[r] = __shfl_up_sync(kFull, wlo[r], o);
+            v[3 + r] = __shfl_up_sync(kFull, whi[r], o);
+          }
+          v[6] = __shfl_up_sync(kFull, wbad, o);
+          if (lane >= o) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              wlo[r] = min(wlo[r], v[r]);
+              whi[r] = max(whi[r], v[3 + r]);
+            }
+            wbad |= v[6];
+          }
         }
-        s_wred[warp][6] = wbad;
+        if (lane == 31) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            s_wred[warp][r] = wlo[r];
+            s_wred[warp][3 + r] = whi[r];
+          }
+          s_wred[warp][6] = wbad;
+        }
+        __syncthreads();
+        for (int w = 0; w < warp; ++w) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            wlo[r] = min(wlo[r], s_wred[w][r]);
+            whi[r] = max(whi[r], s_wred[w][3 + r]);
+          }
+          wbad |= s_wred[w][6];
+        }
+        int rows = 0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) rows += whi[r] - wlo[r] + 1;
+        const bool fit_me = tid < T && !wbad && rows <= cap_rows;
+        // fit_me is monotone in tid (cumulative bounds), so the first Tfit poses form the tile
+        const int Tfit = __syncthreads_count(fit_me);
+        fits = Tfit > 0;
+        T = fits ? Tfit : 1;         // a single pose whose rows do not fit takes the L2 path
+        // the tile's last thread owns the tile's bounds: it restages the window if needed
+        if (tid == T - 1) {
+          int rs = 0;
+          bool contained = true;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) contained = contained && s_cur.lo[r] <= wlo[r] && whi[r] <= s_cur.hi[r];
+          if (fits && !contained) {
+            const int extra = (cap_rows - rows) / 3;
+            int row0 = 0;
+            unsigned bytes = 0;
+            int lo_[3], hi_[3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              lo_[r] = max(0, wlo[r] - extra / 2);
+              hi_[r] = min(a.n - 1, whi[r] + (extra - extra / 2));
+              bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16;
+            }
+            // the window was last read through the generic proxy, before the previous barrier
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&s_bar, bytes);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              s_cur.lo[r] = lo_[r];
+              s_cur.hi[r] = hi_[r];
+              s_cur.off[r] = row0 - lo_[r];
+              tma_load_1d(win + (size_t)row0 * kChp, a.t.Fw[r] + (size_t)lo_[r] * kChp,
+                          (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
+              row0 += hi_[r] - lo_[r] + 1;
+            }
+            rs = 1;
+          }
+          s_restaged = rs;
+          s_next = 0;
+        }
+      } else {
+        if (tid == 0) {
+          s_restaged = 0;
+          s_next = 0;
+        }
       }
       __syncthreads();
-      for (int w = 0; w < warp; ++w) {
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          wlo[r] = min(wlo[r], s_wred[w][r]);
-          whi[r] = max(whi[r], s_wred[w][3 + r]);
-        }
-        wbad |= s_wred[w][6];
+      if (s_restaged) {
+        mbar_wait(&s_bar, phase);
+        phase ^= 1;
       }
-      int rows = 0;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) rows += whi[r] - wlo[r] + 1;
-      const bool fit_me = tid < T && !wbad && rows <= cap_rows;
-      // fit_me is monotone in tid (cumulative bounds), so the first Tfit poses form the tile
-      const int Tfit = __syncthreads_count(fit_me);
-      fits = Tfit > 0;
-      T = fits ? Tfit : 1;         // a single pose whose rows do not fit takes the L2 path
-      // the tile's last thread owns the tile's bounds: it restages the window if needed
-      if (tid == T - 1) {
-        int rs = 0;
-        bool contained = true;
-#pragma unroll
-        for (int r = 0; r < 3; ++r) contained = contained && s_cur.lo[r] <= wlo[r] && whi[r] <= s_cur.hi[r];
-        if (fits && !contained) {
-          const int extra = (cap_rows - rows) / 3;
-          int row0 = 0;
-          unsigned bytes = 0;
-          int lo_[3], hi_[3];
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            lo_[r] = max(0, wlo[r] - extra / 2);
-            hi_[r] = min(a.n - 1, whi[r] + (extra - extra / 2));
-            bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16;
-          }
-          // the window was last read through the generic proxy, before the previous barrier
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&s_bar, bytes);
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            s_cur.lo[r] = lo_[r];
-            s_cur.hi[r] = hi_[r];
-            s_cur.off[r] = row0 - lo_[r];
-            tma_load_1d(win + (size_t)row0 * kChp, a.t.Fw[r] + (size_t)lo_[r] * kChp,
-                        (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
-            row0 += hi_[r] - lo_[r] + 1;
-          }
-          rs = 1;
-        }
-        s_restaged = rs;
-        s_next = 0;
+      const Window W = s_cur;
+      for (;;) {
+        int s = 0;
+        if (lane == 0) s = atomicAdd(&s_next, 1);
+        s = __shfl_sync(kFull, s, 0);
+        if (s >= T) break;
+        score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, smem_u32(win), s_lig, lig_smem_n,
+                       lane, s_ps[warp]);
       }
-    } else {
-      if (tid == 0) {
-        s_restaged = 0;
-        s_next = 0;
-      }
+      __syncthreads();
+      p += T;
     }
-    __syncthreads();
-    if (s_restaged) {
-      mbar_wait(&s_bar, phase);
-      phase ^= 1;
-    }
-    const Window W = s_cur;
-    for (;;) {
-      int s = 0;
-      if (lane == 0) s = atomicAdd(&s_next, 1);
-      s = __shfl_sync(kFull, s, 0);
-      if (s >= T) break;
-      score_pose<RT>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, win, s_lig, lig_smem_n, lane,
-                     s_ps[warp]);
-    }
-    __syncthreads();
-    p += T;
   }
 }
 
 struct DevCache {
   int sms = 0;
   int smem_optin = 0;
-  bool attr_set[8] = {false};
-  int max_dyn[8] = {0};
+  bool attr_set[16] = {false};
+  int max_dyn[16] = {0};
 };
 DevCache g_dev[64];
 
-template <int RT>
+template <int RT, int NA>
 int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window_mode) {
   DevCache& dc = g_dev[dev & 63];
   if (!dc.attr_set[slot]) {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT>);
+    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT, NA>);
     if (e != cudaSuccess) return (int)e;
     dc.max_dyn[slot] = dc.smem_optin - (int)fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(score_kernel<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(score_kernel<RT, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dc.max_dyn[slot]);
     if (e != cudaSuccess) return (int)e;
     dc.attr_set[slot] = true;
   }
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  const size_t fixed = 128 + sizeof(PoseRec) * kTile + sizeof(PairStage) * kWarps;
+  const size_t fixed = 256 + sizeof(PoseRec) * kTile + sizeof(PairStage<NA>) * kWarps;
   const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
   const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
   int cap_rows = 0;
   if (RT > 0 && window_mode && a.t.Fw[0]) {
     cap_rows = (int)std::min<size_t>((avail - lig_res) / (16 * kChp), (1u << 20) / (16 * kChp) - 1);
     if (a.rmax_hint >= 0) {
-      // leave the rest of the 228 KB to L1 (cell lists, records, memo): ~1.15x what one
-      // translation's window needs
+      // leave the rest of the 228 KB to L1 (cell lists, records, memo): what one
+      // translation's window needs plus RS_WIN_SLACK
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
-      cap_rows = std::min(cap_rows, (int)std::max(64.0, 1.15 * need));
+      cap_rows = std::min(cap_rows, (int)std::max(64.0, RS_WIN_SLACK * need));
     }
   }
   const size_t win_b = (size_t)cap_rows * 16 * kChp;
   const int64_t lig_fit = (int64_t)((avail - std::min(avail, win_b)) / sizeof(double4));
   const int lig_n = (int)std::min<int64_t>(a.L, cap_rows > 0 ? std::min<int64_t>(lig_fit, 256) : lig_fit);
   const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
-  const int64_t tiles = (a.P + kTile - 1) / kTile;
-  int grid = (int)std::min<int64_t>(tiles, (int64_t)dc.sms);
+  const int64_t chunks = (a.P + kChunk - 1) / kChunk;
+  int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
-  score_kernel<RT><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
+  score_kernel<RT, NA><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
   return (int)cudaGetLastError();
 }
 
@@ -695,13 +796,13 @@ int launch_fill_short_memo(const double* S0, const double* S1, const double* S2,
 
 const char* score_kernel_variant(int R) {
   switch (R) {
-    case 4: return "score_kernel<4>";
-    case 8: return "score_kernel<8>";
-    case 12: return "score_kernel<12>";
-    case 16: return "score_kernel<16>";
-    case 24: return "score_kernel<24>";
-    case 32: return "score_kernel<32>";
-    default: return "score_kernel<0> (runtime R)";
+    case 4: return "score_kernel<4, NA>";
+    case 8: return "score_kernel<8, NA>";
+    case 12: return "score_kernel<12, NA>";
+    case 16: return "score_kernel<16, NA>";
+    case 24: return "score_kernel<24, NA>";
+    case 32: return "score_kernel<32, NA>";
+    default: return "score_kernel<0, NA> (runtime R)";
   }
 }
 
@@ -747,15 +848,29 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
     const double row_b = 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
     window_mode = rows * row_b <= 0.75 * double(dc.smem_optin);
   }
+  // two atoms per lane and pass when the ligand has more than 32 atoms
+#ifdef RS_FORCE_NA
+  const int na = RS_FORCE_NA, sl = na == 2 ? 8 : 0;
+#else
+  const int na = a.L > 32 ? 2 : 1, sl = na == 2 ? 8 : 0;
+#endif
   int e;
-  switch (a.R) {
-    case 4: e = launch_t<4>(a, st, device, 1, window_mode); break;
-    case 8: e = launch_t<8>(a, st, device, 2, window_mode); break;
-    case 12: e = launch_t<12>(a, st, device, 3, window_mode); break;
-    case 16: e = launch_t<16>(a, st, device, 4, window_mode); break;
-    case 24: e = launch_t<24>(a, st, device, 5, window_mode); break;
-    case 32: e = launch_t<32>(a, st, device, 6, window_mode); break;
-    default: e = launch_t<0>(a, st, device, 0, false); break;
+  switch (a.R * 4 + na) {
+    case 4 * 4 + 1: e = launch_t<4, 1>(a, st, device, 1 + sl, window_mode); break;
+    case 4 * 4 + 2: e = launch_t<4, 2>(a, st, device, 1 + sl, window_mode); break;
+    case 8 * 4 + 1: e = launch_t<8, 1>(a, st, device, 2 + sl, window_mode); break;
+    case 8 * 4 + 2: e = launch_t<8, 2>(a, st, device, 2 + sl, window_mode); break;
+    case 12 * 4 + 1: e = launch_t<12, 1>(a, st, device, 3 + sl, window_mode); break;
+    case 12 * 4 + 2: e = launch_t<12, 2>(a, st, device, 3 + sl, window_mode); break;
+    case 16 * 4 + 1: e = launch_t<16, 1>(a, st, device, 4 + sl, window_mode); break;
+    case 16 * 4 + 2: e = launch_t<16, 2>(a, st, device, 4 + sl, window_mode); break;
+    case 24 * 4 + 1: e = launch_t<24, 1>(a, st, device, 5 + sl, window_mode); break;
+    case 24 * 4 + 2: e = launch_t<24, 2>(a, st, device, 5 + sl, window_mode); break;
+    case 32 * 4 + 1: e = launch_t<32, 1>(a, st, device, 6 + sl, window_mode); break;
+    case 32 * 4 + 2: e = launch_t<32, 2>(a, st, device, 6 + sl, window_mode); break;
+    default:
+      e = na == 2 ? launch_t<0, 2>(a, st, device, 0 + sl, false) : launch_t<0, 1>(a, st, device, 0, false);
+      break;
   }
   if (launches) *launches += 1;
   return e;
