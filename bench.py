@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--nbr-cell", type=float, default=0.0,
+                    help="edge [A] of the neighbour-list cells (0 = the library's automatic choice)")
     args = ap.parse_args()
     if args.impl == "reference":
         return impl_reference(args)
@@ -225,7 +227,8 @@ def main():
     ncpu = os.cpu_count() or 1
     t0 = time.perf_counter()
     prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
-                          device=local, n_threads=max(1, ncpu // max(world, 1)))
+                          device=local, n_threads=max(1, ncpu // max(world, 1)),
+                          nbr_cell=args.nbr_cell)
     setup_s = time.perf_counter() - t0
     info = prot.info
 

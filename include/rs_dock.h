@@ -72,6 +72,9 @@ typedef struct {
     int32_t  n_threads;     /* host threads for the setup (0 = all)                             */
     uint64_t seed;          /* seed of the randomized range finder / ALS init                   */
     uint32_t flags;         /* RS_FLAG_*                                                        */
+    double   nbr_cell;      /* edge [A] of the coarse cells of the neighbour lists used for the
+                               short-range (H5) and vdW (H6) pairs; rounded to h * 2^k
+                               (0 = automatic: about max(D_cap, n_sigma h) / 2)                 */
 } rs_params;
 
 /* Information about a built handle (all host values). */

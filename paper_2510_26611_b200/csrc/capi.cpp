@@ -263,6 +263,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
   if (prm.grid_n < 2 || (prm.grid_n & 1)) { set_err("grid_n must be even and >= 2"); return nullptr; }
   if (prm.grid_n > 32768) { set_err("grid_n too large (max 32768)"); return nullptr; }
   if (prm.rank_R < 0) { set_err("rank_R must be >= 0"); return nullptr; }
+  if (!(prm.nbr_cell >= 0) || !std::isfinite(prm.nbr_cell)) { set_err("nbr_cell must be finite and >= 0"); return nullptr; }
   if (!(prm.eps_compress > 0 && prm.eps_compress < 1)) { set_err("eps_compress must be in (0,1)"); return nullptr; }
   if (!(prm.eps_quad > 0 && prm.eps_quad < 1)) { set_err("eps_quad must be in (0,1)"); return nullptr; }
   if (!(prm.eps_split > 0 && prm.eps_split < 1)) { set_err("eps_split must be in (0,1)"); return nullptr; }
@@ -352,7 +353,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     // S9: cell lists covering every pair that can matter: vdW pairs (< dmin_cap) and the
     // short-range ball (|i_l - i_m|_2 <= n_sigma => |x_l - x_m| <= (n_sigma + sqrt 3) h)
     const double rho = std::max(prm.dmin_cap, (ns + std::sqrt(3.0)) * h);
-    rs::build_cell_lists(n, b, h, hd->xyz, hd->cells, rho, &hd->cg);
+    rs::build_cell_lists(n, b, h, hd->xyz, hd->cells, rho, prm.nbr_cell, &hd->cg);
     // sampled compression error at exterior cells
     const double work = double(n_atoms) * double(tl.size());
     const int nsamp = (int)std::max(100.0, std::min(2000.0, 4e9 / std::max(work, 1.0)));

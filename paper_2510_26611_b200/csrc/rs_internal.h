@@ -51,7 +51,8 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          std::vector<double> F[3], int* R_out, SetupReport* rep);
 
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
-                      const std::vector<int32_t>& cells, double rho, CoarseGrid* cg);
+                      const std::vector<int32_t>& cells, double rho, double cell_edge,
+                      CoarseGrid* cg);
 
 void sample_compression_error(int n, double b, double h, const std::vector<double>& xyz,
                               const std::vector<int32_t>& cells, const std::vector<double>& z,

@@ -622,34 +622,36 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       if (window_mode) {
         // inclusive block scan of the row bounds over the tile's poses: the tile becomes the
         // longest prefix whose cumulative window fits cap_rows
+        if (warp * 32 < T) {             // warps without poses only join the barriers
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int v[7];
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            v[r] = __shfl_up_sync(kFull, wlo[r], o);
-            v[3 + r] = __shfl_up_sync(kFull, whi[r], o);
-          }
-          v[6] = __shfl_up_sync(kFull, wbad, o);
-          if (lane >= o) {
+          for (int o = 1; o < 32; o <<= 1) {
+            int v[7];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              wlo[r] = min(wlo[r], v[r]);
-              whi[r] = max(whi[r], v[3 + r]);
+              v[r] = __shfl_up_sync(kFull, wlo[r], o);
+              v[3 + r] = __shfl_up_sync(kFull, whi[r], o);
             }
-            wbad |= v[6];
-          }
-        }
-        if (lane == 31) {
+            v[6] = __shfl_up_sync(kFull, wbad, o);
+            if (lane >= o) {
 #pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            s_wred[warp][r] = wlo[r];
-            s_wred[warp][3 + r] = whi[r];
+              for (int r = 0; r < 3; ++r) {
+                wlo[r] = min(wlo[r], v[r]);
+                whi[r] = max(whi[r], v[3 + r]);
+              }
+              wbad |= v[6];
+            }
           }
-          s_wred[warp][6] = wbad;
+          if (lane == 31) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              s_wred[warp][r] = wlo[r];
+              s_wred[warp][3 + r] = whi[r];
+            }
+            s_wred[warp][6] = wbad;
+          }
         }
         __syncthreads();
-        for (int w = 0; w < warp; ++w) {
+        for (int w = 0; w < warp && warp * 32 < T; ++w) {
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
             wlo[r] = min(wlo[r], s_wred[w][r]);

@@ -508,11 +508,24 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
 
 // ---- S9: cell lists --------------------------------------------------------------------------
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
-                      const std::vector<int32_t>& cells, double rho, CoarseGrid* cg) {
+                      const std::vector<int32_t>& cells, double rho, double cell_edge,
+                      CoarseGrid* cg) {
   const int64_t M = (int64_t)cells.size() / 3;
-  const double target = rho / 2.0;
+  // automatic edge: about rho/4 (fewer candidates per atom: a pair list holds every atom within
+  // rr of the cell's box, so the false candidates shrink with the cell), coarsened while the
+  // estimated entry count M * |cube (+) ball(rr)| / c^3 exceeds kMaxEntries
+  const double target = cell_edge > 0 ? cell_edge : rho / 4.0;
   int shift = 0;
-  while (shift < 20 && h * double(1 << (shift + 1)) <= target * 1.4142) ++shift;
+  while (shift < 15 && h * double(1 << (shift + 1)) <= target * 1.4142) ++shift;
+  if (cell_edge <= 0) {
+    const double kMaxEntries = 64.0 * (1 << 20);
+    const double r = rho + 2 * h, pi = 3.14159265358979323846;
+    for (; shift < 15; ++shift) {
+      const double c = h * double(1 << shift);
+      const double v = c * c * c + 6 * c * c * r + 3 * pi * c * r * r + 4.0 / 3.0 * pi * r * r * r;
+      if (double(M) * v / (c * c * c) <= kMaxEntries) break;
+    }
+  }
   cg->shift = shift;
   const int pf = (int)std::ceil((rho + 2 * h) / h) + 1;
   for (int a = 0; a < 3; ++a) {

@@ -32,7 +32,8 @@ class rs_params(ctypes.Structure):
                 ("sigma_vdw", ctypes.c_double), ("dmin_cap", ctypes.c_double),
                 ("tucker_rank_max", ctypes.c_int32), ("als_sweeps", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("n_threads", ctypes.c_int32),
-                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32)]
+                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32),
+                ("nbr_cell", ctypes.c_double)]
 
 
 class rs_info(ctypes.Structure):

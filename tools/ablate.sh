@@ -1,14 +1,18 @@
 #!/bin/bash
-# Time librsdock variants (build/variants/librsdock_<name>.so) on one config, then profile the
-# default build with ncu.  Usage: bash tools/ablate.sh TAG CONFIG "name1 name2 ..." [NCU=1]
+# Time librsdock variants on one config, then (optionally) profile the default build with ncu.
+#   bash tools/ablate.sh TAG CONFIG "v1 v2:--nbr-cell+0.5 ..." [NCU=1]
+# A variant "name" loads build/variants/librsdock_<name>.so; "name:ARGS" runs the default
+# library with extra bench.py arguments ('+' stands for a space).
 set -u
 TAG=$1; CFG=$2; NAMES=$3; NCU=${4:-1}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build_library()" > $OUT/build.log 2>&1
-for v in base $NAMES; do
-  if [ "$v" = "base" ]; then LIBP=""; else LIBP=build/variants/librsdock_$v.so; fi
-  RSDOCK_LIB=$LIBP timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench > $OUT/bench_$v.json 2> $OUT/bench_$v.err
-  echo "$v rc=$? $(python -c "import json;d=json.load(open('$OUT/bench_$v.json'));print(round(d['ms_per_step'],4),'ms')" 2>/dev/null)"
+for spec in base $NAMES; do
+  v=${spec%%:*}; extra=""; LIBP=""
+  if [[ "$spec" == *:* ]]; then extra=${spec#*:}; extra=${extra//+/ }
+  elif [ "$v" != "base" ]; then LIBP=build/variants/librsdock_$v.so; fi
+  RSDOCK_LIB=$LIBP timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench $extra > $OUT/bench_$v.json 2> $OUT/bench_$v.err
+  echo "$v rc=$? $(python -c "import json;d=json.load(open('$OUT/bench_$v.json'));print(round(d['ms_per_step'],4),'ms', d['setup'].get('nbr_entries'))" 2>/dev/null)"
 done
 if [ "$NCU" = "1" ]; then
   CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench"
