@@ -118,7 +118,7 @@ def load_workload(name):
     return syn.make(name)
 
 
-def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=20000, seed=7):
+def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7):
     """Time the oracle (as it stands) on a bounded seeded sample of the workload's poses."""
     from oracle import rs_oracle
     from synth import configs as syn
@@ -193,7 +193,7 @@ def config_dict(w, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
