@@ -43,7 +43,7 @@ namespace {
 #define RS_THREADS 512
 #endif
 #ifndef RS_TILE
-#define RS_TILE 128
+#define RS_TILE 256
 #endif
 #ifndef RS_CHUNK
 #define RS_CHUNK 256
@@ -57,6 +57,10 @@ constexpr int kTile = RS_TILE;           // poses per tile (upper bound)
 constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 static_assert(kTile <= kThreads, "one thread per pose of a tile");
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef RS_SLOTS
+#define RS_SLOTS 1
+#endif
+constexpr int kSlots = RS_SLOTS;         // candidate slots per lane and flattened round
 
 template <int R>
 struct Geo {
@@ -67,12 +71,6 @@ struct Geo {
 };
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
-
-// O3 validity: -b <= x <= b  <=>  |x| <= b (b > 0 finite), as an integer compare of the
-// magnitude bits (false for NaN and +-inf)
-__device__ __forceinline__ bool in_box(double x, unsigned long long bbits) {
-  return ((unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull) <= bbits;
-}
 
 // O3 cell of a valid coordinate: u = (x + b) * inv_h in [0, n(1+eps)]; i = clamp(ceil(u)-1)
 __device__ __forceinline__ int snap_dev(double x, double b, double inv_h, int nm1) {
@@ -124,7 +122,11 @@ __device__ __forceinline__ double2 lds2(unsigned addr) {
 
 // One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
 __device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
+#ifdef RS_FMA_PROBE  // timing probe only: not the evaluation contract
+  return __fma_rn(__dmul_rn(a.y, b.y), c.y, __dmul_rn(__dmul_rn(a.x, b.x), c.x));
+#else
   return __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), c.x), __dmul_rn(__dmul_rn(a.y, b.y), c.y));
+#endif
 }
 
 // O4 halving tree over NS pair sums (A20): s_c = s_c + s_{c+m}, m = NS/2 .. 1
@@ -218,7 +220,7 @@ template <int NA>
 struct __align__(16) PairStage {
   double4 xz[32 * NA];  // transformed coordinates x' and charge (slot 32 u + lane)
   int4 cb[32 * NA];     // i0, i1, i2, (list begin - start of the atom's candidate segment)
-  int map[64];          // two rounds: candidate slot where an atom's segment starts -> atom slot
+  int map[32 * kSlots]; // candidate slot where an atom's segment starts -> atom slot
 };
 
 // ---- TMA bulk copy + mbarrier (window staging) ---------------------------------------------
@@ -299,84 +301,111 @@ __device__ __forceinline__ double pair_short(const ScoreArgs& a, const int4 oc, 
 struct AtomState {
   double x0, x1, x2, z;
   int i0, i1, i2, beg, cnt;
+  bool go;                     // a real ligand atom (l < L) inside the box
 };
 
-// H2-H4 for ligand atom l of one pose: transform, snap, candidate range, long-range value
-// (accumulated into (hi, lo)).  bad is set if the atom leaves the box (O8).
-template <int RT>
+// H2, H3 and the candidate-range lookup for ligand atom l of one pose.  bad is set if the atom
+// leaves the box (O8).  Lanes past the ligand's end (l >= L) run them on atom L-1 and get
+// go = false, z = 0 (branch-free; they contribute nothing).
+template <bool LIG_SMEM>
 __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
-                                           const double* tv, bool use_win, const Window& W,
-                                           unsigned win_u32, const double4* s_lig, int lig_smem_n,
-                                           int rho, unsigned long long bbits, AtomState& st,
-                                           double& hi, double& lo, bool& bad) {
-  st.x0 = st.x1 = st.x2 = st.z = 0.0;
-  st.i0 = st.i1 = st.i2 = st.beg = st.cnt = 0;
-  if (l >= a.L) return;
-  double y0, y1, y2;
-  if (l < lig_smem_n) {
-    const double4 v = s_lig[l];
-    y0 = v.x; y1 = v.y; y2 = v.z; st.z = v.w;
+                                           const double* tv, const double4* s_lig, AtomState& st,
+                                           bool& bad) {
+  const bool act = l < a.L;
+  const int lc = act ? l : a.L - 1;
+  double y0, y1, y2, z;
+  if constexpr (LIG_SMEM) {
+    const double4 v = s_lig[lc];
+    y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
   } else {
-    y0 = __ldg(a.yl + 3 * (int64_t)l);
-    y1 = __ldg(a.yl + 3 * (int64_t)l + 1);
-    y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
-    st.z = __ldg(a.zl + l);
+    y0 = __ldg(a.yl + 3 * (int64_t)lc);
+    y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
+    y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
+    z = __ldg(a.zl + lc);
   }
+  st.z = act ? z : 0.0;
   // H2 (O2)
+#ifdef RS_FMA_PROBE  // timing probe only: not the evaluation contract
+  st.x0 = __fma_rn(Rm[0], y0, __fma_rn(Rm[1], y1, __fma_rn(Rm[2], y2, tv[0])));
+  st.x1 = __fma_rn(Rm[3], y0, __fma_rn(Rm[4], y1, __fma_rn(Rm[5], y2, tv[1])));
+  st.x2 = __fma_rn(Rm[6], y0, __fma_rn(Rm[7], y1, __fma_rn(Rm[8], y2, tv[2])));
+#else
   st.x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
   st.x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
   st.x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
-  // H3 (O3)
-  if (!(in_box(st.x0, bbits) && in_box(st.x1, bbits) && in_box(st.x2, bbits))) {
-    bad = true;
-    return;
-  }
+#endif
+  // H3 (O3): valid iff -b <= x'_a <= b on every axis (false for NaN)
+  const bool ok = fabs(st.x0) <= a.b && fabs(st.x1) <= a.b && fabs(st.x2) <= a.b;
+  bad = bad || (act && !ok);
+  st.go = act && ok;
   const int nm1 = a.n - 1;
-  const int i0 = snap_dev(st.x0, a.b, a.inv_h, nm1);
-  const int i1 = snap_dev(st.x1, a.b, a.inv_h, nm1);
-  const int i2 = snap_dev(st.x2, a.b, a.inv_h, nm1);
-  st.i0 = i0;
-  st.i1 = i1;
-  st.i2 = i2;
+  st.i0 = snap_dev(st.x0, a.b, a.inv_h, nm1);
+  st.i1 = snap_dev(st.x1, a.b, a.inv_h, nm1);
+  st.i2 = snap_dev(st.x2, a.b, a.inv_h, nm1);
+  st.beg = 0;
+  st.cnt = 0;
 #if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
   // candidate range of the coarse cell containing i (cell lists cover every protein atom that can
   // matter to H5/H6 for any point of the cell); loaded before H4 so its latency hides behind it
-  {
-    const unsigned cx = (unsigned)((i0 >> a.nb_shift) - a.nb_lo[0]);
-    const unsigned cy = (unsigned)((i1 >> a.nb_shift) - a.nb_lo[1]);
-    const unsigned cz = (unsigned)((i2 >> a.nb_shift) - a.nb_lo[2]);
-    if (cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
-      const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
-      st.beg = bc.x;
-      st.cnt = bc.y;
-    }
+  const unsigned cx = (unsigned)((st.i0 >> a.nb_shift) - a.nb_lo[0]);
+  const unsigned cy = (unsigned)((st.i1 >> a.nb_shift) - a.nb_lo[1]);
+  const unsigned cz = (unsigned)((st.i2 >> a.nb_shift) - a.nb_lo[2]);
+  if (st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
+    const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
+    st.beg = bc.x;
+    st.cnt = bc.y;
   }
 #endif
-  // H4 (O4)
-  double phi;
+}
+
+// H4 (O4) for the NA atoms of a lane: atoms whose rows are staged read the window, real atoms
+// outside it (rare) read L2, lanes past the ligand's end skip it (phi = 0, weight z = 0).
+template <int RT, int NA>
+__device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomState* st,
+                                                 bool use_win, const Window& W, unsigned win_u32,
+                                                 int rho, double* hi, double* lo) {
+  double phi[NA];
+#pragma unroll
+  for (int u = 0; u < NA; ++u) phi[u] = 0.0;
   if constexpr (RT > 0) {
     using G = Geo<RT>;
-    const bool inwin = use_win && (unsigned)(i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
-                       (unsigned)(i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
-                       (unsigned)(i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
-#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
-    if (inwin) {
-      phi = st.z;
-    } else
-#endif
-    if (inwin) {
-      constexpr unsigned kRow = 16u * G::CHP;
-      phi = long_phi_smem<RT>(win_u32 + (unsigned)(i0 + W.off[0]) * kRow,
-                              win_u32 + (unsigned)(i1 + W.off[1]) * kRow,
-                              win_u32 + (unsigned)(i2 + W.off[2]) * kRow, rho);
-    } else {
-      phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2);
+    constexpr unsigned kRow = 16u * G::CHP;
+    bool l2[NA];
+    unsigned r0[NA], r1[NA], r2[NA];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const bool inwin = use_win && (unsigned)(st[u].i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
+                         (unsigned)(st[u].i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
+                         (unsigned)(st[u].i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
+      l2[u] = st[u].go && !inwin;
+      const bool w = st[u].go && inwin;
+      r0[u] = w ? win_u32 + (unsigned)(st[u].i0 + W.off[0]) * kRow : win_u32;
+      r1[u] = w ? win_u32 + (unsigned)(st[u].i1 + W.off[1]) * kRow : win_u32;
+      r2[u] = w ? win_u32 + (unsigned)(st[u].i2 + W.off[2]) * kRow : win_u32;
     }
+    if (use_win) {
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
+        phi[u] = st[u].z;
+#else
+        if (st[u].go && !l2[u]) phi[u] = long_phi_smem<RT>(r0[u], r1[u], r2[u], rho);
+#endif
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NA; ++u)
+      if (l2[u]) phi[u] = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], st[u].i0, st[u].i1, st[u].i2);
   } else {
-    phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
-                      a.t.F[2] + (size_t)i2 * a.R, a.R);
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      if (st[u].go)
+        phi[u] = long_phi_rt(a.t.F[0] + (size_t)st[u].i0 * a.R, a.t.F[1] + (size_t)st[u].i1 * a.R,
+                             a.t.F[2] + (size_t)st[u].i2 * a.R, a.R);
+    }
   }
-  dd_add_prod(hi, lo, st.z, phi);
+#pragma unroll
+  for (int u = 0; u < NA; ++u) dd_add_prod(hi[u], lo[u], st[u].z, phi[u]);
 }
 
 // (hi, lo) += (h2, l2) exactly up to the final lo rounding (TwoSum on the high parts)
@@ -411,16 +440,18 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   for (int u = 0; u < NA; ++u) hi[u] = lo[u] = 0.0;
   bool bad = !ok;
   const int rho = lane & 7;
-  const unsigned long long bbits = (unsigned long long)__double_as_longlong(a.b);
+  const bool lig_all_smem = a.L <= lig_smem_n;
   const int L = ok ? a.L : 0;
   const double2* prec = reinterpret_cast<const double2*>(a.t.prec);
   const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   for (int l0 = 0; l0 < L; l0 += 32 * NA) {
     AtomState st[NA];
 #pragma unroll
-    for (int u = 0; u < NA; ++u)
-      atom_stage<RT>(a, l0 + 32 * u + lane, Rm, tv, use_win, W, win_u32, s_lig, lig_smem_n, rho,
-                     bbits, st[u], hi[u], lo[u], bad);
+    for (int u = 0; u < NA; ++u) {
+      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, st[u], bad);
+      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, st[u], bad);
+    }
+    long_range_stage<RT, NA>(a, st, use_win, W, win_u32, rho, hi, lo);
     if (__any_sync(kFull, bad)) {
       bad = true;
       break;                      // the pose is invalid: NaN outputs, skip the rest
@@ -451,86 +482,99 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       }
     }
     int carry = 0;
-    for (int base = 0; base < total; base += 64) {
-      unsigned m0 = 0, m1 = 0;
+    for (int base = 0; base < total; base += 32 * kSlots) {
+      unsigned m[kSlots];
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) m[q] = 0;
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         const int rel = seg[u] - base;
-        if (st[u].cnt > 0 && rel >= 0 && rel < 64) {
+        if (st[u].cnt > 0 && rel >= 0 && rel < 32 * kSlots) {
           ps.map[rel] = 32 * u + lane;
-          if (rel < 32) m0 |= 1u << rel;
-          else m1 |= 1u << (rel - 32);
+#pragma unroll
+          for (int q = 0; q < kSlots; ++q)
+            if ((rel >> 5) == q) m[q] |= 1u << (rel & 31);
         }
       }
-      m0 = __reduce_or_sync(kFull, m0);
-      m1 = __reduce_or_sync(kFull, m1);
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) m[q] = __reduce_or_sync(kFull, m[q]);
       __syncwarp();
-      // owner of slot base + lane (+ 32): the last segment starting at or before it
-      const unsigned b0 = m0 & lanemask_le, b1 = m1 & lanemask_le;
-      const int ow0 = b0 ? ps.map[31 - __clz(b0)] : carry;
-      const int ow1 = b1 ? ps.map[63 - __clz(b1)] : (m0 ? ps.map[31 - __clz(m0)] : carry);
-      carry = __shfl_sync(kFull, ow1, 31);
-      const int k0 = base + lane, k1 = base + 32 + lane;
-      int4 oc0 = make_int4(0, 0, 0, 0), oc1 = oc0, en0 = oc0, en1 = oc0;
-      if (k0 < total) {
-        oc0 = ps.cb[ow0];
-        en0 = __ldg(a.t.nb_ent + oc0.w + k0);
+      // owner of slot base + 32 q + lane: the last segment starting at or before it
+      int ow[kSlots];
+      {
+        int prev = carry;
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) {
+          const unsigned bq = m[q] & lanemask_le;
+          ow[q] = bq ? ps.map[32 * q + 31 - __clz(bq)] : prev;
+          if (q + 1 < kSlots) prev = m[q] ? ps.map[32 * q + 31 - __clz(m[q])] : prev;
+        }
       }
-      if (k1 < total) {
-        oc1 = ps.cb[ow1];
-        en1 = __ldg(a.t.nb_ent + oc1.w + k1);
+      carry = __shfl_sync(kFull, ow[kSlots - 1], 31);
+      int4 oc[kSlots], en[kSlots];
+      unsigned dd[kSlots];
+      bool sr[kSlots], nr[kSlots];
+      double sv[kSlots];
+      double2 xy[kSlots], zq[kSlots];
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) {
+        const int k = base + 32 * q + lane;
+        oc[q] = make_int4(0, 0, 0, 0);
+        en[q] = oc[q];
+        if (k < total) {
+          oc[q] = ps.cb[ow[q]];
+          en[q] = __ldg(a.t.nb_ent + oc[q].w + k);
+        }
+        dd[q] = k < total ? pair_dd(oc[q], en[q]) : 0xffffffffu;
+        sr[q] = dd[q] <= a.ns2;
+        nr[q] = sr[q] || dd[q] < a.vdw_cells2;
       }
-      const unsigned dd0 = k0 < total ? pair_dd(oc0, en0) : 0xffffffffu;
-      const unsigned dd1 = k1 < total ? pair_dd(oc1, en1) : 0xffffffffu;
-      const bool s0 = dd0 <= a.ns2, s1 = dd1 <= a.ns2;
-      const bool n0 = s0 || dd0 < a.vdw_cells2, n1 = s1 || dd1 < a.vdw_cells2;
       // loads of this round, all independent: memo values, then records
-      const double sv0 = s0 ? pair_short(a, oc0, en0) : 0.0;
-      const double sv1 = s1 ? pair_short(a, oc1, en1) : 0.0;
-      double2 xy0 = make_double2(0.0, 0.0), zq0 = xy0, xy1 = xy0, zq1 = xy0;
-      if (n0) {
-        xy0 = ldg2(prec + 2 * en0.z);
-        zq0 = ldg2(prec + 2 * en0.z + 1);
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) sv[q] = sr[q] ? pair_short(a, oc[q], en[q]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q) {
+        xy[q] = make_double2(0.0, 0.0);
+        zq[q] = xy[q];
+        if (nr[q]) {
+          xy[q] = ldg2(prec + 2 * en[q].z);
+          zq[q] = ldg2(prec + 2 * en[q].z + 1);
+        }
       }
-      if (n1) {
-        xy1 = ldg2(prec + 2 * en1.z);
-        zq1 = ldg2(prec + 2 * en1.z + 1);
-      }
-      if (n0) pair_term(a, ps.xz[ow0], dd0, sv0, xy0, zq0, hi[0], lo[0], best);
-      if (n1) pair_term(a, ps.xz[ow1], dd1, sv1, xy1, zq1, hi[NA - 1], lo[NA - 1], best);
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q)
+        if (nr[q]) pair_term(a, ps.xz[ow[q]], dd[q], sv[q], xy[q], zq[q], hi[q % NA], lo[q % NA], best);
     }
     __syncwarp();
   }
   // H7: double-double butterfly (TwoSum is exact, so all lanes agree); min of d^2 >= +0 by its
   // bit pattern (non-negative doubles order like their unsigned bits)
   bad = __any_sync(kFull, bad);
-  if (bad) {
-    if (lane == 0) {
-      a.E[p] = NAN;
-      a.D[p] = NAN;
-      if (a.invalid) atomicAdd(a.invalid, 1ull);
+  double H = 0.0, Lo = 0.0;
+  unsigned mhi = 0, mlo = 0;
+  if (!bad) {
+    H = hi[0];
+    Lo = lo[0];
+#pragma unroll
+    for (int u = 1; u < NA; ++u) dd_merge(H, Lo, hi[u], lo[u]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double h2 = __shfl_xor_sync(kFull, H, off);
+      const double l2 = __shfl_xor_sync(kFull, Lo, off);
+      dd_merge(H, Lo, h2, l2);
     }
-    return;
+    const unsigned long long bb = (unsigned long long)__double_as_longlong(best);
+    const unsigned bhi = (unsigned)(bb >> 32);
+    mhi = __reduce_min_sync(kFull, bhi);
+    mlo = __reduce_min_sync(kFull, bhi == mhi ? (unsigned)bb : 0xffffffffu);
   }
-  double H = hi[0], Lo = lo[0];
-#pragma unroll
-  for (int u = 1; u < NA; ++u) dd_merge(H, Lo, hi[u], lo[u]);
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double h2 = __shfl_xor_sync(kFull, H, off);
-    const double l2 = __shfl_xor_sync(kFull, Lo, off);
-    dd_merge(H, Lo, h2, l2);
-  }
-  const unsigned long long bb = (unsigned long long)__double_as_longlong(best);
-  const unsigned bhi = (unsigned)(bb >> 32);
-  const unsigned mhi = __reduce_min_sync(kFull, bhi);
-  const unsigned mlo = __reduce_min_sync(kFull, bhi == mhi ? (unsigned)bb : 0xffffffffu);
   // H8
   if (lane == 0) {
     const double m = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-    a.E[p] = __dadd_rn(H, Lo);
-    a.D[p] = m < a.dcap2 ? __dsqrt_rn(m) : INFINITY;
+    a.E[p] = bad ? NAN : __dadd_rn(H, Lo);
+    a.D[p] = bad ? NAN : (m < a.dcap2 ? __dsqrt_rn(m) : INFINITY);
+    if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
   }
 }
 
@@ -719,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         s = __shfl_sync(kFull, s, 0);
         if (s >= T) break;
         score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, smem_u32(win), s_lig, lig_smem_n,
-                       lane, s_ps[warp]);
+                           lane, s_ps[warp]);
       }
       __syncthreads();
       p += T;

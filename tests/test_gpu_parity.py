@@ -193,6 +193,38 @@ def test_linearity_in_ligand_charges(env):
     assert np.array_equal(E2, 2.0 * E) and np.array_equal(D2, D)
 
 
+def test_repeated_and_concurrent_streams(env):
+    """Each launch takes a fresh dynamic-schedule work counter (stream-ordered reset): repeated
+    calls and concurrent calls on two streams give the same bits as one synchronous call."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1()
+    prot = build(rsdock, w)
+    E0, D0, inv0 = gpu_score(torch, rsdock, prot, w, w.poses)
+    dev = torch.device("cuda:0")
+    q = torch.tensor(w.ligand_q, device=dev)
+    y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
+    ps = torch.tensor(w.poses, device=dev).contiguous()
+    h = w.P // 2
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for st in streams:
+        st.wait_stream(torch.cuda.current_stream())
+    for _ in range(3):
+        outs = []
+        for k, (lo, hi) in enumerate([(0, h), (h, w.P)]):
+            E = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+            D = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            streams[k].wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(streams[k]):
+                prot.score_async(q, y, ps[lo:hi], E, D, cnt, stream=streams[k])
+            outs.append((E, D, cnt))
+        torch.cuda.synchronize()
+        E = torch.cat([o[0] for o in outs]).cpu().numpy()
+        D = torch.cat([o[1] for o in outs]).cpu().numpy()
+        assert np.array_equal(E, E0) and np.array_equal(D, D0)
+        assert sum(int(o[2].item()) for o in outs) == inv0
+
+
 # ----------------------------------------------------------------------------- physics on GPU
 
 def test_tolerance_mode_gpu_vs_coulomb(env):
