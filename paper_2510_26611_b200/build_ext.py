@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
                    *[f"-D{d}" for d in defines],
                    "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-c", src, "-o", obj]
         else:
-            cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler",
+            cmd = [NVCC, "-O3", "-std=c++17", *[f"-D{d}" for d in defines], "-Xcompiler",
                    "-fPIC,-O3,-fopenmp,-ffp-contract=off", "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))

@@ -40,7 +40,7 @@ namespace rs {
 namespace {
 
 #ifndef RS_THREADS
-#define RS_THREADS 512
+#define RS_THREADS 1024
 #endif
 #ifndef RS_TILE
 #define RS_TILE 256
@@ -71,6 +71,34 @@ struct Geo {
 };
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
+
+// Read-only global loads issued only when pr holds (the predicate is inside the instruction, so
+// the compiler cannot turn a guarded load into an unguarded speculative one: the address may be
+// meaningless when pr is false, and untaken lanes cost no L1 tag lookups).  Result 0 if !pr.
+__device__ __forceinline__ double ldg_if(const double* p, bool pr) {
+  double v = 0.0;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
+      : "+d"(v) : "l"(p), "r"((int)pr));
+  return v;
+}
+__device__ __forceinline__ double2 ldg_if(const double2* p, bool pr) {
+  double2 v = make_double2(0.0, 0.0);
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.global.nc.v2.f64 {%0, %1}, [%2];\n}"
+      : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((int)pr));
+  return v;
+}
+__device__ __forceinline__ int2 ldg_if(const int2* p, bool pr) {
+  int2 v = make_int2(0, 0);
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.global.nc.v2.s32 {%0, %1}, [%2];\n}"
+      : "+r"(v.x), "+r"(v.y) : "l"(p), "r"((int)pr));
+  return v;
+}
+__device__ __forceinline__ int4 ldg_if(const int4* p, bool pr) {
+  int4 v = make_int4(0, 0, 0, 0);
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];\n}"
+      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w) : "l"(p), "r"((int)pr));
+  return v;
+}
 
 // O3 cell of a valid coordinate: u = (x + b) * inv_h in [0, n(1+eps)]; i = clamp(ceil(u)-1)
 __device__ __forceinline__ int snap_dev(double x, double b, double inv_h, int nm1) {
@@ -114,12 +142,6 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
   lo = __dadd_rn(lo, __dadd_rn(err, e));
 }
 
-__device__ __forceinline__ double2 lds2(unsigned addr) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
-}
-
 // One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
 __device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
 #ifdef RS_FMA_PROBE  // timing probe only: not the evaluation contract
@@ -140,14 +162,15 @@ __device__ __forceinline__ double halving_tree(double* s) {
   return s[0];
 }
 
-// O4 with compile-time R from the shared-memory window.  rK = byte address of row K (aligned
-// to the row size).  Slot c reads physical chunk c ^ rho (rho = lane & 7): the 8 lanes of a
-// quarter-warp hit 8 distinct 16-byte bank groups whatever rows they read.  Physical chunk p
-// holds pair p (padded widths: zero beyond CH; replicated widths: pair p mod CH), so slot c
-// holds pair (c ^ rho) mod NS, and the halving tree, which combines c with c ^ m at every
-// level, is bitwise invariant under that relabelling.
+// O4 with compile-time R from the shared-memory window.  rK = byte offset of row K from the
+// window base (a multiple of the row size, the base 256-B aligned).  Slot c reads physical
+// chunk c ^ rho (rho = lane & 7): the 8 lanes of a quarter-warp hit 8 distinct 16-byte bank
+// groups whatever rows they read.  Physical chunk p holds pair p (padded widths: zero beyond CH;
+// replicated widths: pair p mod CH), so slot c holds pair (c ^ rho) mod NS, and the halving
+// tree, which combines c with c ^ m at every level, is bitwise invariant under that relabelling.
 template <int R>
-__device__ __forceinline__ double long_phi_smem(unsigned r0, unsigned r1, unsigned r2, int rho) {
+__device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, unsigned r1,
+                                                unsigned r2, int rho) {
   using G = Geo<R>;
   const unsigned x = (unsigned)rho << 4;
   r0 |= x;
@@ -157,7 +180,9 @@ __device__ __forceinline__ double long_phi_smem(unsigned r0, unsigned r1, unsign
 #pragma unroll
   for (int c = 0; c < G::NS; ++c) {
     const unsigned o = (unsigned)c << 4;
-    s[c] = pair_prod(lds2(r0 ^ o), lds2(r1 ^ o), lds2(r2 ^ o));
+    s[c] = pair_prod(*reinterpret_cast<const double2*>(win + (r0 ^ o)),
+                     *reinterpret_cast<const double2*>(win + (r1 ^ o)),
+                     *reinterpret_cast<const double2*>(win + (r2 ^ o)));
   }
   return halving_tree<G::NS>(s);
 }
@@ -218,7 +243,8 @@ struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
 // Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
 template <int NA>
 struct __align__(16) PairStage {
-  double4 xz[32 * NA];  // transformed coordinates x' and charge (slot 32 u + lane)
+  double2 x01[32 * NA]; // x'_0, x'_1 of slot 32 u + lane (written only for atoms with candidates)
+  double2 x2z[32 * NA]; // x'_2, charge
   int4 cb[32 * NA];     // i0, i1, i2, (list begin - start of the atom's candidate segment)
   int map[32 * kSlots]; // candidate slot where an atom's segment starts -> atom slot
 };
@@ -256,7 +282,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2) {
   if (a.t.short_memo) {
     const int d = a.n_sigma + 1;
-    return __ldg(a.t.short_memo + (abs(e0) * d + abs(e1)) * d + abs(e2));
+    return ldg_if(a.t.short_memo + (abs(e0) * d + abs(e1)) * d + abs(e2), true);
   }
   const double* s0 = a.t.S[0] + (size_t)(e0 + a.n_sigma) * a.Rs;
   const double* s1 = a.t.S[1] + (size_t)(e1 + a.n_sigma) * a.Rs;
@@ -309,14 +335,16 @@ struct AtomState {
 // go = false, z = 0 (branch-free; they contribute nothing).
 template <bool LIG_SMEM>
 __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
-                                           const double* tv, const double4* s_lig, AtomState& st,
+                                           const double* tv, const double2* s_lig, int lig_n,
+                                           AtomState& st,
                                            bool& bad) {
   const bool act = l < a.L;
   const int lc = act ? l : a.L - 1;
   double y0, y1, y2, z;
   if constexpr (LIG_SMEM) {
-    const double4 v = s_lig[lc];
-    y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
+    // ligand staged structure-of-arrays: (y0, y1) then (y2, z), conflict-free 16-byte loads
+    const double2 v0 = s_lig[lc], v1 = s_lig[lig_n + lc];
+    y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
   } else {
     y0 = __ldg(a.yl + 3 * (int64_t)lc);
     y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
@@ -350,8 +378,9 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
   const unsigned cx = (unsigned)((st.i0 >> a.nb_shift) - a.nb_lo[0]);
   const unsigned cy = (unsigned)((st.i1 >> a.nb_shift) - a.nb_lo[1]);
   const unsigned cz = (unsigned)((st.i2 >> a.nb_shift) - a.nb_lo[2]);
-  if (st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2]) {
-    const int2 bc = __ldg(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz);
+  {
+    const bool in = st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
+    const int2 bc = ldg_if(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz, in);
     st.beg = bc.x;
     st.cnt = bc.y;
   }
@@ -362,7 +391,7 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
 // outside it (rare) read L2, lanes past the ligand's end skip it (phi = 0, weight z = 0).
 template <int RT, int NA>
 __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomState* st,
-                                                 bool use_win, const Window& W, unsigned win_u32,
+                                                 bool use_win, const Window& W, const char* win,
                                                  int rho, double* hi, double* lo) {
   double phi[NA];
 #pragma unroll
@@ -379,9 +408,9 @@ __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomS
                          (unsigned)(st[u].i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
       l2[u] = st[u].go && !inwin;
       const bool w = st[u].go && inwin;
-      r0[u] = w ? win_u32 + (unsigned)(st[u].i0 + W.off[0]) * kRow : win_u32;
-      r1[u] = w ? win_u32 + (unsigned)(st[u].i1 + W.off[1]) * kRow : win_u32;
-      r2[u] = w ? win_u32 + (unsigned)(st[u].i2 + W.off[2]) * kRow : win_u32;
+      r0[u] = w ? (unsigned)(st[u].i0 + W.off[0]) * kRow : 0u;
+      r1[u] = w ? (unsigned)(st[u].i1 + W.off[1]) * kRow : 0u;
+      r2[u] = w ? (unsigned)(st[u].i2 + W.off[2]) * kRow : 0u;
     }
     if (use_win) {
 #pragma unroll
@@ -389,7 +418,7 @@ __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomS
 #if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
         phi[u] = st[u].z;
 #else
-        if (st[u].go && !l2[u]) phi[u] = long_phi_smem<RT>(r0[u], r1[u], r2[u], rho);
+        if (st[u].go && !l2[u]) phi[u] = long_phi_smem<RT>(win, r0[u], r1[u], r2[u], rho);
 #endif
       }
     }
@@ -417,24 +446,28 @@ __device__ __forceinline__ void dd_merge(double& hi, double& lo, double h2, doub
   lo = __dadd_rn(__dadd_rn(lo, l2), e);
 }
 
+__device__ __forceinline__ void load_pose(const PoseRec& pr, double* Rm, double* tv) {
+  const double2* m2 = reinterpret_cast<const double2*>(pr.m);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double2 v = m2[i];
+    const int k0 = 2 * i, k1 = 2 * i + 1;
+    if (k0 < 9) Rm[k0] = v.x; else tv[k0 - 9] = v.x;
+    if (k1 < 9) Rm[k1] = v.y; else tv[k1 - 9] = v.y;
+  }
+}
+
 // Score one pose with one warp: lanes over ligand atoms, NA atoms per lane and pass (NA = 2
 // gives every lane two independent dependency chains and halves the per-pass overheads).
 template <int RT, int NA>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
-                                           unsigned win_u32, const double4* s_lig, int lig_smem_n,
+                                           const char* win, const double2* s_lig, int lig_smem_n,
                                            int lane, PairStage<NA>& ps) {
+#ifdef RS_RM_PER_POSE
   double Rm[9], tv[3];
-  {
-    const double2* m2 = reinterpret_cast<const double2*>(pr.m);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      const double2 v = m2[i];
-      const int k0 = 2 * i, k1 = 2 * i + 1;
-      if (k0 < 9) Rm[k0] = v.x; else tv[k0 - 9] = v.x;
-      if (k1 < 9) Rm[k1] = v.y; else tv[k1 - 9] = v.y;
-    }
-  }
+  load_pose(pr, Rm, tv);
+#endif
   double hi[NA], lo[NA], best = INFINITY;
 #pragma unroll
   for (int u = 0; u < NA; ++u) hi[u] = lo[u] = 0.0;
@@ -445,13 +478,19 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   const double2* prec = reinterpret_cast<const double2*>(a.t.prec);
   const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   for (int l0 = 0; l0 < L; l0 += 32 * NA) {
+#ifndef RS_RM_PER_POSE
+    // the pose's R and t, re-read from shared memory (broadcast) each pass: they are live only
+    // during H2, which keeps registers for more resident warps
+    double Rm[9], tv[3];
+    load_pose(pr, Rm, tv);
+#endif
     AtomState st[NA];
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
-      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, st[u], bad);
-      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, st[u], bad);
+      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
+      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
     }
-    long_range_stage<RT, NA>(a, st, use_win, W, win_u32, rho, hi, lo);
+    long_range_stage<RT, NA>(a, st, use_win, W, win, rho, hi, lo);
     if (__any_sync(kFull, bad)) {
       bad = true;
       break;                      // the pose is invalid: NaN outputs, skip the rest
@@ -476,8 +515,11 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         seg[u] = s0;
-        ps.xz[32 * u + lane] = make_double4(st[u].x0, st[u].x1, st[u].x2, st[u].z);
-        ps.cb[32 * u + lane] = make_int4(st[u].i0, st[u].i1, st[u].i2, st[u].beg - s0);
+        if (st[u].cnt > 0) {        // only atoms with candidates are ever read back
+          ps.x01[32 * u + lane] = make_double2(st[u].x0, st[u].x1);
+          ps.x2z[32 * u + lane] = make_double2(st[u].x2, st[u].z);
+          ps.cb[32 * u + lane] = make_int4(st[u].i0, st[u].i1, st[u].i2, st[u].beg - s0);
+        }
         s0 += st[u].cnt;
       }
     }
@@ -522,10 +564,8 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
         const int k = base + 32 * q + lane;
         oc[q] = make_int4(0, 0, 0, 0);
         en[q] = oc[q];
-        if (k < total) {
-          oc[q] = ps.cb[ow[q]];
-          en[q] = __ldg(a.t.nb_ent + oc[q].w + k);
-        }
+        if (k < total) oc[q] = ps.cb[ow[q]];
+        en[q] = ldg_if(a.t.nb_ent + oc[q].w + k, k < total);
         dd[q] = k < total ? pair_dd(oc[q], en[q]) : 0xffffffffu;
         sr[q] = dd[q] <= a.ns2;
         nr[q] = sr[q] || dd[q] < a.vdw_cells2;
@@ -537,14 +577,16 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       for (int q = 0; q < kSlots; ++q) {
         xy[q] = make_double2(0.0, 0.0);
         zq[q] = xy[q];
-        if (nr[q]) {
-          xy[q] = ldg2(prec + 2 * en[q].z);
-          zq[q] = ldg2(prec + 2 * en[q].z + 1);
-        }
+        xy[q] = ldg_if(prec + 2 * en[q].z, nr[q]);
+        zq[q] = ldg_if(prec + 2 * en[q].z + 1, nr[q]);
       }
 #pragma unroll
       for (int q = 0; q < kSlots; ++q)
-        if (nr[q]) pair_term(a, ps.xz[ow[q]], dd[q], sv[q], xy[q], zq[q], hi[q % NA], lo[q % NA], best);
+        if (nr[q]) {
+          const double2 o01 = ps.x01[ow[q]], o2z = ps.x2z[ow[q]];
+          pair_term(a, make_double4(o01.x, o01.y, o2z.x, o2z.y), dd[q], sv[q], xy[q], zq[q],
+                    hi[q % NA], lo[q % NA], best);
+        }
     }
     __syncwarp();
   }
@@ -582,14 +624,14 @@ template <int RT, int NA>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
                                                             int lig_smem_n) {
   // dynamic shared memory: [factor-row window (256-B aligned)][PoseRec x kTile]
-  //                        [PairStage x warps][ligand double4 x lig_smem_n]
+  //                        [PairStage x warps][ligand 2 x double2 x lig_smem_n]
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
   unsigned char* base = smem_raw + ((256 - (smem_u32(smem_raw) & 255)) & 255);
   double2* win = reinterpret_cast<double2*>(base);
   PoseRec* s_pose = reinterpret_cast<PoseRec*>(base + (size_t)cap_rows * kChp * 16);
   PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(s_pose + kTile);
-  double4* s_lig = reinterpret_cast<double4*>(s_ps + kWarps);
+  double2* s_lig = reinterpret_cast<double2*>(s_ps + kWarps);   // [lig_smem_n] (y0,y1), then (y2,z)
   __shared__ int s_ok[kTile];
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
@@ -604,7 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     const double y0 = __ldg(a.yl + 3 * (int64_t)l), y1 = __ldg(a.yl + 3 * (int64_t)l + 1),
                  y2 = __ldg(a.yl + 3 * (int64_t)l + 2);
     r2 = fmax(r2, y0 * y0 + y1 * y1 + y2 * y2);
-    if (l < lig_smem_n) s_lig[l] = make_double4(y0, y1, y2, __ldg(a.zl + l));
+    if (l < lig_smem_n) {
+      s_lig[l] = make_double2(y0, y1);
+      s_lig[lig_smem_n + l] = make_double2(y2, __ldg(a.zl + l));
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) r2 = fmax(r2, __shfl_xor_sync(kFull, r2, off));
@@ -762,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(kFull, s, 0);
         if (s >= T) break;
-        score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, smem_u32(win), s_lig, lig_smem_n,
+        score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
                            lane, s_ps[warp]);
       }
       __syncthreads();
@@ -894,11 +939,12 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
     const double row_b = 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
     window_mode = rows * row_b <= 0.75 * double(dc.smem_optin);
   }
-  // two atoms per lane and pass when the ligand has more than 32 atoms
+  // one atom per lane and pass (NA = 2, two independent chains per lane, needs the registers
+  // of a 512-thread CTA and measured slower than 32 resident warps with NA = 1)
 #ifdef RS_FORCE_NA
   const int na = RS_FORCE_NA, sl = na == 2 ? 8 : 0;
 #else
-  const int na = a.L > 32 ? 2 : 1, sl = na == 2 ? 8 : 0;
+  const int na = (kThreads <= 512 && a.L > 32) ? 2 : 1, sl = na == 2 ? 8 : 0;
 #endif
   int e;
   switch (a.R * 4 + na) {
