@@ -87,6 +87,13 @@ __device__ __forceinline__ double2 ldg_if(const double2* p, bool pr) {
       : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((int)pr));
   return v;
 }
+// one 256-bit load (LDG.E.ENL2.256 on sm_100): one L1 tag lookup for a 32-byte record
+__device__ __forceinline__ double4 ldg_if(const double4* p, bool pr) {
+  double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n}"
+      : "+d"(v.x), "+d"(v.y), "+d"(v.z), "+d"(v.w) : "l"(p), "r"((int)pr));
+  return v;
+}
 __device__ __forceinline__ int2 ldg_if(const int2* p, bool pr) {
   int2 v = make_int2(0, 0);
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.global.nc.v2.s32 {%0, %1}, [%2];\n}"
@@ -234,7 +241,14 @@ __device__ __noinline__ double long_phi_global(const double* F0, const double* F
 
 struct Window {
   int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
+#ifdef RS_NB_BITMAP
+  int blo[3], bdim[3];         // coarse cells covered by the occupancy bitmap (bdim 0: none)
+#endif
 };
+
+#ifdef RS_NB_BITMAP
+constexpr int kBitWords = 2048;  // occupancy bitmap of the window's coarse cells (64 K cells)
+#endif
 
 struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
   double m[12];
@@ -336,7 +350,7 @@ struct AtomState {
 template <bool LIG_SMEM>
 __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
                                            const double* tv, const double2* s_lig, int lig_n,
-                                           AtomState& st,
+                                           const Window& W, const unsigned* bits, AtomState& st,
                                            bool& bad) {
   const bool act = l < a.L;
   const int lc = act ? l : a.L - 1;
@@ -379,7 +393,20 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
   const unsigned cy = (unsigned)((st.i1 >> a.nb_shift) - a.nb_lo[1]);
   const unsigned cz = (unsigned)((st.i2 >> a.nb_shift) - a.nb_lo[2]);
   {
-    const bool in = st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
+    bool maybe = true;
+#ifdef RS_NB_BITMAP
+    {
+      // coarse cells of the window: a shared-memory bitmap says whether the list is empty
+      const unsigned bx = (unsigned)((st.i0 >> a.nb_shift) - W.blo[0]);
+      const unsigned by = (unsigned)((st.i1 >> a.nb_shift) - W.blo[1]);
+      const unsigned bz = (unsigned)((st.i2 >> a.nb_shift) - W.blo[2]);
+      if (bx < (unsigned)W.bdim[0] && by < (unsigned)W.bdim[1] && bz < (unsigned)W.bdim[2]) {
+        const unsigned c = (bx * W.bdim[1] + by) * W.bdim[2] + bz;
+        maybe = (bits[c >> 5] >> (c & 31)) & 1u;
+      }
+    }
+#endif
+    const bool in = maybe && st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
     const int2 bc = ldg_if(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz, in);
     st.beg = bc.x;
     st.cnt = bc.y;
@@ -463,7 +490,7 @@ template <int RT, int NA>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
                                            const char* win, const double2* s_lig, int lig_smem_n,
-                                           int lane, PairStage<NA>& ps) {
+                                           const unsigned* bits, int lane, PairStage<NA>& ps) {
 #ifdef RS_RM_PER_POSE
   double Rm[9], tv[3];
   load_pose(pr, Rm, tv);
@@ -475,20 +502,29 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   const int rho = lane & 7;
   const bool lig_all_smem = a.L <= lig_smem_n;
   const int L = ok ? a.L : 0;
-  const double2* prec = reinterpret_cast<const double2*>(a.t.prec);
   const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   for (int l0 = 0; l0 < L; l0 += 32 * NA) {
 #ifndef RS_RM_PER_POSE
     // the pose's R and t, re-read from shared memory (broadcast) each pass: they are live only
     // during H2, which keeps registers for more resident warps
     double Rm[9], tv[3];
+#ifdef RS_POSE_SHFL
+    {
+      const double v = lane < 12 ? pr.m[lane] : 0.0;   // one 96-byte shared load, then shuffles
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Rm[i] = __shfl_sync(kFull, v, i);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tv[i] = __shfl_sync(kFull, v, 9 + i);
+    }
+#else
     load_pose(pr, Rm, tv);
+#endif
 #endif
     AtomState st[NA];
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
-      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
-      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
+      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
+      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
     }
     long_range_stage<RT, NA>(a, st, use_win, W, win, rho, hi, lo);
     if (__any_sync(kFull, bad)) {
@@ -577,8 +613,9 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       for (int q = 0; q < kSlots; ++q) {
         xy[q] = make_double2(0.0, 0.0);
         zq[q] = xy[q];
-        xy[q] = ldg_if(prec + 2 * en[q].z, nr[q]);
-        zq[q] = ldg_if(prec + 2 * en[q].z + 1, nr[q]);
+        const double4 r4 = ldg_if(a.t.prec + en[q].z, nr[q]);
+        xy[q] = make_double2(r4.x, r4.y);
+        zq[q] = make_double2(r4.z, r4.w);
       }
 #pragma unroll
       for (int q = 0; q < kSlots; ++q)
@@ -636,6 +673,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
   __shared__ int s_next, s_restaged, s_chunk;
+#ifdef RS_NB_BITMAP
+  __shared__ unsigned s_bits[kBitWords];
+#endif
   __shared__ double s_rmax2[kWarps];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -658,6 +698,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     s_cur.lo[0] = s_cur.lo[1] = s_cur.lo[2] = 1;
     s_cur.hi[0] = s_cur.hi[1] = s_cur.hi[2] = 0;   // empty
     s_cur.off[0] = s_cur.off[1] = s_cur.off[2] = 0;
+#ifdef RS_NB_BITMAP
+    s_cur.bdim[0] = s_cur.bdim[1] = s_cur.bdim[2] = 0;
+    s_cur.blo[0] = s_cur.blo[1] = s_cur.blo[2] = 0;
+#endif
     mbar_init(&s_bar);
   }
   __syncthreads();
@@ -781,6 +825,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               s_cur.lo[r] = lo_[r];
               s_cur.hi[r] = hi_[r];
               s_cur.off[r] = row0 - lo_[r];
+#ifdef RS_NB_BITMAP
+              {
+                const int c0 = max(lo_[r] >> a.nb_shift, a.nb_lo[r]);
+                const int c1 = min(hi_[r] >> a.nb_shift, a.nb_lo[r] + a.nb_dim[r] - 1);
+                s_cur.blo[r] = c0;
+                s_cur.bdim[r] = max(c1 - c0 + 1, 0);
+              }
+#endif
               tma_load_1d(win + (size_t)row0 * kChp, a.t.Fw[r] + (size_t)lo_[r] * kChp,
                           (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
               row0 += hi_[r] - lo_[r] + 1;
@@ -800,6 +852,31 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       if (s_restaged) {
         mbar_wait(&s_bar, phase);
         phase ^= 1;
+#ifdef RS_NB_BITMAP
+        {
+          // occupancy bitmap of the new window's coarse cells (bit = list not empty)
+          const int d0 = s_cur.bdim[0], d1 = s_cur.bdim[1], d2 = s_cur.bdim[2];
+          const int ncell = d0 * d1 * d2;
+          if (ncell > 32 * kBitWords) {
+            __syncthreads();
+            if (tid == 0) s_cur.bdim[0] = s_cur.bdim[1] = s_cur.bdim[2] = 0;
+          } else {
+            for (int w0 = 0; w0 < (ncell + 31) / 32; w0 += kWarps) {
+              const int c = (w0 + warp) * 32 + lane;
+              bool occ = false;
+              if (c < ncell) {
+                const int x = c / (d1 * d2), y = (c / d2) % d1, z = c % d2;
+                const int g = ((x + s_cur.blo[0] - a.nb_lo[0]) * a.nb_dim[1] + (y + s_cur.blo[1] - a.nb_lo[1])) *
+                                  a.nb_dim[2] + (z + s_cur.blo[2] - a.nb_lo[2]);
+                occ = __ldg(a.t.nb_range + g).y > 0;
+              }
+              const unsigned m = __ballot_sync(kFull, occ);
+              if (lane == 0 && w0 + warp < kBitWords) s_bits[w0 + warp] = m;
+            }
+          }
+          __syncthreads();
+        }
+#endif
       }
       const Window W = s_cur;
       for (;;) {
@@ -807,8 +884,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(kFull, s, 0);
         if (s >= T) break;
+#ifdef RS_NB_BITMAP
+        const unsigned* bits = s_bits;
+#else
+        const unsigned* bits = nullptr;
+#endif
         score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
-                           lane, s_ps[warp]);
+                           bits, lane, s_ps[warp]);
       }
       __syncthreads();
       p += T;
