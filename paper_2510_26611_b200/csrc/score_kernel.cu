@@ -657,18 +657,23 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   }
 }
 
+template <int NA>
+__host__ __device__ constexpr size_t win_offset() {
+  return ((sizeof(PoseRec) * kTile + sizeof(PairStage<NA>) * kWarps) + 255) / 256 * 256;
+}
+
 template <int RT, int NA>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
                                                             int lig_smem_n) {
-  // dynamic shared memory: [factor-row window (256-B aligned)][PoseRec x kTile]
-  //                        [PairStage x warps][ligand 2 x double2 x lig_smem_n]
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // dynamic shared memory (256-B aligned base; every offset but the ligand's is a compile-time
+  // constant, so addresses are immediates rather than recomputed values):
+  //   [PoseRec x kTile][PairStage x warps][factor-row window, 256-B aligned][ligand 2 x double2 x n]
+  extern __shared__ __align__(256) unsigned char smem_raw[];
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  unsigned char* base = smem_raw + ((256 - (smem_u32(smem_raw) & 255)) & 255);
-  double2* win = reinterpret_cast<double2*>(base);
-  PoseRec* s_pose = reinterpret_cast<PoseRec*>(base + (size_t)cap_rows * kChp * 16);
-  PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(s_pose + kTile);
-  double2* s_lig = reinterpret_cast<double2*>(s_ps + kWarps);   // [lig_smem_n] (y0,y1), then (y2,z)
+  PoseRec* s_pose = reinterpret_cast<PoseRec*>(smem_raw);
+  PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(smem_raw + sizeof(PoseRec) * kTile);
+  double2* win = reinterpret_cast<double2*>(smem_raw + win_offset<NA>());
+  double2* s_lig = reinterpret_cast<double2*>(smem_raw + win_offset<NA>() + (size_t)cap_rows * kChp * 16);
   __shared__ int s_ok[kTile];
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
@@ -920,7 +925,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
     dc.attr_set[slot] = true;
   }
   constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
-  const size_t fixed = 256 + sizeof(PoseRec) * kTile + sizeof(PairStage<NA>) * kWarps;
+  const size_t fixed = win_offset<NA>();
   const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
   const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
   int cap_rows = 0;
