@@ -175,11 +175,33 @@ __device__ __forceinline__ double halving_tree(double* s) {
 // groups whatever rows they read.  Physical chunk p holds pair p (padded widths: zero beyond CH;
 // replicated widths: pair p mod CH), so slot c holds pair (c ^ rho) mod NS, and the halving
 // tree, which combines c with c ^ m at every level, is bitwise invariant under that relabelling.
+// The halving tree evaluated depth-first: T(c, stride, cnt) = T(c, 2 stride, cnt/2) +
+// T(c + stride, 2 stride, cnt/2), leaves = slot pair sums.  Same pairings as the level-by-level
+// loop (pair c meets c + NS/2 first), but partial sums retire as soon as their chunks arrive,
+// so fewer values are live while the gathers are in flight.
+template <int C, int STRIDE, int CNT>
+struct SmemTree {
+  static __device__ __forceinline__ double eval(const char* win, unsigned r0, unsigned r1,
+                                                unsigned r2) {
+    if constexpr (CNT == 1) {
+      constexpr unsigned o = (unsigned)C << 4;
+      return pair_prod(*reinterpret_cast<const double2*>(win + (r0 ^ o)),
+                       *reinterpret_cast<const double2*>(win + (r1 ^ o)),
+                       *reinterpret_cast<const double2*>(win + (r2 ^ o)));
+    } else {
+      const double lhs = SmemTree<C, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      const double rhs = SmemTree<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      return __dadd_rn(lhs, rhs);
+    }
+  }
+};
+
 template <int R>
 __device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, unsigned r1,
                                                 unsigned r2, int rho) {
   using G = Geo<R>;
   const unsigned x = (unsigned)rho << 4;
+#ifdef RS_TREE_LEVELS
   r0 |= x;
   r1 |= x;
   r2 |= x;
@@ -192,6 +214,9 @@ __device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, un
                      *reinterpret_cast<const double2*>(win + (r2 ^ o)));
   }
   return halving_tree<G::NS>(s);
+#else
+  return SmemTree<0, 1, G::NS>::eval(win, r0 | x, r1 | x, r2 | x);
+#endif
 }
 
 // O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
