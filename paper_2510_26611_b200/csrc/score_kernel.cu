@@ -43,10 +43,10 @@ namespace {
 #define RS_THREADS 1024
 #endif
 #ifndef RS_TILE
-#define RS_TILE 256
+#define RS_TILE 512
 #endif
 #ifndef RS_CHUNK
-#define RS_CHUNK 256
+#define RS_CHUNK 512
 #endif
 #ifndef RS_WIN_SLACK
 #define RS_WIN_SLACK 1.03
@@ -515,7 +515,8 @@ template <int RT, int NA>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
                                            const char* win, const double2* s_lig, int lig_smem_n,
-                                           const unsigned* bits, int lane, PairStage<NA>& ps) {
+                                           const unsigned* bits, int lane, PairStage<NA>& ps,
+                                           double2& out) {
 #ifdef RS_RM_PER_POSE
   double Rm[9], tv[3];
   load_pose(pr, Rm, tv);
@@ -673,11 +674,10 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
     mhi = __reduce_min_sync(kFull, bhi);
     mlo = __reduce_min_sync(kFull, bhi == mhi ? (unsigned)bb : 0xffffffffu);
   }
-  // H8
+  // H8 is finished per tile (one thread per pose, coalesced stores): keep E and min d^2
   if (lane == 0) {
-    const double m = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-    a.E[p] = bad ? NAN : __dadd_rn(H, Lo);
-    a.D[p] = bad ? NAN : (m < a.dcap2 ? __dsqrt_rn(m) : INFINITY);
+    out.x = bad ? NAN : __dadd_rn(H, Lo);
+    out.y = bad ? NAN : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
     if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
   }
 }
@@ -700,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   double2* win = reinterpret_cast<double2*>(smem_raw + win_offset<NA>());
   double2* s_lig = reinterpret_cast<double2*>(smem_raw + win_offset<NA>() + (size_t)cap_rows * kChp * 16);
   __shared__ int s_ok[kTile];
+  __shared__ double2 s_out[kTile];    // per pose of the tile: (E, min d^2), NaN if invalid
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
   __shared__ int s_next, s_restaged, s_chunk;
@@ -920,9 +921,15 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         const unsigned* bits = nullptr;
 #endif
         score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
-                           bits, lane, s_ps[warp]);
+                           bits, lane, s_ps[warp], s_out[s]);
       }
       __syncthreads();
+      // H8: d = sqrt(min d^2) below D_cap^2, else +inf; NaN for invalid poses (O8)
+      if (tid < T) {
+        const double2 o = s_out[tid];
+        a.E[p + tid] = o.x;
+        a.D[p + tid] = isnan(o.y) ? NAN : (o.y < a.dcap2 ? __dsqrt_rn(o.y) : INFINITY);
+      }
       p += T;
     }
   }
