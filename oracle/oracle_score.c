@@ -122,6 +122,38 @@ double oracle_long_value(const double *F1, const double *F2, const double *F3, i
     return s[0];
 }
 
+/* ---- O4-f32: the fp32-factor variant of O4 (north_star: "an fp32-factor variant"; DESIGN.md
+ * reading A21).  Each factor entry is rounded to binary32, f = fl32(F); then, in binary32,
+ *   q_k = (f1[i0][k] * f2[i1][k]) * f3[i2][k]      for k < R,   q_k = 0 for R <= k < 4 C4,
+ *   C4  = smallest power of two >= ceil(R/4)       (number of rank quads),
+ *   s_c = (q_4c + q_4c+1) + (q_4c+2 + q_4c+3)      for c < C4,
+ *   for m = C4/2, ..., 1:  s_c = s_c + s_{c+m}      for c < m,
+ *   phi = (double) s_0                              (exact widening).
+ * The energy accumulation (O6) stays double-double in binary64. */
+double oracle_long_value_f32(const double *F1, const double *F2, const double *F3, int R,
+                             int i0, int i1, int i2)
+{
+    const double *a = F1 + (int64_t)i0 * R, *b = F2 + (int64_t)i1 * R, *c = F3 + (int64_t)i2 * R;
+    int C = 1;
+    while (4 * C < R) C *= 2;
+    float s[C];
+    for (int j = 0; j < C; ++j) {
+        float q[4];
+        for (int t = 0; t < 4; ++t) {
+            int k = 4 * j + t;
+            q[t] = 0.0f;
+            if (k < R) {
+                float fa = (float)a[k], fb = (float)b[k], fc = (float)c[k];
+                q[t] = (fa * fb) * fc;
+            }
+        }
+        s[j] = (q[0] + q[1]) + (q[2] + q[3]);
+    }
+    for (int m = C / 2; m >= 1; m /= 2)
+        for (int j = 0; j < m; ++j) s[j] = s[j] + s[j + m];
+    return (double)s[0];
+}
+
 /* ---- O5: short-range reference value S(Delta) for |Delta|_2 <= n_sigma (Def. 2.1) ---- */
 double oracle_short_value(const double *S1, const double *S2, const double *S3, int Rs,
                           int n_sigma, int d0, int d1, int d2)
@@ -141,7 +173,8 @@ double oracle_short_value(const double *S1, const double *S2, const double *S3, 
  *   X (M x 3), zM (M)      : protein atoms (continuous coordinates) and charges
  *   Y (L x 3), zL (L)      : ligand body coordinates (centred) and charges
  *   poses (P x 7)          : w,x,y,z,tx,ty,tz
- *   long_only != 0         : skip O5 and O7 (Lemma 3.2's cost alone; CPU like-for-like rate)
+ *   mode                   : bit 0 = long_only: skip O5 and O7 (Lemma 3.2's cost alone; the CPU
+ *                            like-for-like rate); bit 1 = fp32 factors (O4-f32 instead of O4)
  * Outputs E (P), dmin (P).  Returns the number of invalid poses (O8: NaN outputs).
  * Protein cells are recomputed here with oracle_snap (never taken from the library).
  */
@@ -149,9 +182,10 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
                            const double *F3, int n_sigma, int Rs, const double *S1,
                            const double *S2, const double *S3, int64_t M, const double *X,
                            const double *zM, int64_t L, const double *Y, const double *zL,
-                           int64_t P, const double *poses, double dcap, int long_only,
+                           int64_t P, const double *poses, double dcap, int mode,
                            double *E, double *dmin)
 {
+    int long_only = mode & 1, f32 = (mode >> 1) & 1;
     double inv_h = (double)n / (2.0 * b);
     int *iM = (int *)malloc(sizeof(int) * 3 * (size_t)(M > 0 ? M : 1));
     for (int64_t m = 0; m < M; ++m)
@@ -177,7 +211,8 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
             }
             if (!ok) break;
             /* O4 */
-            double phi = oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
+            double phi = f32 ? oracle_long_value_f32(F1, F2, F3, R, il[0], il[1], il[2])
+                             : oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
             dd_add_product(&acc, zL[l], phi);
             if (long_only) continue;
             for (int64_t m = 0; m < M; ++m) {

@@ -53,6 +53,8 @@ def lib():
         L.oracle_long_value.argtypes = [dp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_int]
         L.oracle_long_value.restype = ctypes.c_double
+        L.oracle_long_value_f32.argtypes = L.oracle_long_value.argtypes
+        L.oracle_long_value_f32.restype = ctypes.c_double
         L.oracle_score_poses.argtypes = [
             ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, dp, ctypes.c_int, ctypes.c_int,
             dp, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp,
@@ -312,8 +314,8 @@ def K_h(delta, h, order=12):
 # O1-O8 scorer (C) wrapper
 # ------------------------------------------------------------------------------------------
 
-def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False):
-    """Per-pose (E, dmin, n_invalid) from exported tables.
+def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=False):
+    """Per-pose (E, dmin, n_invalid) from exported tables (f32: the O4-f32 long-range part).
 
     tables: n, b, R, F1, F2, F3 (n x R), n_sigma, Rs, S1, S2, S3 ((2 n_sigma+1) x Rs)."""
     n, b = int(tables["n"]), float(tables["b"])
@@ -330,7 +332,8 @@ def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False):
     inv = lib().oracle_score_poses(
         n, b, R, _p(F1), _p(F2), _p(F3), ns, Rs, _p(S1 if S1.size else dummy),
         _p(S2 if S2.size else dummy), _p(S3 if S3.size else dummy), X.shape[0], _p(X), _p(qM),
-        Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap), 1 if long_only else 0, _p(E), _p(d))
+        Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap),
+        (1 if long_only else 0) | (2 if f32 else 0), _p(E), _p(d))
     return E, d, int(inv)
 
 

@@ -496,3 +496,95 @@ def test_table2_first_order_grid_convergence(oracle):
         errs.append(np.mean(e))
     ratios = [errs[i] / errs[i + 1] for i in range(3)]
     assert all(1.4 < r < 2.9 for r in ratios), (errs, ratios)
+
+
+# ---------------------------------------------------------------------------------- O4-f32
+def _lv32(oracle, F1, F2, F3, i=(0, 0, 0)):
+    c = lambda x: oracle._p(np.ascontiguousarray(x, dtype=np.float64))
+    return oracle.lib().oracle_long_value_f32(c(F1), c(F2), c(F3), F1.shape[1], *i)
+
+
+def test_long_value_f32_exact_tables_equal_fp64(oracle):
+    """Tables of small integers times powers of two: every product and partial sum is exact in
+    binary32, so O4-f32 must equal O4 bit for bit (pins indexing, padding and widening)."""
+    rng = np.random.default_rng(3)
+    for R in [1, 3, 4, 5, 8, 12, 16, 24, 32]:
+        # |entries| <= 8 on a 2^-1 grid: products on a 2^-3 grid below 2^9, sums below 2^14,
+        # so every binary32 intermediate is exact
+        F = [rng.integers(-4, 5, size=(6, R)).astype(float) * 2.0 ** rng.integers(-1, 2, size=(6, R))
+             for _ in range(3)]
+        for i in [(0, 1, 2), (5, 5, 5), (3, 0, 4)]:
+            assert _lv32(oracle, *F, i=i) == _lv(oracle, *F, i=i)
+
+
+def test_long_value_f32_order_worked_example(oracle):
+    """O4-f32 order (reading A21), worked by hand in binary32 with
+    q = (2^24, 1, 1, -2^24, 3) (R = 5, C4 = 2 quads):
+      quad 0: (2^24 + 1) + (1 - 2^24) = 2^24 + (-(2^24 - 1)) = 1   [2^24 + 1 ties to 2^24]
+      quad 1: (3 + 0) + (0 + 0) = 3;  phi = 1 + 3 = 4.
+    The exact sum is 5; the sequential binary32 chain gives 3 (its first three terms round to 2^24)."""
+    q = np.array([[2.0 ** 24, 1.0, 1.0, -2.0 ** 24, 3.0]])
+    ones = np.ones_like(q)
+    assert _lv32(oracle, q, ones, ones) == 4.0
+    # inputs are rounded to binary32 first: 1 + 2^-30 becomes 1
+    assert _lv32(oracle, np.array([[1.0 + 2.0 ** -30]]), np.ones((1, 1)), np.ones((1, 1))) == 1.0
+    # and the product is rounded as (f1 f2) f3 in binary32
+    t = float(np.float32(1.0 / 3.0))
+    assert _lv32(oracle, np.array([[3.0]]), np.array([[1.0 / 3.0]]), np.array([[3.0]])) == \
+        float((np.float32(3.0) * np.float32(t)) * np.float32(3.0))
+
+
+@pytest.mark.parametrize("R", [4, 8, 12, 16, 24, 32])
+def test_long_value_f32_rotation_invariance_and_bound(oracle, R):
+    """Invariant under cyclic rotations of the rank quads (the kernel's XOR chunk order relies on
+    it) and within gamma_k sum |q| of the exact sum of the products of the binary32-rounded
+    factors, k = 2 (products) + 2 (quad) + log2(C4), u = 2^-24."""
+    rng = np.random.default_rng(100 + R)
+    C = 1
+    while 4 * C < R:
+        C *= 2
+    for trial in range(40):
+        F = [rng.normal(size=(1, 4 * C)) * np.exp(rng.normal(0, 2, size=(1, 4 * C))) for _ in range(3)]
+        for f in F:
+            f[:, R:] = 0.0
+        base = _lv32(oracle, *[f[:, :R] for f in F])
+        for rot in range(1, C):
+            perm = np.concatenate([np.arange(4 * ((c + rot) % C), 4 * ((c + rot) % C) + 4) for c in range(C)])
+            assert _lv32(oracle, *[f[:, perm] for f in F]) == base
+        g = [np.float32(f[0, :R]).astype(np.float64) for f in F]
+        ex = sum(Fraction(float(g[0][k])) * Fraction(float(g[1][k])) * Fraction(float(g[2][k]))
+                 for k in range(R))
+        mag = float(np.sum(np.abs(g[0] * g[1] * g[2])))
+        k = 4 + int(np.log2(C))
+        u = 2.0 ** -24
+        assert abs(float(Fraction(base) - ex)) <= k * u / (1 - k * u) * mag * (1 + 1e-9)
+
+
+def test_scorer_f32_mode_matches_long_value_f32(oracle):
+    """mode bit 1 routes O4 through O4-f32: a one-atom ligand at the identity pose scores
+    z * O4-f32 at its cell, and the fp32 energies stay within 1e-6 of sum |z phi| of fp64's."""
+    rng = np.random.default_rng(8)
+    n, b, R = 32, 8.0, 12
+    F = [rng.normal(size=(n, R)) for _ in range(3)]
+    tables = _tables(F, n=n, b=b)
+    X = np.array([[7.9, 7.9, 7.9]])
+    qM = np.array([0.0])
+    Y = np.zeros((1, 3))
+    zL = np.array([0.75])
+    poses = np.array([[1.0, 0.0, 0.0, 0.0, 1.3, -2.2, 0.4]])
+    E, _, _ = oracle.score_poses(tables, X, qM, Y, zL, poses, 1.0, long_only=True, f32=True)
+    inv_h = n / (2 * b)
+    i = tuple(int(oracle.lib().oracle_snap(float(v), b, inv_h, n)) for v in poses[0, 4:])
+    assert E[0] == 0.75 * _lv32(oracle, *F, i=i)
+    Yb = rng.normal(size=(40, 3))
+    zb = rng.uniform(-1, 1, 40)
+    pb = np.c_[np.tile([1.0, 0, 0, 0], (30, 1)), rng.uniform(-3, 3, size=(30, 3))]
+    E32, _, _ = oracle.score_poses(tables, X, qM, Yb, zb, pb, 1.0, long_only=True, f32=True)
+    E64, _, _ = oracle.score_poses(tables, X, qM, Yb, zb, pb, 1.0, long_only=True)
+    for p in range(30):
+        S = 0.0
+        for l in range(40):
+            x = Yb[l] + pb[p, 4:]
+            il = tuple(int(oracle.lib().oracle_snap(float(v), b, inv_h, n)) for v in x)
+            S += abs(zb[l] * _lv(oracle, *F, i=il))
+        assert abs(E32[p] - E64[p]) <= 1e-6 * S
