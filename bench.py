@@ -118,20 +118,20 @@ def load_workload(name):
     return syn.make(name)
 
 
-def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7):
+def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7, f32=False):
     """Time the oracle (as it stands) on a bounded seeded sample of the workload's poses."""
     from oracle import rs_oracle
     from synth import configs as syn
     _, probe = syn.subsample(w.poses, 64, seed=seed)
     t0 = time.perf_counter()
     rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, probe,
-                          w.dmin_cap)
+                          w.dmin_cap, f32=f32)
     dt = time.perf_counter() - t0
     k = int(min(max_poses, max(64, 64 * budget_s / max(dt, 1e-6))))
     idx, sample = syn.subsample(w.poses, k, seed=seed + 1)
     t0 = time.perf_counter()
     rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, sample,
-                          w.dmin_cap)
+                          w.dmin_cap, f32=f32)
     dt = time.perf_counter() - t0
     return k, dt, rs_oracle.num_threads()
 
@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--f32", action="store_true",
+                    help="the fp32-factor variant (RS_FLAG_F32_FACTORS, DESIGN.md reading A21)")
     ap.add_argument("--nbr-cell", type=float, default=0.0,
                     help="edge [A] of the neighbour-list cells (0 = the library's automatic choice)")
     args = ap.parse_args()
@@ -228,7 +230,8 @@ def main():
     t0 = time.perf_counter()
     prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
                           device=local, n_threads=max(1, ncpu // max(world, 1)),
-                          nbr_cell=args.nbr_cell)
+                          nbr_cell=args.nbr_cell,
+                          flags=rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0)
     setup_s = time.perf_counter() - t0
     info = prot.info
 
@@ -304,13 +307,14 @@ def main():
     mb = None if args.no_microbench else run_microbench()
     peaks = _peaks()
     R = info["R"]
-    gather_bytes = 24.0 * R * P * L                 # H4: 3 rows x R fp64 per atom evaluation
+    fbytes = 4.0 if args.f32 else 8.0
+    gather_bytes = 3.0 * fbytes * R * P * L         # H4: 3 rows x R factors per atom evaluation
     t_s = ms * 1e-3
     achieved = gather_bytes / t_s / 1e9
     smem_peak = mb.get("lds128_random_row_rotated_gbs") if mb else None
     l2_peak = mb.get("l2_gather_1p5MB_gbs") if mb else None
     fp64_rate = mb.get("dfma_instr_per_s") if mb else None
-    dp_instr = (3.0 * R + 25.0) * P * L            # R DMUL + R DMUL + R DADD + ~25 per atom
+    dp_instr = ((0.0 if args.f32 else 3.0 * R) + 25.0) * P * L   # 2R DMUL + R DADD + ~25 per atom
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tfile):
@@ -331,14 +335,15 @@ def main():
     }
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        k, dt, cores = cpu_reference_rate(w, prot.export_tables())
+        k, dt, cores = cpu_reference_rate(w, prot.export_tables(), f32=args.f32)
         cpu = {"value": k / dt, "unit": "poses/s", "cores": cores, "kind": "oracle",
                "sample": f"{k} seeded poses of {w.name} ({dt:.1f} s; brute-force short-range/vdW "
                          f"over all {w.M} protein atoms)"}
     line = {
         "metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32-factors/f64" if args.f32 else "f64",
         "data": "synthetic", "atom_evals_per_s": value * L,
         "config": config_dict(w, args),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -49,6 +49,11 @@ extern "C" {
 #define RS_E_NO_DEVICE   (-4) /* handle built with RS_FLAG_HOST_ONLY or no CUDA device     */
 
 #define RS_FLAG_HOST_ONLY 1u  /* build the tables on the host only (no upload); for tests */
+#define RS_FLAG_F32_FACTORS 2u /* score with the long-range factors rounded to binary32 (the
+                                  north_star's fp32-factor variant, reading A21):
+                                  half the gather bytes, products and rank sums in binary32,
+                                  energies within 1e-6 of sum_l |z_l phi(x_l)| of the binary64
+                                  path; needs a compiled width R in {4, 8, 12, 16, 24, 32} */
 
 typedef struct rs_handle rs_handle; /* opaque, immutable after build */
 
@@ -103,6 +108,7 @@ typedef struct {
     int64_t  device_bytes;  /* bytes uploaded to the device */
     double   setup_seconds; /* wall time of the whole build */
     int32_t  on_device;     /* 1 when the tables are resident on a device */
+    int32_t  factor_bits;   /* 64, or 32 with RS_FLAG_F32_FACTORS */
 } rs_info;
 
 void rs_params_default(rs_params* p);

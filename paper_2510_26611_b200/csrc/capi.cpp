@@ -58,6 +58,7 @@ void free_device(rs_handle* h) {
   if (h->d_work) cudaFree(h->d_work);
   h->d_work = nullptr;
   for (void** p : {&h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
+                   &h->d_Fw32[0], &h->d_Fw32[1], &h->d_Fw32[2],
                    &h->d_nb_range}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -129,7 +130,14 @@ int upload_handle(rs_handle* h) {
     }
     if (int e = upload(&h->d_nb_range, rng, &bytes)) return e;
   }
-  if (rs::window_row_chunks(h->R) > 0) {
+  if (h->f32) {
+    // binary32 copy of the factors (A21), rows as 16-byte quads padded/replicated like Fw
+    std::vector<float> packed;
+    for (int a = 0; a < 3; ++a) {
+      rs::pack_window_rows32(h->F[a], h->n, h->R, packed);
+      if (int e = upload(&h->d_Fw32[a], packed, &bytes)) return e;
+    }
+  } else if (rs::window_row_chunks(h->R) > 0) {
     // row-padded copy of the factors: the shared-memory window is staged by 1-D bulk copies
     std::vector<double> packed;
     for (int a = 0; a < 3; ++a) {
@@ -171,6 +179,7 @@ rs::ScoreArgs base_args(const rs_handle* h) {
     a.nb_dim[i] = h->cg.dim[i];
     a.t.F[i] = (const double*)h->dmem[i];
     a.t.Fw[i] = (const double2*)h->d_Fw[i];
+    a.t.Fw32[i] = (const float4*)h->d_Fw32[i];
     a.t.S[i] = (const double*)h->dmem[3 + i];
   }
   a.t.nb_ent = (const int4*)h->d_nb_ent;
@@ -178,6 +187,7 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.t.short_memo = (const double*)h->d_memo;
   a.t.nb_range = (const int2*)h->d_nb_range;
   a.ns2 = (unsigned)((int64_t)h->n_sigma * h->n_sigma);
+  a.f32 = h->f32 ? 1 : 0;
   {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
     const double t = h->prm.dmin_cap / h->h + std::sqrt(3.0) + 2.0;
@@ -336,6 +346,12 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     // S5-S7
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
                             prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep);
+    hd->f32 = (prm.flags & RS_FLAG_F32_FACTORS) != 0;
+    if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
+      set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
+              std::to_string(hd->R));
+      return nullptr;
+    }
     if (hd->R > (1 << 20)) {
       set_err("compressed CP width " + std::to_string(hd->R) + " exceeds 2^20 (raise eps_compress or fix rank_R)");
       return nullptr;
@@ -406,6 +422,7 @@ int rs_get_info(const rs_handle* h, rs_info* out) {
   out->device_bytes = h->device_bytes;
   out->setup_seconds = h->setup_seconds;
   out->on_device = h->on_device ? 1 : 0;
+  out->factor_bits = h->f32 ? 32 : 64;
   return 0;
 }
 

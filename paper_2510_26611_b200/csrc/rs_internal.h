@@ -66,6 +66,7 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
 struct DeviceTables {
   const double* F[3] = {nullptr, nullptr, nullptr};
   const double2* Fw[3] = {nullptr, nullptr, nullptr};  // rows padded/replicated to CHP chunks
+  const float4* Fw32[3] = {nullptr, nullptr, nullptr}; // binary32 rows (A21), 16-byte quads
   const int2* nb_range = nullptr;     // per coarse cell: (list begin, count)
   const double* S[3] = {nullptr, nullptr, nullptr};
   const int4* nb_ent = nullptr;       // per list entry: (i0 | i1 << 16, i2, sorted atom, 0)
@@ -90,6 +91,7 @@ struct ScoreArgs {               // one launch of the scoring kernel
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
+  int f32;                       // long-range part from the binary32 factors (A21)
 };
 
 // Fill the dense short-range memo table s(d0,d1,d2), d_a = 0..n_sigma, with the O5 chain.
@@ -106,6 +108,9 @@ const char* score_kernel_variant(int R);
 // the host packing of that copy (rows padded with zeros or replicated to CHP chunks).
 int window_row_chunks(int R);
 void pack_window_rows(const std::vector<double>& F, int n, int R, std::vector<double>& out);
+// The same for the binary32 variant: rows of 16-byte quads of floats (0: width not compiled).
+int window_row_chunks32(int R);
+void pack_window_rows32(const std::vector<double>& F, int n, int R, std::vector<float>& out);
 
 }  // namespace rs
 
@@ -132,6 +137,8 @@ struct rs_handle {
   void* d_prec = nullptr;
   void* d_memo = nullptr;
   void* d_Fw[3] = {nullptr, nullptr, nullptr};
+  void* d_Fw32[3] = {nullptr, nullptr, nullptr};
+  bool f32 = false;
   void* d_nb_range = nullptr;
   int* d_work = nullptr;               // kWorkSlots zeroed-per-launch work counters
   std::atomic<unsigned> work_slot{0};

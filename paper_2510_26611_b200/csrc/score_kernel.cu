@@ -264,6 +264,62 @@ __device__ __noinline__ double long_phi_global(const double* F0, const double* F
                          (const double2*)(F2 + (size_t)i2 * RT));
 }
 
+// ---- the binary32-factor variant (reading A21) -----------------------------------
+// Rows of R floats as 16-byte quads of ranks: CHA = smallest power of two >= ceil(R/4) quads,
+// zero-padded, replicated to 8 chunks (128 B) when CHA < 8.
+template <int R>
+struct Geo32 {
+  static constexpr int CH = (R + 3) / 4;
+  static constexpr int CHA = CH <= 1 ? 1 : CH <= 2 ? 2 : CH <= 4 ? 4 : CH <= 8 ? 8 : 16;
+  static constexpr int CHP = CHA < 8 ? 8 : CHA;
+  static constexpr int NS = CHA;
+};
+
+// One rank quad: s_c = ((a0 b0) c0 + (a1 b1) c1) + ((a2 b2) c2 + (a3 b3) c3), binary32
+__device__ __forceinline__ float quad_prod(float4 a, float4 b, float4 c) {
+  const float q0 = __fmul_rn(__fmul_rn(a.x, b.x), c.x), q1 = __fmul_rn(__fmul_rn(a.y, b.y), c.y);
+  const float q2 = __fmul_rn(__fmul_rn(a.z, b.z), c.z), q3 = __fmul_rn(__fmul_rn(a.w, b.w), c.w);
+  return __fadd_rn(__fadd_rn(q0, q1), __fadd_rn(q2, q3));
+}
+
+// The quad halving tree, depth-first, from the shared-memory window (XOR chunk order as in
+// the binary64 path: the tree is invariant under the relabelling)
+template <int C, int STRIDE, int CNT>
+struct SmemTree32 {
+  static __device__ __forceinline__ float eval(const char* win, unsigned r0, unsigned r1,
+                                               unsigned r2) {
+    if constexpr (CNT == 1) {
+      constexpr unsigned o = (unsigned)C << 4;
+      return quad_prod(*reinterpret_cast<const float4*>(win + (r0 ^ o)),
+                       *reinterpret_cast<const float4*>(win + (r1 ^ o)),
+                       *reinterpret_cast<const float4*>(win + (r2 ^ o)));
+    } else {
+      const float lhs = SmemTree32<C, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      const float rhs = SmemTree32<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      return __fadd_rn(lhs, rhs);
+    }
+  }
+};
+
+// L2 path of O4-f32: rows of the packed binary32 copy, quads in natural order
+template <int R>
+__device__ __noinline__ double long_phi_global32(const float4* F0, const float4* F1,
+                                                 const float4* F2, int i0, int i1, int i2) {
+  using G = Geo32<R>;
+  const float4* r0 = F0 + (size_t)i0 * G::CHP;
+  const float4* r1 = F1 + (size_t)i1 * G::CHP;
+  const float4* r2 = F2 + (size_t)i2 * G::CHP;
+  float s[G::NS];
+#pragma unroll
+  for (int c = 0; c < G::NS; ++c) s[c] = quad_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
+#pragma unroll
+  for (int m = G::NS / 2; m >= 1; m /= 2) {
+#pragma unroll
+    for (int c = 0; c < m; ++c) s[c] = __fadd_rn(s[c], s[c + m]);
+  }
+  return (double)s[0];
+}
+
 struct Window {
   int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
 #ifdef RS_NB_BITMAP
@@ -441,7 +497,8 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
 
 // H4 (O4) for the NA atoms of a lane: atoms whose rows are staged read the window, real atoms
 // outside it (rare) read L2, lanes past the ligand's end skip it (phi = 0, weight z = 0).
-template <int RT, int NA>
+// F32: O4-f32 from the binary32 rows (A21).
+template <int RT, int NA, bool F32>
 __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomState* st,
                                                  bool use_win, const Window& W, const char* win,
                                                  int rho, double* hi, double* lo) {
@@ -449,8 +506,8 @@ __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomS
 #pragma unroll
   for (int u = 0; u < NA; ++u) phi[u] = 0.0;
   if constexpr (RT > 0) {
-    using G = Geo<RT>;
-    constexpr unsigned kRow = 16u * G::CHP;
+    constexpr int kChp = F32 ? Geo32<RT>::CHP : Geo<RT>::CHP;
+    constexpr unsigned kRow = 16u * kChp;
     bool l2[NA];
     unsigned r0[NA], r1[NA], r2[NA];
 #pragma unroll
@@ -470,13 +527,25 @@ __device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomS
 #if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
         phi[u] = st[u].z;
 #else
-        if (st[u].go && !l2[u]) phi[u] = long_phi_smem<RT>(win, r0[u], r1[u], r2[u], rho);
+        if (st[u].go && !l2[u]) {
+          if constexpr (F32) {
+            const unsigned x = (unsigned)rho << 4;
+            phi[u] = (double)SmemTree32<0, 1, Geo32<RT>::NS>::eval(win, r0[u] | x, r1[u] | x, r2[u] | x);
+          } else {
+            phi[u] = long_phi_smem<RT>(win, r0[u], r1[u], r2[u], rho);
+          }
+        }
 #endif
       }
     }
 #pragma unroll
     for (int u = 0; u < NA; ++u)
-      if (l2[u]) phi[u] = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], st[u].i0, st[u].i1, st[u].i2);
+      if (l2[u]) {
+        if constexpr (F32)
+          phi[u] = long_phi_global32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], st[u].i0, st[u].i1, st[u].i2);
+        else
+          phi[u] = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], st[u].i0, st[u].i1, st[u].i2);
+      }
   } else {
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
@@ -511,7 +580,7 @@ __device__ __forceinline__ void load_pose(const PoseRec& pr, double* Rm, double*
 
 // Score one pose with one warp: lanes over ligand atoms, NA atoms per lane and pass (NA = 2
 // gives every lane two independent dependency chains and halves the per-pass overheads).
-template <int RT, int NA>
+template <int RT, int NA, bool F32>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
                                            const char* win, const double2* s_lig, int lig_smem_n,
@@ -552,7 +621,7 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
       if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
       else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
     }
-    long_range_stage<RT, NA>(a, st, use_win, W, win, rho, hi, lo);
+    long_range_stage<RT, NA, F32>(a, st, use_win, W, win, rho, hi, lo);
     if (__any_sync(kFull, bad)) {
       bad = true;
       break;                      // the pose is invalid: NaN outputs, skip the rest
@@ -687,14 +756,14 @@ __host__ __device__ constexpr size_t win_offset() {
   return ((sizeof(PoseRec) * kTile + sizeof(PairStage<NA>) * kWarps) + 255) / 256 * 256;
 }
 
-template <int RT, int NA>
+template <int RT, int NA, bool F32>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
                                                             int lig_smem_n) {
   // dynamic shared memory (256-B aligned base; every offset but the ligand's is a compile-time
   // constant, so addresses are immediates rather than recomputed values):
   //   [PoseRec x kTile][PairStage x warps][factor-row window, 256-B aligned][ligand 2 x double2 x n]
   extern __shared__ __align__(256) unsigned char smem_raw[];
-  constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
+  constexpr int kChp = F32 ? Geo32<(RT > 0 ? RT : 4)>::CHP : Geo<(RT > 0 ? RT : 2)>::CHP;
   PoseRec* s_pose = reinterpret_cast<PoseRec*>(smem_raw);
   PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(smem_raw + sizeof(PoseRec) * kTile);
   double2* win = reinterpret_cast<double2*>(smem_raw + win_offset<NA>());
@@ -864,7 +933,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
                 s_cur.bdim[r] = max(c1 - c0 + 1, 0);
               }
 #endif
-              tma_load_1d(win + (size_t)row0 * kChp, a.t.Fw[r] + (size_t)lo_[r] * kChp,
+              const void* src = F32 ? (const void*)(a.t.Fw32[r] + (size_t)lo_[r] * kChp)
+                                    : (const void*)(a.t.Fw[r] + (size_t)lo_[r] * kChp);
+              tma_load_1d(win + (size_t)row0 * kChp, src,
                           (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
               row0 += hi_[r] - lo_[r] + 1;
             }
@@ -920,7 +991,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 #else
         const unsigned* bits = nullptr;
 #endif
-        score_pose<RT, NA>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
+        score_pose<RT, NA, F32>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
                            bits, lane, s_ps[warp], s_out[s]);
       }
       __syncthreads();
@@ -938,30 +1009,30 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 struct DevCache {
   int sms = 0;
   int smem_optin = 0;
-  bool attr_set[16] = {false};
-  int max_dyn[16] = {0};
+  bool attr_set[24] = {false};
+  int max_dyn[24] = {0};
 };
 DevCache g_dev[64];
 
-template <int RT, int NA>
+template <int RT, int NA, bool F32>
 int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window_mode) {
   DevCache& dc = g_dev[dev & 63];
   if (!dc.attr_set[slot]) {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT, NA>);
+    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT, NA, F32>);
     if (e != cudaSuccess) return (int)e;
     dc.max_dyn[slot] = dc.smem_optin - (int)fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(score_kernel<RT, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(score_kernel<RT, NA, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dc.max_dyn[slot]);
     if (e != cudaSuccess) return (int)e;
     dc.attr_set[slot] = true;
   }
-  constexpr int kChp = Geo<(RT > 0 ? RT : 2)>::CHP;
+  constexpr int kChp = F32 ? Geo32<(RT > 0 ? RT : 4)>::CHP : Geo<(RT > 0 ? RT : 2)>::CHP;
   const size_t fixed = win_offset<NA>();
   const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
   const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
   int cap_rows = 0;
-  if (RT > 0 && window_mode && a.t.Fw[0]) {
+  if (RT > 0 && window_mode && (F32 ? (const void*)a.t.Fw32[0] : (const void*)a.t.Fw[0])) {
     cap_rows = (int)std::min<size_t>((avail - lig_res) / (16 * kChp), (1u << 20) / (16 * kChp) - 1);
     if (a.rmax_hint >= 0) {
       // leave the rest of the 228 KB to L1 (cell lists, records, memo): what one
@@ -977,7 +1048,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   const int64_t chunks = (a.P + kChunk - 1) / kChunk;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
-  score_kernel<RT, NA><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
+  score_kernel<RT, NA, F32><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
   return (int)cudaGetLastError();
 }
 
@@ -1043,6 +1114,32 @@ void pack_window_rows(const std::vector<double>& F, int n, int R, std::vector<do
     }
 }
 
+int window_row_chunks32(int R) {
+  switch (R) {
+    case 4: return Geo32<4>::CHP;
+    case 8: return Geo32<8>::CHP;
+    case 12: return Geo32<12>::CHP;
+    case 16: return Geo32<16>::CHP;
+    case 24: return Geo32<24>::CHP;
+    case 32: return Geo32<32>::CHP;
+    default: return 0;
+  }
+}
+
+void pack_window_rows32(const std::vector<double>& F, int n, int R, std::vector<float>& out) {
+  const int chp = window_row_chunks32(R);
+  out.assign((size_t)n * chp * 4, 0.0f);
+  if (chp == 0) return;
+  int cha = 1;
+  while (4 * cha < R) cha *= 2;                       // quads incl. zero padding (A21)
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < chp; ++c)
+      for (int t = 0; t < 4; ++t) {
+        const int k = 4 * (c % cha) + t;              // replicated when cha < chp
+        out[((size_t)i * chp + c) * 4 + t] = k < R ? (float)F[(size_t)i * R + k] : 0.0f;
+      }
+}
+
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   if (a.P <= 0) return 0;
   DevCache& dc = g_dev[device & 63];
@@ -1055,7 +1152,7 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   bool window_mode = true;
   if (a.rmax_hint >= 0) {
     const double rows = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 4.0);
-    const double row_b = 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
+    const double row_b = a.f32 ? 128.0 : 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
     window_mode = rows * row_b <= 0.75 * double(dc.smem_optin);
   }
   // one atom per lane and pass (NA = 2, two independent chains per lane, needs the registers
@@ -1066,22 +1163,37 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   const int na = (kThreads <= 512 && a.L > 32) ? 2 : 1, sl = na == 2 ? 8 : 0;
 #endif
   int e;
-  switch (a.R * 4 + na) {
-    case 4 * 4 + 1: e = launch_t<4, 1>(a, st, device, 1 + sl, window_mode); break;
-    case 4 * 4 + 2: e = launch_t<4, 2>(a, st, device, 1 + sl, window_mode); break;
-    case 8 * 4 + 1: e = launch_t<8, 1>(a, st, device, 2 + sl, window_mode); break;
-    case 8 * 4 + 2: e = launch_t<8, 2>(a, st, device, 2 + sl, window_mode); break;
-    case 12 * 4 + 1: e = launch_t<12, 1>(a, st, device, 3 + sl, window_mode); break;
-    case 12 * 4 + 2: e = launch_t<12, 2>(a, st, device, 3 + sl, window_mode); break;
-    case 16 * 4 + 1: e = launch_t<16, 1>(a, st, device, 4 + sl, window_mode); break;
-    case 16 * 4 + 2: e = launch_t<16, 2>(a, st, device, 4 + sl, window_mode); break;
-    case 24 * 4 + 1: e = launch_t<24, 1>(a, st, device, 5 + sl, window_mode); break;
-    case 24 * 4 + 2: e = launch_t<24, 2>(a, st, device, 5 + sl, window_mode); break;
-    case 32 * 4 + 1: e = launch_t<32, 1>(a, st, device, 6 + sl, window_mode); break;
-    case 32 * 4 + 2: e = launch_t<32, 2>(a, st, device, 6 + sl, window_mode); break;
-    default:
-      e = na == 2 ? launch_t<0, 2>(a, st, device, 0 + sl, false) : launch_t<0, 1>(a, st, device, 0, false);
-      break;
+  if (a.f32) {
+    // binary32 factors (A21): compiled widths only (the build refuses others)
+    switch (a.R) {
+      case 4: e = launch_t<4, 1, true>(a, st, device, 17, window_mode); break;
+      case 8: e = launch_t<8, 1, true>(a, st, device, 18, window_mode); break;
+      case 12: e = launch_t<12, 1, true>(a, st, device, 19, window_mode); break;
+      case 16: e = launch_t<16, 1, true>(a, st, device, 20, window_mode); break;
+      case 24: e = launch_t<24, 1, true>(a, st, device, 21, window_mode); break;
+      case 32: e = launch_t<32, 1, true>(a, st, device, 22, window_mode); break;
+      default: return (int)cudaErrorInvalidValue;
+    }
+  } else if (kThreads <= 512 && na == 2) {
+    switch (a.R) {
+      case 4: e = launch_t<4, 2, false>(a, st, device, 9, window_mode); break;
+      case 8: e = launch_t<8, 2, false>(a, st, device, 10, window_mode); break;
+      case 12: e = launch_t<12, 2, false>(a, st, device, 11, window_mode); break;
+      case 16: e = launch_t<16, 2, false>(a, st, device, 12, window_mode); break;
+      case 24: e = launch_t<24, 2, false>(a, st, device, 13, window_mode); break;
+      case 32: e = launch_t<32, 2, false>(a, st, device, 14, window_mode); break;
+      default: e = launch_t<0, 2, false>(a, st, device, 8, false); break;
+    }
+  } else {
+    switch (a.R) {
+      case 4: e = launch_t<4, 1, false>(a, st, device, 1, window_mode); break;
+      case 8: e = launch_t<8, 1, false>(a, st, device, 2, window_mode); break;
+      case 12: e = launch_t<12, 1, false>(a, st, device, 3, window_mode); break;
+      case 16: e = launch_t<16, 1, false>(a, st, device, 4, window_mode); break;
+      case 24: e = launch_t<24, 1, false>(a, st, device, 5, window_mode); break;
+      case 32: e = launch_t<32, 1, false>(a, st, device, 6, window_mode); break;
+      default: e = launch_t<0, 1, false>(a, st, device, 0, false); break;
+    }
   }
   if (launches) *launches += 1;
   return e;

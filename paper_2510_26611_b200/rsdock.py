@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("RSDOCK_LIB") or os.path.join(_PKG, "librsdock.so")
 
 RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
 RS_FLAG_HOST_ONLY = 1
+RS_FLAG_F32_FACTORS = 2
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_score_poses", "rs_score_poses_async",
             "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
@@ -49,7 +50,8 @@ class rs_info(ctypes.Structure):
                 ("sigma_vdw", ctypes.c_double), ("dmin_cap", ctypes.c_double),
                 ("nbr_cells", ctypes.c_int64), ("nbr_entries", ctypes.c_int64),
                 ("nbr_shift", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
-                ("setup_seconds", ctypes.c_double), ("on_device", ctypes.c_int32)]
+                ("setup_seconds", ctypes.c_double), ("on_device", ctypes.c_int32),
+                ("factor_bits", ctypes.c_int32)]
 
 
 _lib = None

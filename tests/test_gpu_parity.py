@@ -292,3 +292,50 @@ def test_c5_full_size_sampled(env, R, mult):
     idx, _ = syn.subsample(w.poses, 24, seed=5)
     Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
     compare(Eg[idx], Dg[idx], Eo, Do)
+
+
+# ----------------------------------------------------------------------------- fp32 factors (N5)
+
+def _atom_scale(rs_oracle, prot, w, poses):
+    """S_p = sum_l |z_l phi(x_l)| per pose (the north_star's scale for the fp32-factor variant),
+    from the oracle with one-atom ligands."""
+    tb = prot.export_tables()
+    S = np.zeros(len(poses))
+    for l in range(w.L):
+        El, _, _ = rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz[l:l + 1],
+                                         w.ligand_q[l:l + 1], poses, w.dmin_cap)
+        S += np.abs(El)
+    return S
+
+
+@pytest.mark.parametrize("name,k", [("C1", None), ("C2", 300), ("C3", 200)])
+def test_f32_factors_parity_and_accuracy(env, name, k):
+    """RS_FLAG_F32_FACTORS (reading A21): the kernel matches the O4-f32 oracle to the
+    1e-12 parity bar, and stays within 1e-6 * sum_l |z_l phi(x_l)| of the binary64 path."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    prot32 = build(rsdock, w, flags=rsdock.RS_FLAG_F32_FACTORS)
+    assert prot32.info["factor_bits"] == 32
+    idx = None if k is None else syn.subsample(w.poses, k, seed=3)[0]
+    poses = w.poses if idx is None else w.poses[idx]
+    E32, D32, inv32 = gpu_score(torch, rsdock, prot32, w, poses)
+    tb = prot32.export_tables()
+    Eo, Do, invo = rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q,
+                                         poses, w.dmin_cap, f32=True)
+    compare(E32, D32, Eo, Do, inv32, invo)
+    E64, D64, _ = oracle_score(rs_oracle, prot32, w, poses)       # same tables, binary64 O4
+    S = _atom_scale(rs_oracle, prot32, w, poses[:100])
+    assert np.array_equal(D32, D64)
+    assert np.all(np.abs(E32[:100] - E64[:100]) <= 1e-6 * S)
+
+
+@pytest.mark.parametrize("R", [4, 8, 12, 16, 24, 32])
+def test_f32_factors_all_widths(env, R):
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=20 + R, M=40, L=20, n=64, b=8.0, R=R, P=333)
+    prot = build(rsdock, w, flags=rsdock.RS_FLAG_F32_FACTORS)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    tb = prot.export_tables()
+    Eo, Do, invo = rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q,
+                                         w.poses, w.dmin_cap, f32=True)
+    compare(Eg, Dg, Eo, Do, inv, invo)

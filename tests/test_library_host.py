@@ -38,6 +38,7 @@ def test_exports_every_declared_symbol(rsd):
 def test_struct_layouts_match_header(rsd):
     # rs_params: 2 int32, 6 double, 4 int32, uint64, uint32 (+pad) -> 88 bytes
     assert ctypes.sizeof(rsd.rs_params) == 96
+    assert ctypes.sizeof(rsd.rs_info) % 8 == 0 and rsd.rs_info.factor_bits.offset > rsd.rs_info.on_device.offset
     p = rsd.rs_params_default()
     assert p.grid_n == 256 and p.rank_R == 16 and p.sigma_vdw == 2.5 and p.flags == 0
 
