@@ -247,6 +247,78 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
     return invalid;
 }
 
+/*
+ * ---- N1: forces on the rigid ligand (NEXT row N1; reading A22) --------------------
+ * PAPER.md §3.3: the force on ligand atom l is minus the gradient of the binding energy, taken
+ * by one-dimensional finite differences of the long-range CP value on the grid (Eq. (21),
+ * "differ_ligand", backward differences); §4 (Eqs. (24)-(25),
+ * PAPER.md:1612-1627, Lemma 4.1) sums the atom forces into the resultants on
+ * the rigid ligand.  Per ligand atom (cells i from O1-O3, phi from O4):
+ *   g_a   = (phi(i) - phi(i - e_a)) * inv_h     (at i_a = 0: (phi(i + e_a) - phi(i)) * inv_h)
+ *   F_l   = -(z_l * g)                          (force = minus the energy gradient)
+ *   r_l   = x'_l - t                            (from the ligand's geometric centre)
+ *   tau_l = (r1 F2 - r2 F1, r2 F0 - r0 F2, r0 F1 - r1 F0)
+ *   rad_l = c r_l,  c = ((F0 r0 + F1 r1) + F2 r2) / ((r0 r0 + r1 r1) + r2 r2)   (0 if r_l = 0)
+ * and per pose the double-double sums over atoms (O6) of F_l (the net force), tau_l (the torque
+ * about t) and rad_l (Eq. (24)'s F_0(x_0), the sum of the radial projections):
+ *   out[9 p + 0..2] = F, out[9 p + 3..5] = tau, out[9 p + 6..8] = F_0.  NaN for invalid poses.
+ * Every product is rounded as written; no contraction.
+ */
+int64_t oracle_score_forces(int n, double b, int R, const double *F1, const double *F2,
+                            const double *F3, int64_t L, const double *Y, const double *zL,
+                            int64_t P, const double *poses, double *out)
+{
+    double inv_h = (double)n / (2.0 * b);
+    int64_t invalid = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : invalid)
+    for (int64_t p = 0; p < P; ++p) {
+        const double *pq = poses + 7 * p;
+        double Rm[9];
+        int ok = oracle_quat_to_rot(pq, Rm);
+        dd_t acc[9];
+        for (int j = 0; j < 9; ++j) { acc[j].hi = 0.0; acc[j].lo = 0.0; }
+        for (int64_t l = 0; l < L && ok; ++l) {
+            double xp[3];
+            int il[3];
+            oracle_transform(Rm, Y + 3 * l, pq + 4, xp);
+            for (int a = 0; a < 3; ++a) {
+                il[a] = oracle_snap(xp[a], b, inv_h, n);
+                if (il[a] < 0) ok = 0;
+            }
+            if (!ok) break;
+            double phi = oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
+            double g[3], Fl[3], r[3], tau[3], rad[3];
+            for (int a = 0; a < 3; ++a) {
+                int jm[3] = {il[0], il[1], il[2]};
+                if (il[a] > 0) {
+                    jm[a] = il[a] - 1;
+                    g[a] = (phi - oracle_long_value(F1, F2, F3, R, jm[0], jm[1], jm[2])) * inv_h;
+                } else {
+                    jm[a] = il[a] + 1;
+                    g[a] = (oracle_long_value(F1, F2, F3, R, jm[0], jm[1], jm[2]) - phi) * inv_h;
+                }
+                Fl[a] = -(zL[l] * g[a]);
+                r[a] = xp[a] - pq[4 + a];
+            }
+            tau[0] = r[1] * Fl[2] - r[2] * Fl[1];
+            tau[1] = r[2] * Fl[0] - r[0] * Fl[2];
+            tau[2] = r[0] * Fl[1] - r[1] * Fl[0];
+            double rr = (r[0] * r[0] + r[1] * r[1]) + r[2] * r[2];
+            double c = 0.0;
+            if (rr > 0.0) c = ((Fl[0] * r[0] + Fl[1] * r[1]) + Fl[2] * r[2]) / rr;
+            for (int a = 0; a < 3; ++a) rad[a] = c * r[a];
+            for (int a = 0; a < 3; ++a) {
+                dd_add_product(&acc[a], 1.0, Fl[a]);
+                dd_add_product(&acc[3 + a], 1.0, tau[a]);
+                dd_add_product(&acc[6 + a], 1.0, rad[a]);
+            }
+        }
+        for (int j = 0; j < 9; ++j) out[9 * p + j] = ok ? acc[j].hi + acc[j].lo : NAN;
+        if (!ok) invalid += 1;
+    }
+    return invalid;
+}
+
 /* number of OpenMP threads the scorer uses (reported as cpu_baseline.cores) */
 int oracle_num_threads(void)
 {

@@ -61,6 +61,9 @@ def lib():
             ctypes.c_double, ctypes.c_int, dp, dp]
         L.oracle_score_poses.restype = ctypes.c_int64
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_score_forces.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, dp,
+                                          ctypes.c_int64, dp, dp, ctypes.c_int64, dp, dp]
+        L.oracle_score_forces.restype = ctypes.c_int64
         _LIB = L
     return _LIB
 
@@ -335,6 +338,19 @@ def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=Fa
         Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap),
         (1 if long_only else 0) | (2 if f32 else 0), _p(E), _p(d))
     return E, d, int(inv)
+
+
+def score_forces(tables: dict, Y, zL, poses):
+    """Per-pose (P x 9: net force, torque about t, Eq. (24) radial resultant; n_invalid)."""
+    n, b = int(tables["n"]), float(tables["b"])
+    F1, F2, F3 = (_c(tables[k]) for k in ("F1", "F2", "F3"))
+    R = F1.shape[1]
+    Y, zL, poses = _c(Y), _c(zL), _c(poses)
+    P = poses.shape[0]
+    out = np.empty((P, 9))
+    inv = lib().oracle_score_forces(n, b, R, _p(F1), _p(F2), _p(F3), Y.shape[0], _p(Y), _p(zL), P,
+                                    _p(poses), _p(out))
+    return out, int(inv)
 
 
 def num_threads():

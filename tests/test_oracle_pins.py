@@ -588,3 +588,80 @@ def test_scorer_f32_mode_matches_long_value_f32(oracle):
             il = tuple(int(oracle.lib().oracle_snap(float(v), b, inv_h, n)) for v in x)
             S += abs(zb[l] * _lv(oracle, *F, i=il))
         assert abs(E32[p] - E64[p]) <= 1e-6 * S
+
+
+# ---------------------------------------------------------------------------------- N1 forces
+def _forces_one_atom(oracle, F, n, b, t, z=1.0):
+    tables = _tables(F, n=n, b=b)
+    poses = np.array([[1.0, 0.0, 0.0, 0.0, *t]])
+    out, inv = oracle.score_forces(tables, np.zeros((1, 3)), np.array([z]), poses)
+    assert inv == 0
+    return out[0]
+
+
+def test_forces_linear_potential_exact(oracle):
+    """phi = i0 (rank 1: F1[i] = i, F2 = F3 = 1): the backward difference is exactly 1 cell, so
+    g = inv_h e0 and F = -z inv_h e0; a single atom at the centre has zero torque and radial
+    resultant (r = 0).  At i0 = 0 the forward difference gives the same slope."""
+    n, b = 16, 4.0
+    inv_h = n / (2 * b)
+    F = [np.arange(n, dtype=float)[:, None], np.ones((n, 1)), np.ones((n, 1))]
+    for t0 in [0.3, -3.9]:                       # interior cell and cell 0
+        out = _forces_one_atom(oracle, F, n, b, (t0, 1.1, -2.0), z=0.5)
+        assert np.array_equal(out, [-0.5 * inv_h, 0, 0, 0, 0, 0, 0, 0, 0])
+
+
+def test_forces_separable_exponential_closed_form(oracle):
+    """phi(i) = exp(al i0) exp(be i1) exp(ga i2) (rank 1): the backward differences have the
+    closed form g_a = phi(i) (1 - exp(-c_a)) inv_h (forward at i_a = 0: phi (exp(c_a) - 1))."""
+    n, b = 16, 4.0
+    inv_h = n / (2 * b)
+    c = np.array([0.3, -0.2, 0.11])
+    idx = np.arange(n)
+    F = [np.exp(c[a] * idx)[:, None] for a in range(3)]
+    for t in [(0.3, 1.1, -2.0), (-3.9, 2.6, 0.7)]:
+        i = [int(oracle.lib().oracle_snap(float(v), b, inv_h, n)) for v in t]
+        phi = np.exp(np.dot(c, i))
+        g = np.array([phi * (1 - np.exp(-c[a])) if i[a] > 0 else phi * (np.exp(c[a]) - 1)
+                      for a in range(3)]) * inv_h
+        out = _forces_one_atom(oracle, F, n, b, t, z=-0.7)
+        assert np.allclose(out[:3], 0.7 * g, rtol=1e-13, atol=0)
+
+
+def test_forces_two_atom_torque_and_radial(oracle):
+    """Two atoms at t +- d e1 with charges z, -z in phi = i0: atom forces -+z inv_h e0, radial
+    projections 0 (F perpendicular to r), net force 0 and torque (0, 0, 2 d z inv_h) by hand."""
+    n, b = 32, 8.0
+    inv_h = n / (2 * b)
+    F = [np.arange(n, dtype=float)[:, None], np.ones((n, 1)), np.ones((n, 1))]
+    d, z = 1.25, 0.6
+    Y = np.array([[0.0, d, 0.0], [0.0, -d, 0.0]])
+    zL = np.array([z, -z])
+    poses = np.array([[1.0, 0.0, 0.0, 0.0, 0.1, 0.2, 0.3]])
+    out, _ = oracle.score_forces(_tables(F, n=n, b=b), Y, zL, poses)
+    assert np.allclose(out[0], [0, 0, 0, 0, 0, 2 * d * z * inv_h, 0, 0, 0], atol=1e-12, rtol=0)
+    # a rotation by 90 degrees about e2 maps e1 -> -e0: forces along r, torque 0, radial = net
+    q = np.array([np.cos(np.pi / 4), 0, 0, np.sin(np.pi / 4)])
+    out2, _ = oracle.score_forces(_tables(F, n=n, b=b), Y, zL, np.r_[q, 0.1, 0.2, 0.3][None])
+    assert np.allclose(out2[0, 3:6], 0, atol=1e-12) and np.allclose(out2[0, 6:], out2[0, :3], atol=1e-12)
+
+
+def test_forces_vs_analytic_coulomb_field(oracle):
+    """Physics pin (the analytic field E_M): with the uncompressed long-range
+    factors, the FD net force on well-separated ligands matches
+    F = sum_l z_l sum_m z_m (x_l - x_m)/|x_l - x_m|^3 within the first-order FD/snapping error
+    (relative 8 % of sum |F_l|, h = 0.16 A at 7.5-8 A) and with the right sign."""
+    b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng = _chain_case(oracle, seed=4)
+    P = 20
+    u = syn.unit_vectors(rng, P)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), u * rng.uniform(7.5, 8.0, (P, 1))], 1)
+    out, inv = oracle.score_forces(tables, Y, zL, poses)
+    assert inv == 0
+    for p in range(P):
+        R = oracle.quat_to_rot(poses[p, :4])
+        xl = Y @ R.T + poses[p, 4:]
+        dx = xl[:, None, :] - X[None, :, :]
+        r3 = np.linalg.norm(dx, axis=2) ** 3
+        Fl = zL[:, None] * np.einsum("m,lmk->lk", qM, dx / r3[:, :, None])
+        scale = np.abs(Fl).sum()
+        assert np.linalg.norm(out[p, :3] - Fl.sum(0)) <= 0.08 * scale
