@@ -187,6 +187,8 @@ def config_dict(w, args):
             "config": args.config, "M": w.M, "L": w.L, "n": w.grid_n, "R": w.rank_R,
             "poses": w.P, "sigma_split": w.sigma_split, "sigma_vdw": w.sigma_vdw,
             "parallelism": f"pose-shard x{args.gpus} (replicated handle)",
+            "mode": ("forces (rs_score_forces, N1)" if getattr(args, "forces", False) else "energy + mindist")
+                    + (", fp32 factors (A21)" if getattr(args, "f32", False) else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
@@ -201,6 +203,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--forces", action="store_true",
+                    help="time rs_score_forces (NEXT row N1) instead of the energy path")
     ap.add_argument("--f32", action="store_true",
                     help="the fp32-factor variant (RS_FLAG_F32_FACTORS, DESIGN.md reading A21)")
     ap.add_argument("--nbr-cell", type=float, default=0.0,
@@ -245,8 +249,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    Fout = torch.empty((P, 9), dtype=torch.float64, device=dev) if args.forces else None
+
     def step():
-        prot.score_async(q, y, poses, E, D, cnt, stream=stream)
+        if args.forces:
+            prot.forces_async(q, y, poses, Fout, cnt, stream=stream)
+        else:
+            prot.score_async(q, y, poses, E, D, cnt, stream=stream)
 
     for _ in range(args.warmup):
         step()

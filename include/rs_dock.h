@@ -157,6 +157,23 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
                              double* energies_out, double* mindist_out,
                              int64_t* invalid_count_dev, void* cuda_stream);
 
+/*
+ * Forces on the rigid ligand for P poses (NEXT row N1; §3.3 Eq. (21)
+ * "differ_ligand" PAPER.md:1032-1036 and §4 Eqs. (24)-(25), Lemma 4.1 PAPER.md:1612-1640;
+ * DESIGN.md reading A22).  Per ligand atom, the backward difference of the long-range CP value
+ * on the grid g_a = (phi(i) - phi(i - e_a)) * n/(2b) (forward at i_a = 0) gives the force
+ * F_l = -z_l g; per pose forces_out[9 p + 0..8] = (sum_l F_l, sum_l r_l x F_l,
+ * sum_l (F_l . r_l / |r_l|^2) r_l) with r_l = x'_l - t: the net force, the torque about the
+ * ligand centre t and Eq. (24)'s radial resultant F_0.  Long-range part only, binary64 factors.
+ * All pointers are device pointers (P x 7 poses, P x 9 outputs); the work is enqueued on
+ * cuda_stream (asynchronous).  Invalid poses (as rs_score_poses) get NaN and are counted in
+ * *invalid_count_dev when it is not NULL (zeroed on the stream first).  Returns 0 or a negative
+ * RS_E_* code.
+ */
+int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                        const double* poses, int64_t P, double* forces_out,
+                        int64_t* invalid_count_dev, void* cuda_stream);
+
 /* Fill *out.  Returns 0 or RS_E_INVALID_ARG. */
 int rs_get_info(const rs_handle* h, rs_info* out);
 

@@ -495,6 +495,38 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
   return 0;
 }
 
+int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                        const double* poses, int64_t P, double* forces_out,
+                        int64_t* invalid_count_dev, void* cuda_stream) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
+  if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
+  if (P > 0 && (!poses || !forces_out)) { set_err("null pose/output pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > 0 && (!q_lig || !xyz_lig)) { set_err("null ligand pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > (int64_t)1 << 30) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
+  const void* ptrs[4] = {q_lig, xyz_lig, poses, forces_out};
+  for (const void* p : ptrs)
+    if (p && pointer_kind(p) != 1) { set_err("rs_score_forces needs device pointers"); return RS_E_INVALID_ARG; }
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (invalid_count_dev)
+    CUDA_TRY(cudaMemsetAsync(invalid_count_dev, 0, sizeof(int64_t), st), RS_E_CUDA);
+  if (P == 0) return 0;
+  rs::ScoreArgs a = base_args(h);
+  a.zl = q_lig;
+  a.yl = xyz_lig;
+  a.L = n_lig;
+  a.poses = poses;
+  a.P = P;
+  a.invalid = (unsigned long long*)invalid_count_dev;
+  int e = rs::launch_forces(a, forces_out, st, h->device);
+  if (e != 0) {
+    set_err(std::string("force kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
+    return RS_E_CUDA;
+  }
+  return 0;
+}
+
 int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
                        const double* poses, int64_t P, double* energies_out, double* mindist_out) {
   if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }

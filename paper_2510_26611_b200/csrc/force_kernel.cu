@@ -1,0 +1,243 @@
+// Forces on the rigid ligand (NEXT row N1): PAPER.md §3.3 Eq. (21) "differ_ligand"
+// (finite differences of the long-range CP value on the grid) and §4
+// Eqs. (24)-(25) / Lemma 4.1 (resultants on the rigid cluster).  Reading
+// DESIGN.md A22; the oracle is oracle/oracle_score.c: oracle_score_forces (no shared code).
+//
+// One warp per pose (grid-stride), lanes over ligand atoms.  Per atom: O1-O3 as the scoring
+// kernel, then four O4 values phi(i), phi(i - e_a) (a = 0, 1, 2; forward at i_a = 0) from the
+// L2-resident factor rows (the shifted value reuses two of the three rows), the backward
+// differences g_a = (phi(i) - phi(i - e_a)) * inv_h, F_l = -(z_l g), r_l = x'_l - t, the
+// torque r_l x F_l and the radial part c r_l, c = (F_l . r_l) / |r_l|^2; per pose nine
+// double-double sums (order-free, O6), reduced by xor butterflies.  Every op is an explicit
+// round-to-nearest intrinsic in the oracle's order (the file is compiled with -fmad=false).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "rs_internal.h"
+
+namespace rs {
+namespace {
+
+constexpr int kForceThreads = 256;
+constexpr unsigned kAll = 0xffffffffu;
+
+__device__ __forceinline__ bool quat_rot(const double* q, double* R) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double nn = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)),
+                              __dmul_rn(z, z));
+  if (!(nn > 0.0) || !isfinite(nn)) return false;
+  const double s = __ddiv_rn(2.0, nn);
+  const double xs = __dmul_rn(x, s), ys = __dmul_rn(y, s), zs = __dmul_rn(z, s);
+  const double wx = __dmul_rn(w, xs), wy = __dmul_rn(w, ys), wz = __dmul_rn(w, zs);
+  const double xx = __dmul_rn(x, xs), xy = __dmul_rn(x, ys), xz = __dmul_rn(x, zs);
+  const double yy = __dmul_rn(y, ys), yz = __dmul_rn(y, zs), zz = __dmul_rn(z, zs);
+  R[0] = __dsub_rn(1.0, __dadd_rn(yy, zz));
+  R[1] = __dsub_rn(xy, wz);
+  R[2] = __dadd_rn(xz, wy);
+  R[3] = __dadd_rn(xy, wz);
+  R[4] = __dsub_rn(1.0, __dadd_rn(xx, zz));
+  R[5] = __dsub_rn(yz, wx);
+  R[6] = __dsub_rn(xz, wy);
+  R[7] = __dadd_rn(yz, wx);
+  R[8] = __dsub_rn(1.0, __dadd_rn(xx, yy));
+  return true;
+}
+
+// O4: rank pairs, then the pairwise halving tree (reading A20), rows from L2
+template <int R>
+__device__ __forceinline__ double phi_rows(const double* a, const double* b, const double* c) {
+  constexpr int CH = R / 2;
+  constexpr int C = CH <= 1 ? 1 : CH <= 2 ? 2 : CH <= 4 ? 4 : CH <= 8 ? 8 : 16;
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  const double2* c2 = reinterpret_cast<const double2*>(c);
+  double s[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    s[j] = 0.0;
+    if (j < CH) {
+      const double2 x = __ldg(a2 + j), y = __ldg(b2 + j), z = __ldg(c2 + j);
+      s[j] = __dadd_rn(__dmul_rn(__dmul_rn(x.x, y.x), z.x), __dmul_rn(__dmul_rn(x.y, y.y), z.y));
+    }
+  }
+#pragma unroll
+  for (int m = C / 2; m >= 1; m /= 2) {
+#pragma unroll
+    for (int j = 0; j < m; ++j) s[j] = __dadd_rn(s[j], s[j + m]);
+  }
+  return s[0];
+}
+
+// the same for a runtime width (odd R or widths without a compiled variant)
+__device__ double phi_rows_rt(const double* a, const double* b, const double* c, int R) {
+  int C = 1;
+  while (2 * C < R) C *= 2;
+  double st[24];
+  int lg = 0;
+  while ((1 << lg) < C) ++lg;
+  int top = 0;
+  for (int j = 0; j < C; ++j) {
+    const int k = lg ? (int)(__brev((unsigned)j) >> (32 - lg)) : 0;
+    double q0 = 0.0, q1 = 0.0;
+    if (2 * k < R) q0 = __dmul_rn(__dmul_rn(__ldg(a + 2 * k), __ldg(b + 2 * k)), __ldg(c + 2 * k));
+    if (2 * k + 1 < R)
+      q1 = __dmul_rn(__dmul_rn(__ldg(a + 2 * k + 1), __ldg(b + 2 * k + 1)), __ldg(c + 2 * k + 1));
+    double v = __dadd_rn(q0, q1);
+    for (int t = j; t & 1; t >>= 1) v = __dadd_rn(st[--top], v);
+    st[top++] = v;
+  }
+  return st[0];
+}
+
+template <int R>
+__device__ __forceinline__ double phi_at(const ScoreArgs& a, int i0, int i1, int i2) {
+  const int r = R > 0 ? R : a.R;
+  const double* f0 = a.t.F[0] + (size_t)i0 * r;
+  const double* f1 = a.t.F[1] + (size_t)i1 * r;
+  const double* f2 = a.t.F[2] + (size_t)i2 * r;
+  if constexpr (R > 0 && (R % 2) == 0) return phi_rows<R>(f0, f1, f2);
+  else return phi_rows_rt(f0, f1, f2, r);
+}
+
+__device__ __forceinline__ void dd_acc(double& hi, double& lo, double p) {
+  const double s = __dadd_rn(hi, p);
+  const double bb = __dsub_rn(s, hi);
+  const double err = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(p, bb));
+  hi = s;
+  lo = __dadd_rn(lo, err);
+}
+
+__device__ __forceinline__ void dd_join(double& hi, double& lo, double h2, double l2) {
+  const double s = __dadd_rn(hi, h2);
+  const double bb = __dsub_rn(s, hi);
+  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
+  hi = s;
+  lo = __dadd_rn(__dadd_rn(lo, l2), e);
+}
+
+__device__ __forceinline__ int snap_cell(double x, double b, double inv_h, int nm1) {
+  const double u = __dmul_rn(__dadd_rn(x, b), inv_h);
+  int c;
+  asm("cvt.rpi.s32.f64 %0, %1;" : "=r"(c) : "d"(u));
+  return min(max(c - 1, 0), nm1);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kForceThreads) force_kernel(const ScoreArgs a, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * kForceThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kForceThreads) >> 5;
+  const int nm1 = a.n - 1;
+  for (int64_t p = warp0; p < a.P; p += nwarps) {
+    const double* pq = a.poses + 7 * p;
+    double q[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) q[i] = __ldg(pq + i);
+    double Rm[9];
+    bool ok = quat_rot(q, Rm);
+    double hi[9], lo[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) hi[j] = lo[j] = 0.0;
+    for (int l0 = 0; ok && l0 < a.L; l0 += 32) {
+      const int l = l0 + lane;
+      bool bad = false;
+      if (l < a.L) {
+        const double y0 = __ldg(a.yl + 3 * (int64_t)l), y1 = __ldg(a.yl + 3 * (int64_t)l + 1),
+                     y2 = __ldg(a.yl + 3 * (int64_t)l + 2), z = __ldg(a.zl + l);
+        double xp[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          xp[r] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3 * r], y0), __dmul_rn(Rm[3 * r + 1], y1)),
+                                      __dmul_rn(Rm[3 * r + 2], y2)),
+                            q[4 + r]);
+        if (!(fabs(xp[0]) <= a.b && fabs(xp[1]) <= a.b && fabs(xp[2]) <= a.b)) {
+          bad = true;
+        } else {
+          int i[3];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) i[r] = snap_cell(xp[r], a.b, a.inv_h, nm1);
+          const double phi = phi_at<R>(a, i[0], i[1], i[2]);
+          double F[3], rv[3];
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            int j[3] = {i[0], i[1], i[2]};
+            double g;
+            if (i[ax] > 0) {
+              j[ax] = i[ax] - 1;
+              g = __dmul_rn(__dsub_rn(phi, phi_at<R>(a, j[0], j[1], j[2])), a.inv_h);
+            } else {
+              j[ax] = i[ax] + 1;
+              g = __dmul_rn(__dsub_rn(phi_at<R>(a, j[0], j[1], j[2]), phi), a.inv_h);
+            }
+            F[ax] = -__dmul_rn(z, g);
+            rv[ax] = __dsub_rn(xp[ax], q[4 + ax]);
+          }
+          const double tau0 = __dsub_rn(__dmul_rn(rv[1], F[2]), __dmul_rn(rv[2], F[1]));
+          const double tau1 = __dsub_rn(__dmul_rn(rv[2], F[0]), __dmul_rn(rv[0], F[2]));
+          const double tau2 = __dsub_rn(__dmul_rn(rv[0], F[1]), __dmul_rn(rv[1], F[0]));
+          const double rr = __dadd_rn(__dadd_rn(__dmul_rn(rv[0], rv[0]), __dmul_rn(rv[1], rv[1])),
+                                      __dmul_rn(rv[2], rv[2]));
+          double c = 0.0;
+          if (rr > 0.0)
+            c = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(F[0], rv[0]), __dmul_rn(F[1], rv[1])),
+                                    __dmul_rn(F[2], rv[2])),
+                          rr);
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) dd_acc(hi[ax], lo[ax], F[ax]);
+          dd_acc(hi[3], lo[3], tau0);
+          dd_acc(hi[4], lo[4], tau1);
+          dd_acc(hi[5], lo[5], tau2);
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) dd_acc(hi[6 + ax], lo[6 + ax], __dmul_rn(c, rv[ax]));
+        }
+      }
+      if (__any_sync(kAll, bad)) ok = false;
+    }
+    double res[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        dd_join(hi[j], lo[j], __shfl_xor_sync(kAll, hi[j], off), __shfl_xor_sync(kAll, lo[j], off));
+      res[j] = ok ? __dadd_rn(hi[j], lo[j]) : NAN;
+    }
+    // lanes 0..8 write one component each (coalesced 72-byte row)
+    double mine = res[0];
+#pragma unroll
+    for (int j = 1; j < 9; ++j)
+      if (lane == j) mine = res[j];
+    if (lane < 9) out[9 * p + lane] = mine;
+    if (!ok && lane == 0 && a.invalid) atomicAdd(a.invalid, 1ull);
+  }
+}
+
+template <int R>
+int launch_forces_t(const ScoreArgs& a, double* out, cudaStream_t st, int sms) {
+  const int64_t warps_needed = a.P;
+  const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)sms * 8);
+  force_kernel<R><<<(int)std::max<int64_t>(blocks, 1), kForceThreads, 0, st>>>(a, out);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_forces(const ScoreArgs& a, double* out, void* stream, int device) {
+  if (a.P <= 0) return 0;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (a.R) {
+    case 4: return launch_forces_t<4>(a, out, st, sms);
+    case 8: return launch_forces_t<8>(a, out, st, sms);
+    case 12: return launch_forces_t<12>(a, out, st, sms);
+    case 16: return launch_forces_t<16>(a, out, st, sms);
+    case 24: return launch_forces_t<24>(a, out, st, sms);
+    case 32: return launch_forces_t<32>(a, out, st, sms);
+    default: return launch_forces_t<0>(a, out, st, sms);
+  }
+}
+
+}  // namespace rs

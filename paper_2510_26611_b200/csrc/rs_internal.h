@@ -104,6 +104,8 @@ constexpr int kWorkSlots = 64;   // concurrent launches per handle with distinct
 // (if not null) is incremented by the number of kernels enqueued.
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
 const char* score_kernel_variant(int R);
+// NEXT row N1: forces on the rigid ligand (force_kernel.cu), P x 9 outputs, device pointers.
+int launch_forces(const ScoreArgs& a, double* out, void* stream, int device);
 // Chunks (16 B) per row of the window copy of the factors for compiled width R (0: none), and
 // the host packing of that copy (rows padded with zeros or replicated to CHP chunks).
 int window_row_chunks(int R);

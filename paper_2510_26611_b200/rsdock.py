@@ -23,6 +23,7 @@ RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_score_poses", "rs_score_poses_async",
+            "rs_score_forces",
             "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
 
@@ -77,6 +78,8 @@ def load():
     L.rs_score_poses_async.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
                                        _vp, _vp, _vp]
     L.rs_score_poses_async.restype = ctypes.c_int64
+    L.rs_score_forces.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp, _vp]
+    L.rs_score_forces.restype = ctypes.c_int64
     L.rs_get_info.argtypes = [_vp, ctypes.POINTER(rs_info)]
     L.rs_get_info.restype = ctypes.c_int
     L.rs_export_tables.argtypes = [_vp] + [_vp] * 6
@@ -137,6 +140,15 @@ def rs_score_poses_async(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindi
                                     stream)
     if r < 0:
         raise RuntimeError(f"rs_score_poses_async ({r}): " + rs_last_error())
+    return int(r)
+
+
+def rs_score_forces(h, q_lig, xyz_lig, n_lig, poses, P, forces_out, invalid_count=None,
+                    stream=None) -> int:
+    r = load().rs_score_forces(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
+                               _ptr(forces_out), _ptr(invalid_count), stream)
+    if r < 0:
+        raise RuntimeError(f"rs_score_forces ({r}): " + rs_last_error())
     return int(r)
 
 
@@ -236,6 +248,16 @@ class Protein:
                 mindist_out = torch.empty(P, dtype=torch.float64, device=poses.device)
         inv = rs_score_poses(self._h, q_lig, xyz_lig, L, poses, P, energies_out, mindist_out)
         return energies_out, mindist_out, inv
+
+    def forces_async(self, q_lig, xyz_lig, poses, forces_out, invalid_count=None, stream=None):
+        """Enqueue the rigid-ligand forces (P x 9 device tensor: net force, torque about the
+        centre, Eq. (24) radial resultant) on `stream` (default: torch's current stream)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(poses.device)
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        return rs_score_forces(self._h, q_lig, xyz_lig, int(q_lig.shape[0]), poses,
+                               int(poses.shape[0]), forces_out, invalid_count, s)
 
     def score_async(self, q_lig, xyz_lig, poses, energies_out, mindist_out, invalid_count=None,
                     stream=None):

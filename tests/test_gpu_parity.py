@@ -339,3 +339,58 @@ def test_f32_factors_all_widths(env, R):
     Eo, Do, invo = rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q,
                                          w.poses, w.dmin_cap, f32=True)
     compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+# ----------------------------------------------------------------------------- forces (N1)
+
+def gpu_forces(torch, prot, w, poses):
+    dev = torch.device("cuda:0")
+    q = torch.tensor(w.ligand_q, device=dev)
+    y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
+    ps = torch.tensor(poses, device=dev).contiguous()
+    out = torch.empty((ps.shape[0], 9), dtype=torch.float64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    prot.forces_async(q, y, ps, out, cnt)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), int(cnt.item())
+
+
+def compare_forces(Fg, Fo, ig, io):
+    assert ig == io
+    assert np.array_equal(np.isnan(Fg), np.isnan(Fo))
+    ok = ~np.isnan(Fo)
+    scale = np.maximum(np.abs(Fo), 1e-300)
+    # per component: bitwise expected; 1e-12 relative to the pose's largest component otherwise
+    big = np.nanmax(np.abs(Fo), axis=1, keepdims=True) * np.ones_like(Fo)
+    assert np.all((Fg[ok] == Fo[ok]) | (np.abs(Fg[ok] - Fo[ok]) <= 1e-12 * big[ok])), \
+        float(np.nanmax(np.abs(Fg - Fo) / scale))
+    return float(np.mean(Fg[ok] == Fo[ok]))
+
+
+@pytest.mark.parametrize("R", [4, 8, 12, 16, 24, 32, 10])
+def test_forces_all_widths(env, R):
+    """rs_score_forces (NEXT row N1) vs oracle_score_forces, every compiled width and a runtime
+    width; invalid poses (zero quaternion, NaN, leaving the box) give NaN rows and are counted."""
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=40 + R, M=40, L=20, n=64, b=8.0, R=R, P=333)
+    prot = build(rsdock, w)
+    poses = w.poses.copy()
+    poses[3, :4] = 0.0
+    poses[5, 4] = np.nan
+    poses[7, 5] = 7.9
+    Fg, ig = gpu_forces(torch, prot, w, poses)
+    Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, poses)
+    compare_forces(Fg, Fo, ig, io)
+    assert np.isnan(Fg[[3, 5, 7]]).all() and ig >= 3
+
+
+@pytest.mark.parametrize("name,k", [("C1", None), ("C3", 2000)])
+def test_forces_configs(env, name, k):
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    prot = build(rsdock, w)
+    poses = w.poses if k is None else w.poses[syn.subsample(w.poses, k, seed=9)[0]]
+    Fg, ig = gpu_forces(torch, prot, w, poses)
+    Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, poses)
+    frac = compare_forces(Fg, Fo, ig, io)
+    assert frac > 0.99
