@@ -193,6 +193,37 @@ int rs_export_tables(const rs_handle* h, double* F1, double* F2, double* F3, dou
 int rs_export_setup(const rs_handle* h, double* t, double* a, int32_t* is_long,
                     int32_t* protein_cells);
 
+/*
+ * PPIEM scan (NEXT row N2; Algorithm PPIEM steps A3-A6; DESIGN.md reading
+ * A23).  For every position j (direction dirs[j], unit 3-vector) and ligand orientation k
+ * (quats[k], w,x,y,z), the ligand centre starts at centre + s_start dirs[j] and approaches the
+ * centre along the line (A3) by sphere tracing on the pose's minimum distance d (a step never
+ * exceeds the clearance, so the first contact is never jumped over):
+ *     d = +inf (no protein atom within D_cap):  s <- s - (D_cap - sigma_vdw)
+ *     d - sigma_vdw <= tol:                      converged (vdW contact)
+ *     otherwise:                                 s <- s - (d - sigma_vdw) * 0.999
+ * all poses advancing together, one batched scoring launch per iteration (at most max_iter).
+ * Outputs (host arrays, row j, column k, m_P x m_L): energy at the final position (A4-A5; NaN
+ * unless status is 0 or 4), the final s and a status: 0 contact reached, 1 a ligand atom left
+ * the box, 2 clash at s_start, 3 passed the centre without contact (s < 0), 4 max_iter reached
+ * (feasible, not converged).  Needs dmin_cap > sigma_vdw (the build's D_cap is the step).
+ * The ligand arrays may be host or device pointers.  Returns 0 or a negative RS_E_* code.
+ */
+int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                      const double* centre, const double* dirs, int32_t m_P, const double* quats,
+                      int32_t m_L, double s_start, double tol, int32_t max_iter,
+                      double* energies_out, double* s_out, int32_t* status_out);
+
+/*
+ * Local minima of an m_P x m_L landscape (PPIEM step A6): entries strictly below all 8
+ * neighbours on the grid periodic in both indices (plateaus: the lexicographically smallest
+ * index), NaN entries excluded and never neighbours; sorted by energy, ties by (j, k).  Writes
+ * up to top_k flat indices j m_L + k and returns their count (>= 0) or RS_E_INVALID_ARG.
+ * Host-only.
+ */
+int32_t rs_landscape_minima(const double* energies, int32_t m_P, int32_t m_L, int32_t top_k,
+                            int32_t* idx_out);
+
 /* Message of the last error on this thread ("" if none). */
 const char* rs_last_error(void);
 

@@ -611,4 +611,131 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   return (int64_t)(cnts[0] + cnts[1]);
 }
 
+int32_t rs_landscape_minima(const double* E, int32_t m_P, int32_t m_L, int32_t top_k,
+                            int32_t* idx_out) {
+  if (!E || m_P <= 0 || m_L <= 0 || top_k < 0 || (top_k > 0 && !idx_out)) {
+    set_err("rs_landscape_minima: bad arguments");
+    return RS_E_INVALID_ARG;
+  }
+  // PPIEM step A6 (reading A23): strict local minima on the periodic grid; a tie with
+  // a neighbour goes to the lexicographically smaller index; NaN entries are skipped
+  std::vector<int32_t> mins;
+  for (int32_t j = 0; j < m_P; ++j)
+    for (int32_t k = 0; k < m_L; ++k) {
+      const double e = E[(int64_t)j * m_L + k];
+      if (std::isnan(e)) continue;
+      bool is_min = true;
+      for (int dj = -1; dj <= 1 && is_min; ++dj)
+        for (int dk = -1; dk <= 1 && is_min; ++dk) {
+          const int32_t jj = ((j + dj) % m_P + m_P) % m_P, kk = ((k + dk) % m_L + m_L) % m_L;
+          if (jj == j && kk == k) continue;
+          const double f = E[(int64_t)jj * m_L + kk];
+          if (std::isnan(f)) continue;
+          if (f < e || (f == e && (jj < j || (jj == j && kk < k)))) is_min = false;
+        }
+      if (is_min) mins.push_back(j * m_L + k);
+    }
+  std::stable_sort(mins.begin(), mins.end(), [&](int32_t x, int32_t y) { return E[x] < E[y]; });
+  const int32_t cnt = std::min<int32_t>(top_k, (int32_t)mins.size());
+  for (int32_t i = 0; i < cnt; ++i) idx_out[i] = mins[i];
+  return cnt;
+}
+
+int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
+                      const double* centre, const double* dirs, int32_t m_P, const double* quats,
+                      int32_t m_L, double s_start, double tol, int32_t max_iter,
+                      double* energies_out, double* s_out, int32_t* status_out) {
+  if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
+  if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
+  if (!centre || !dirs || !quats || !energies_out || !s_out || !status_out || m_P <= 0 || m_L <= 0 ||
+      max_iter < 1 || !(tol > 0) || !std::isfinite(s_start) || s_start < 0 || n_lig < 0 ||
+      (n_lig > 0 && (!q_lig || !xyz_lig))) {
+    set_err("rs_ppiem_scan: bad arguments");
+    return RS_E_INVALID_ARG;
+  }
+  if (!(h->prm.dmin_cap > h->prm.sigma_vdw)) {
+    set_err("rs_ppiem_scan needs dmin_cap > sigma_vdw (the sphere-tracing step)");
+    return RS_E_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(h->mtx);
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  const int64_t P = (int64_t)m_P * m_L;
+  const bool lig_dev = n_lig == 0 || (pointer_kind(q_lig) == 1 && pointer_kind(xyz_lig) == 1);
+  // device scratch: [ligand 4L][centre 3][dirs 3 m_P][quats 4 m_L][poses 7P][E P][D P][s P]
+  //                 [status P int][active int][invalid u64]
+  const size_t nd = 4 * (size_t)std::max<int64_t>(n_lig, 1) + 3 + 3 * (size_t)m_P + 4 * (size_t)m_L +
+                    10 * (size_t)P;
+  const size_t bytes = nd * sizeof(double) + ((size_t)P + 4) * sizeof(int) + 16;
+  void* buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, bytes), RS_E_NOMEM);
+  struct Free { void* p; ~Free() { cudaFree(p); } } guard{buf};
+  double* d_lig = (double*)buf;
+  double* d_c = d_lig + 4 * std::max<int64_t>(n_lig, 1);
+  double* d_dirs = d_c + 3;
+  double* d_q = d_dirs + 3 * (size_t)m_P;
+  double* d_pose = d_q + 4 * (size_t)m_L;
+  double* d_E = d_pose + 7 * P;
+  double* d_D = d_E + P;
+  double* d_s = d_D + P;
+  int* d_st = (int*)(d_s + P);
+  int* d_active = d_st + P;
+  unsigned long long* d_inv = (unsigned long long*)(((uintptr_t)(d_active + 1) + 7) & ~(uintptr_t)7);
+  const double *zl = q_lig, *yl = xyz_lig;
+  if (!lig_dev) {
+    CUDA_TRY(cudaMemcpy(d_lig, q_lig, n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpy(d_lig + n_lig, xyz_lig, 3 * n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+    zl = d_lig;
+    yl = d_lig + n_lig;
+  }
+  CUDA_TRY(cudaMemcpy(d_c, centre, 3 * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+  CUDA_TRY(cudaMemcpy(d_dirs, dirs, 3 * (size_t)m_P * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+  CUDA_TRY(cudaMemcpy(d_q, quats, 4 * (size_t)m_L * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+  cudaStream_t st = nullptr;
+  if (int e = rs::launch_scan_init(d_c, d_dirs, d_q, m_P, m_L, s_start, d_pose, d_s, d_st, st)) {
+    set_err(std::string("scan init failed: ") + cudaGetErrorString((cudaError_t)e));
+    return RS_E_CUDA;
+  }
+  rs::ScoreArgs a = base_args(h);
+  a.zl = zl;
+  a.yl = yl;
+  a.L = n_lig;
+  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
+  a.poses = d_pose;
+  a.P = P;
+  a.E = d_E;
+  a.D = d_D;
+  a.invalid = d_inv;
+  const double sigma = h->prm.sigma_vdw, dcap = h->prm.dmin_cap;
+  auto score = [&]() -> int {
+    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
+    if (cudaMemsetAsync(a.work, 0, sizeof(int), st) != cudaSuccess) return 1;
+    return rs::launch_score(a, st, h->device, nullptr);
+  };
+  int active = 1, it = 0;
+  for (; it < max_iter && active > 0; ++it) {
+    if (score() != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+    CUDA_TRY(cudaMemsetAsync(d_active, 0, sizeof(int), st), RS_E_CUDA);
+    if (int e = rs::launch_scan_update(d_c, d_dirs, d_q, m_P, m_L, d_D, sigma, dcap, tol, it == 0,
+                                       d_pose, d_s, d_st, d_active, st)) {
+      set_err(std::string("scan update failed: ") + cudaGetErrorString((cudaError_t)e));
+      return RS_E_CUDA;
+    }
+    CUDA_TRY(cudaMemcpy(&active, d_active, sizeof(int), cudaMemcpyDeviceToHost), RS_E_CUDA);
+  }
+  // poses still moving after max_iter were stepped after their last scoring: score them where
+  // they stand (feasible by construction) and report status 4
+  if (active > 0 && score() != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+  CUDA_TRY(cudaDeviceSynchronize(), RS_E_CUDA);
+  std::vector<int> stv(P);
+  CUDA_TRY(cudaMemcpy(energies_out, d_E, P * sizeof(double), cudaMemcpyDeviceToHost), RS_E_CUDA);
+  CUDA_TRY(cudaMemcpy(s_out, d_s, P * sizeof(double), cudaMemcpyDeviceToHost), RS_E_CUDA);
+  CUDA_TRY(cudaMemcpy(stv.data(), d_st, P * sizeof(int), cudaMemcpyDeviceToHost), RS_E_CUDA);
+  for (int64_t p = 0; p < P; ++p) {
+    const int sv = stv[p] == -1 ? 4 : stv[p];
+    status_out[p] = sv;
+    if (sv != 0 && sv != 4) energies_out[p] = NAN;
+  }
+  return 0;
+}
+
 }  // extern "C"

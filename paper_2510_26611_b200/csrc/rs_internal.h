@@ -104,6 +104,12 @@ constexpr int kWorkSlots = 64;   // concurrent launches per handle with distinct
 // (if not null) is incremented by the number of kernels enqueued.
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
 const char* score_kernel_variant(int R);
+// NEXT row N2: PPIEM scan kernels (scan_kernel.cu)
+int launch_scan_init(const double* centre, const double* dirs, const double* quats, int m_P,
+                     int m_L, double s_start, double* poses, double* s, int* status, void* st);
+int launch_scan_update(const double* centre, const double* dirs, const double* quats, int m_P,
+                       int m_L, const double* D, double sigma, double dcap, double tol, int first,
+                       double* poses, double* s, int* status, int* active, void* st);
 // NEXT row N1: forces on the rigid ligand (force_kernel.cu), P x 9 outputs, device pointers.
 int launch_forces(const ScoreArgs& a, double* out, void* stream, int device);
 // Chunks (16 B) per row of the window copy of the factors for compiled width R (0: none), and

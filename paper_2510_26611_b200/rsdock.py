@@ -23,7 +23,7 @@ RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_score_poses", "rs_score_poses_async",
-            "rs_score_forces",
+            "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",
             "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
 
@@ -80,6 +80,12 @@ def load():
     L.rs_score_poses_async.restype = ctypes.c_int64
     L.rs_score_forces.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp, _vp]
     L.rs_score_forces.restype = ctypes.c_int64
+    L.rs_ppiem_scan.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp, ctypes.c_int32, _vp,
+                                ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                _vp, _vp, _vp]
+    L.rs_ppiem_scan.restype = ctypes.c_int64
+    L.rs_landscape_minima.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp]
+    L.rs_landscape_minima.restype = ctypes.c_int32
     L.rs_get_info.argtypes = [_vp, ctypes.POINTER(rs_info)]
     L.rs_get_info.restype = ctypes.c_int
     L.rs_export_tables.argtypes = [_vp] + [_vp] * 6
@@ -150,6 +156,36 @@ def rs_score_forces(h, q_lig, xyz_lig, n_lig, poses, P, forces_out, invalid_coun
     if r < 0:
         raise RuntimeError(f"rs_score_forces ({r}): " + rs_last_error())
     return int(r)
+
+
+def rs_ppiem_scan(h, q_lig, xyz_lig, centre, dirs, quats, s_start, tol=1e-3, max_iter=64):
+    """PPIEM scan (NEXT row N2): returns (energies, s, status), each m_P x m_L (numpy)."""
+    q_lig = np.ascontiguousarray(q_lig, dtype=np.float64) if isinstance(q_lig, np.ndarray) else q_lig
+    xyz_lig = np.ascontiguousarray(xyz_lig, dtype=np.float64) if isinstance(xyz_lig, np.ndarray) else xyz_lig
+    centre = np.ascontiguousarray(centre, dtype=np.float64)
+    dirs = np.ascontiguousarray(dirs, dtype=np.float64)
+    quats = np.ascontiguousarray(quats, dtype=np.float64)
+    m_P, m_L = dirs.shape[0], quats.shape[0]
+    E = np.empty((m_P, m_L))
+    s = np.empty((m_P, m_L))
+    st = np.empty((m_P, m_L), dtype=np.int32)
+    n_lig = int(q_lig.shape[0])
+    r = load().rs_ppiem_scan(h, _ptr(q_lig), _ptr(xyz_lig), n_lig, _ptr(centre), _ptr(dirs), m_P,
+                             _ptr(quats), m_L, float(s_start), float(tol), int(max_iter), _ptr(E),
+                             _ptr(s), _ptr(st))
+    if r < 0:
+        raise RuntimeError(f"rs_ppiem_scan ({r}): " + rs_last_error())
+    return E, s, st
+
+
+def rs_landscape_minima(E, top_k):
+    """PPIEM step A6: flat indices j*m_L + k of up to top_k local minima, by energy."""
+    E = np.ascontiguousarray(E, dtype=np.float64)
+    out = np.empty(max(int(top_k), 1), dtype=np.int32)
+    r = load().rs_landscape_minima(_ptr(E), E.shape[0], E.shape[1], int(top_k), _ptr(out))
+    if r < 0:
+        raise RuntimeError("rs_landscape_minima: " + rs_last_error())
+    return out[:r].copy()
 
 
 def rs_get_info(h) -> dict:

@@ -343,3 +343,14 @@ def random_small(seed=0, M=30, L=7, n=32, b=8.0, R=4, P=64, protein_radius=3.0,
     t = g[5].uniform(-trans, trans, size=(P, 3))
     return Workload(f"small{seed}", X, q, Y, z, np.concatenate([quats, t], axis=1), grid_n=n,
                     box_half_width=b, rank_R=R, sigma_split=1.0, sigma_vdw=1.0, dmin_cap=1.5)
+
+
+def planar_scan(m_P: int, m_L: int):
+    """PPIEM scan grid in the z = 0 plane (A0): m_P directions
+    (cos phi_j, sin phi_j, 0), phi_j = 2 pi j / m_P, and m_L ligand self-rotations about e_z,
+    quaternions (cos(phi_k / 2), 0, 0, sin(phi_k / 2)), phi_k = 2 pi k / m_L."""
+    phi = 2.0 * math.pi * np.arange(m_P) / m_P
+    dirs = np.stack([np.cos(phi), np.sin(phi), np.zeros(m_P)], axis=1)
+    psi = 2.0 * math.pi * np.arange(m_L) / m_L
+    quats = np.stack([np.cos(psi / 2), np.zeros(m_L), np.zeros(m_L), np.sin(psi / 2)], axis=1)
+    return dirs, quats

@@ -394,3 +394,30 @@ def test_forces_configs(env, name, k):
     Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, poses)
     frac = compare_forces(Fg, Fo, ig, io)
     assert frac > 0.99
+
+
+# ----------------------------------------------------------------------------- PPIEM scan (N2)
+
+@pytest.mark.parametrize("mP,mL", [(12, 8), (5, 3)])
+def test_ppiem_scan_matches_oracle(env, mP, mL):
+    """rs_ppiem_scan (NEXT row N2, reading A23) vs the PPIEM oracle on C1 geometry with a
+    D_cap > sigma build: the same statuses and contact distances bit for bit (the minimum
+    distances are bitwise equal), energies within 1e-12, and the same landscape minima."""
+    torch, rsdock, rs_oracle = env
+    from oracle import ppiem_oracle as po
+    w = syn.config_c1(n_poses=4)
+    prot = build(rsdock, w, dmin_cap=4.5)
+    dirs, quats = syn.planar_scan(mP, mL)
+    centre = w.protein_xyz.mean(0)
+    s_start = float(np.max(np.linalg.norm(w.protein_xyz - centre, axis=1)) + 6.0)
+    E, s, st = rsdock.rs_ppiem_scan(prot.handle, w.ligand_q, w.ligand_xyz, centre, dirs, quats,
+                                    s_start, tol=1e-3, max_iter=64)
+    Eo, so, sto = po.scan(prot.export_tables(), w.protein_xyz, w.protein_q, w.ligand_xyz,
+                          w.ligand_q, centre, dirs, quats, s_start, w.sigma_vdw, 4.5, 1e-3, 64)
+    assert np.array_equal(st, sto)
+    assert np.array_equal(s, so)
+    ok = ~np.isnan(Eo)
+    assert np.array_equal(np.isnan(E), np.isnan(Eo))
+    assert np.all(np.abs(E[ok] - Eo[ok]) <= 1e-12 * np.abs(Eo[ok]) + 1e-300)
+    assert (st == 0).mean() > 0.9
+    assert list(rsdock.rs_landscape_minima(E, 10)) == list(po.landscape_minima(Eo, 10))

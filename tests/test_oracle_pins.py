@@ -665,3 +665,51 @@ def test_forces_vs_analytic_coulomb_field(oracle):
         Fl = zL[:, None] * np.einsum("m,lmk->lk", qM, dx / r3[:, :, None])
         scale = np.abs(Fl).sum()
         assert np.linalg.norm(out[p, :3] - Fl.sum(0)) <= 0.08 * scale
+
+
+# ---------------------------------------------------------------------------------- N2 PPIEM
+def test_landscape_minima_rules():
+    """PPIEM A6 (reading A23): strict minima on the periodic grid, ties toward the smaller
+    index, NaN skipped; the oracle's and the library's host implementation agree."""
+    from oracle import ppiem_oracle as po
+    from paper_2510_26611_b200 import rsdock
+    E = np.full((4, 5), 2.0)
+    assert list(po.landscape_minima(E, 3)) == [0]            # constant: the smallest index only
+    E[2, 3] = -1.0
+    E[0, 0] = -0.5                                           # corner: neighbours wrap around
+    E[3, 4] = -0.5 + 1e-9
+    assert list(po.landscape_minima(E, 5)) == [2 * 5 + 3, 0]
+    E[1, 1] = np.nan
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        L = rng.integers(-3, 3, size=(rng.integers(1, 7), rng.integers(1, 7))).astype(float)
+        L[rng.random(L.shape) < 0.2] = np.nan
+        assert list(rsdock.rs_landscape_minima(L, 50)) == list(po.landscape_minima(L, 50))
+    assert list(rsdock.rs_landscape_minima(E, 5)) == list(po.landscape_minima(E, 5))
+
+
+def test_ppiem_oracle_two_charges_contact(oracle):
+    """Single-atom protein at the origin and single-atom ligand: every direction stops at the
+    vdW contact (sigma <= d <= sigma + tol) and the energy approaches z_M z_L / sigma within the
+    grid and quadrature error (SPEC ppiem example, 'energy ~ z_M z_L / sigma')."""
+    from oracle import ppiem_oracle as po
+    b, n = 10.0, 128
+    h, t, a, lm, ns = _rs_setup(oracle, b, n, 1e-8, 1.0)
+    X = np.array([[0.01, -0.02, 0.03]])
+    qM = np.array([0.8])
+    iM = oracle.snap_np(X, b, n)
+    F = oracle.uncompressed_long_factors(iM, qM, t, a, lm, n, h)
+    S = oracle.short_tables(t, a, lm, h, ns)
+    tables = dict(n=n, b=b, R=F[0].shape[1], F1=F[0], F2=F[1], F3=F[2], n_sigma=ns,
+                  S1=S[0], S2=S[1], S3=S[2])
+    dirs, quats = syn.planar_scan(8, 3)
+    sigma, dcap, tol = 2.5, 4.5, 1e-3
+    E, s, st = po.scan(tables, X, qM, np.zeros((1, 3)), np.array([-0.6]), X[0], dirs, quats,
+                       8.0, sigma, dcap, tol)
+    assert np.all(st == 0)
+    d = np.abs(s)       # the ligand centre is the atom: d = |t - x_M| ~ s (X is the centre)
+    assert np.all(d >= sigma) and np.all(d <= sigma + 2 * tol)
+    # snapping moves each of the two charges by <= sqrt(3) h / 2, so their distance changes by
+    # <= sqrt(3) h: relative error of 1/r <= sqrt(3) h / (sigma - sqrt(3) h)
+    bound = math.sqrt(3) * h / (sigma - math.sqrt(3) * h)
+    assert np.all(np.abs(E - 0.8 * -0.6 / s) <= (bound + 1e-6) * np.abs(0.8 * 0.6 / s))
