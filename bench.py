@@ -192,6 +192,46 @@ def config_dict(w, args):
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
+def bench_ppiem(args):
+    """PPIEM scan (rs_ppiem_scan, reading A23) on the config's protein and ligand: planar grid of
+    M positions x M self-rotations, approach to vdW contact by sphere tracing on the device
+    (D_cap = sigma + 2 A), landscape and minima.  Wall time of the synchronous call."""
+    import torch
+    from paper_2510_26611_b200 import rsdock
+    from synth import configs as syn
+    import __graft_entry__
+    __graft_entry__.build_library()
+    w = load_workload(args.config)
+    prm = dict(w.params())
+    prm["dmin_cap"] = w.sigma_vdw + 2.0
+    prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **prm)
+    dirs, quats = syn.planar_scan(args.ppiem, args.ppiem)
+    centre = w.protein_xyz.mean(0)
+    rl = float(np.max(np.linalg.norm(w.ligand_xyz, axis=1)))
+    s_start = float(np.max(np.linalg.norm(w.protein_xyz - centre, axis=1))) + rl + 3.0
+    s_start = min(s_start, w.box_half_width - rl - 1.0)
+    q = torch.tensor(w.ligand_q, device="cuda")
+    y = torch.tensor(w.ligand_xyz, device="cuda").contiguous()
+    rsdock.rs_ppiem_scan(prot.handle, q, y, centre, dirs, quats, s_start)     # warm-up
+    times = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        E, sv, st = rsdock.rs_ppiem_scan(prot.handle, q, y, centre, dirs, quats, s_start)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    mins = rsdock.rs_landscape_minima(E, 10)
+    line = {"metric": "PPIEM scan landscape entries/s (approach + energy)", "value": E.size / t,
+            "unit": "entries/s", "n_gpus": 1, "steps": len(times), "ms_per_scan": 1e3 * t,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "m_P": args.ppiem, "m_L": args.ppiem, "s_start": s_start,
+                       "dmin_cap": prm["dmin_cap"]},
+            "status_counts": {str(k): int((st == k).sum()) for k in range(5)},
+            "best": [{"j": int(i // args.ppiem), "k": int(i % args.ppiem), "E": float(E.flat[i]),
+                      "s": float(sv.flat[i])} for i in mins[:3]]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +243,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-microbench", action="store_true")
+    ap.add_argument("--ppiem", type=int, default=0, metavar="M",
+                    help="time a PPIEM scan (NEXT row N2) with M positions x M self-rotations")
     ap.add_argument("--forces", action="store_true",
                     help="time rs_score_forces (NEXT row N1) instead of the energy path")
     ap.add_argument("--f32", action="store_true",
@@ -212,6 +254,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return impl_reference(args)
+    if args.ppiem:
+        return bench_ppiem(args)
 
     import torch
     world = _env_int("WORLD_SIZE", 1)
