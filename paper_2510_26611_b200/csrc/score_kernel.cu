@@ -818,9 +818,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   for (;;) {
     if (tid == 0) s_chunk = atomicAdd(a.work, 1);
     __syncthreads();
-    const int64_t c0 = (int64_t)s_chunk * kChunk;
+    // guided tail: full chunks for the first ~7/8 of the poses, then kChunk/8-pose chunks so
+    // the CTAs finish together
+    const int64_t nbig = (a.P - a.P / 8) / kChunk;
+    const int64_t c0 = s_chunk < nbig ? (int64_t)s_chunk * kChunk
+                                      : nbig * kChunk + (int64_t)(s_chunk - nbig) * (kChunk / 8);
     if (c0 >= a.P) break;
-    const int64_t p_end = c0 + kChunk < a.P ? c0 + kChunk : a.P;
+    const int64_t csz = s_chunk < nbig ? kChunk : kChunk / 8;
+    const int64_t p_end = c0 + csz < a.P ? c0 + csz : a.P;
     int64_t p = c0;
     while (p < p_end) {
       int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
@@ -1045,7 +1050,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   const int64_t lig_fit = (int64_t)((avail - std::min(avail, win_b)) / sizeof(double4));
   const int lig_n = (int)std::min<int64_t>(a.L, cap_rows > 0 ? std::min<int64_t>(lig_fit, 256) : lig_fit);
   const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
-  const int64_t chunks = (a.P + kChunk - 1) / kChunk;
+  const int64_t chunks = (a.P + kChunk - 1) / kChunk;   // at least one per CTA
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
   score_kernel<RT, NA, F32><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
