@@ -46,7 +46,7 @@ namespace {
 #define RS_TILE 512
 #endif
 #ifndef RS_CHUNK
-#define RS_CHUNK 512
+#define RS_CHUNK 1024
 #endif
 #ifndef RS_WIN_SLACK
 #define RS_WIN_SLACK 1.03
@@ -55,6 +55,13 @@ constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = RS_TILE;           // poses per tile (upper bound)
 constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
+#ifndef RS_TAIL_DIV
+#define RS_TAIL_DIV 8
+#endif
+#ifndef RS_TAIL_CHUNK
+#define RS_TAIL_CHUNK 128
+#endif
+constexpr int kTailChunk = RS_TAIL_CHUNK;  // chunk size over the last 1/RS_TAIL_DIV of the poses
 static_assert(kTile <= kThreads, "one thread per pose of a tile");
 constexpr unsigned kFull = 0xffffffffu;
 #ifndef RS_SLOTS
@@ -818,13 +825,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   for (;;) {
     if (tid == 0) s_chunk = atomicAdd(a.work, 1);
     __syncthreads();
-    // guided tail: full chunks for the first ~7/8 of the poses, then kChunk/8-pose chunks so
-    // the CTAs finish together
-    const int64_t nbig = (a.P - a.P / 8) / kChunk;
+    // guided tail: full chunks for the first (1 - 1/RS_TAIL_DIV) of the poses, then
+    // kTailChunk-pose chunks so that the CTAs finish together
+    const int64_t nbig = (a.P - a.P / RS_TAIL_DIV) / kChunk;
     const int64_t c0 = s_chunk < nbig ? (int64_t)s_chunk * kChunk
-                                      : nbig * kChunk + (int64_t)(s_chunk - nbig) * (kChunk / 8);
+                                      : nbig * kChunk + (int64_t)(s_chunk - nbig) * kTailChunk;
     if (c0 >= a.P) break;
-    const int64_t csz = s_chunk < nbig ? kChunk : kChunk / 8;
+    const int64_t csz = s_chunk < nbig ? kChunk : kTailChunk;
     const int64_t p_end = c0 + csz < a.P ? c0 + csz : a.P;
     int64_t p = c0;
     while (p < p_end) {

@@ -361,9 +361,9 @@ def compare_forces(Fg, Fo, ig, io):
     ok = ~np.isnan(Fo)
     scale = np.maximum(np.abs(Fo), 1e-300)
     # per component: bitwise expected; 1e-12 relative to the pose's largest component otherwise
-    big = np.nanmax(np.abs(Fo), axis=1, keepdims=True) * np.ones_like(Fo)
+    big = np.max(np.where(ok, np.abs(Fo), 0.0), axis=1, keepdims=True) * np.ones_like(Fo)
     assert np.all((Fg[ok] == Fo[ok]) | (np.abs(Fg[ok] - Fo[ok]) <= 1e-12 * big[ok])), \
-        float(np.nanmax(np.abs(Fg - Fo) / scale))
+        float(np.max(np.where(ok, np.abs(Fg - Fo) / scale, 0.0)))
     return float(np.mean(Fg[ok] == Fo[ok]))
 
 
