@@ -16,7 +16,8 @@
 // lanes accumulate and the reduction tree are free.  The snap (O3) is finished in integers
 // after the two fp64 ops that define it (ceil of a value in [0, n+1) is exact).
 //
-// Work layout: persistent CTAs (one per SM) own contiguous pose ranges; a warp
+// Work layout: persistent CTAs (one per SM, 32 warps) take chunks of
+// consecutive poses from a global counter (guided: smaller chunks over the last poses); a warp
 // scores one pose at a time (lanes over ligand atoms), taking poses from a per-tile queue.
 // A tile is the longest run of poses whose rows fit the shared-memory window (a block scan of
 // per-pose row bounds); the window's rows of the three factor matrices arrive by TMA bulk
@@ -25,7 +26,8 @@
 // replicated (R=4, 8) to whole 128-byte lines; lane l reads chunk c ^ (l & 7) of its own row in
 // slot c, so the 8 lanes of every quarter-warp hit 8 distinct bank groups whatever rows they
 // gather (conflict-free LDS.128); the halving tree over rank pairs is invariant under that
-// relabelling, so no un-permute is needed.
+// relabelling, so no un-permute is needed.  RS_FLAG_F32_FACTORS (reading A21) runs the same
+// machinery on binary32 rows of rank quads.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -158,11 +160,7 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
 
 // One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
 __device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
-#ifdef RS_FMA_PROBE  // timing probe only: not the evaluation contract
-  return __fma_rn(__dmul_rn(a.y, b.y), c.y, __dmul_rn(__dmul_rn(a.x, b.x), c.x));
-#else
   return __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), c.x), __dmul_rn(__dmul_rn(a.y, b.y), c.y));
-#endif
 }
 
 // O4 halving tree over NS pair sums (A20): s_c = s_c + s_{c+m}, m = NS/2 .. 1
@@ -208,22 +206,7 @@ __device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, un
                                                 unsigned r2, int rho) {
   using G = Geo<R>;
   const unsigned x = (unsigned)rho << 4;
-#ifdef RS_TREE_LEVELS
-  r0 |= x;
-  r1 |= x;
-  r2 |= x;
-  double s[G::NS];
-#pragma unroll
-  for (int c = 0; c < G::NS; ++c) {
-    const unsigned o = (unsigned)c << 4;
-    s[c] = pair_prod(*reinterpret_cast<const double2*>(win + (r0 ^ o)),
-                     *reinterpret_cast<const double2*>(win + (r1 ^ o)),
-                     *reinterpret_cast<const double2*>(win + (r2 ^ o)));
-  }
-  return halving_tree<G::NS>(s);
-#else
   return SmemTree<0, 1, G::NS>::eval(win, r0 | x, r1 | x, r2 | x);
-#endif
 }
 
 // O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
@@ -329,14 +312,8 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
 
 struct Window {
   int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
-#ifdef RS_NB_BITMAP
-  int blo[3], bdim[3];         // coarse cells covered by the occupancy bitmap (bdim 0: none)
-#endif
 };
 
-#ifdef RS_NB_BITMAP
-constexpr int kBitWords = 2048;  // occupancy bitmap of the window's coarse cells (64 K cells)
-#endif
 
 struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
   double m[12];
@@ -438,7 +415,7 @@ struct AtomState {
 template <bool LIG_SMEM>
 __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
                                            const double* tv, const double2* s_lig, int lig_n,
-                                           const Window& W, const unsigned* bits, AtomState& st,
+                                           AtomState& st,
                                            bool& bad) {
   const bool act = l < a.L;
   const int lc = act ? l : a.L - 1;
@@ -455,15 +432,9 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
   }
   st.z = act ? z : 0.0;
   // H2 (O2)
-#ifdef RS_FMA_PROBE  // timing probe only: not the evaluation contract
-  st.x0 = __fma_rn(Rm[0], y0, __fma_rn(Rm[1], y1, __fma_rn(Rm[2], y2, tv[0])));
-  st.x1 = __fma_rn(Rm[3], y0, __fma_rn(Rm[4], y1, __fma_rn(Rm[5], y2, tv[1])));
-  st.x2 = __fma_rn(Rm[6], y0, __fma_rn(Rm[7], y1, __fma_rn(Rm[8], y2, tv[2])));
-#else
   st.x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
   st.x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
   st.x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
-#endif
   // H3 (O3): valid iff -b <= x'_a <= b on every axis (false for NaN)
   const bool ok = fabs(st.x0) <= a.b && fabs(st.x1) <= a.b && fabs(st.x2) <= a.b;
   bad = bad || (act && !ok);
@@ -481,20 +452,7 @@ __device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const doub
   const unsigned cy = (unsigned)((st.i1 >> a.nb_shift) - a.nb_lo[1]);
   const unsigned cz = (unsigned)((st.i2 >> a.nb_shift) - a.nb_lo[2]);
   {
-    bool maybe = true;
-#ifdef RS_NB_BITMAP
-    {
-      // coarse cells of the window: a shared-memory bitmap says whether the list is empty
-      const unsigned bx = (unsigned)((st.i0 >> a.nb_shift) - W.blo[0]);
-      const unsigned by = (unsigned)((st.i1 >> a.nb_shift) - W.blo[1]);
-      const unsigned bz = (unsigned)((st.i2 >> a.nb_shift) - W.blo[2]);
-      if (bx < (unsigned)W.bdim[0] && by < (unsigned)W.bdim[1] && bz < (unsigned)W.bdim[2]) {
-        const unsigned c = (bx * W.bdim[1] + by) * W.bdim[2] + bz;
-        maybe = (bits[c >> 5] >> (c & 31)) & 1u;
-      }
-    }
-#endif
-    const bool in = maybe && st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
+    const bool in = st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
     const int2 bc = ldg_if(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz, in);
     st.beg = bc.x;
     st.cnt = bc.y;
@@ -591,12 +549,8 @@ template <int RT, int NA, bool F32>
 __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
                                            bool ok, bool use_win, const Window& W,
                                            const char* win, const double2* s_lig, int lig_smem_n,
-                                           const unsigned* bits, int lane, PairStage<NA>& ps,
+                                           int lane, PairStage<NA>& ps,
                                            double2& out) {
-#ifdef RS_RM_PER_POSE
-  double Rm[9], tv[3];
-  load_pose(pr, Rm, tv);
-#endif
   double hi[NA], lo[NA], best = INFINITY;
 #pragma unroll
   for (int u = 0; u < NA; ++u) hi[u] = lo[u] = 0.0;
@@ -606,27 +560,15 @@ __device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const 
   const int L = ok ? a.L : 0;
   const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   for (int l0 = 0; l0 < L; l0 += 32 * NA) {
-#ifndef RS_RM_PER_POSE
     // the pose's R and t, re-read from shared memory (broadcast) each pass: they are live only
     // during H2, which keeps registers for more resident warps
     double Rm[9], tv[3];
-#ifdef RS_POSE_SHFL
-    {
-      const double v = lane < 12 ? pr.m[lane] : 0.0;   // one 96-byte shared load, then shuffles
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Rm[i] = __shfl_sync(kFull, v, i);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) tv[i] = __shfl_sync(kFull, v, 9 + i);
-    }
-#else
     load_pose(pr, Rm, tv);
-#endif
-#endif
     AtomState st[NA];
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
-      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
-      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, W, bits, st[u], bad);
+      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
+      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
     }
     long_range_stage<RT, NA, F32>(a, st, use_win, W, win, rho, hi, lo);
     if (__any_sync(kFull, bad)) {
@@ -780,9 +722,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
   __shared__ int s_next, s_restaged, s_chunk;
-#ifdef RS_NB_BITMAP
-  __shared__ unsigned s_bits[kBitWords];
-#endif
   __shared__ double s_rmax2[kWarps];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -805,10 +744,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     s_cur.lo[0] = s_cur.lo[1] = s_cur.lo[2] = 1;
     s_cur.hi[0] = s_cur.hi[1] = s_cur.hi[2] = 0;   // empty
     s_cur.off[0] = s_cur.off[1] = s_cur.off[2] = 0;
-#ifdef RS_NB_BITMAP
-    s_cur.bdim[0] = s_cur.bdim[1] = s_cur.bdim[2] = 0;
-    s_cur.blo[0] = s_cur.blo[1] = s_cur.blo[2] = 0;
-#endif
     mbar_init(&s_bar);
   }
   __syncthreads();
@@ -937,14 +872,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               s_cur.lo[r] = lo_[r];
               s_cur.hi[r] = hi_[r];
               s_cur.off[r] = row0 - lo_[r];
-#ifdef RS_NB_BITMAP
-              {
-                const int c0 = max(lo_[r] >> a.nb_shift, a.nb_lo[r]);
-                const int c1 = min(hi_[r] >> a.nb_shift, a.nb_lo[r] + a.nb_dim[r] - 1);
-                s_cur.blo[r] = c0;
-                s_cur.bdim[r] = max(c1 - c0 + 1, 0);
-              }
-#endif
               const void* src = F32 ? (const void*)(a.t.Fw32[r] + (size_t)lo_[r] * kChp)
                                     : (const void*)(a.t.Fw[r] + (size_t)lo_[r] * kChp);
               tma_load_1d(win + (size_t)row0 * kChp, src,
@@ -966,31 +893,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       if (s_restaged) {
         mbar_wait(&s_bar, phase);
         phase ^= 1;
-#ifdef RS_NB_BITMAP
-        {
-          // occupancy bitmap of the new window's coarse cells (bit = list not empty)
-          const int d0 = s_cur.bdim[0], d1 = s_cur.bdim[1], d2 = s_cur.bdim[2];
-          const int ncell = d0 * d1 * d2;
-          if (ncell > 32 * kBitWords) {
-            __syncthreads();
-            if (tid == 0) s_cur.bdim[0] = s_cur.bdim[1] = s_cur.bdim[2] = 0;
-          } else {
-            for (int w0 = 0; w0 < (ncell + 31) / 32; w0 += kWarps) {
-              const int c = (w0 + warp) * 32 + lane;
-              bool occ = false;
-              if (c < ncell) {
-                const int x = c / (d1 * d2), y = (c / d2) % d1, z = c % d2;
-                const int g = ((x + s_cur.blo[0] - a.nb_lo[0]) * a.nb_dim[1] + (y + s_cur.blo[1] - a.nb_lo[1])) *
-                                  a.nb_dim[2] + (z + s_cur.blo[2] - a.nb_lo[2]);
-                occ = __ldg(a.t.nb_range + g).y > 0;
-              }
-              const unsigned m = __ballot_sync(kFull, occ);
-              if (lane == 0 && w0 + warp < kBitWords) s_bits[w0 + warp] = m;
-            }
-          }
-          __syncthreads();
-        }
-#endif
       }
       const Window W = s_cur;
       for (;;) {
@@ -998,13 +900,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(kFull, s, 0);
         if (s >= T) break;
-#ifdef RS_NB_BITMAP
-        const unsigned* bits = s_bits;
-#else
-        const unsigned* bits = nullptr;
-#endif
         score_pose<RT, NA, F32>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
-                           bits, lane, s_ps[warp], s_out[s]);
+                           lane, s_ps[warp], s_out[s]);
       }
       __syncthreads();
       // H8: d = sqrt(min d^2) below D_cap^2, else +inf; NaN for invalid poses (O8)
