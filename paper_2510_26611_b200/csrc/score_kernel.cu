@@ -310,6 +310,11 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
   return (double)s[0];
 }
 
+struct ChunkPlan {             // dynamic schedule: nbig chunks of `big` poses, then `tail`-pose chunks
+  int64_t nbig;
+  int big, tail;
+};
+
 struct Window {
   int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
 };
@@ -707,7 +712,7 @@ __host__ __device__ constexpr size_t win_offset() {
 
 template <int RT, int NA, bool F32>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
-                                                            int lig_smem_n) {
+                                                            int lig_smem_n, const ChunkPlan cp) {
   // dynamic shared memory (256-B aligned base; every offset but the ligand's is a compile-time
   // constant, so addresses are immediates rather than recomputed values):
   //   [PoseRec x kTile][PairStage x warps][factor-row window, 256-B aligned][ligand 2 x double2 x n]
@@ -760,13 +765,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   for (;;) {
     if (tid == 0) s_chunk = atomicAdd(a.work, 1);
     __syncthreads();
-    // guided tail: full chunks for the first (1 - 1/RS_TAIL_DIV) of the poses, then
-    // kTailChunk-pose chunks so that the CTAs finish together
-    const int64_t nbig = (a.P - a.P / RS_TAIL_DIV) / kChunk;
-    const int64_t c0 = s_chunk < nbig ? (int64_t)s_chunk * kChunk
-                                      : nbig * kChunk + (int64_t)(s_chunk - nbig) * kTailChunk;
+    // guided schedule (host-computed, ChunkPlan): nbig chunks of `big` poses, then chunks of
+    // `tail` poses so that the CTAs finish together
+    const int64_t nbig = cp.nbig;
+    const int64_t c0 = s_chunk < nbig ? (int64_t)s_chunk * cp.big
+                                      : nbig * cp.big + (int64_t)(s_chunk - nbig) * cp.tail;
     if (c0 >= a.P) break;
-    const int64_t csz = s_chunk < nbig ? kChunk : kTailChunk;
+    const int64_t csz = s_chunk < nbig ? cp.big : cp.tail;
     const int64_t p_end = c0 + csz < a.P ? c0 + csz : a.P;
     int64_t p = c0;
     while (p < p_end) {
@@ -859,9 +864,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             unsigned bytes = 0;
             int lo_[3], hi_[3];
 #pragma unroll
+            const bool all = cap_rows >= 3 * a.n;     // the whole factor set fits
             for (int r = 0; r < 3; ++r) {
-              lo_[r] = max(0, wlo[r] - extra / 2);
-              hi_[r] = min(a.n - 1, whi[r] + (extra - extra / 2));
+              lo_[r] = all ? 0 : max(0, wlo[r] - extra / 2);
+              hi_[r] = all ? a.n - 1 : min(a.n - 1, whi[r] + (extra - extra / 2));
               bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16;
             }
             // the window was last read through the generic proxy, before the previous barrier
@@ -943,7 +949,10 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   int cap_rows = 0;
   if (RT > 0 && window_mode && (F32 ? (const void*)a.t.Fw32[0] : (const void*)a.t.Fw[0])) {
     cap_rows = (int)std::min<size_t>((avail - lig_res) / (16 * kChp), (1u << 20) / (16 * kChp) - 1);
-    if (a.rmax_hint >= 0) {
+    if (3 * a.n <= cap_rows) {
+      // the whole factor set fits (small grids, e.g. C1): stage it once, every tile fits
+      cap_rows = 3 * a.n;
+    } else if (a.rmax_hint >= 0) {
       // leave the rest of the 228 KB to L1 (cell lists, records, memo): what one
       // translation's window needs plus RS_WIN_SLACK
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
@@ -954,10 +963,17 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   const int64_t lig_fit = (int64_t)((avail - std::min(avail, win_b)) / sizeof(double4));
   const int lig_n = (int)std::min<int64_t>(a.L, cap_rows > 0 ? std::min<int64_t>(lig_fit, 256) : lig_fit);
   const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
-  const int64_t chunks = (a.P + kChunk - 1) / kChunk;   // at least one per CTA
+  // chunk plan: big chunks for the first (1 - 1/RS_TAIL_DIV) of the poses, then tail chunks of
+  // at most kTailChunk poses, small enough that every SM gets work when P is small
+  ChunkPlan cp;
+  cp.big = kChunk;
+  cp.nbig = (a.P - a.P / RS_TAIL_DIV) / kChunk;
+  const int64_t rest = a.P - cp.nbig * kChunk;
+  cp.tail = (int)std::max<int64_t>(1, std::min<int64_t>(kTailChunk, (rest + 2 * dc.sms - 1) / (2 * dc.sms)));
+  const int64_t chunks = cp.nbig + (rest + cp.tail - 1) / cp.tail;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
-  score_kernel<RT, NA, F32><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n);
+  score_kernel<RT, NA, F32><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n, cp);
   return (int)cudaGetLastError();
 }
 
