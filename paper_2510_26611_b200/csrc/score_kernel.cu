@@ -51,7 +51,7 @@ namespace {
 #define RS_CHUNK 1024
 #endif
 #ifndef RS_WIN_SLACK
-#define RS_WIN_SLACK 1.03
+#define RS_WIN_SLACK 1.5
 #endif
 constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
