@@ -8,7 +8,10 @@
  *   - rs_build_protein  = Algorithm TEP, once per protein, host C++;
  *   - rs_score_poses    = Algorithm PLIE with Lemma 3.2 / Eq. (18)
  *     (PAPER.md:864-891), the RS entry formula and the van der Waals
- *     constraint of Eq. (22), one fused sm_100a kernel.
+ *     constraint of Eq. (22), one fused sm_100a kernel;
+ *   - rs_score_forces   = forces on the rigid ligand (§3.3 Eq. (21), §4 Eqs. (24)-(25));
+ *   - rs_ppiem_scan     = Algorithm PPIEM steps A3-A6 on the device,
+ *     with rs_landscape_minima (A6) on the host.
  *
  * Units: the library is unit-agnostic.  Lengths in the caller's unit (the tests and bench
  * use Angstrom), charges in e, energies in charge^2/length (x 0.529177210903 = hartree
