@@ -22,6 +22,9 @@ namespace rs {
 namespace {
 
 constexpr int kForceThreads = 256;
+#ifndef RS_FORCE_MINB
+#define RS_FORCE_MINB 1          // resident blocks per SM the register budget must allow
+#endif
 constexpr unsigned kAll = 0xffffffffu;
 
 __device__ __forceinline__ bool quat_rot(const double* q, double* R) {
@@ -126,7 +129,8 @@ __device__ __forceinline__ int snap_cell(double x, double b, double inv_h, int n
 }
 
 template <int R>
-__global__ void __launch_bounds__(kForceThreads) force_kernel(const ScoreArgs a, double* out) {
+__global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(const ScoreArgs a,
+                                                                             double* out) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = ((int64_t)blockIdx.x * kForceThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kForceThreads) >> 5;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kForceThreads) force_kernel(const ScoreArgs a,
 template <int R>
 int launch_forces_t(const ScoreArgs& a, double* out, cudaStream_t st, int sms) {
   const int64_t warps_needed = a.P;
-  const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)sms * 8);
+  const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)sms * 8 * RS_FORCE_MINB);
   force_kernel<R><<<(int)std::max<int64_t>(blocks, 1), kForceThreads, 0, st>>>(a, out);
   return (int)cudaGetLastError();
 }

@@ -965,10 +965,11 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
   // chunk plan: big chunks for the first (1 - 1/RS_TAIL_DIV) of the poses, then tail chunks of
   // at most kTailChunk poses, small enough that every SM gets work when P is small
+  // (big chunks also shrink with P: at least ~4 per SM, so one chunk never dominates a launch)
   ChunkPlan cp;
-  cp.big = kChunk;
-  cp.nbig = (a.P - a.P / RS_TAIL_DIV) / kChunk;
-  const int64_t rest = a.P - cp.nbig * kChunk;
+  cp.big = (int)std::max<int64_t>(kTailChunk, std::min<int64_t>(kChunk, a.P / (4 * (int64_t)dc.sms)));
+  cp.nbig = (a.P - a.P / RS_TAIL_DIV) / cp.big;
+  const int64_t rest = a.P - cp.nbig * cp.big;
   cp.tail = (int)std::max<int64_t>(1, std::min<int64_t>(kTailChunk, (rest + 2 * dc.sms - 1) / (2 * dc.sms)));
   const int64_t chunks = cp.nbig + (rest + cp.tail - 1) / cp.tail;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
