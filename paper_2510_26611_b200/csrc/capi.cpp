@@ -543,12 +543,15 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   const bool pose_dev = pointer_kind(poses) == 1;
   const bool e_dev = pointer_kind(energies_out) == 1;
   const bool d_dev = pointer_kind(mindist_out) == 1;
-  // chunked 2-stream pipeline: H2D(poses chunk) -> kernel -> D2H(outputs chunk), so the copies
-  // of one chunk overlap the kernel of the other
-  const int64_t CH = std::min<int64_t>(P, std::max<int64_t>(1 << 16, (P + 7) / 8));
+  // pipeline over kStreams streams: H2D(chunk) -> kernel -> D2H(chunk), chunk sizes growing
+  // geometrically (x1.5 from ~P/64), so the first copy exposes little and the later copies hide
+  // behind the kernels of the earlier chunks; every chunk has its own staging region, and the
+  // kernels of different chunks may overlap on the device
+  constexpr int kStreams = 3;
   const size_t lig_b = (size_t)4 * std::max<int64_t>(n_lig, 1) * sizeof(double);
-  const size_t pose_b = (size_t)CH * 7 * sizeof(double), out_b = (size_t)CH * sizeof(double);
-  const size_t need = lig_b + 2 * pose_b + 4 * out_b + 64;
+  const size_t pose_b = pose_dev ? 0 : (size_t)P * 7 * sizeof(double);
+  const size_t out_b = (size_t)P * sizeof(double);
+  const size_t need = lig_b + pose_b + (e_dev ? 0 : out_b) + (d_dev ? 0 : out_b) + 64 * kStreams;
   if (h->stage_bytes < need) {
     if (h->stage) cudaFree(h->stage);
     h->stage = nullptr;
@@ -560,39 +563,45 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     if (!s) CUDA_TRY(cudaStreamCreateWithFlags((cudaStream_t*)&s, cudaStreamNonBlocking), RS_E_CUDA);
   char* base = (char*)h->stage;
   double* d_lig = (double*)base;
-  double* d_pose[2] = {(double*)(base + lig_b), (double*)(base + lig_b + pose_b)};
-  double* d_E[2] = {(double*)(base + lig_b + 2 * pose_b), (double*)(base + lig_b + 2 * pose_b + out_b)};
-  double* d_D[2] = {(double*)(base + lig_b + 2 * pose_b + 2 * out_b),
-                    (double*)(base + lig_b + 2 * pose_b + 3 * out_b)};
-  unsigned long long* d_cnt = (unsigned long long*)(base + lig_b + 2 * pose_b + 4 * out_b);
+  double* d_pose = (double*)(base + lig_b);
+  double* d_E = (double*)(base + lig_b + pose_b);
+  double* d_D = (double*)(base + lig_b + pose_b + (e_dev ? 0 : out_b));
+  unsigned long long* d_cnt =
+      (unsigned long long*)(base + lig_b + pose_b + (e_dev ? 0 : out_b) + (d_dev ? 0 : out_b));
+  cudaStream_t st[kStreams];
+  for (int i = 0; i < kStreams; ++i) st[i] = (cudaStream_t)h->streams[i];
   const double *zl = q_lig, *yl = xyz_lig;
   if (!lig_dev) {
-    CUDA_TRY(cudaMemcpy(d_lig, q_lig, n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
-    CUDA_TRY(cudaMemcpy(d_lig + n_lig, xyz_lig, 3 * n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpyAsync(d_lig, q_lig, n_lig * sizeof(double), cudaMemcpyHostToDevice, st[0]), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpyAsync(d_lig + n_lig, xyz_lig, 3 * n_lig * sizeof(double), cudaMemcpyHostToDevice, st[0]), RS_E_CUDA);
     zl = d_lig;
     yl = d_lig + n_lig;
   }
-  cudaStream_t st[2] = {(cudaStream_t)h->streams[0], (cudaStream_t)h->streams[1]};
-  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), st[0]), RS_E_CUDA);
-  CUDA_TRY(cudaStreamSynchronize(st[0]), RS_E_CUDA);
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, kStreams * sizeof(unsigned long long), st[0]), RS_E_CUDA);
+  cudaEvent_t ready;
+  CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), RS_E_CUDA);
+  CUDA_TRY(cudaEventRecord(ready, st[0]), RS_E_CUDA);
+  for (int i = 1; i < kStreams; ++i) CUDA_TRY(cudaStreamWaitEvent(st[i], ready, 0), RS_E_CUDA);
+  cudaEventDestroy(ready);
   rs::ScoreArgs a = base_args(h);
   a.zl = zl;
   a.yl = yl;
   a.L = n_lig;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
   int chunk = 0;
-  for (int64_t off = 0; off < P; off += CH, ++chunk) {
-    const int64_t cnt = std::min(CH, P - off);
-    const int s = chunk & 1;
+  int64_t csz = std::min<int64_t>(P, std::max<int64_t>(4096, P / 64));
+  for (int64_t off = 0; off < P; off += csz, csz = csz + csz / 2, ++chunk) {
+    const int64_t cnt = std::min(csz, P - off);
+    const int s = chunk % kStreams;
     const double* pp = poses + 7 * off;
     if (!pose_dev) {
-      CUDA_TRY(cudaMemcpyAsync(d_pose[s], pp, cnt * 7 * sizeof(double), cudaMemcpyHostToDevice, st[s]), RS_E_CUDA);
-      pp = d_pose[s];
+      CUDA_TRY(cudaMemcpyAsync(d_pose + 7 * off, pp, cnt * 7 * sizeof(double), cudaMemcpyHostToDevice, st[s]), RS_E_CUDA);
+      pp = d_pose + 7 * off;
     }
     a.poses = pp;
     a.P = cnt;
-    a.E = e_dev ? energies_out + off : d_E[s];
-    a.D = d_dev ? mindist_out + off : d_D[s];
+    a.E = e_dev ? energies_out + off : d_E + off;
+    a.D = d_dev ? mindist_out + off : d_D + off;
     a.invalid = d_cnt + s;
     a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
     CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st[s]), RS_E_CUDA);
@@ -601,14 +610,13 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
       set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
       return RS_E_CUDA;
     }
-    if (!e_dev) CUDA_TRY(cudaMemcpyAsync(energies_out + off, d_E[s], cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
-    if (!d_dev) CUDA_TRY(cudaMemcpyAsync(mindist_out + off, d_D[s], cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
+    if (!e_dev) CUDA_TRY(cudaMemcpyAsync(energies_out + off, d_E + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
+    if (!d_dev) CUDA_TRY(cudaMemcpyAsync(mindist_out + off, d_D + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, st[s]), RS_E_CUDA);
   }
-  CUDA_TRY(cudaStreamSynchronize(st[1]), RS_E_CUDA);
-  CUDA_TRY(cudaStreamSynchronize(st[0]), RS_E_CUDA);
-  unsigned long long cnts[2] = {0, 0};
+  for (int i = 0; i < kStreams; ++i) CUDA_TRY(cudaStreamSynchronize(st[i]), RS_E_CUDA);
+  unsigned long long cnts[kStreams] = {0, 0, 0};
   CUDA_TRY(cudaMemcpy(cnts, d_cnt, sizeof(cnts), cudaMemcpyDeviceToHost), RS_E_CUDA);
-  return (int64_t)(cnts[0] + cnts[1]);
+  return (int64_t)(cnts[0] + cnts[1] + cnts[2]);
 }
 
 int32_t rs_landscape_minima(const double* E, int32_t m_P, int32_t m_L, int32_t top_k,

@@ -155,7 +155,7 @@ struct rs_handle {
   std::mutex mtx;
   void* stage = nullptr;
   size_t stage_bytes = 0;
-  void* streams[2] = {nullptr, nullptr};
+  void* streams[3] = {nullptr, nullptr, nullptr};
   // cached ligand radius for device-resident ligands (only steers the launch shape)
   const void* rmax_key = nullptr;
   int64_t rmax_L = -1;
