@@ -421,3 +421,31 @@ def test_ppiem_scan_matches_oracle(env, mP, mL):
     assert np.all(np.abs(E[ok] - Eo[ok]) <= 1e-12 * np.abs(Eo[ok]) + 1e-300)
     assert (st == 0).mean() > 0.9
     assert list(rsdock.rs_landscape_minima(E, 10)) == list(po.landscape_minima(Eo, 10))
+
+
+def test_ppiem_scan_statuses(env):
+    """Every status of rs_ppiem_scan against the oracle: 2 (clash at the start: s_start inside
+    the protein), 1 (a ligand atom leaves the box: s_start beyond b), 3 (the line misses the
+    protein, s goes below 0: the centre is offset from a small protein), 4 (max_iter reached)."""
+    torch, rsdock, rs_oracle = env
+    from oracle import ppiem_oracle as po
+    w = syn.random_small(seed=77, M=12, L=6, n=64, b=8.0, R=8, P=4, protein_radius=1.5)
+    prot = build(rsdock, w, dmin_cap=4.0, sigma_vdw=1.5)
+    dirs, quats = syn.planar_scan(6, 2)
+    tb = prot.export_tables()
+    cases = [(w.protein_xyz.mean(0), 0.5, 64),                   # clash at the start
+             (w.protein_xyz.mean(0), 9.0, 64),                   # starts outside the box
+             (w.protein_xyz.mean(0) + [0.0, 0.0, 3.5], 4.0, 64),  # lines above the protein
+             (w.protein_xyz.mean(0), 6.0, 1)]                    # one iteration only
+    seen = set()
+    for centre, s0, it in cases:
+        E, s, st = rsdock.rs_ppiem_scan(prot.handle, w.ligand_q, w.ligand_xyz, centre, dirs, quats,
+                                        s0, tol=1e-3, max_iter=it)
+        Eo, so, sto = po.scan(tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, centre,
+                              dirs, quats, s0, 1.5, 4.0, 1e-3, it)
+        assert np.array_equal(st, sto) and np.array_equal(s, so)
+        assert np.array_equal(np.isnan(E), np.isnan(Eo))
+        ok = ~np.isnan(Eo)
+        assert np.all(np.abs(E[ok] - Eo[ok]) <= 1e-12 * np.abs(Eo[ok]) + 1e-300)
+        seen |= set(np.unique(st).tolist())
+    assert {1, 2, 3, 4} <= seen
