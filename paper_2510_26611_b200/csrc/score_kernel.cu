@@ -96,6 +96,20 @@ __device__ __forceinline__ double2 ldg_if(const double2* p, bool pr) {
       : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((int)pr));
   return v;
 }
+// one 256-bit read-only load (LDG.E.ENL2.256 on sm_100): a whole 32-byte sector per lane
+__device__ __forceinline__ double4 ldg256(const double4* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ldg256x2(const float4* p, float4& hi) {
+  float4 v;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+  return v;
+}
+
 // one 256-bit load (LDG.E.ENL2.256 on sm_100): one L1 tag lookup for a 32-byte record
 __device__ __forceinline__ double4 ldg_if(const double4* p, bool pr) {
   double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -212,13 +226,26 @@ __device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, un
 // O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
 template <int R>
 __device__ __forceinline__ double long_phi_l2(const double2* r0, const double2* r1, const double2* r2) {
+  // 32-byte loads (two rank pairs, LDG.E.ENL2.256): a whole L2 sector per lane and request,
+  // twice the useful bytes per sector of 16-byte loads when every lane reads its own row
   using G = Geo<R>;
   constexpr int C = G::REP ? G::CH : G::CHP;
+  static_assert(G::CH % 2 == 0 || G::CH == 1, "rows are whole 32-byte sectors");
   double s[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    if (c < G::CH) s[c] = pair_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
-    else s[c] = 0.0;
+  for (int c = 0; c < C; ++c) s[c] = 0.0;
+  if constexpr (G::CH == 1) {
+    s[0] = pair_prod(__ldg(r0), __ldg(r1), __ldg(r2));
+  } else {
+    const double4* q0 = reinterpret_cast<const double4*>(r0);
+    const double4* q1 = reinterpret_cast<const double4*>(r1);
+    const double4* q2 = reinterpret_cast<const double4*>(r2);
+#pragma unroll
+    for (int c = 0; c < G::CH / 2; ++c) {
+      const double4 a = ldg256(q0 + c), b = ldg256(q1 + c), cc = ldg256(q2 + c);
+      s[2 * c] = pair_prod(make_double2(a.x, a.y), make_double2(b.x, b.y), make_double2(cc.x, cc.y));
+      s[2 * c + 1] = pair_prod(make_double2(a.z, a.w), make_double2(b.z, b.w), make_double2(cc.z, cc.w));
+    }
   }
   return halving_tree<C>(s);
 }
@@ -300,8 +327,18 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
   const float4* r1 = F1 + (size_t)i1 * G::CHP;
   const float4* r2 = F2 + (size_t)i2 * G::CHP;
   float s[G::NS];
+  if constexpr (G::NS == 1) {
+    s[0] = quad_prod(__ldg(r0), __ldg(r1), __ldg(r2));
+  } else {
+    // 32-byte loads: two quads per lane and request
 #pragma unroll
-  for (int c = 0; c < G::NS; ++c) s[c] = quad_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
+    for (int c = 0; c < G::NS; c += 2) {
+      float4 a1, b1, c1;
+      const float4 a0 = ldg256x2(r0 + c, a1), b0 = ldg256x2(r1 + c, b1), c0 = ldg256x2(r2 + c, c1);
+      s[c] = quad_prod(a0, b0, c0);
+      s[c + 1] = quad_prod(a1, b1, c1);
+    }
+  }
 #pragma unroll
   for (int m = G::NS / 2; m >= 1; m /= 2) {
 #pragma unroll
