@@ -270,7 +270,10 @@ def main():
         dist = dist_mod
 
     import __graft_entry__
-    __graft_entry__.build_library()
+    if rank == 0:
+        __graft_entry__.build_library()        # one rank (re)builds if stale; the others wait
+    if dist:
+        dist.barrier()
     from paper_2510_26611_b200 import rsdock
 
     w = load_workload(args.config)
