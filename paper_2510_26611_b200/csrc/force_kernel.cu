@@ -228,10 +228,14 @@ template <int R>
 __global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(const ScoreArgs a,
                                                                              double* out) {
   const int lane = threadIdx.x & 31;
-  const int64_t warp0 = ((int64_t)blockIdx.x * kForceThreads + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kForceThreads) >> 5;
+  // each block owns a contiguous pose range (its warps interleave inside it), so consecutive
+  // poses of one block share translations and their factor rows stay in the SM's L1
+  const int64_t p_lo = a.P * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t p_hi = a.P * (int64_t)(blockIdx.x + 1) / gridDim.x;
+  const int64_t warp0 = p_lo + (threadIdx.x >> 5);
+  constexpr int64_t nwarps = kForceThreads / 32;
   const int nm1 = a.n - 1;
-  for (int64_t p = warp0; p < a.P; p += nwarps) {
+  for (int64_t p = warp0; p < p_hi; p += nwarps) {
     const double* pq = a.poses + 7 * p;
     double q[7];
 #pragma unroll
