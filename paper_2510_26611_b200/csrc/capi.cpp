@@ -57,6 +57,9 @@ void free_device(rs_handle* h) {
   }
   if (h->d_work) cudaFree(h->d_work);
   h->d_work = nullptr;
+  if (h->scan_buf) cudaFree(h->scan_buf);
+  h->scan_buf = nullptr;
+  h->scan_bytes = 0;
   for (void** p : {&h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
                    &h->d_Fw32[0], &h->d_Fw32[1], &h->d_Fw32[2],
                    &h->d_nb_range}) {
@@ -669,25 +672,32 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
   const int64_t P = (int64_t)m_P * m_L;
   const bool lig_dev = n_lig == 0 || (pointer_kind(q_lig) == 1 && pointer_kind(xyz_lig) == 1);
-  // device scratch: [ligand 4L][centre 3][dirs 3 m_P][quats 4 m_L][poses 7P][E P][D P][s P]
-  //                 [status P int][active int][invalid u64]
+  // device scratch, kept on the handle (grow-only):
+  //   [ligand 4L][centre 3][dirs 3 m_P][quats 4 m_L][poses 2 x 7P][Ec P][Dc P][E P][s P]
+  //   [status P int][slot P int][count 2 int][invalid u64]
   const size_t nd = 4 * (size_t)std::max<int64_t>(n_lig, 1) + 3 + 3 * (size_t)m_P + 4 * (size_t)m_L +
-                    10 * (size_t)P;
-  const size_t bytes = nd * sizeof(double) + ((size_t)P + 4) * sizeof(int) + 16;
-  void* buf = nullptr;
-  CUDA_TRY(cudaMalloc(&buf, bytes), RS_E_NOMEM);
-  struct Free { void* p; ~Free() { cudaFree(p); } } guard{buf};
-  double* d_lig = (double*)buf;
+                    18 * (size_t)P;
+  const size_t bytes = nd * sizeof(double) + (2 * (size_t)P + 4) * sizeof(int) + 16;
+  if (h->scan_bytes < bytes) {
+    if (h->scan_buf) cudaFree(h->scan_buf);
+    h->scan_buf = nullptr;
+    h->scan_bytes = 0;
+    CUDA_TRY(cudaMalloc(&h->scan_buf, bytes), RS_E_NOMEM);
+    h->scan_bytes = bytes;
+  }
+  double* d_lig = (double*)h->scan_buf;
   double* d_c = d_lig + 4 * std::max<int64_t>(n_lig, 1);
   double* d_dirs = d_c + 3;
   double* d_q = d_dirs + 3 * (size_t)m_P;
-  double* d_pose = d_q + 4 * (size_t)m_L;
-  double* d_E = d_pose + 7 * P;
-  double* d_D = d_E + P;
-  double* d_s = d_D + P;
+  double* d_pose[2] = {d_q + 4 * (size_t)m_L, d_q + 4 * (size_t)m_L + 7 * P};
+  double* d_Ec = d_pose[1] + 7 * P;
+  double* d_Dc = d_Ec + P;
+  double* d_E = d_Dc + P;
+  double* d_s = d_E + P;
   int* d_st = (int*)(d_s + P);
-  int* d_active = d_st + P;
-  unsigned long long* d_inv = (unsigned long long*)(((uintptr_t)(d_active + 1) + 7) & ~(uintptr_t)7);
+  int* d_slot = d_st + P;
+  int* d_count = d_slot + P;
+  unsigned long long* d_inv = (unsigned long long*)(((uintptr_t)(d_count + 2) + 7) & ~(uintptr_t)7);
   const double *zl = q_lig, *yl = xyz_lig;
   if (!lig_dev) {
     CUDA_TRY(cudaMemcpy(d_lig, q_lig, n_lig * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
@@ -699,7 +709,7 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   CUDA_TRY(cudaMemcpy(d_dirs, dirs, 3 * (size_t)m_P * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
   CUDA_TRY(cudaMemcpy(d_q, quats, 4 * (size_t)m_L * sizeof(double), cudaMemcpyHostToDevice), RS_E_CUDA);
   cudaStream_t st = nullptr;
-  if (int e = rs::launch_scan_init(d_c, d_dirs, d_q, m_P, m_L, s_start, d_pose, d_s, d_st, st)) {
+  if (int e = rs::launch_scan_init(d_c, d_dirs, d_q, m_P, m_L, s_start, d_pose[0], d_s, d_st, d_slot, st)) {
     set_err(std::string("scan init failed: ") + cudaGetErrorString((cudaError_t)e));
     return RS_E_CUDA;
   }
@@ -708,31 +718,42 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   a.yl = yl;
   a.L = n_lig;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
-  a.poses = d_pose;
-  a.P = P;
-  a.E = d_E;
-  a.D = d_D;
+  a.E = d_Ec;
+  a.D = d_Dc;
   a.invalid = d_inv;
   const double sigma = h->prm.sigma_vdw, dcap = h->prm.dmin_cap;
-  auto score = [&]() -> int {
+  auto score = [&](const double* poses_cur, int64_t n) -> int {
+    a.poses = poses_cur;
+    a.P = n;
     a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
     if (cudaMemsetAsync(a.work, 0, sizeof(int), st) != cudaSuccess) return 1;
     return rs::launch_score(a, st, h->device, nullptr);
   };
-  int active = 1, it = 0;
-  for (; it < max_iter && active > 0; ++it) {
-    if (score() != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
-    CUDA_TRY(cudaMemsetAsync(d_active, 0, sizeof(int), st), RS_E_CUDA);
-    if (int e = rs::launch_scan_update(d_c, d_dirs, d_q, m_P, m_L, d_D, sigma, dcap, tol, it == 0,
-                                       d_pose, d_s, d_st, d_active, st)) {
+  int cur = 0;
+  int64_t n_cur = P;
+  for (int it = 0; it < max_iter && n_cur > 0; ++it) {
+    // score the poses still moving (compacted), then step them and compact the next list
+    if (score(d_pose[cur], n_cur) != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+    CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int), st), RS_E_CUDA);
+    if (int e = rs::launch_scan_update(d_c, d_dirs, d_q, m_P, m_L, d_Dc, d_Ec, sigma, dcap, tol,
+                                       it == 0, d_E, d_s, d_st, d_slot, d_pose[1 - cur], d_count, st)) {
       set_err(std::string("scan update failed: ") + cudaGetErrorString((cudaError_t)e));
       return RS_E_CUDA;
     }
-    CUDA_TRY(cudaMemcpy(&active, d_active, sizeof(int), cudaMemcpyDeviceToHost), RS_E_CUDA);
+    int n_next = 0;
+    CUDA_TRY(cudaMemcpy(&n_next, d_count, sizeof(int), cudaMemcpyDeviceToHost), RS_E_CUDA);
+    n_cur = n_next;
+    cur = 1 - cur;
   }
   // poses still moving after max_iter were stepped after their last scoring: score them where
   // they stand (feasible by construction) and report status 4
-  if (active > 0 && score() != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+  if (n_cur > 0) {
+    if (score(d_pose[cur], n_cur) != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+    if (int e = rs::launch_scan_gather(P, d_st, d_slot, d_Ec, d_E, st)) {
+      set_err(std::string("scan gather failed: ") + cudaGetErrorString((cudaError_t)e));
+      return RS_E_CUDA;
+    }
+  }
   CUDA_TRY(cudaDeviceSynchronize(), RS_E_CUDA);
   std::vector<int> stv(P);
   CUDA_TRY(cudaMemcpy(energies_out, d_E, P * sizeof(double), cudaMemcpyDeviceToHost), RS_E_CUDA);

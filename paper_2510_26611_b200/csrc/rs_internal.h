@@ -106,10 +106,14 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
 const char* score_kernel_variant(int R);
 // NEXT row N2: PPIEM scan kernels (scan_kernel.cu)
 int launch_scan_init(const double* centre, const double* dirs, const double* quats, int m_P,
-                     int m_L, double s_start, double* poses, double* s, int* status, void* st);
+                     int m_L, double s_start, double* poses, double* s, int* status, int* slot,
+                     void* st);
 int launch_scan_update(const double* centre, const double* dirs, const double* quats, int m_P,
-                       int m_L, const double* D, double sigma, double dcap, double tol, int first,
-                       double* poses, double* s, int* status, int* active, void* st);
+                       int m_L, const double* Dc, const double* Ec, double sigma, double dcap,
+                       double tol, int first, double* E, double* s, int* status, int* slot,
+                       double* poses_next, int* count, void* st);
+int launch_scan_gather(int64_t P, const int* status, const int* slot, const double* Ec, double* E,
+                       void* st);
 // NEXT row N1: forces on the rigid ligand (force_kernel.cu), P x 9 outputs, device pointers.
 int launch_forces(const ScoreArgs& a, double* out, void* stream, int device);
 // Chunks (16 B) per row of the window copy of the factors for compiled width R (0: none), and
@@ -149,6 +153,8 @@ struct rs_handle {
   bool f32 = false;
   void* d_nb_range = nullptr;
   int* d_work = nullptr;               // kWorkSlots zeroed-per-launch work counters
+  void* scan_buf = nullptr;            // rs_ppiem_scan scratch (grow-only)
+  size_t scan_bytes = 0;
   std::atomic<unsigned> work_slot{0};
   int64_t device_bytes = 0;
   // staging for host-pointer calls

@@ -1,7 +1,9 @@
 // PPIEM scan (NEXT row N2): Algorithm PPIEM steps A3-A5, DESIGN.md
 // reading A23.  The scoring itself is the fused kernel (score_kernel.cu); this file holds the
-// two small per-pose kernels of the approach loop: the initial poses and the sphere-tracing
-// update of the distance s along each position's line toward the protein centre.
+// small per-pose kernels of the approach loop: the initial poses and the sphere-tracing update
+// of the distance s along each position's line toward the protein centre.  Only the poses still
+// moving are scored again: the update compacts them into the next launch's pose list (slot[p] is
+// a pose's place in that list; the order of the list is free, every pose is scored alone).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,30 +24,34 @@ __device__ __forceinline__ void write_pose(double* pose, const double* centre, c
 
 __global__ void scan_init_kernel(const double* centre, const double* dirs, const double* quats,
                                  int m_P, int m_L, double s_start, double* poses, double* s,
-                                 int* status) {
+                                 int* status, int* slot) {
   const int64_t P = (int64_t)m_P * m_L;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(p / m_L), k = (int)(p % m_L);
     s[p] = s_start;
     status[p] = -1;                                   // active
+    slot[p] = (int)p;
     write_pose(poses + 7 * p, centre, dirs + 3 * j, quats + 4 * k, s_start);
   }
 }
 
-// One sphere-tracing step from the scored minimum distances D (+inf at or beyond D_cap, NaN for
-// an invalid pose).  Status: -1 active, 0 contact, 1 left the box, 2 clash at the start,
-// 3 passed the centre.
+// One sphere-tracing step from the scored minimum distances Dc (+inf at or beyond D_cap, NaN
+// for an invalid pose) and energies Ec of the current list (pose p at slot[p]).  Status: -1
+// active, 0 contact, 1 left the box, 2 clash at the start, 3 passed the centre.  Poses that
+// move are appended to the next list (poses_next, slot[p], *count).
 __global__ void scan_update_kernel(const double* centre, const double* dirs, const double* quats,
-                                   int m_P, int m_L, const double* D, double sigma, double dcap,
-                                   double tol, int first, double* poses, double* s, int* status,
-                                   int* active) {
+                                   int m_P, int m_L, const double* Dc, const double* Ec,
+                                   double sigma, double dcap, double tol, int first, double* E,
+                                   double* s, int* status, int* slot, double* poses_next,
+                                   int* count) {
   const int64_t P = (int64_t)m_P * m_L;
-  int mine = 0;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     if (status[p] != -1) continue;
-    const double d = D[p];
+    const int sl = slot[p];
+    const double d = Dc[sl];
+    E[p] = Ec[sl];
     double sn;
     if (isnan(d)) {
       status[p] = 1;
@@ -71,33 +77,45 @@ __global__ void scan_update_kernel(const double* centre, const double* dirs, con
     }
     s[p] = sn;
     const int j = (int)(p / m_L), k = (int)(p % m_L);
-    write_pose(poses + 7 * p, centre, dirs + 3 * j, quats + 4 * k, sn);
-    ++mine;
+    const int ns = atomicAdd(count, 1);
+    slot[p] = ns;
+    write_pose(poses_next + 7 * (int64_t)ns, centre, dirs + 3 * j, quats + 4 * k, sn);
   }
-  // warp-aggregated count of poses still moving
-  for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(active, mine);
 }
+
+// energies of the poses still moving after the last iteration, scored where they stand
+__global__ void scan_gather_kernel(int64_t P, const int* status, const int* slot, const double* Ec,
+                                   double* E) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (status[p] == -1) E[p] = Ec[slot[p]];
+}
+
+int blocks_for(int64_t P) { return (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 4096)); }
 
 }  // namespace
 
 int launch_scan_init(const double* centre, const double* dirs, const double* quats, int m_P,
-                     int m_L, double s_start, double* poses, double* s, int* status, void* st) {
-  const int64_t P = (int64_t)m_P * m_L;
-  const int blocks = (int)std::min<int64_t>((P + 255) / 256, 4096);
-  scan_init_kernel<<<blocks, 256, 0, (cudaStream_t)st>>>(centre, dirs, quats, m_P, m_L, s_start,
-                                                         poses, s, status);
+                     int m_L, double s_start, double* poses, double* s, int* status, int* slot,
+                     void* st) {
+  scan_init_kernel<<<blocks_for((int64_t)m_P * m_L), 256, 0, (cudaStream_t)st>>>(
+      centre, dirs, quats, m_P, m_L, s_start, poses, s, status, slot);
   return (int)cudaGetLastError();
 }
 
 int launch_scan_update(const double* centre, const double* dirs, const double* quats, int m_P,
-                       int m_L, const double* D, double sigma, double dcap, double tol, int first,
-                       double* poses, double* s, int* status, int* active, void* st) {
-  const int64_t P = (int64_t)m_P * m_L;
-  const int blocks = (int)std::min<int64_t>((P + 255) / 256, 4096);
-  scan_update_kernel<<<blocks, 256, 0, (cudaStream_t)st>>>(centre, dirs, quats, m_P, m_L, D, sigma,
-                                                           dcap, tol, first, poses, s, status,
-                                                           active);
+                       int m_L, const double* Dc, const double* Ec, double sigma, double dcap,
+                       double tol, int first, double* E, double* s, int* status, int* slot,
+                       double* poses_next, int* count, void* st) {
+  scan_update_kernel<<<blocks_for((int64_t)m_P * m_L), 256, 0, (cudaStream_t)st>>>(
+      centre, dirs, quats, m_P, m_L, Dc, Ec, sigma, dcap, tol, first, E, s, status, slot,
+      poses_next, count);
+  return (int)cudaGetLastError();
+}
+
+int launch_scan_gather(int64_t P, const int* status, const int* slot, const double* Ec, double* E,
+                       void* st) {
+  scan_gather_kernel<<<blocks_for(P), 256, 0, (cudaStream_t)st>>>(P, status, slot, Ec, E);
   return (int)cudaGetLastError();
 }
 
