@@ -991,9 +991,12 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
       cap_rows = 3 * a.n;
     } else if (a.rmax_hint >= 0) {
       // leave the rest of the 228 KB to L1 (cell lists, records, memo): what one
-      // translation's window needs plus RS_WIN_SLACK
+      // translation's window needs plus RS_WIN_SLACK; no window at all when even one
+      // translation's rows do not fit (every pose would be its own tile with its own restage:
+      // the L2 path is faster then)
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
-      cap_rows = std::min(cap_rows, (int)std::max(64.0, RS_WIN_SLACK * need));
+      if (need > cap_rows) cap_rows = 0;
+      else cap_rows = std::min(cap_rows, (int)std::max(64.0, RS_WIN_SLACK * need));
     }
   }
   const size_t win_b = (size_t)cap_rows * 16 * kChp;

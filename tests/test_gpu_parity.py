@@ -449,3 +449,23 @@ def test_ppiem_scan_statuses(env):
         assert np.all(np.abs(E[ok] - Eo[ok]) <= 1e-12 * np.abs(Eo[ok]) + 1e-300)
         seen |= set(np.unique(st).tolist())
     assert {1, 2, 3, 4} <= seen
+
+
+def test_window_too_small_takes_l2_path(env):
+    """A ligand whose rows for one translation exceed the shared memory left for the window
+    (n = 4096 grid, 5.6 A ligand radius): the launch falls back to the L2 path for the whole
+    batch instead of one-pose tiles; results still match the oracle."""
+    torch, rsdock, rs_oracle = env
+    rng = np.random.default_rng(31)
+    X = syn.packed_ball(rng, 80, 6.0, 1.2)
+    q = rng.uniform(-1, 1, 80)
+    Y = syn.packed_ball(rng, 40, 5.6, 1.2)
+    Y -= Y.mean(0)
+    Y *= 5.6 / np.max(np.linalg.norm(Y, axis=1))
+    P = 150
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), rng.uniform(-12, 12, (P, 3))], 1)
+    w = syn.Workload("bigwin", X, q, Y, rng.uniform(-1, 1, 40), poses, 4096, 64.0, 16)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
