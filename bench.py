@@ -188,7 +188,9 @@ def config_dict(w, args):
             "poses": w.P, "sigma_split": w.sigma_split, "sigma_vdw": w.sigma_vdw,
             "parallelism": f"pose-shard x{args.gpus} (replicated handle)",
             "mode": ("forces (rs_score_forces, N1)" if getattr(args, "forces", False) else "energy + mindist")
-                    + (", fp32 factors (A21)" if getattr(args, "f32", False) else ""),
+                    + (", fp32 factors (A21)" if getattr(args, "f32", False) else "")
+                    + (", Eq. (23) complex: 2 proteins x R/2, rank-concatenated (A24)"
+                       if getattr(args, "complex", False) else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
@@ -247,6 +249,9 @@ def main():
                     help="time a PPIEM scan (NEXT row N2) with M positions x M self-rotations")
     ap.add_argument("--forces", action="store_true",
                     help="time rs_score_forces (NEXT row N1) instead of the energy path")
+    ap.add_argument("--complex", action="store_true",
+                    help="build the config's protein as a two-protein complex (Eq. (23), N4): "
+                         "one RS tensor of width R/2 per protein, rank-concatenated")
     ap.add_argument("--f32", action="store_true",
                     help="the fp32-factor variant (RS_FLAG_F32_FACTORS, DESIGN.md reading A21)")
     ap.add_argument("--nbr-cell", type=float, default=0.0,
@@ -279,10 +284,21 @@ def main():
     w = load_workload(args.config)
     ncpu = os.cpu_count() or 1
     t0 = time.perf_counter()
-    prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
-                          device=local, n_threads=max(1, ncpu // max(world, 1)),
-                          nbr_cell=args.nbr_cell,
-                          flags=rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0)
+    fl = rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0
+    if args.complex:
+        # NEXT row N4 (Eq. (23)): one RS tensor per protein (R/2 each), combined on the device
+        from synth import configs as syn
+        prm = dict(w.params(), rank_R=w.rank_R // 2)
+        parts = [rsdock.Protein(qp, Xp, w.box_half_width, **prm, device=local,
+                                n_threads=max(1, ncpu // max(world, 1)), nbr_cell=args.nbr_cell,
+                                flags=rsdock.RS_FLAG_HOST_ONLY)
+                 for Xp, qp in syn.complex_parts(w)]
+        prot = rsdock.Protein.combine(parts, flags=fl)
+        del parts
+    else:
+        prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                              device=local, n_threads=max(1, ncpu // max(world, 1)),
+                              nbr_cell=args.nbr_cell, flags=fl)
     setup_s = time.perf_counter() - t0
     info = prot.info
 

@@ -134,6 +134,23 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
                             double box_half_width, const rs_params* params);
 
 /*
+ * Multi-protein complex (NEXT row N4; Eq. (23): the ligand's energy in
+ * the field of several proteins is sum_l z_l (sum_p P_{M_p})(x_l); reading A24).
+ *   parts   : n_parts >= 1 handles from rs_build_protein (host-only handles are fine), built
+ *             with the same grid_n, box_half_width, eps_quad, sigma_split, eps_split,
+ *             sigma_vdw and dmin_cap (so their short-range rows are identical)
+ *   flags   : RS_FLAG_* of the new handle (device and the other parameters are part 0's)
+ * The new handle's long-range factors are the parts' factors concatenated along the rank,
+ * F_a = [F_a^(0) | F_a^(1) | ...] (n x sum_p R_p, no recompression; the O4 tree runs over the
+ * concatenated width), its short-range part and vdW distance run over the union of the atoms
+ * (part 0's atoms first), and its cell lists are rebuilt for the union.  The parts are not
+ * modified and stay owned by the caller; the result is released with rs_free.  Returns NULL on
+ * error (mismatched parts, width > 2^20, RS_FLAG_F32_FACTORS with an uncompiled width, no
+ * CUDA device unless RS_FLAG_HOST_ONLY, allocation or upload failure).
+ */
+rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, int32_t flags);
+
+/*
  * Score P poses of a rigid ligand (Algorithm PLIE + Eq. (22)), synchronously.
  *   q_lig (n_lig), xyz_lig (n_lig x 3) : ligand charges and body-frame coordinates
  *   poses (P x 7)                      : see conventions above

@@ -340,6 +340,41 @@ def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=Fa
     return E, d, int(inv)
 
 
+def combine_tables(parts: list) -> dict:
+    """Eq. (23) on one grid, reading A24: sum_p P_{M_p} is a CP tensor
+    whose terms are all the parts' terms, i.e. the factors concatenated along the rank axis
+    (part 0's columns first).  The short-range rows are a property of the shared grid and
+    split, so the parts must agree on them."""
+    t0 = parts[0]
+    for t in parts[1:]:
+        assert int(t["n"]) == int(t0["n"]) and float(t["b"]) == float(t0["b"])
+        assert int(t["n_sigma"]) == int(t0["n_sigma"])
+        for k in ("S1", "S2", "S3"):
+            assert np.array_equal(t[k], t0[k])
+    out = dict(t0)
+    for k in ("F1", "F2", "F3"):
+        out[k] = np.concatenate([np.asarray(t[k]).reshape(int(t0["n"]), -1) for t in parts],
+                                axis=1)
+    out["R"] = out["F1"].shape[1]
+    return out
+
+
+def score_complex(parts: list, proteins: list, Y, zL, poses, dcap):
+    """Eq. (23) literally: E = sum_l z_l sum_p P_{M_p}(x_l) = sum_p E_p, each part scored on
+    its own tables and atoms; the vdW distance of the complex is the minimum over the parts.
+    proteins: list of (X_p, q_p).  Returns (E, dmin, n_invalid)."""
+    E = None
+    d = None
+    inv = 0
+    for tb, (X, q) in zip(parts, proteins):
+        Ep, dp, inv = score_poses(tb, X, q, Y, zL, poses, dcap)
+        E = Ep if E is None else E + Ep
+        d = dp if d is None else np.fmin(d, dp)
+    if E is not None:
+        d = np.where(np.isnan(E), np.nan, d)
+    return E, d, inv
+
+
 def score_forces(tables: dict, Y, zL, poses):
     """Per-pose (P x 9: net force, torque about t, Eq. (24) radial resultant; n_invalid)."""
     n, b = int(tables["n"]), float(tables["b"])

@@ -394,6 +394,117 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
   return H.release();
 }
 
+// NEXT row N4 (multi-protein, Eq. (23); reading A24): the
+// potential of a complex is the sum of its proteins' potentials, so on a shared grid the
+// long-range CP factors concatenate along the rank (R = sum R_p, no recompression), and the
+// short-range part and the vdW distance run over the union of the atoms.
+rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, int32_t flags) {
+  g_err.clear();
+  auto t0 = std::chrono::steady_clock::now();
+  if (!parts || n_parts < 1) { set_err("need n_parts >= 1 handles"); return nullptr; }
+  for (int32_t p = 0; p < n_parts; ++p)
+    if (!parts[p]) { set_err("null part handle " + std::to_string(p)); return nullptr; }
+  const rs_handle* p0 = parts[0];
+  for (int32_t p = 1; p < n_parts; ++p) {
+    const rs_handle* q = parts[p];
+    // Same grid, quadrature and split => identical short-range rows and n_sigma; same vdW rule.
+    if (q->n != p0->n || q->b != p0->b || q->prm.eps_quad != p0->prm.eps_quad ||
+        q->prm.sigma_split != p0->prm.sigma_split || q->prm.eps_split != p0->prm.eps_split ||
+        q->prm.sigma_vdw != p0->prm.sigma_vdw || q->prm.dmin_cap != p0->prm.dmin_cap) {
+      set_err("part " + std::to_string(p) + " differs from part 0 in grid_n, b, eps_quad, "
+              "sigma_split, eps_split, sigma_vdw or dmin_cap");
+      return nullptr;
+    }
+    for (int a = 0; a < 3; ++a)
+      if (q->S[a] != p0->S[a]) { set_err("short-range rows differ between parts"); return nullptr; }
+  }
+  int64_t R = 0, M = 0;
+  for (int32_t p = 0; p < n_parts; ++p) { R += parts[p]->R; M += parts[p]->M; }
+  if (R > (1 << 20)) { set_err("combined CP width exceeds 2^20"); return nullptr; }
+  rs_params prm = p0->prm;
+  prm.flags = flags;
+  const bool host_only = (flags & RS_FLAG_HOST_ONLY) != 0;
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= prm.device || prm.device < 0) {
+      cudaGetLastError();
+      set_err("no CUDA device (there is no CPU fallback; use RS_FLAG_HOST_ONLY for host-only tables)");
+      return nullptr;
+    }
+  }
+  if ((flags & RS_FLAG_F32_FACTORS) && rs::window_row_chunks32((int)R) == 0) {
+    set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
+            std::to_string(R));
+    return nullptr;
+  }
+  std::unique_ptr<rs_handle> H;
+  try {
+    H.reset(new rs_handle());
+    rs_handle* hd = H.get();
+    hd->prm = prm;
+    hd->n = p0->n;
+    hd->b = p0->b;
+    hd->h = p0->h;
+    hd->inv_h = p0->inv_h;
+    hd->quad = p0->quad;
+    hd->is_long = p0->is_long;
+    hd->R = (int)R;
+    hd->Rs = p0->Rs;
+    hd->n_sigma = p0->n_sigma;
+    hd->R_long_ref = p0->R_long_ref;
+    hd->device = prm.device;
+    hd->f32 = (flags & RS_FLAG_F32_FACTORS) != 0;
+    for (int a = 0; a < 3; ++a) hd->S[a] = p0->S[a];
+    // factor rows i: [F_a^(0)[i, :] | F_a^(1)[i, :] | ...]  (rank concatenation)
+    const size_t n = (size_t)hd->n;
+    for (int a = 0; a < 3; ++a) {
+      hd->F[a].assign(n * (size_t)R, 0.0);
+      size_t col = 0;
+      for (int32_t p = 0; p < n_parts; ++p) {
+        const int Rp = parts[p]->R;
+        for (size_t i = 0; i < n; ++i)
+          std::copy(parts[p]->F[a].begin() + i * Rp, parts[p]->F[a].begin() + (i + 1) * Rp,
+                    hd->F[a].begin() + i * R + col);
+        col += (size_t)Rp;
+      }
+    }
+    hd->M = M;
+    for (int32_t p = 0; p < n_parts; ++p) {
+      hd->xyz.insert(hd->xyz.end(), parts[p]->xyz.begin(), parts[p]->xyz.end());
+      hd->z.insert(hd->z.end(), parts[p]->z.begin(), parts[p]->z.end());
+      hd->cells.insert(hd->cells.end(), parts[p]->cells.begin(), parts[p]->cells.end());
+    }
+    // report: ranks add; the sampled errors are the parts' worst (each part's own samples)
+    hd->rep.R_exact = 0;
+    for (int32_t p = 0; p < n_parts; ++p) {
+      const rs::SetupReport& r = parts[p]->rep;
+      hd->rep.R_exact += r.R_exact;
+      for (int a = 0; a < 3; ++a) hd->rep.tucker_r[a] += r.tucker_r[a];
+      hd->rep.tucker_err = std::max(hd->rep.tucker_err, r.tucker_err);
+      hd->rep.cp_core_err = std::max(hd->rep.cp_core_err, r.cp_core_err);
+      hd->rep.sampled_max = std::max(hd->rep.sampled_max, r.sampled_max);
+      hd->rep.sampled_rms = std::max(hd->rep.sampled_rms, r.sampled_rms);
+      hd->rep.n_samples += r.n_samples;
+    }
+    const double rho = std::max(prm.dmin_cap, (hd->n_sigma + std::sqrt(3.0)) * hd->h);
+    rs::build_cell_lists(hd->n, hd->b, hd->h, hd->xyz, hd->cells, rho, prm.nbr_cell, &hd->cg);
+  } catch (const std::bad_alloc&) {
+    set_err("out of host memory while combining");
+    return nullptr;
+  }
+  rs_handle* hd = H.get();
+  if (!host_only) {
+    if (upload_handle(hd) != 0) {
+      std::string msg = g_err;
+      free_device(hd);
+      set_err(msg.empty() ? "upload failed" : msg);
+      return nullptr;
+    }
+  }
+  hd->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return H.release();
+}
+
 int rs_get_info(const rs_handle* h, rs_info* out) {
   if (!h || !out) { set_err("null argument"); return RS_E_INVALID_ARG; }
   std::memset(out, 0, sizeof(*out));

@@ -22,7 +22,7 @@ RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
 RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 
-EXPORTED = ["rs_params_default", "rs_build_protein", "rs_score_poses", "rs_score_poses_async",
+EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_score_poses", "rs_score_poses_async",
             "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",
             "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
@@ -73,6 +73,8 @@ def load():
     L.rs_build_protein.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_double,
                                    ctypes.POINTER(rs_params)]
     L.rs_build_protein.restype = _vp
+    L.rs_combine_proteins.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32]
+    L.rs_combine_proteins.restype = _vp
     L.rs_score_poses.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp]
     L.rs_score_poses.restype = ctypes.c_int64
     L.rs_score_poses_async.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
@@ -128,6 +130,15 @@ def rs_build_protein(q, xyz, box_half_width, params: rs_params | None = None):
                                 ctypes.byref(params) if params is not None else None)
     if not h:
         raise RuntimeError("rs_build_protein: " + rs_last_error())
+    return h
+
+
+def rs_combine_proteins(parts, flags=0):
+    """parts: sequence of rs_handle pointers (Eq. (23) complex; see include/rs_dock.h)."""
+    arr = (ctypes.c_void_p * len(parts))(*parts)
+    h = load().rs_combine_proteins(ctypes.cast(arr, ctypes.c_void_p), len(parts), int(flags))
+    if not h:
+        raise RuntimeError("rs_combine_proteins: " + rs_last_error())
     return h
 
 
@@ -240,6 +251,17 @@ class Protein:
         self.params = rs_params_default(**params)
         self._h = rs_build_protein(q, xyz, box_half_width, self.params)
         self.info = rs_get_info(self._h)
+
+    @classmethod
+    def combine(cls, parts, flags=0):
+        """The complex of several proteins on one grid (Eq. (23)): rank-concatenated factors,
+        union of the atoms.  The parts stay valid and owned by their objects."""
+        self = cls.__new__(cls)
+        self._h = None
+        self.params = parts[0].params
+        self._h = rs_combine_proteins([p.handle for p in parts], flags)
+        self.info = rs_get_info(self._h)
+        return self
 
     @property
     def handle(self):

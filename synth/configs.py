@@ -354,3 +354,32 @@ def planar_scan(m_P: int, m_L: int):
     psi = 2.0 * math.pi * np.arange(m_L) / m_L
     quats = np.stack([np.cos(psi / 2), np.zeros(m_L), np.zeros(m_L), np.sin(psi / 2)], axis=1)
     return dirs, quats
+
+
+def complex_parts(w: Workload, axis: int = 0) -> list:
+    """The proteins of a two-protein complex whose members lie on either side of the plane
+    x_axis = 0 (C4's two ellipsoids; complex_small): [(X_A, q_A), (X_B, q_B)], A at x < 0."""
+    left = w.protein_xyz[:, axis] < 0.0
+    return [(np.ascontiguousarray(w.protein_xyz[m]), np.ascontiguousarray(w.protein_q[m]))
+            for m in (left, ~left)]
+
+
+def complex_small(seed=0, M=(30, 24), L=7, n=64, b=8.0, R=4, P=160, radius=2.5,
+                  trans=4.0) -> Workload:
+    """Small two-protein complex for Eq. (23) parity: balls of M[0] and M[1] atoms (radius
+    2.5 A) centred at (-3.2, 0, 0) and (+3.2, 0, 0) (in general +-(radius + 0.7)); ligand and
+    poses as random_small, the translations uniform in [-trans, trans]^3 (many poses clash with
+    one protein or sit between)."""
+    g = _streams(seed + 100)
+    c = radius + 0.7
+    XA = packed_ball(g[0], M[0], radius, 0.8) + np.array([-c, 0.0, 0.0])
+    XB = packed_ball(g[1], M[1], radius, 0.8) + np.array([c, 0.0, 0.0])
+    q = g[2].uniform(-1, 1, M[0] + M[1])
+    Y = packed_ball(g[3], L, 1.5, 0.8)
+    Y = Y - Y.mean(axis=0)
+    z = g[4].uniform(-1, 1, L)
+    quats = shoemake_quaternions(g[5], P)
+    t = g[5].uniform(-trans, trans, size=(P, 3))
+    return Workload(f"complex{seed}", np.concatenate([XA, XB]), q, Y, z,
+                    np.concatenate([quats, t], axis=1), grid_n=n, box_half_width=b, rank_R=R,
+                    sigma_split=1.0, sigma_vdw=1.0, dmin_cap=1.5)

@@ -469,3 +469,69 @@ def test_window_too_small_takes_l2_path(env):
     Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
     Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
     compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+# ----------------------------------------------------------------------------- N4: Eq. (23) complex
+
+def _complex(rsdock, w, R=(4, 8), flags=0):
+    parts = syn.complex_parts(w)
+    prm = dict(w.params())
+    prots = [rsdock.Protein(q, X, w.box_half_width, **dict(prm, rank_R=r,
+                                                           flags=rsdock.RS_FLAG_HOST_ONLY))
+             for (X, q), r in zip(parts, R)]
+    return parts, prots, rsdock.Protein.combine(prots, flags=flags)
+
+
+@pytest.mark.parametrize("seed,R", [(0, (4, 8)), (1, (8, 8)), (2, (12, 12)), (3, (5, 6))])
+def test_complex_parity(env, seed, R):
+    """rs_combine_proteins (reading A24): the kernel on the combined handle matches the oracle on
+    the concatenated tables (1e-12, D bitwise) for compiled and runtime widths, and the literal
+    Eq. (23) sum over the proteins, sum_p E_p (oracle.score_complex), within the dd bound."""
+    torch, rsdock, rs_oracle = env
+    w = syn.complex_small(seed=seed, P=333)
+    parts, prots, C = _complex(rsdock, w, R)
+    Eg, Dg, inv = gpu_score(torch, rsdock, C, w, w.poses)
+    tabs = [p.export_tables() for p in prots]
+    comb = rs_oracle.combine_tables(tabs)
+    Xu = np.concatenate([X for X, _ in parts])
+    qu = np.concatenate([q for _, q in parts])
+    Eo, Do, invo = rs_oracle.score_poses(comb, Xu, qu, w.ligand_xyz, w.ligand_q, w.poses,
+                                         w.dmin_cap)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    Es, Ds, _ = rs_oracle.score_complex(tabs, parts, w.ligand_xyz, w.ligand_q, w.poses, w.dmin_cap)
+    ok = ~np.isnan(Eo)
+    assert np.array_equal(Dg[ok], Ds[ok])
+    scale = sum(np.abs(rs_oracle.score_poses(t, X, q, w.ligand_xyz, w.ligand_q, w.poses,
+                                             w.dmin_cap)[0]) for t, (X, q) in zip(tabs, parts))
+    assert np.all(np.abs(Eg[ok] - Es[ok]) <= 1e-13 * np.maximum(scale[ok], 1e-300))
+
+
+def test_complex_f32_parity(env):
+    torch, rsdock, rs_oracle = env
+    w = syn.complex_small(seed=5, P=257)
+    parts, prots, C = _complex(rsdock, w, (8, 8), flags=rsdock.RS_FLAG_F32_FACTORS)
+    assert C.info["factor_bits"] == 32
+    Eg, Dg, inv = gpu_score(torch, rsdock, C, w, w.poses)
+    comb = rs_oracle.combine_tables([p.export_tables() for p in prots])
+    Xu = np.concatenate([X for X, _ in parts])
+    qu = np.concatenate([q for _, q in parts])
+    Eo, Do, invo = rs_oracle.score_poses(comb, Xu, qu, w.ligand_xyz, w.ligand_q, w.poses,
+                                         w.dmin_cap, f32=True)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_complex_mid_size_sample(env):
+    """A 700 + 500-atom complex at n = 256 (several windows of tiles, 20,000 poses in one launch),
+    a seeded sample of poses scored by the oracle one by one."""
+    torch, rsdock, rs_oracle = env
+    w = syn.complex_small(seed=7, M=(700, 500), L=24, n=256, b=24.0, R=8, P=20000, radius=7.0,
+                          trans=14.0)
+    parts, prots, C = _complex(rsdock, w, (8, 8))
+    Eg, Dg, inv = gpu_score(torch, rsdock, C, w, w.poses)
+    idx, _ = syn.subsample(w.poses, 600)
+    comb = rs_oracle.combine_tables([p.export_tables() for p in prots])
+    Xu = np.concatenate([X for X, _ in parts])
+    qu = np.concatenate([q for _, q in parts])
+    Eo, Do, _ = rs_oracle.score_poses(comb, Xu, qu, w.ligand_xyz, w.ligand_q, w.poses[idx],
+                                      w.dmin_cap)
+    compare(Eg[idx], Dg[idx], Eo, Do)

@@ -191,3 +191,36 @@ def test_setup_deterministic(rsd):
     b = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, n_threads=4, **kw).export_tables()
     for k in ("F1", "F2", "F3", "S1"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_combine_proteins_host(rsd):
+    """NEXT row N4 (Eq. (23)): rs_combine_proteins concatenates the parts' factors along the
+    rank (bitwise, part 0 first), keeps the shared short-range rows, unions the atoms, and
+    rejects parts built on different grids or splits."""
+    w = syn.complex_small(seed=1)
+    (XA, qA), (XB, qB) = syn.complex_parts(w)
+    kw = dict(grid_n=w.grid_n, rank_R=4, sigma_split=1.0, sigma_vdw=1.0, dmin_cap=1.5,
+              flags=rsd.RS_FLAG_HOST_ONLY)
+    A = rsd.Protein(qA, XA, w.box_half_width, **kw)
+    B = rsd.Protein(qB, XB, w.box_half_width, **dict(kw, rank_R=8))
+    C = rsd.Protein.combine([A, B], flags=rsd.RS_FLAG_HOST_ONLY)
+    ta, tb, tc = A.export_tables(), B.export_tables(), C.export_tables()
+    assert C.info["R"] == 12 and C.info["n_atoms"] == len(qA) + len(qB)
+    for k in ("F1", "F2", "F3"):
+        assert np.array_equal(tc[k], np.concatenate([ta[k], tb[k]], axis=1))
+    for k in ("S1", "S2", "S3"):
+        assert np.array_equal(tc[k], ta[k])
+    cells = C.export_setup()["cells"]
+    assert np.array_equal(cells, np.concatenate([A.export_setup()["cells"],
+                                                 B.export_setup()["cells"]]))
+    one = rsd.Protein.combine([A], flags=rsd.RS_FLAG_HOST_ONLY)
+    for k in ("F1", "F2", "F3", "S1"):
+        assert np.array_equal(one.export_tables()[k], ta[k])
+    for bad in (dict(kw, grid_n=32), dict(kw, sigma_split=1.5), dict(kw, sigma_vdw=1.2)):
+        D = rsd.Protein(qB, XB, w.box_half_width, **bad)
+        with pytest.raises(RuntimeError, match="differs from part 0"):
+            rsd.Protein.combine([A, D], flags=rsd.RS_FLAG_HOST_ONLY)
+    with pytest.raises(RuntimeError, match="n_parts"):
+        rsd.rs_combine_proteins([], rsd.RS_FLAG_HOST_ONLY)
+    with pytest.raises(RuntimeError, match="F32"):
+        rsd.Protein.combine([B, B, A], flags=rsd.RS_FLAG_HOST_ONLY | rsd.RS_FLAG_F32_FACTORS)  # R = 20

@@ -713,3 +713,81 @@ def test_ppiem_oracle_two_charges_contact(oracle):
     # <= sqrt(3) h: relative error of 1/r <= sqrt(3) h / (sigma - sqrt(3) h)
     bound = math.sqrt(3) * h / (sigma - math.sqrt(3) * h)
     assert np.all(np.abs(E - 0.8 * -0.6 / s) <= (bound + 1e-6) * np.abs(0.8 * 0.6 / s))
+
+
+# ---------------------------------------------------------------------------------- N4 Eq. (23)
+def _two_proteins(oracle, seed):
+    b, n, h, t, a, lm, ns, X, qM, Y, zL, iM, tables, rng = _chain_case(oracle, seed=seed)
+    XB = syn.packed_ball(rng, 20, 3.5, 1.2) + np.array([0.0, 0.0, 6.5])
+    qB = rng.uniform(-1, 1, 20)
+    iB = oracle.snap_np(XB, b, n)
+    FB = oracle.uncompressed_long_factors(iB, qB, t, a, lm, n, h)
+    tB = dict(tables, F1=FB[0], F2=FB[1], F3=FB[2], R=FB[0].shape[1])
+    return b, n, h, t, a, lm, ns, (X, qM, iM, tables), (XB, qB, iB, tB), Y, zL, rng
+
+
+def test_complex_concatenation_is_the_union_protein(oracle):
+    """Eq. (23), reading A24: the uncompressed factors of the union of two
+    proteins (Eq. (6) over all atoms, A first) are exactly the rank concatenation of the parts'
+    factors, so combine_tables reproduces the union tables bit for bit; and the concatenated
+    scorer equals the literal sum over proteins, sum_p E_p, within the dd rounding bound."""
+    b, n, h, t, a, lm, ns, A, B, Y, zL, rng = _two_proteins(oracle, seed=3)
+    X = np.concatenate([A[0], B[0]])
+    q = np.concatenate([A[1], B[1]])
+    F = oracle.uncompressed_long_factors(np.concatenate([A[2], B[2]]), q, t, a, lm, n, h)
+    comb = oracle.combine_tables([A[3], B[3]])
+    for k, Fk in zip(("F1", "F2", "F3"), F):
+        assert np.array_equal(comb[k], Fk)
+    P = 24
+    u = syn.unit_vectors(rng, P)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), u * rng.uniform(3.0, 7.0, (P, 1))], 1)
+    E, d, inv = oracle.score_poses(comb, X, q, Y, zL, poses, 2.5)
+    Es, ds, invs = oracle.score_complex([A[3], B[3]], [(A[0], A[1]), (B[0], B[1])], Y, zL, poses,
+                                        2.5)
+    assert inv == invs
+    assert np.array_equal(np.isnan(E), np.isnan(Es))
+    ok = ~np.isnan(E)
+    assert ok.sum() > P // 2
+    assert np.array_equal(d[ok], ds[ok])                 # min over the union = min of the mins
+    EA, _, _ = oracle.score_poses(A[3], A[0], A[1], Y, zL, poses, 2.5)
+    EB, _, _ = oracle.score_poses(B[3], B[0], B[1], Y, zL, poses, 2.5)
+    for p in np.nonzero(ok)[0]:
+        scale = abs(EA[p]) + abs(EB[p])
+        assert abs(E[p] - Es[p]) <= 1e-13 * max(scale, 1e-300)
+
+
+def test_complex_vs_brute_force_coulomb_of_both_proteins(oracle):
+    """Eq. (23) against Eq. (13) summed over both proteins: the complex's RS energy at
+    non-clashing poses matches the point-Coulomb energy of the ligand in the field of A and B
+    at the snapped cell centres (O(h^2/r^2) + eps_q bound, as for one protein), while leaving
+    either protein out misses by far more."""
+    b, n, h, t, a, lm, ns, A, B, Y, zL, rng = _two_proteins(oracle, seed=4)
+    comb = oracle.combine_tables([A[3], B[3]])
+    X = np.concatenate([A[0], B[0]])
+    q = np.concatenate([A[1], B[1]])
+    P = 16
+    u = syn.unit_vectors(rng, P)
+    poses = np.concatenate([syn.shoemake_quaternions(rng, P), u * rng.uniform(8.0, 8.5, (P, 1))], 1)
+    poses[:, 4:] += np.array([0.0, 0.0, 1.5])
+    E, d, inv = oracle.score_poses(comb, X, q, Y, zL, poses, 2.5)
+    centres = lambda i: -b + (i + 0.5) * h
+    iX = oracle.snap_np(X, b, n)
+    n_checked = n_missing_A = n_missing_B = 0
+    for p in range(P):
+        if np.isnan(E[p]):
+            continue
+        R_ = oracle.quat_to_rot(poses[p, :4])
+        Xp = np.stack([oracle.transform(R_, y, poses[p, 4:]) for y in Y])
+        if np.min(np.linalg.norm(Xp[:, None, :] - X[None, :, :], axis=2)) < 2.5:
+            continue
+        S = oracle.coulomb_scale(X, q, Xp, zL)
+        iP = oracle.snap_np(Xp, b, n)
+        e_snap = oracle.coulomb_binding(centres(iX), q, centres(iP), zL)
+        assert abs(E[p] - e_snap) <= 1e-6 * S
+        e_A = oracle.coulomb_binding(centres(A[2]), A[1], centres(iP), zL)
+        e_B = oracle.coulomb_binding(centres(B[2]), B[1], centres(iP), zL)
+        n_missing_B += abs(E[p] - e_A) > 1e-4 * S        # a dropped part would fail the bound
+        n_missing_A += abs(E[p] - e_B) > 1e-4 * S
+        n_checked += 1
+    assert n_checked >= P // 2
+    assert n_missing_A == n_checked and n_missing_B == n_checked
