@@ -190,7 +190,9 @@ def config_dict(w, args):
             "mode": ("forces (rs_score_forces, N1)" if getattr(args, "forces", False) else "energy + mindist")
                     + (", fp32 factors (A21)" if getattr(args, "f32", False) else "")
                     + (", Eq. (23) complex: 2 proteins x R/2, rank-concatenated (A24)"
-                       if getattr(args, "complex", False) else ""),
+                       if getattr(args, "complex", False) else "")
+                    + (f", box-restricted width {args.box} (N3, A25)" if getattr(args, "box", 0)
+                       else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
@@ -249,6 +251,9 @@ def main():
                     help="time a PPIEM scan (NEXT row N2) with M positions x M self-rotations")
     ap.add_argument("--forces", action="store_true",
                     help="time rs_score_forces (NEXT row N1) instead of the energy path")
+    ap.add_argument("--box", type=int, default=0, metavar="R_PI",
+                    help="score on a box-restricted handle of width R_PI covering the poses "
+                         "(N3, scheme (C): rs_restrict_box)")
     ap.add_argument("--complex", action="store_true",
                     help="build the config's protein as a two-protein complex (Eq. (23), N4): "
                          "one RS tensor of width R/2 per protein, rank-concatenated")
@@ -285,6 +290,7 @@ def main():
     ncpu = os.cpu_count() or 1
     t0 = time.perf_counter()
     fl = rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0
+    box_info = None
     if args.complex:
         # NEXT row N4 (Eq. (23)): one RS tensor per protein (R/2 each), combined on the device
         from synth import configs as syn
@@ -295,6 +301,26 @@ def main():
                  for Xp, qp in syn.complex_parts(w)]
         prot = rsdock.Protein.combine(parts, flags=fl)
         del parts
+    elif args.box:
+        # NEXT row N3 (scheme (C)): a parent with a rank-64 Tucker form on the host, recompressed
+        # to width args.box inside the cell box that covers every pose's atoms
+        parent = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                                tucker_rank_max=64, device=local,
+                                n_threads=max(1, ncpu // max(world, 1)), nbr_cell=args.nbr_cell,
+                                flags=rsdock.RS_FLAG_HOST_ONLY)
+        rl = float(np.linalg.norm(w.ligand_xyz, axis=1).max())
+        tr = w.poses[:, 4:]
+        inv_h = w.grid_n / (2 * w.box_half_width)
+        cell = lambda x: np.clip(np.ceil((x + w.box_half_width) * inv_h) - 1, 0, w.grid_n - 1)
+        lo = cell(tr.min(0) - rl - 0.5).astype(np.int32)
+        hi = cell(tr.max(0) + rl + 0.5).astype(np.int32)
+        prot = parent.restrict_box(lo, hi, args.box, flags=fl)
+        box_info = {"lo": lo.tolist(), "hi": hi.tolist(), "R_pi": args.box,
+                    "box_cp_core_err": prot.info["cp_core_err"],
+                    "parent_cp_core_err": parent.info["cp_core_err"],
+                    "parent_sampled_max_err": parent.info["sampled_max_err"],
+                    "parent_tucker_r": parent.info["tucker_r"]}
+        del parent
     else:
         prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
                               device=local, n_threads=max(1, ncpu // max(world, 1)),
@@ -426,6 +452,8 @@ def main():
                                        "cp_core_err", "nbr_entries", "device_bytes")},
         "step_ms_min": float(np.min(step_ms)), "step_ms_max": float(np.max(step_ms)),
     }
+    if box_info:
+        line["box"] = box_info
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

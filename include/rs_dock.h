@@ -74,7 +74,9 @@ typedef struct {
     double   sigma_vdw;     /* vdW threshold: a pose clashes iff mindist < sigma_vdw (Eq. (22)) */
     double   dmin_cap;      /* D_cap >= sigma_vdw: mindist is reported exactly below D_cap,
                                +inf otherwise                                                   */
-    int32_t  tucker_rank_max; /* cap on the Tucker ranks r_l (0 = automatic)                    */
+    int32_t  tucker_rank_max; /* cap on the Tucker ranks r_l, which follow eps_compress below it
+                               (0 = automatic: at most rank_R + 8 when rank_R > 0).  A larger
+                               cap keeps a richer Tucker form for rs_restrict_box              */
     int32_t  als_sweeps;    /* CP-ALS sweeps when R < the exact C2T2C rank (0 = default 300)    */
     int32_t  device;        /* CUDA device ordinal                                              */
     int32_t  n_threads;     /* host threads for the setup (0 = all)                             */
@@ -112,6 +114,7 @@ typedef struct {
     double   setup_seconds; /* wall time of the whole build */
     int32_t  on_device;     /* 1 when the tables are resident on a device */
     int32_t  factor_bits;   /* 64, or 32 with RS_FLAG_F32_FACTORS */
+    int32_t  box_lo[3], box_hi[3]; /* rs_restrict_box cell box (hi < lo: the whole grid) */
 } rs_info;
 
 void rs_params_default(rs_params* p);
@@ -149,6 +152,26 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
  * CUDA device unless RS_FLAG_HOST_ONLY, allocation or upload failure).
  */
 rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, int32_t flags);
+
+/*
+ * Box-restricted recompression (NEXT row N3; schemes (B)/(C), Table 1
+ * the potential restricted to a ligand box Pi has CP rank R_Pi << R_Omega;
+ * DESIGN.md reading A25).  Scheme (C), hybrid: the handle's Tucker form of the long-range part
+ * (kept from the RHOSVD step S5-S6, factors U_l of n x r_l and core G) is restricted to the
+ * cell box lo[l] <= i_l <= hi[l] (0 <= lo <= hi < n, per axis), re-orthonormalised there by an
+ * SVD of the restricted rows, and its core recompressed to CP width rank (0: the smallest width
+ * within the handle's eps_compress).  The new handle carries these factors in rows inside the
+ * box and NaN in every other row, so a pose with a ligand atom outside the box gets E = NaN
+ * (its minimum distance is still computed); the short-range part and the vdW distance are the
+ * parent's, exactly.  Scoring, forces and scans run unchanged on it.
+ *   h     : a handle from rs_build_protein (not from rs_combine_proteins: no Tucker form)
+ *   lo, hi: 3 cell indices each (host)
+ *   rank  : R_Pi >= 0;   flags: RS_FLAG_* of the new handle
+ * Returns NULL on error (bad box, no Tucker form, RS_FLAG_F32_FACTORS with an uncompiled width,
+ * no device unless RS_FLAG_HOST_ONLY, allocation or upload failure).  Release with rs_free.
+ */
+rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t* hi, int32_t rank,
+                           int32_t flags);
 
 /*
  * Score P poses of a rigid ligand (Algorithm PLIE + Eq. (22)), synchronously.

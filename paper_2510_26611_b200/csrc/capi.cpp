@@ -348,7 +348,8 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     hd->n_sigma = (int)std::ceil(prm.sigma_split / h);
     // S5-S7
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
-                            prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep);
+                            prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep,
+                            &hd->tucker);
     hd->f32 = (prm.flags & RS_FLAG_F32_FACTORS) != 0;
     if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
       set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
@@ -505,6 +506,81 @@ rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, i
   return H.release();
 }
 
+rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t* hi, int32_t rank,
+                           int32_t flags) {
+  g_err.clear();
+  auto t0 = std::chrono::steady_clock::now();
+  if (!h || !lo || !hi) { set_err("null argument"); return nullptr; }
+  if (rank < 0) { set_err("rank must be >= 0"); return nullptr; }
+  for (int a = 0; a < 3; ++a)
+    if (lo[a] < 0 || hi[a] >= h->n || lo[a] > hi[a]) {
+      set_err("need 0 <= lo <= hi < n on every axis");
+      return nullptr;
+    }
+  if (h->tucker.G.empty()) {
+    set_err("handle has no Tucker form (combined or restricted handles cannot be restricted)");
+    return nullptr;
+  }
+  const bool host_only = (flags & RS_FLAG_HOST_ONLY) != 0;
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= h->prm.device || h->prm.device < 0) {
+      cudaGetLastError();
+      set_err("no CUDA device (there is no CPU fallback; use RS_FLAG_HOST_ONLY for host-only tables)");
+      return nullptr;
+    }
+  }
+  std::unique_ptr<rs_handle> H;
+  try {
+    H.reset(new rs_handle());
+    rs_handle* hd = H.get();
+    hd->prm = h->prm;
+    hd->prm.flags = flags;
+    hd->n = h->n;
+    hd->b = h->b;
+    hd->h = h->h;
+    hd->inv_h = h->inv_h;
+    hd->quad = h->quad;
+    hd->is_long = h->is_long;
+    hd->Rs = h->Rs;
+    hd->n_sigma = h->n_sigma;
+    hd->R_long_ref = h->R_long_ref;
+    for (int a = 0; a < 3; ++a) hd->S[a] = h->S[a];
+    hd->M = h->M;
+    hd->xyz = h->xyz;
+    hd->z = h->z;
+    hd->cells = h->cells;
+    hd->cg = h->cg;
+    hd->device = h->device;
+    hd->f32 = (flags & RS_FLAG_F32_FACTORS) != 0;
+    int lo_[3], hi_[3];
+    for (int a = 0; a < 3; ++a) { lo_[a] = lo[a]; hi_[a] = hi[a]; hd->box_lo[a] = lo[a]; hd->box_hi[a] = hi[a]; }
+    hd->rep.tucker_err = h->rep.tucker_err;
+    hd->R = rs::restrict_to_box(h->n, h->tucker, lo_, hi_, rank, h->prm.eps_compress,
+                                h->prm.als_sweeps, hd->F, &hd->rep);
+    if (hd->R > (1 << 20)) { set_err("box CP width exceeds 2^20"); return nullptr; }
+    if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
+      set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
+              std::to_string(hd->R));
+      return nullptr;
+    }
+  } catch (const std::bad_alloc&) {
+    set_err("out of host memory while restricting");
+    return nullptr;
+  }
+  rs_handle* hd = H.get();
+  if (!host_only) {
+    if (upload_handle(hd) != 0) {
+      std::string msg = g_err;
+      free_device(hd);
+      set_err(msg.empty() ? "upload failed" : msg);
+      return nullptr;
+    }
+  }
+  hd->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return H.release();
+}
+
 int rs_get_info(const rs_handle* h, rs_info* out) {
   if (!h || !out) { set_err("null argument"); return RS_E_INVALID_ARG; }
   std::memset(out, 0, sizeof(*out));
@@ -537,6 +613,7 @@ int rs_get_info(const rs_handle* h, rs_info* out) {
   out->setup_seconds = h->setup_seconds;
   out->on_device = h->on_device ? 1 : 0;
   out->factor_bits = h->f32 ? 32 : 64;
+  for (int a = 0; a < 3; ++a) { out->box_lo[a] = h->box_lo[a]; out->box_hi[a] = h->box_hi[a]; }
   return 0;
 }
 

@@ -42,13 +42,29 @@ struct SetupReport {
   int n_samples = 0;
 };
 
+struct TuckerRep {           // the long-range part in Tucker format (S5-S6), kept for N3
+  int r[3] = {0, 0, 0};
+  std::vector<double> U[3];  // n x r_l, column-major (column a contiguous)
+  std::vector<double> G;     // r0 x r1 x r2, row-major
+};
+
+// S7: Tucker core -> CP of width rank_R (0: eps mode); returns R
+int core_to_cp(const std::vector<double>& G, int r0, int r1, int r2, int rank_R, double eps,
+               int als_sweeps, std::vector<double>& A, std::vector<double>& B,
+               std::vector<double>& C, int* R_exact, double* rel_err);
+
+// N3 scheme (C): CP of the long-range part restricted to the cell box [lo, hi] (rows outside NaN)
+int restrict_to_box(int n, const TuckerRep& tk, const int lo[3], const int hi[3], int rank,
+                    double eps, int als_sweeps, std::vector<double> F[3], SetupReport* rep);
+
 // S5-S7: rank-R CP factors (n x R row-major each) of the protein's long-range potential
 // P_l[i] = sum_m z_m sum_{k long} a_k prod_a g_k[i_a - i_{m,a}]   (Eq. (6))
 void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& z, const std::vector<double>& t_long,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
-                         std::vector<double> F[3], int* R_out, SetupReport* rep);
+                         std::vector<double> F[3], int* R_out, SetupReport* rep,
+                         TuckerRep* tk = nullptr);
 
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
                       const std::vector<int32_t>& cells, double rho, double cell_edge,
@@ -140,6 +156,8 @@ struct rs_handle {
   std::vector<int32_t> cells;          // M x 3
   rs::CoarseGrid cg;
   rs::SetupReport rep;
+  rs::TuckerRep tucker;                // S5-S6 Tucker form of the long-range part (N3)
+  int box_lo[3] = {0, 0, 0}, box_hi[3] = {-1, -1, -1};   // N3 restriction box (hi < lo: none)
   double setup_seconds = 0;
   // device
   bool on_device = false;

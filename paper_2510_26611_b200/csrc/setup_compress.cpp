@@ -12,6 +12,7 @@
 // Then F_l = U_l X_l (n x R), weights folded into F_0.
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -239,7 +240,9 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       continue;
     }
     int r;
-    if (rank_R > 0) r = std::max(rank_R, std::min(r_tol, rank_R + 8));
+    // fixed width R: Tucker rank r_tol at eps, limited to R + 8 by default or to an explicit
+    // tucker_cap (a richer Tucker form for rs_restrict_box, N3); tolerance mode: r_tol
+    if (rank_R > 0) r = std::max(rank_R, std::min(r_tol, tucker_cap > 0 ? tucker_cap : rank_R + 8));
     else r = r_tol;
     if (tucker_cap > 0) r = std::min(r, tucker_cap);
     r = std::min(r, std::min(p, n));
@@ -390,11 +393,75 @@ void cp_als(const std::vector<double>& G, int r0, int r1, int r2, int R, int swe
 
 }  // namespace
 
+// S7: core G (r0 x r1 x r2) -> CP of width rank_R (0: the smallest width whose dropped slice
+// singular values stay within eps of the core norm): the exact canonical expansion from the
+// SVDs of the slices G[a,:,:] = sum sigma u v^T, truncated, then CP-ALS when it was truncated.
+// A (R blocks of r0), B, C: term q is A[q] o B[q] o C[q].  Returns R.
+int core_to_cp(const std::vector<double>& G, int r0, int r1, int r2, int rank_R, double eps,
+               int als_sweeps, std::vector<double>& A, std::vector<double>& B,
+               std::vector<double>& C, int* R_exact, double* rel_err) {
+  double gnorm = 0;
+  for (double v : G) gnorm += v * v;
+  gnorm = std::sqrt(gnorm);
+  struct Trip { int a; double s; std::vector<double> u, v; };
+  std::vector<Trip> trips;
+  const bool tr = r1 < r2;              // Jacobi SVD wants rows >= cols
+  const int mr = tr ? r2 : r1, nc = tr ? r1 : r2;
+  for (int a = 0; a < r0; ++a) {
+    std::vector<double> S((size_t)mr * nc), V((size_t)nc * nc), U((size_t)mr * nc), sv(nc);
+    for (int b = 0; b < r1; ++b)
+      for (int c = 0; c < r2; ++c) {
+        const double v = G[((size_t)a * r1 + b) * r2 + c];
+        if (!tr) S[(size_t)c * mr + b] = v; else S[(size_t)b * mr + c] = v;
+      }
+    la::jacobi_svd(S.data(), mr, nc, sv.data(), V.data(), U.data());
+    for (int q = 0; q < nc; ++q) {
+      if (!(sv[q] > 1e-15 * gnorm)) continue;
+      Trip t;
+      t.a = a;
+      t.s = sv[q];
+      std::vector<double> uu(U.begin() + (size_t)q * mr, U.begin() + (size_t)(q + 1) * mr);
+      std::vector<double> vv(V.begin() + (size_t)q * nc, V.begin() + (size_t)(q + 1) * nc);
+      if (!tr) { t.u = uu; t.v = vv; } else { t.u = vv; t.v = uu; }
+      trips.push_back(std::move(t));
+    }
+  }
+  std::stable_sort(trips.begin(), trips.end(), [](const Trip& x, const Trip& y) { return x.s > y.s; });
+  *R_exact = (int)trips.size();
+  int R;
+  size_t keep = trips.size();
+  if (rank_R <= 0) {
+    double tot = 0, drop = 0;
+    for (auto& t : trips) tot += t.s * t.s;
+    while (keep > 1 && drop + trips[keep - 1].s * trips[keep - 1].s <= eps * eps * tot) {
+      drop += trips[keep - 1].s * trips[keep - 1].s;
+      --keep;
+    }
+    R = (int)keep;
+  } else {
+    R = rank_R;
+    keep = std::min(trips.size(), (size_t)rank_R);
+  }
+  A.assign((size_t)r0 * R, 0.0);
+  B.assign((size_t)r1 * R, 0.0);
+  C.assign((size_t)r2 * R, 0.0);
+  for (size_t q = 0; q < keep; ++q) {
+    A[q * r0 + trips[q].a] = trips[q].s;
+    for (int i = 0; i < r1; ++i) B[q * r1 + i] = trips[q].u[i];
+    for (int i = 0; i < r2; ++i) C[q * r2 + i] = trips[q].v[i];
+  }
+  if (rank_R > 0 && (int)trips.size() > rank_R)
+    cp_als(G, r0, r1, r2, R, als_sweeps > 0 ? als_sweeps : 300, A, B, C);
+  *rel_err = gnorm > 0 ? cp_error(G, r0, r1, r2, A, B, C, R) / gnorm : 0.0;
+  return R;
+}
+
 void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& z, const std::vector<double>& t_long,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
-                         std::vector<double> F[3], int* R_out, SetupReport* rep) {
+                         std::vector<double> F[3], int* R_out, SetupReport* rep,
+                         TuckerRep* tk) {
   ConvOps ops(n, h, t_long);
   const int RL = ops.RL;
   const int64_t M = (int64_t)z.size();
@@ -436,59 +503,14 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       for (size_t i = 0; i < row.size(); ++i) g[i] += row[i];
     }
   }
-  double gnorm = 0;
-  for (double v : G) gnorm += v * v;
-  gnorm = std::sqrt(gnorm);
-
-  // S7: slice SVDs G[a,:,:] = sum sigma u v^T -> exact canonical expansion
-  struct Trip { int a; double s; std::vector<double> u, v; };
-  std::vector<Trip> trips;
-  const bool tr = r1 < r2;              // Jacobi SVD wants rows >= cols
-  const int mr = tr ? r2 : r1, nc = tr ? r1 : r2;
-  for (int a = 0; a < r0; ++a) {
-    std::vector<double> S((size_t)mr * nc), V((size_t)nc * nc), U((size_t)mr * nc), sv(nc);
-    for (int b = 0; b < r1; ++b)
-      for (int c = 0; c < r2; ++c) {
-        const double v = G[((size_t)a * r1 + b) * r2 + c];
-        if (!tr) S[(size_t)c * mr + b] = v; else S[(size_t)b * mr + c] = v;
-      }
-    la::jacobi_svd(S.data(), mr, nc, sv.data(), V.data(), U.data());
-    for (int q = 0; q < nc; ++q) {
-      if (!(sv[q] > 1e-15 * gnorm)) continue;
-      Trip t;
-      t.a = a;
-      t.s = sv[q];
-      std::vector<double> uu(U.begin() + (size_t)q * mr, U.begin() + (size_t)(q + 1) * mr);
-      std::vector<double> vv(V.begin() + (size_t)q * nc, V.begin() + (size_t)(q + 1) * nc);
-      if (!tr) { t.u = uu; t.v = vv; } else { t.u = vv; t.v = uu; }
-      trips.push_back(std::move(t));
-    }
+  // S7: core -> CP of width R
+  std::vector<double> A, B, C;
+  const int R = core_to_cp(G, r0, r1, r2, rank_R, eps, als_sweeps, A, B, C, &rep->R_exact,
+                           &rep->cp_core_err);
+  if (tk) {
+    for (int l = 0; l < 3; ++l) { tk->r[l] = mb[l].r; tk->U[l] = mb[l].U; }
+    tk->G = G;
   }
-  std::stable_sort(trips.begin(), trips.end(), [](const Trip& x, const Trip& y) { return x.s > y.s; });
-  rep->R_exact = (int)trips.size();
-  int R;
-  size_t keep = trips.size();
-  if (rank_R <= 0) {
-    double tot = 0, drop = 0;
-    for (auto& t : trips) tot += t.s * t.s;
-    while (keep > 1 && drop + trips[keep - 1].s * trips[keep - 1].s <= eps * eps * tot) {
-      drop += trips[keep - 1].s * trips[keep - 1].s;
-      --keep;
-    }
-    R = (int)keep;
-  } else {
-    R = rank_R;
-    keep = std::min(trips.size(), (size_t)rank_R);
-  }
-  std::vector<double> A((size_t)r0 * R, 0.0), B((size_t)r1 * R, 0.0), C((size_t)r2 * R, 0.0);
-  for (size_t q = 0; q < keep; ++q) {
-    A[q * r0 + trips[q].a] = trips[q].s;
-    for (int i = 0; i < r1; ++i) B[q * r1 + i] = trips[q].u[i];
-    for (int i = 0; i < r2; ++i) C[q * r2 + i] = trips[q].v[i];
-  }
-  if (rank_R > 0 && (int)trips.size() > rank_R)
-    cp_als(G, r0, r1, r2, R, als_sweeps > 0 ? als_sweeps : 300, A, B, C);
-  rep->cp_core_err = gnorm > 0 ? cp_error(G, r0, r1, r2, A, B, C, R) / gnorm : 0.0;
 
   // F_l = U_l X_l  (n x R row-major)
   const std::vector<double>* X[3] = {&A, &B, &C};
@@ -504,6 +526,84 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       }
   }
   *R_out = R;
+}
+
+// ---- NEXT row N3: scheme (C), recompression inside a box ------------------
+// Rows lo_l..hi_l of the Tucker bases U_l (n x r_l) of the long-range part: their SVD
+// U_l[lo:hi] = Q_l diag(s_l) V_l^T gives orthonormal Q_l (m_l x r'_l) and S_l = diag(s_l) V_l^T
+// (r'_l x r_l, singular values above 1e-13 s_max kept); the box's Tucker core is
+// G_box = G x_0 S_0 x_1 S_1 x_2 S_2 and its CP (core_to_cp, width rank or eps) gives the box
+// factors F_l = Q_l X_l in rows lo_l..hi_l.  Rows outside the box are NaN: a ligand atom outside
+// the box makes the pose's energy NaN (the restricted tensor says nothing there).
+int restrict_to_box(int n, const TuckerRep& tk, const int lo[3], const int hi[3], int rank,
+                    double eps, int als_sweeps, std::vector<double> F[3], SetupReport* rep) {
+  std::vector<double> Q[3], S[3];
+  int rp[3];
+  for (int l = 0; l < 3; ++l) {
+    const int r = tk.r[l], m = hi[l] - lo[l] + 1;
+    const bool tall = m >= r;
+    const int mr = tall ? m : r, nc = tall ? r : m;
+    std::vector<double> Aw((size_t)mr * nc), V((size_t)nc * nc), U((size_t)mr * nc), sv(nc);
+    for (int a = 0; a < r; ++a)
+      for (int i = 0; i < m; ++i) {
+        const double u = tk.U[l][(size_t)a * n + lo[l] + i];
+        if (tall) Aw[(size_t)a * mr + i] = u; else Aw[(size_t)i * mr + a] = u;
+      }
+    la::jacobi_svd(Aw.data(), mr, nc, sv.data(), V.data(), U.data());
+    // tall: U_box = U diag(s) V^T;  wide: U_box^T = U diag(s) V^T, so U_box = V diag(s) U^T
+    int keep = 0;
+    while (keep < nc && sv[keep] > 1e-13 * sv[0]) ++keep;
+    rp[l] = keep;
+    Q[l].assign((size_t)m * keep, 0.0);          // column-major m x keep
+    S[l].assign((size_t)keep * r, 0.0);          // row j: s_j (right vector)^T over a
+    for (int j = 0; j < keep; ++j) {
+      const double* left = tall ? &U[(size_t)j * mr] : &V[(size_t)j * nc];    // length m
+      const double* right = tall ? &V[(size_t)j * nc] : &U[(size_t)j * mr];   // length r
+      for (int i = 0; i < m; ++i) Q[l][(size_t)j * m + i] = left[i];
+      for (int a = 0; a < r; ++a) S[l][(size_t)j * r + a] = sv[j] * right[a];
+    }
+  }
+  // G_box[j0,j1,j2] = sum_abc S0[j0,a] S1[j1,b] S2[j2,c] G[a,b,c], one mode at a time
+  const int r0 = tk.r[0], r1 = tk.r[1], r2 = tk.r[2];
+  std::vector<double> T2((size_t)r0 * r1 * rp[2], 0.0);
+  for (size_t ab = 0; ab < (size_t)r0 * r1; ++ab)
+    for (int j = 0; j < rp[2]; ++j) {
+      double s = 0;
+      for (int c = 0; c < r2; ++c) s += tk.G[ab * r2 + c] * S[2][(size_t)j * r2 + c];
+      T2[ab * rp[2] + j] = s;
+    }
+  std::vector<double> T1((size_t)r0 * rp[1] * rp[2], 0.0);
+  for (int a = 0; a < r0; ++a)
+    for (int j = 0; j < rp[1]; ++j)
+      for (int b = 0; b < r1; ++b) {
+        const double w = S[1][(size_t)j * r1 + b];
+        const double* src = &T2[((size_t)a * r1 + b) * rp[2]];
+        double* dst = &T1[((size_t)a * rp[1] + j) * rp[2]];
+        for (int c = 0; c < rp[2]; ++c) dst[c] += w * src[c];
+      }
+  std::vector<double> Gb((size_t)rp[0] * rp[1] * rp[2], 0.0);
+  const size_t slab = (size_t)rp[1] * rp[2];
+  for (int j = 0; j < rp[0]; ++j)
+    for (int a = 0; a < r0; ++a) {
+      const double w = S[0][(size_t)j * r0 + a];
+      for (size_t x = 0; x < slab; ++x) Gb[j * slab + x] += w * T1[a * slab + x];
+    }
+  std::vector<double> A, B, C;
+  const int R = core_to_cp(Gb, rp[0], rp[1], rp[2], rank, eps, als_sweeps, A, B, C,
+                           &rep->R_exact, &rep->cp_core_err);
+  for (int l = 0; l < 3; ++l) rep->tucker_r[l] = rp[l];
+  const std::vector<double>* X[3] = {&A, &B, &C};
+  for (int l = 0; l < 3; ++l) {
+    const int m = hi[l] - lo[l] + 1;
+    F[l].assign((size_t)n * R, std::numeric_limits<double>::quiet_NaN());
+    for (int i = 0; i < m; ++i)
+      for (int q = 0; q < R; ++q) {
+        double s = 0;
+        for (int j = 0; j < rp[l]; ++j) s += Q[l][(size_t)j * m + i] * (*X[l])[(size_t)q * rp[l] + j];
+        F[l][(size_t)(lo[l] + i) * R + q] = s;
+      }
+  }
+  return R;
 }
 
 // ---- S9: cell lists --------------------------------------------------------------------------

@@ -22,7 +22,7 @@ RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
 RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 
-EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_score_poses", "rs_score_poses_async",
+EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_restrict_box", "rs_score_poses", "rs_score_poses_async",
             "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",
             "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
@@ -52,7 +52,8 @@ class rs_info(ctypes.Structure):
                 ("nbr_cells", ctypes.c_int64), ("nbr_entries", ctypes.c_int64),
                 ("nbr_shift", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
                 ("setup_seconds", ctypes.c_double), ("on_device", ctypes.c_int32),
-                ("factor_bits", ctypes.c_int32)]
+                ("factor_bits", ctypes.c_int32), ("box_lo", ctypes.c_int32 * 3),
+                ("box_hi", ctypes.c_int32 * 3)]
 
 
 _lib = None
@@ -75,6 +76,8 @@ def load():
     L.rs_build_protein.restype = _vp
     L.rs_combine_proteins.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32]
     L.rs_combine_proteins.restype = _vp
+    L.rs_restrict_box.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32]
+    L.rs_restrict_box.restype = _vp
     L.rs_score_poses.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp]
     L.rs_score_poses.restype = ctypes.c_int64
     L.rs_score_poses_async.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
@@ -142,6 +145,16 @@ def rs_combine_proteins(parts, flags=0):
     return h
 
 
+def rs_restrict_box(h, lo, hi, rank, flags=0):
+    """Box-restricted recompression (N3, scheme (C)); lo, hi: 3 cell indices each."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    hi = np.ascontiguousarray(hi, dtype=np.int32)
+    r = load().rs_restrict_box(h, lo.ctypes.data, hi.ctypes.data, int(rank), int(flags))
+    if not r:
+        raise RuntimeError("rs_restrict_box: " + rs_last_error())
+    return r
+
+
 def rs_score_poses(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out) -> int:
     r = load().rs_score_poses(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
                               _ptr(energies_out), _ptr(mindist_out))
@@ -206,7 +219,7 @@ def rs_get_info(h) -> dict:
     out = {}
     for name, _ in rs_info._fields_:
         v = getattr(info, name)
-        out[name] = list(v) if name == "tucker_r" else v
+        out[name] = list(v) if name in ("tucker_r", "box_lo", "box_hi") else v
     return out
 
 
@@ -251,6 +264,16 @@ class Protein:
         self.params = rs_params_default(**params)
         self._h = rs_build_protein(q, xyz, box_half_width, self.params)
         self.info = rs_get_info(self._h)
+
+    def restrict_box(self, lo, hi, rank, flags=0):
+        """A new Protein whose long-range factors are recompressed inside the cell box
+        [lo, hi] (N3, scheme (C)); NaN rows outside it."""
+        new = type(self).__new__(type(self))
+        new._h = None
+        new.params = self.params
+        new._h = rs_restrict_box(self._h, lo, hi, rank, flags)
+        new.info = rs_get_info(new._h)
+        return new
 
     @classmethod
     def combine(cls, parts, flags=0):

@@ -535,3 +535,60 @@ def test_complex_mid_size_sample(env):
     Eo, Do, _ = rs_oracle.score_poses(comb, Xu, qu, w.ligand_xyz, w.ligand_q, w.poses[idx],
                                       w.dmin_cap)
     compare(Eg[idx], Dg[idx], Eo, Do)
+
+
+# ----------------------------------------------------------------------------- N3: box restriction
+
+def _site_poses(w, centre, spread, P, seed):
+    rng = np.random.default_rng(seed)
+    quats = syn.shoemake_quaternions(rng, P)
+    return np.concatenate([quats, centre + rng.uniform(-spread, spread, (P, 3))], axis=1)
+
+
+def _box_cells(w, lo_x, hi_x):
+    inv_h = w.grid_n / (2 * w.box_half_width)
+    lo = np.clip(np.ceil((lo_x + w.box_half_width) * inv_h) - 1, 0, w.grid_n - 1).astype(np.int32)
+    hi = np.clip(np.ceil((hi_x + w.box_half_width) * inv_h) - 1, 0, w.grid_n - 1).astype(np.int32)
+    return lo, hi
+
+
+@pytest.mark.parametrize("R,f32", [(4, False), (8, False), (6, False), (8, True)])
+def test_restricted_box_parity(env, R, f32):
+    """rs_restrict_box (reading A25): the kernel on the box handle matches the oracle on its
+    exported tables; poses with an atom outside the box give NaN on both sides, their minimum
+    distance still bitwise equal."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1()
+    parent = build(rsdock, w, rank_R=0, eps_compress=1e-4, flags=rsdock.RS_FLAG_HOST_ONLY)
+    c = w.protein_xyz.mean(0) + np.array([12.0, 0.0, 0.0])
+    rl = float(np.linalg.norm(w.ligand_xyz, axis=1).max())
+    lo, hi = _box_cells(w, c - 2.0 - rl, c + 2.0 + rl)
+    box = parent.restrict_box(lo, hi, R, flags=rsdock.RS_FLAG_F32_FACTORS if f32 else 0)
+    poses = _site_poses(w, c, 3.0, 517, seed=R)
+    Eg, Dg, inv = gpu_score(torch, rsdock, box, w, poses)
+    Eo, Do, invo = rs_oracle.score_poses(box.export_tables(), w.protein_xyz, w.protein_q,
+                                         w.ligand_xyz, w.ligand_q, poses, w.dmin_cap, f32=f32)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    assert np.array_equal(Dg, Do, equal_nan=True)
+    nan = np.isnan(Eg)
+    assert 0.1 < nan.mean() < 0.9                      # both kinds present
+
+
+def test_restricted_box_c2_site_sample(env):
+    """C2's docking site (1000-translation lattice x 100 rotations) on a box handle of width 8
+    from a parent with a rank-64 Tucker form: the full 10^5-pose launch, a seeded sample against the oracle;
+    every pose lies inside the box, so no energy is NaN."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c2()
+    parent = build(rsdock, w, eps_compress=1e-4, tucker_rank_max=64,
+                   flags=rsdock.RS_FLAG_HOST_ONLY)
+    rl = float(np.linalg.norm(w.ligand_xyz, axis=1).max())
+    t = w.poses[:, 4:]
+    lo, hi = _box_cells(w, t.min(0) - rl - 0.5, t.max(0) + rl + 0.5)
+    box = parent.restrict_box(lo, hi, 8)
+    Eg, Dg, inv = gpu_score(torch, rsdock, box, w, w.poses)
+    assert not np.isnan(Eg).any()
+    idx, sample = syn.subsample(w.poses, 300)
+    Eo, Do, _ = rs_oracle.score_poses(box.export_tables(), w.protein_xyz, w.protein_q,
+                                      w.ligand_xyz, w.ligand_q, sample, w.dmin_cap)
+    compare(Eg[idx], Dg[idx], Eo, Do)
