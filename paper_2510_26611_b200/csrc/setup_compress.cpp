@@ -234,7 +234,12 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       }
       r_tol = std::max(r_tol, 1);
     }
-    const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax || p >= n;
+    // resolved: the spectrum fell below the tolerance, or the sketch already oversamples the
+    // largest rank this build can keep (r_cap) by r_cap + 16 columns (one power iteration)
+    const int r_cap = rank_R > 0 ? (tucker_cap > 0 ? std::max(rank_R, tucker_cap) : rank_R + 8)
+                                 : (tucker_cap > 0 ? tucker_cap : n);
+    const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax || p >= n ||
+                          p >= 2 * r_cap + 16;
     if (!resolved && r_tol >= p - 4) {
       p = std::min(pmax, 2 * p);
       continue;

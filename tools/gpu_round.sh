@@ -8,7 +8,7 @@ OUT=gpurun_out/$TAG; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo build failed; tail -20 $OUT/build.log; exit 1; }
 if [ "$TESTS" = "1" ]; then
-  timeout 900 python -m pytest tests -m gpu -x -q > $OUT/gpu_tests.log 2>&1; echo "tests_rc=$?" >> $OUT/gpu_tests.log
+  timeout 1800 python -m pytest tests -m gpu -x -q > $OUT/gpu_tests.log 2>&1; echo "tests_rc=$?" >> $OUT/gpu_tests.log
   tail -3 $OUT/gpu_tests.log
 fi
 timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench_rc=$?"
