@@ -406,13 +406,17 @@ def main():
     peaks = _peaks()
     R = info["R"]
     fbytes = 4.0 if args.f32 else 8.0
-    gather_bytes = 3.0 * fbytes * R * P * L         # H4: 3 rows x R factors per atom evaluation
+    # H4: 3 rows x R factors per atom evaluation; forces (N1): 6 rows (phi(i), phi(i - e_a))
+    rows = 6.0 if args.forces else 3.0
+    gather_bytes = rows * fbytes * R * P * L
     t_s = ms * 1e-3
     achieved = gather_bytes / t_s / 1e9
     smem_peak = mb.get("lds128_random_row_rotated_gbs") if mb else None
     l2_peak = mb.get("l2_gather_1p5MB_gbs") if mb else None
     fp64_rate = mb.get("dfma_instr_per_s") if mb else None
     dp_instr = ((0.0 if args.f32 else 3.0 * R) + 25.0) * P * L   # 2R DMUL + R DADD + ~25 per atom
+    if args.forces:
+        dp_instr = (12.0 * R + 80.0) * P * L      # four values (8R DMUL + 4R DADD) + resultants
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tfile):
@@ -423,7 +427,8 @@ def main():
     roofline = {
         "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
         "frac": (achieved / smem_peak) if smem_peak else None, "traffic": traffic,
-        "kernel": rsdock.load() and f"score_kernel<{R}>",
+        "kernel": (f"force_window_kernel<{R}>" if R in (4, 8, 16, 32) else f"force_kernel<{R}>")
+                  if args.forces else f"score_kernel<{R}>",
         "peak_source": "tools/microbench (same run): conflict-free random-row LDS.128 "
                        "(lane-rotated chunks), 148 SMs",
         "algorithmic_bytes_per_launch": gather_bytes,

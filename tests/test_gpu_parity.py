@@ -396,6 +396,32 @@ def test_forces_configs(env, name, k):
     assert frac > 0.99
 
 
+def test_forces_c3_contiguous_window(env):
+    """The windowed force kernel on C3's launch order (16 translations x 1000 rotations,
+    contiguous: each block restages its window per translation) against the oracle."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c3()
+    prot = build(rsdock, w)
+    poses = w.poses[:16000]
+    Fg, ig = gpu_forces(torch, prot, w, poses)
+    Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, poses)
+    assert compare_forces(Fg, Fo, ig, io) > 0.99
+
+
+@pytest.mark.parametrize("R", [8, 16])
+def test_forces_window_and_fallback_mix(env, R):
+    """n = 2048 (h = 1/128 A): tiles of one translation fit the window, tiles of scattered
+    translations do not and read L2; atoms beyond the window edge read L2 too."""
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=60 + R, M=40, L=20, n=2048, b=8.0, R=R, P=400, trans=3.0)
+    poses = w.poses.copy()
+    poses[:200, 4:] = poses[0, 4:]                     # 200 poses at one translation
+    prot = build(rsdock, w)
+    Fg, ig = gpu_forces(torch, prot, w, poses)
+    Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, poses)
+    compare_forces(Fg, Fo, ig, io)
+
+
 # ----------------------------------------------------------------------------- PPIEM scan (N2)
 
 @pytest.mark.parametrize("mP,mL", [(12, 8), (5, 3)])
@@ -592,3 +618,21 @@ def test_restricted_box_c2_site_sample(env):
     Eo, Do, _ = rs_oracle.score_poses(box.export_tables(), w.protein_xyz, w.protein_q,
                                       w.ligand_xyz, w.ligand_q, sample, w.dmin_cap)
     compare(Eg[idx], Dg[idx], Eo, Do)
+
+
+def test_shards_concatenate_bitwise(env):
+    """§8(e): the G-way sharded outputs (shard.shard_bounds, each shard its own launch)
+    concatenate to the 1-launch output bit for bit (per-pose arithmetic never depends on the
+    tiling, chunking or launch)."""
+    torch, rsdock, rs_oracle = env
+    from paper_2510_26611_b200.shard import shard_bounds
+    w = syn.config_c2()
+    prot = build(rsdock, w)
+    poses = w.poses[:30011]
+    E, D, inv = gpu_score(torch, rsdock, prot, w, poses)
+    for G in (2, 3, 8):
+        parts = [gpu_score(torch, rsdock, prot, w, poses[a:b])
+                 for a, b in (shard_bounds(len(poses), G, r) for r in range(G))]
+        assert np.array_equal(np.concatenate([p[0] for p in parts]), E, equal_nan=True)
+        assert np.array_equal(np.concatenate([p[1] for p in parts]), D, equal_nan=True)
+        assert sum(p[2] for p in parts) == inv
