@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_26611_b200.shard import score_sharded, shard_bounds
+from paper_2510_26611_b200.shard import ppiem_sharded, score_sharded, shard_bounds
 from synth import configs as syn
 
 
@@ -67,4 +67,41 @@ def test_sharded_scoring_gloo_world2():
     out = mgr.dict()
     port = _free_port()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] and out[1]
+
+
+def _ppiem_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ppiem_oracle as po
+    from oracle import rs_oracle
+    w = syn.random_small(seed=31, M=30, L=5, n=64, b=10.0, R=4, P=1)
+    rng = np.random.default_rng(3)
+    tb = dict(n=64, b=10.0, R=4, F1=rng.normal(size=(64, 4)) * 0.1, F2=rng.normal(size=(64, 4)),
+              F3=rng.normal(size=(64, 4)), n_sigma=2, S1=rng.normal(size=(5, 3)) * 0.1,
+              S2=rng.normal(size=(5, 3)), S3=rng.normal(size=(5, 3)))
+    dirs, quats = syn.planar_scan(7, 4)
+    centre = w.protein_xyz.mean(0)
+    args = (tb, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, centre)
+
+    def scan(d, q):
+        return po.scan(*args, d, q, 7.0, 1.0, 2.5, 1e-3, 40)
+
+    E, s, st, mins = ppiem_sharded(scan, dirs, quats, po.landscape_minima, 5)
+    E1, s1, st1 = scan(dirs, quats)
+    ok = (np.array_equal(E, E1, equal_nan=True) and np.array_equal(s, s1) and
+          np.array_equal(st, st1) and list(mins) == list(po.landscape_minima(E1, 5)) and
+          (st1 == 0).sum() > 0)
+    out[rank] = bool(ok)
+    dist.destroy_process_group()
+
+
+def test_ppiem_sharded_gloo_world2():
+    """PPIEM rows split over two ranks (7 positions: 4 + 3), one all-gather: the landscape,
+    distances, statuses and minima equal the 1-rank scan bit for bit."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_ppiem_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] and out[1]
