@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -346,6 +348,14 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     hd->R_long_ref = (int)tl.size();
     hd->Rs = (int)ts.size();
     hd->n_sigma = (int)std::ceil(prm.sigma_split / h);
+    auto lap = [&](const char* what) {
+      static const bool on = std::getenv("RS_SETUP_TIMING") != nullptr;
+      if (on)
+        std::fprintf(stderr, "[rs setup] %-22s %8.3f s (at %.3f)\n", what,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                     std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
+    };
+    lap("S1-S4");
     // S5-S7
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
                             prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep,
@@ -360,6 +370,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
       set_err("compressed CP width " + std::to_string(hd->R) + " exceeds 2^20 (raise eps_compress or fix rank_R)");
       return nullptr;
     }
+    lap("S5-S7 (RHOSVD, core, CP)");
     // S8: short-range reference rows, a_k folded into S1 (Def. 2.1, A_0)
     const int ns = hd->n_sigma, Rs = hd->Rs;
     for (int a = 0; a < 3; ++a) hd->S[a].assign((size_t)(2 * ns + 1) * Rs, 0.0);
@@ -374,11 +385,13 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     // short-range ball (|i_l - i_m|_2 <= n_sigma => |x_l - x_m| <= (n_sigma + sqrt 3) h)
     const double rho = std::max(prm.dmin_cap, (ns + std::sqrt(3.0)) * h);
     rs::build_cell_lists(n, b, h, hd->xyz, hd->cells, rho, prm.nbr_cell, &hd->cg);
+    lap("S8-S9 (short, cells)");
     // sampled compression error at exterior cells
     const double work = double(n_atoms) * double(tl.size());
     const int nsamp = (int)std::max(100.0, std::min(2000.0, 4e9 / std::max(work, 1.0)));
     rs::sample_compression_error(n, b, h, hd->xyz, hd->cells, hd->z, tl, al, hd->F, hd->R,
                                  std::max(prm.sigma_vdw, h), hd->cg, nsamp, prm.seed, &hd->rep);
+    lap("error samples");
   } catch (const std::bad_alloc&) {
     set_err("out of host memory during setup");
     return nullptr;

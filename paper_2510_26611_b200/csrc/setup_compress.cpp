@@ -11,8 +11,11 @@
 //       else CP-ALS to width R initialised from the dominant slice triplets.
 // Then F_l = U_l X_l (n x R), weights folded into F_0.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -120,7 +123,11 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
     if (occ[j]) occj.push_back(j);
 
   const int pmax = std::min(n, 512);
-  int p = (rank_R > 0) ? std::min(pmax, std::max(2 * rank_R + 16, 48)) : std::min(pmax, 64);
+  // the largest Tucker rank this build can keep; a fixed-width build starts its sketch at the
+  // 2 r_cap + 16 columns that resolve it (one range-finder pass instead of a doubling sequence)
+  const int r_cap = rank_R > 0 ? (tucker_cap > 0 ? std::max(rank_R, tucker_cap) : rank_R + 8)
+                               : (tucker_cap > 0 ? tucker_cap : n);
+  int p = (rank_R > 0) ? std::min(pmax, std::max(2 * r_cap + 16, 48)) : std::min(pmax, 64);
   ModeBasis out;
   for (;;) {
     // range finder: Y = sum_k T_k (sqrt(c_k) .* Xi_k).  Per-k results are summed in k order
@@ -236,8 +243,6 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
     }
     // resolved: the spectrum fell below the tolerance, or the sketch already oversamples the
     // largest rank this build can keep (r_cap) by r_cap + 16 columns (one power iteration)
-    const int r_cap = rank_R > 0 ? (tucker_cap > 0 ? std::max(rank_R, tucker_cap) : rank_R + 8)
-                                 : (tucker_cap > 0 ? tucker_cap : n);
     const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax || p >= n ||
                           p >= 2 * r_cap + 16;
     if (!resolved && r_tol >= p - 4) {
@@ -475,6 +480,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
     mb[l] = mode_basis(ops, l, cells, z, a_long, rank_R, eps, tucker_cap, seed);
   const int r0 = mb[0].r, r1 = mb[1].r, r2 = mb[2].r;
   for (int l = 0; l < 3; ++l) rep->tucker_r[l] = mb[l].r;
+  if (std::getenv("RS_SETUP_TIMING")) std::fprintf(stderr, "[rs setup]   mode bases done at %.3f\n", std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
   rep->tucker_err = std::sqrt(mb[0].tail * mb[0].tail + mb[1].tail * mb[1].tail +
                               mb[2].tail * mb[2].tail);
 
@@ -508,6 +514,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       for (size_t i = 0; i < row.size(); ++i) g[i] += row[i];
     }
   }
+  if (std::getenv("RS_SETUP_TIMING")) std::fprintf(stderr, "[rs setup]   core done at %.3f\n", std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
   // S7: core -> CP of width R
   std::vector<double> A, B, C;
   const int R = core_to_cp(G, r0, r1, r2, rank_R, eps, als_sweeps, A, B, C, &rep->R_exact,
