@@ -191,8 +191,9 @@ def config_dict(w, args):
                     + (", fp32 factors (A21)" if getattr(args, "f32", False) else "")
                     + (", Eq. (23) complex: 2 proteins x R/2, rank-concatenated (A24)"
                        if getattr(args, "complex", False) else "")
-                    + (f", box-restricted width {args.box} (N3, A25)" if getattr(args, "box", 0)
-                       else ""),
+                    + (f", box-restricted width {args.box}, scheme "
+                       f"({getattr(args, 'box_scheme', 'b').upper()}) (N3, A25)"
+                       if getattr(args, "box", 0) else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
@@ -287,6 +288,9 @@ def main():
     ap.add_argument("--box", type=int, default=0, metavar="R_PI",
                     help="score on a box-restricted handle of width R_PI covering the poses "
                          "(N3, scheme (C): rs_restrict_box)")
+    ap.add_argument("--box-scheme", default="b", choices=["b", "c"],
+                    help="N3 scheme: (B) new RHOSVD over the box rows, or (C) from a rank-64 "
+                         "Tucker form of the whole potential")
     ap.add_argument("--complex", action="store_true",
                     help="build the config's protein as a two-protein complex (Eq. (23), N4): "
                          "one RS tensor of width R/2 per protein, rank-concatenated")
@@ -335,10 +339,12 @@ def main():
         prot = rsdock.Protein.combine(parts, flags=fl)
         del parts
     elif args.box:
-        # NEXT row N3 (scheme (C)): a parent with a rank-64 Tucker form on the host, recompressed
-        # to width args.box inside the cell box that covers every pose's atoms
+        # NEXT row N3: the box that covers every pose's atoms, width args.box; scheme (B) (a new
+        # RHOSVD over the box rows, from the ordinary handle) or (C) (from a parent with a
+        # rank-64 Tucker form)
+        scheme_b = args.box_scheme == "b"
         parent = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
-                                tucker_rank_max=64, device=local,
+                                tucker_rank_max=0 if scheme_b else 64, device=local,
                                 n_threads=max(1, ncpu // max(world, 1)), nbr_cell=args.nbr_cell,
                                 flags=rsdock.RS_FLAG_HOST_ONLY)
         rl = float(np.linalg.norm(w.ligand_xyz, axis=1).max())
@@ -347,8 +353,11 @@ def main():
         cell = lambda x: np.clip(np.ceil((x + w.box_half_width) * inv_h) - 1, 0, w.grid_n - 1)
         lo = cell(tr.min(0) - rl - 0.5).astype(np.int32)
         hi = cell(tr.max(0) + rl + 0.5).astype(np.int32)
-        prot = parent.restrict_box(lo, hi, args.box, flags=fl)
-        box_info = {"lo": lo.tolist(), "hi": hi.tolist(), "R_pi": args.box,
+        t1 = time.perf_counter()
+        prot = parent.restrict_box(lo, hi, args.box,
+                                   flags=fl | (rsdock.RS_FLAG_BOX_SCHEME_B if scheme_b else 0))
+        box_info = {"scheme": args.box_scheme.upper(), "restrict_seconds": time.perf_counter() - t1,
+                    "lo": lo.tolist(), "hi": hi.tolist(), "R_pi": args.box,
                     "box_cp_core_err": prot.info["cp_core_err"],
                     "parent_cp_core_err": parent.info["cp_core_err"],
                     "parent_sampled_max_err": parent.info["sampled_max_err"],

@@ -58,6 +58,10 @@ extern "C" {
                                   energies within 1e-6 of sum_l |z_l phi(x_l)| of the binary64
                                   path; needs a compiled width R in {4, 8, 12, 16, 24, 32} */
 
+#define RS_FLAG_BOX_SCHEME_B 4u /* rs_restrict_box: scheme (B), a new RHOSVD + CP of the
+                                  long-range sum restricted to the box,
+                                  instead of scheme (C) from the kept Tucker form            */
+
 typedef struct rs_handle rs_handle; /* opaque, immutable after build */
 
 /* Build parameters.  Initialise with rs_params_default() and override fields. */
@@ -167,6 +171,10 @@ rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, i
  *   h     : a handle from rs_build_protein (not from rs_combine_proteins: no Tucker form)
  *   lo, hi: 3 cell indices each (host)
  *   rank  : R_Pi >= 0;   flags: RS_FLAG_* of the new handle
+ * With RS_FLAG_BOX_SCHEME_B in flags the box factors come from scheme (B) instead: the
+ * randomized RHOSVD (S5) of the long-range sum restricted to the box rows (the side matrices
+ * P_box A_l, the other modes' column norms over their box rows), its core (S6) and S7, from the
+ * parent's atoms, quadrature and split; any handle with atoms (combined ones too) qualifies.
  * Returns NULL on error (bad box, no Tucker form, RS_FLAG_F32_FACTORS with an uncompiled width,
  * no device unless RS_FLAG_HOST_ONLY, allocation or upload failure).  Release with rs_free.
  */

@@ -530,8 +530,12 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
       set_err("need 0 <= lo <= hi < n on every axis");
       return nullptr;
     }
-  if (h->tucker.G.empty()) {
+  if (h->tucker.G.empty() && !(flags & RS_FLAG_BOX_SCHEME_B)) {
     set_err("handle has no Tucker form (combined or restricted handles cannot be restricted)");
+    return nullptr;
+  }
+  if ((flags & RS_FLAG_BOX_SCHEME_B) && h->z.size() != (size_t)h->M) {
+    set_err("handle has no protein atoms");
     return nullptr;
   }
   const bool host_only = (flags & RS_FLAG_HOST_ONLY) != 0;
@@ -568,9 +572,19 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
     hd->f32 = (flags & RS_FLAG_F32_FACTORS) != 0;
     int lo_[3], hi_[3];
     for (int a = 0; a < 3; ++a) { lo_[a] = lo[a]; hi_[a] = hi[a]; hd->box_lo[a] = lo[a]; hd->box_hi[a] = hi[a]; }
-    hd->rep.tucker_err = h->rep.tucker_err;
-    hd->R = rs::restrict_to_box(h->n, h->tucker, lo_, hi_, rank, h->prm.eps_compress,
-                                h->prm.als_sweeps, hd->F, &hd->rep);
+    if (flags & RS_FLAG_BOX_SCHEME_B) {
+      // scheme (B): a new RHOSVD of the long-range sum restricted to the box rows
+      std::vector<double> tl, al;
+      for (size_t k = 0; k < h->quad.t.size(); ++k)
+        if (h->is_long[k]) { tl.push_back(h->quad.t[k]); al.push_back(h->quad.a[k]); }
+      rs::compress_long_range(h->n, h->h, h->cells, h->z, tl, al, rank, h->prm.eps_compress,
+                              h->prm.tucker_rank_max, h->prm.als_sweeps, h->prm.seed, hd->F,
+                              &hd->R, &hd->rep, nullptr, lo_, hi_);
+    } else {
+      hd->rep.tucker_err = h->rep.tucker_err;
+      hd->R = rs::restrict_to_box(h->n, h->tucker, lo_, hi_, rank, h->prm.eps_compress,
+                                  h->prm.als_sweeps, hd->F, &hd->rep);
+    }
     if (hd->R > (1 << 20)) { set_err("box CP width exceeds 2^20"); return nullptr; }
     if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
       set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +

@@ -64,7 +64,8 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
-                         TuckerRep* tk = nullptr);
+                         TuckerRep* tk = nullptr, const int* box_lo = nullptr,
+                         const int* box_hi = nullptr);
 
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
                       const std::vector<int32_t>& cells, double rho, double cell_edge,

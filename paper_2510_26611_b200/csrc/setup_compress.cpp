@@ -35,6 +35,7 @@ struct ConvOps {
   std::vector<std::vector<double>> G;     // G[k][d], d = 0..n-1 (even kernel)
   std::vector<std::vector<cplx>> FG;      // FFT of the centred kernel, size N
   std::vector<std::vector<double>> nrm;   // windowed column norms N_k(j)
+  std::vector<std::vector<double>> pre;   // prefix sums of G^2 over d = -(n-1)..(n-1)
 
   ConvOps(int n_, double h, const std::vector<double>& t_long) : n(n_), RL((int)t_long.size()) {
     N = 1;
@@ -43,6 +44,7 @@ struct ConvOps {
     G.assign(RL, std::vector<double>(n));
     FG.assign(RL, std::vector<cplx>(N));
     nrm.assign(RL, std::vector<double>(n));
+    pre.assign(RL, std::vector<double>(2 * n, 0.0));
 #pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < RL; ++k) {
       for (int d = 0; d < n; ++d) G[k][d] = cell_average(t_long[k], h, d);
@@ -51,17 +53,20 @@ struct ConvOps {
       for (int m = 0; m < 2 * n - 1; ++m) f[m] = G[k][std::abs(m - (n - 1))];
       fft.forward(f.data());
       // prefix sums of G^2 over d = -(n-1)..(n-1)
-      std::vector<double> pre(2 * n, 0.0);
+      std::vector<double>& pk = pre[k];
       for (int m = 0; m < 2 * n - 1; ++m) {
         double g = G[k][std::abs(m - (n - 1))];
-        pre[m + 1] = pre[m] + g * g;
+        pk[m + 1] = pk[m] + g * g;
       }
       // N_k(j)^2 = sum_{i=0}^{n-1} G[i-j]^2 = sum_{d=-j}^{n-1-j}; index m = d + n - 1
-      for (int j = 0; j < n; ++j) {
-        int m0 = -j + n - 1, m1 = (n - 1 - j) + n - 1;
-        nrm[k][j] = std::sqrt(std::max(0.0, pre[m1 + 1] - pre[m0]));
-      }
+      for (int j = 0; j < n; ++j) nrm[k][j] = wnorm(k, j, 0, n - 1);
     }
+  }
+
+  // sqrt(sum_{i=lo}^{hi} G[i-j]^2): the column norm over the rows of a box (scheme (B))
+  double wnorm(int k, int j, int lo, int hi) const {
+    const int m0 = lo - j + n - 1, m1 = hi - j + n - 1;
+    return std::sqrt(std::max(0.0, pre[k][m1 + 1] - pre[k][m0]));
   }
 
   // y_s = T_k x_s for the columns s of X (n x p column-major); Y likewise.
@@ -102,10 +107,20 @@ struct ModeBasis {
   double tail = 0;            // relative discarded energy sqrt(sum_{i>=r} s^2 / sum s^2)
 };
 
+// box (scheme (B), N3): the side matrix of this mode is restricted to the rows lo..hi of the
+// box (P_box A), and the other modes' column norms to their box rows; null = the whole grid.
 ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& cells,
                      const std::vector<double>& z, const std::vector<double>& a_long,
-                     int rank_R, double eps, int tucker_cap, uint64_t seed) {
+                     int rank_R, double eps, int tucker_cap, uint64_t seed,
+                     const int* box_lo = nullptr, const int* box_hi = nullptr) {
   const int n = ops.n, RL = ops.RL;
+  const int row_lo = box_lo ? box_lo[mode] : 0, row_hi = box_hi ? box_hi[mode] : n - 1;
+  auto clip_rows = [&](std::vector<double>& Y, int cols) {   // P_box
+    if (!box_lo) return;
+    for (int s_ = 0; s_ < cols; ++s_)
+      for (int i = 0; i < n; ++i)
+        if (i < row_lo || i > row_hi) Y[(size_t)s_ * n + i] = 0.0;
+  };
   const int64_t M = (int64_t)z.size();
   const int l1 = (mode + 1) % 3, l2 = (mode + 2) % 3;
   std::vector<std::vector<double>> c(RL, std::vector<double>(n, 0.0));
@@ -114,7 +129,11 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
     const int j = cells[3 * m + mode];
     occ[j] = 1;
     for (int k = 0; k < RL; ++k) {
-      double d = z[m] * a_long[k] * ops.nrm[k][cells[3 * m + l1]] * ops.nrm[k][cells[3 * m + l2]];
+      const double n1 = box_lo ? ops.wnorm(k, cells[3 * m + l1], box_lo[l1], box_hi[l1])
+                               : ops.nrm[k][cells[3 * m + l1]];
+      const double n2 = box_lo ? ops.wnorm(k, cells[3 * m + l2], box_lo[l2], box_hi[l2])
+                               : ops.nrm[k][cells[3 * m + l2]];
+      double d = z[m] * a_long[k] * n1 * n2;
       c[k][j] += d * d;
     }
   }
@@ -122,7 +141,7 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
   for (int j = 0; j < n; ++j)
     if (occ[j]) occj.push_back(j);
 
-  const int pmax = std::min(n, 512);
+  const int pmax = std::min(row_hi - row_lo + 1, 512);
   // the largest Tucker rank this build can keep; a fixed-width build starts its sketch at the
   // 2 r_cap + 16 columns that resolve it (one range-finder pass instead of a doubling sequence)
   const int r_cap = rank_R > 0 ? (tucker_cap > 0 ? std::max(rank_R, tucker_cap) : rank_R + 8)
@@ -152,7 +171,9 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       for (size_t i = 0; i < Y.size(); ++i) Y[i] += Yk[k][i];
       std::vector<double>().swap(Yk[k]);
     }
+    clip_rows(Y, p);
     orthonormalise(Y, n, p);
+    clip_rows(Y, p);
     // one power iteration: Y = sum_k T_k (c_k .* (T_k Q))
     {
       std::vector<double> Y2((size_t)n * p, 0.0);
@@ -173,7 +194,9 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
         std::vector<double>().swap(Yk[k]);
       }
       Y.swap(Y2);
+      clip_rows(Y, p);
       orthonormalise(Y, n, p);
+      clip_rows(Y, p);
     }
     // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :]; streaming QR.
     std::vector<double> Rt((size_t)p * p, 0.0);
@@ -243,7 +266,7 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
     }
     // resolved: the spectrum fell below the tolerance, or the sketch already oversamples the
     // largest rank this build can keep (r_cap) by r_cap + 16 columns (one power iteration)
-    const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax || p >= n ||
+    const bool resolved = sv[p - 1] <= 0.1 * eps * sv[0] || p >= pmax ||
                           p >= 2 * r_cap + 16;
     if (!resolved && r_tol >= p - 4) {
       p = std::min(pmax, 2 * p);
@@ -471,13 +494,13 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
-                         TuckerRep* tk) {
+                         TuckerRep* tk, const int* box_lo, const int* box_hi) {
   ConvOps ops(n, h, t_long);
   const int RL = ops.RL;
   const int64_t M = (int64_t)z.size();
   ModeBasis mb[3];
   for (int l = 0; l < 3; ++l)
-    mb[l] = mode_basis(ops, l, cells, z, a_long, rank_R, eps, tucker_cap, seed);
+    mb[l] = mode_basis(ops, l, cells, z, a_long, rank_R, eps, tucker_cap, seed, box_lo, box_hi);
   const int r0 = mb[0].r, r1 = mb[1].r, r2 = mb[2].r;
   for (int l = 0; l < 3; ++l) rep->tucker_r[l] = mb[l].r;
   if (std::getenv("RS_SETUP_TIMING")) std::fprintf(stderr, "[rs setup]   mode bases done at %.3f\n", std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
@@ -537,6 +560,11 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
         F[l][(size_t)i * R + q] = s;
       }
   }
+  if (box_lo)                           // scheme (B): the tensor says nothing outside the box
+    for (int l = 0; l < 3; ++l)
+      for (int i = 0; i < n; ++i)
+        if (i < box_lo[l] || i > box_hi[l])
+          for (int q = 0; q < R; ++q) F[l][(size_t)i * R + q] = std::numeric_limits<double>::quiet_NaN();
   *R_out = R;
 }
 

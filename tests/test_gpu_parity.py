@@ -578,8 +578,9 @@ def _box_cells(w, lo_x, hi_x):
     return lo, hi
 
 
-@pytest.mark.parametrize("R,f32", [(4, False), (8, False), (6, False), (8, True)])
-def test_restricted_box_parity(env, R, f32):
+@pytest.mark.parametrize("R,f32,scheme_b", [(4, False, False), (8, False, False), (6, False, False),
+                                            (8, True, False), (8, False, True), (4, True, True)])
+def test_restricted_box_parity(env, R, f32, scheme_b):
     """rs_restrict_box (reading A25): the kernel on the box handle matches the oracle on its
     exported tables; poses with an atom outside the box give NaN on both sides, their minimum
     distance still bitwise equal."""
@@ -589,7 +590,8 @@ def test_restricted_box_parity(env, R, f32):
     c = w.protein_xyz.mean(0) + np.array([12.0, 0.0, 0.0])
     rl = float(np.linalg.norm(w.ligand_xyz, axis=1).max())
     lo, hi = _box_cells(w, c - 2.0 - rl, c + 2.0 + rl)
-    box = parent.restrict_box(lo, hi, R, flags=rsdock.RS_FLAG_F32_FACTORS if f32 else 0)
+    box = parent.restrict_box(lo, hi, R, flags=(rsdock.RS_FLAG_F32_FACTORS if f32 else 0) |
+                              (rsdock.RS_FLAG_BOX_SCHEME_B if scheme_b else 0))
     poses = _site_poses(w, c, 3.0, 517, seed=R)
     Eg, Dg, inv = gpu_score(torch, rsdock, box, w, poses)
     Eo, Do, invo = rs_oracle.score_poses(box.export_tables(), w.protein_xyz, w.protein_q,

@@ -298,3 +298,48 @@ def test_restrict_box_accuracy_vs_uncompressed(oracle, rsd):
         assert eg > 5e-2 and eg > 50 * e[8], (eg, e)
         errs[tuple(lo)] = e
     assert len(errs) == 2
+
+
+def test_restrict_box_scheme_b_accuracy(oracle, rsd):
+    """Scheme (B) (RS_FLAG_BOX_SCHEME_B): a fresh RHOSVD + CP of the long-range
+    sum restricted to the box rows, from the ordinary fixed-width handle (no rich Tucker form
+    needed), reproduces the oracle's uncompressed sum in two C1 boxes to < 1e-3 at width 8
+    and < 1e-2 at width 4 (monotone in the width), where the global width-8 CP misses by > 5 %
+    and scheme (C) from that handle's own (rank R + 8) Tucker form by > 10x more; rows outside
+    the box are NaN, and a
+    combined (Eq. (23)) handle qualifies."""
+    w = syn.config_c1()
+    glob = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                       flags=rsd.RS_FLAG_HOST_ONLY)
+    st = glob.export_setup()
+    c = w.protein_xyz.mean(0)
+    rad = float(np.linalg.norm(w.protein_xyz - c, axis=1).max())
+    rng = np.random.default_rng(22)
+    for d in (np.array([1.0, 0.0, 0.0]), np.array([0.0, -0.6, 0.8])):
+        lo, hi = _site_box(oracle, w, c + (rad + 6.0) * d, 3.0)
+        pts = np.stack([rng.integers(lo[a], hi[a] + 1, 100) for a in range(3)], 1)
+        ref = _uncompressed_long(oracle, w, st, st["cells"], pts)
+        scale = np.max(np.abs(ref))
+
+        def err(p):
+            t = p.export_tables()
+            v = np.einsum("pk,pk,pk->p", t["F1"][pts[:, 0]], t["F2"][pts[:, 1]], t["F3"][pts[:, 2]])
+            return float(np.max(np.abs(v - ref)) / scale)
+
+        fl = rsd.RS_FLAG_HOST_ONLY | rsd.RS_FLAG_BOX_SCHEME_B
+        boxes = {R: glob.restrict_box(lo, hi, R, flags=fl) for R in (2, 4, 8)}
+        e = {R: err(b) for R, b in boxes.items()}
+        assert e[8] < 1e-3 and e[4] < 1e-2 and e[8] < e[4] < e[2], e
+        assert err(glob) > 5e-2
+        assert err(glob.restrict_box(lo, hi, 8, flags=rsd.RS_FLAG_HOST_ONLY)) > 10 * e[8]
+        t = boxes[8].export_tables()
+        for a, k in enumerate(("F1", "F2", "F3")):
+            inside = np.zeros(w.grid_n, bool)
+            inside[lo[a]:hi[a] + 1] = True
+            assert np.isfinite(t[k][inside]).all() and np.isnan(t[k][~inside]).all()
+    (XA, qA), (XB, qB) = syn.complex_parts(syn.complex_small(seed=2))
+    kw = dict(grid_n=64, rank_R=4, sigma_split=1.0, sigma_vdw=1.0, dmin_cap=1.5,
+              flags=rsd.RS_FLAG_HOST_ONLY)
+    C = rsd.Protein.combine([rsd.Protein(qA, XA, 8.0, **kw), rsd.Protein(qB, XB, 8.0, **kw)],
+                           flags=rsd.RS_FLAG_HOST_ONLY)
+    assert C.restrict_box([20, 20, 20], [40, 40, 40], 4, flags=fl).info["R"] == 4
