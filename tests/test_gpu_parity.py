@@ -638,3 +638,39 @@ def test_shards_concatenate_bitwise(env):
         assert np.array_equal(np.concatenate([p[0] for p in parts]), E, equal_nan=True)
         assert np.array_equal(np.concatenate([p[1] for p in parts]), D, equal_nan=True)
         assert sum(p[2] for p in parts) == inv
+
+
+# ----------------------------------------------------------------------------- maximum sizes
+
+def test_max_grid_no_memo_no_window(env):
+    """n = 32768 (the largest grid; cells need all 15 bits of the packed entries), h = 1/256 A:
+    n_sigma = 256, so the dense short-range memo would exceed its budget and every O5 value
+    runs the explicit chain; a translation's rows exceed shared memory, so H4 reads L2."""
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=90, M=60, L=12, n=32768, b=64.0, R=8, P=200, protein_radius=4.0,
+                         trans=3.0)
+    prot = build(rsdock, w)
+    assert prot.info["n_sigma"] == 256
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_large_ligand_beyond_smem_staging(env):
+    """L = 300 ligand atoms (more than the 256 a windowed launch stages in shared memory: the
+    rest read L2) with the whole factor set in the window; R = 16 and a runtime width."""
+    torch, rsdock, rs_oracle = env
+    import dataclasses
+    rng = np.random.default_rng(5)
+    Y = syn.ligand_body(rng, 300)
+    Y = Y - Y.mean(0)
+    for R in (16, 10):
+        w = syn.random_small(seed=91, M=40, L=7, n=64, b=12.0, R=R, P=150, trans=2.0)
+        w = dataclasses.replace(w, ligand_xyz=Y, ligand_q=rng.uniform(-1, 1, 300))
+        prot = build(rsdock, w)
+        Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+        Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
+        compare(Eg, Dg, Eo, Do, inv, invo)
+        Fg, ig = gpu_forces(torch, prot, w, w.poses)
+        Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, w.poses)
+        compare_forces(Fg, Fo, ig, io)
