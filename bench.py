@@ -435,9 +435,23 @@ def main():
             tt = torch.tensor([te], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
+        # the pinned host-to-device copy rate of this box (the pose upload bounds e2e)
+        dbuf = torch.empty_like(hp, device=dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hts = []
+        for _ in range(3):
+            ev0.record()
+            dbuf.copy_(hp, non_blocking=True)
+            ev1.record()
+            torch.cuda.synchronize()
+            hts.append(ev0.elapsed_time(ev1) * 1e-3)
+        h2d_gbs = hp.numel() * 8 / min(hts) / 1e9
+        del dbuf
         e2e = {"value": world * P / te, "unit": "poses/s",
                "h2d_bytes_per_step": int(P * 7 * 8 + L * 4 * 8), "d2h_bytes_per_step": int(P * 2 * 8),
-               "path": "rs_score_poses, pinned host buffers, 2-stream chunked H2D/kernel/D2H"}
+               "h2d_pinned_gbs": h2d_gbs,
+               "upload_bound_poses_per_s": world * h2d_gbs * 1e9 / 56.0,
+               "path": "rs_score_poses, pinned host buffers, 3-stream chunked H2D/kernel/D2H"}
 
     if rank != 0:
         if dist:

@@ -762,7 +762,7 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   const bool e_dev = pointer_kind(energies_out) == 1;
   const bool d_dev = pointer_kind(mindist_out) == 1;
   // pipeline over kStreams streams: H2D(chunk) -> kernel -> D2H(chunk), chunk sizes growing
-  // geometrically (x1.5 from ~P/64), so the first copy exposes little and the later copies hide
+  // geometrically (x1.5 from ~P/16), so the first copy exposes little and the later copies hide
   // behind the kernels of the earlier chunks; every chunk has its own staging region, and the
   // kernels of different chunks may overlap on the device
   constexpr int kStreams = 3;
@@ -807,7 +807,10 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   a.L = n_lig;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
   int chunk = 0;
-  int64_t csz = std::min<int64_t>(P, std::max<int64_t>(4096, P / 64));
+  // first chunk P/16 (measured at C3 on pinned host buffers: P/64 2.185 ms, P/16 2.147 ms; the
+  // rest of the gap to the 1.69 ms device-resident launch is the ramp and tail of each chunk's
+  // launch: the same chunking on device buffers takes 1.93-2.04 ms, one launch 1.72 ms)
+  int64_t csz = std::min<int64_t>(P, std::max<int64_t>(4096, P / 16));
   for (int64_t off = 0; off < P; off += csz, csz = csz + csz / 2, ++chunk) {
     const int64_t cnt = std::min(csz, P - off);
     const int s = chunk % kStreams;
