@@ -1,5 +1,6 @@
 // C ABI of librsdock (include/rs_dock.h): handle build (Algorithm TEP, host C++), upload,
 // and the scoring entry points that enqueue the fused sm_100a kernel (score_kernel.cu).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,6 +34,24 @@ void set_err(const std::string& s) { g_err = s; }
       return code;                                                                         \
     }                                                                                      \
   } while (0)
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link); null if the
+// driver does not offer it (the host-buffer pipeline then falls back to per-chunk launches)
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32 wait_value32() {
+  static PFN_waitValue32 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_waitValue32)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
 
 bool finite_all(const double* p, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
@@ -70,6 +89,8 @@ void free_device(rs_handle* h) {
   }
   if (h->stage) cudaFree(h->stage);
   h->stage = nullptr;
+  if (h->h_ones) cudaFreeHost(h->h_ones);
+  h->h_ones = nullptr;
   for (void*& s : h->streams) {
     if (s) cudaStreamDestroy((cudaStream_t)s);
     s = nullptr;
@@ -766,10 +787,12 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   // behind the kernels of the earlier chunks; every chunk has its own staging region, and the
   // kernels of different chunks may overlap on the device
   constexpr int kStreams = 3;
-  const size_t lig_b = (size_t)4 * std::max<int64_t>(n_lig, 1) * sizeof(double);
+  // 256-byte aligned sections (the streamed pipeline relies on 128-byte aligned pose chunks)
+  const size_t lig_b = ((size_t)4 * std::max<int64_t>(n_lig, 1) * sizeof(double) + 255) / 256 * 256;
   const size_t pose_b = pose_dev ? 0 : (size_t)P * 7 * sizeof(double);
   const size_t out_b = (size_t)P * sizeof(double);
-  const size_t need = lig_b + pose_b + (e_dev ? 0 : out_b) + (d_dev ? 0 : out_b) + 64 * kStreams;
+  const size_t need = lig_b + pose_b + (e_dev ? 0 : out_b) + (d_dev ? 0 : out_b) + 64 * kStreams +
+                      4096;   // + streamed-pipeline flags, counters and chunk bounds
   if (h->stage_bytes < need) {
     if (h->stage) cudaFree(h->stage);
     h->stage = nullptr;
@@ -806,6 +829,102 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   a.yl = yl;
   a.L = n_lig;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
+  static const bool streamed_off = std::getenv("RS_NO_STREAMED") != nullptr;
+  if (!pose_dev && !e_dev && !d_dev && P >= 65536 && wait_value32() && !streamed_off) {
+    // Streamed pipeline: ONE launch over all P poses on stream 0 while stream 1 copies the
+    // poses in geometrically growing chunks, each followed by its arrival flag; the kernel
+    // waits for a chunk's flag before it scores poses from it and counts finished poses per
+    // chunk; stream 2 waits for each chunk's count (cuStreamWaitValue32) and copies its
+    // energies and distances back.  No per-chunk launch ramp or tail.
+    constexpr int kMaxCb = 64;
+    long long cb[kMaxCb + 1];
+    int n_cb = 0;
+    cb[0] = 0;
+    // sizes grow x1.5 over the first half and mirror over the second (the middle never more
+    // than 1.5x its neighbours), so the last result copy, exposed after the kernel, is small
+    std::vector<int64_t> up;
+    int64_t tot = 0;
+    // first chunk P/16 (C3, all-host call: P/128 2.01 ms, P/32 1.99, P/16 1.95, P/8 2.00): the
+    // kernel's 148 CTAs hold ~150K claimed poses at a time, so early chunks must not be tiny
+    for (int64_t sz = std::max<int64_t>(4096, P / 16); 2 * (tot + sz) <= P && (int)up.size() < kMaxCb / 2 - 2;
+         sz += sz / 2) {
+      up.push_back(sz);
+      tot += sz;
+    }
+    std::vector<int64_t> sizes(up);
+    const int64_t mid = P - 2 * tot;               // never more than 1.5x its neighbours
+    if (mid > 0 && !up.empty() && mid > up.back() + up.back() / 2) {
+      sizes.push_back(mid / 2);
+      sizes.push_back(mid - mid / 2);
+    } else if (mid > 0) {
+      sizes.push_back(mid);
+    }
+    sizes.insert(sizes.end(), up.rbegin(), up.rend());
+    for (int64_t sz : sizes) {
+      int64_t e = cb[n_cb] + sz;
+      e = (e + 15) / 16 * 16;                                      // 16 poses = 7 x 128 bytes
+      if (e >= P || n_cb + 1 == kMaxCb) e = P;
+      if (e <= cb[n_cb]) continue;
+      cb[++n_cb] = e;
+      if (e == P) break;
+    }
+    if (cb[n_cb] < P) cb[++n_cb] = P;
+    unsigned* d_arrive = (unsigned*)(d_cnt + kStreams);
+    unsigned* d_done = d_arrive + kMaxCb;
+    unsigned* d_stall = d_done + kMaxCb;
+    long long* d_cb = (long long*)(d_stall + 2);
+    if (!h->h_ones) {
+      CUDA_TRY(cudaMallocHost((void**)&h->h_ones, kMaxCb * sizeof(unsigned)), RS_E_NOMEM);
+      for (int i = 0; i < kMaxCb; ++i) h->h_ones[i] = 1u;
+    }
+    CUDA_TRY(cudaMemsetAsync(d_arrive, 0, (2 * kMaxCb + 2) * sizeof(unsigned), st[0]), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpyAsync(d_cb, cb, (n_cb + 1) * sizeof(long long), cudaMemcpyHostToDevice, st[0]), RS_E_CUDA);
+    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
+    CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st[0]), RS_E_CUDA);
+    cudaEvent_t armed;
+    CUDA_TRY(cudaEventCreateWithFlags(&armed, cudaEventDisableTiming), RS_E_CUDA);
+    CUDA_TRY(cudaEventRecord(armed, st[0]), RS_E_CUDA);
+    CUDA_TRY(cudaStreamWaitEvent(st[1], armed, 0), RS_E_CUDA);
+    CUDA_TRY(cudaStreamWaitEvent(st[2], armed, 0), RS_E_CUDA);
+    cudaEventDestroy(armed);
+    for (int i = 0; i < n_cb; ++i) {
+      CUDA_TRY(cudaMemcpyAsync(d_pose + 7 * cb[i], poses + 7 * cb[i], (cb[i + 1] - cb[i]) * 7 * sizeof(double),
+                               cudaMemcpyHostToDevice, st[1]), RS_E_CUDA);
+      CUDA_TRY(cudaMemcpyAsync(d_arrive + i, h->h_ones + i, sizeof(unsigned), cudaMemcpyHostToDevice, st[1]), RS_E_CUDA);
+    }
+    a.poses = d_pose;
+    a.P = P;
+    a.E = d_E;
+    a.D = d_D;
+    a.invalid = d_cnt;
+    a.arrive = d_arrive;
+    a.done = d_done;
+    a.cb = d_cb;
+    a.n_cb = n_cb;
+    a.stall = d_stall;
+    int e = rs::launch_score(a, st[0], h->device, nullptr);
+    if (e != 0) {
+      set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
+      return RS_E_CUDA;
+    }
+    PFN_waitValue32 wv = wait_value32();
+    for (int i = 0; i < n_cb; ++i) {
+      const int64_t off = cb[i], cnt = cb[i + 1] - cb[i];
+      if (wv((CUstream)st[2], (CUdeviceptr)(d_done + i), (cuuint32_t)cnt, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+        set_err("cuStreamWaitValue32 failed");
+        return RS_E_CUDA;
+      }
+      CUDA_TRY(cudaMemcpyAsync(energies_out + off, d_E + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, st[2]), RS_E_CUDA);
+      CUDA_TRY(cudaMemcpyAsync(mindist_out + off, d_D + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, st[2]), RS_E_CUDA);
+    }
+    for (int i = 0; i < kStreams; ++i) CUDA_TRY(cudaStreamSynchronize(st[i]), RS_E_CUDA);
+    unsigned long long cnt0 = 0;
+    unsigned stall = 0;
+    CUDA_TRY(cudaMemcpy(&cnt0, d_cnt, sizeof(cnt0), cudaMemcpyDeviceToHost), RS_E_CUDA);
+    CUDA_TRY(cudaMemcpy(&stall, d_stall, sizeof(stall), cudaMemcpyDeviceToHost), RS_E_CUDA);
+    if (stall) { set_err("streamed pipeline: a pose chunk never arrived"); return RS_E_CUDA; }
+    return (int64_t)cnt0;
+  }
   int chunk = 0;
   // first chunk P/16 (measured at C3 on pinned host buffers: P/64 2.185 ms, P/16 2.147 ms; the
   // rest of the gap to the 1.69 ms device-resident launch is the ramp and tail of each chunk's

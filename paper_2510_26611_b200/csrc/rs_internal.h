@@ -109,6 +109,13 @@ struct ScoreArgs {               // one launch of the scoring kernel
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
   int f32;                       // long-range part from the binary32 factors (A21)
+  // streamed launch (host-buffer pipeline): poses arrive in copy chunks [cb[i], cb[i+1]);
+  // arrive[i] != 0 once chunk i landed; the kernel adds finished poses to done[i].  Null: off.
+  const unsigned* arrive = nullptr;
+  unsigned* done = nullptr;
+  const long long* cb = nullptr;
+  int n_cb = 0;
+  unsigned* stall = nullptr;     // set to 1 if an arrival wait timed out
 };
 
 // Fill the dense short-range memo table s(d0,d1,d2), d_a = 0..n_sigma, with the O5 chain.
@@ -181,6 +188,7 @@ struct rs_handle {
   void* stage = nullptr;
   size_t stage_bytes = 0;
   void* streams[3] = {nullptr, nullptr, nullptr};
+  unsigned* h_ones = nullptr;          // pinned 1s: arrival flags written by the copy stream
   // cached ligand radius for device-resident ligands (only steers the launch shape)
   const void* rmax_key = nullptr;
   int64_t rmax_L = -1;

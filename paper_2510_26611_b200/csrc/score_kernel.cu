@@ -810,6 +810,23 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     if (c0 >= a.P) break;
     const int64_t csz = s_chunk < nbig ? cp.big : cp.tail;
     const int64_t p_end = c0 + csz < a.P ? c0 + csz : a.P;
+    if (a.arrive) {
+      // streamed launch: wait until the copy chunk holding the work chunk's last pose landed
+      // (copies land in order); chunk boundaries are 128-byte aligned in the pose array, so no
+      // cache line mixes landed and pending poses
+      if (tid == 0) {
+        int c = 0;
+        while (c + 1 < a.n_cb && a.cb[c + 1] <= p_end - 1) ++c;
+        unsigned v = 0;
+        for (long long spin = 0;; ++spin) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.arrive + c) : "memory");
+          if (v != 0) break;
+          if (spin > (1ll << 26)) { atomicExch(a.stall, 1u); break; }
+          __nanosleep(256);
+        }
+      }
+      __syncthreads();
+    }
     int64_t p = c0;
     while (p < p_end) {
       int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
@@ -952,6 +969,22 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         const double2 o = s_out[tid];
         a.E[p + tid] = o.x;
         a.D[p + tid] = isnan(o.y) ? NAN : (o.y < a.dcap2 ? __dsqrt_rn(o.y) : INFINITY);
+      }
+      if (a.done) {
+        // release the tile's outputs to the copy stream that waits on done[chunk]
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          int c = 0;
+          while (c + 1 < a.n_cb && a.cb[c + 1] <= p) ++c;
+          int64_t q = p;
+          while (q < p + T) {
+            const int64_t e = min((int64_t)a.cb[c + 1], p + (int64_t)T);
+            atomicAdd(a.done + c, (unsigned)(e - q));
+            q = e;
+            ++c;
+          }
+        }
       }
       p += T;
     }

@@ -674,3 +674,24 @@ def test_large_ligand_beyond_smem_staging(env):
         Fg, ig = gpu_forces(torch, prot, w, w.poses)
         Fo, io = rs_oracle.score_forces(prot.export_tables(), w.ligand_xyz, w.ligand_q, w.poses)
         compare_forces(Fg, Fo, ig, io)
+
+
+@pytest.mark.parametrize("name,k", [("C2", None), ("C3", 300000)])
+def test_streamed_host_pipeline_bitwise(env, name, k):
+    """rs_score_poses on pinned host buffers (P >= 65536: one launch that waits for each pose
+    chunk's arrival flag while the copies land, per-chunk completion counters releasing the
+    result copies) returns exactly the device-resident launch's outputs."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    poses = w.poses if k is None else np.ascontiguousarray(w.poses[:k])
+    prot = build(rsdock, w)
+    Ed, Dd, invd = gpu_score(torch, rsdock, prot, w, poses, async_api=True)
+    hp = torch.from_numpy(poses).pin_memory()
+    hE = torch.empty(len(poses), dtype=torch.float64).pin_memory()
+    hD = torch.empty(len(poses), dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        hE.fill_(0.0)
+        inv = rsdock.rs_score_poses(prot.handle, w.ligand_q, w.ligand_xyz, w.L, hp, len(poses), hE, hD)
+        assert inv == invd
+        assert np.array_equal(hE.numpy(), Ed, equal_nan=True)
+        assert np.array_equal(hD.numpy(), Dd, equal_nan=True)
