@@ -451,7 +451,7 @@ def main():
                "h2d_bytes_per_step": int(P * 7 * 8 + L * 4 * 8), "d2h_bytes_per_step": int(P * 2 * 8),
                "h2d_pinned_gbs": h2d_gbs,
                "upload_bound_poses_per_s": world * h2d_gbs * 1e9 / 56.0,
-               "path": "rs_score_poses, pinned host buffers, 3-stream chunked H2D/kernel/D2H"}
+               "path": "rs_score_poses, pinned host buffers: one launch streaming behind chunked H2D (arrival flags), per-chunk D2H released by completion counters"}
 
     if rank != 0:
         if dist:
