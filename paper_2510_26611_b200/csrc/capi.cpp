@@ -830,7 +830,9 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   a.L = n_lig;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
   static const bool streamed_off = std::getenv("RS_NO_STREAMED") != nullptr;
-  if (!pose_dev && !e_dev && !d_dev && P >= 65536 && wait_value32() && !streamed_off) {
+  // streamed only for large batches: below ~4e5 poses (C2: 1e5) the per-chunk stream waits cost
+  // more than the launch ramps they save (measured: C2 all-host 0.40 ms streamed, 0.36 chunked)
+  if (!pose_dev && !e_dev && !d_dev && P >= 400000 && wait_value32() && !streamed_off) {
     // Streamed pipeline: ONE launch over all P poses on stream 0 while stream 1 copies the
     // poses in geometrically growing chunks, each followed by its arrival flag; the kernel
     // waits for a chunk's flag before it scores poses from it and counts finished poses per
