@@ -696,3 +696,7 @@ def test_streamed_host_pipeline_bitwise(env, name, k):
         assert inv == invd
         assert np.array_equal(hE.numpy(), Ed, equal_nan=True)
         assert np.array_equal(hD.numpy(), Dd, equal_nan=True)
+    # pageable numpy buffers take the same path (copies staged by the driver)
+    Eh, Dh, invh = prot.score(w.ligand_q, w.ligand_xyz, poses)
+    assert invh == invd and np.array_equal(Eh, Ed, equal_nan=True)
+    assert np.array_equal(Dh, Dd, equal_nan=True)
