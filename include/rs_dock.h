@@ -190,7 +190,10 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
  *   mindist_out (P)                    : min_{l,m} |x'_l - x_m| if < dmin_cap, else +inf
  * Pointers may be host (pageable or pinned) or device memory of the handle's device; each
  * is detected with cudaPointerGetAttributes.  Host data are copied in and out inside the
- * call.  A pose with a zero quaternion, a non-finite value, or any transformed atom outside
+ * call, pipelined: with host poses and outputs and P >= 4e5 one kernel launch scores each
+ * pose chunk as soon as its copy lands and each chunk's results are copied back as soon as
+ * they are final; otherwise chunks are copied and launched in turn on three
+ * streams.  The outputs never depend on the path.  A pose with a zero quaternion, a non-finite value, or any transformed atom outside
  * [-b, b]^3 is invalid: both outputs are NaN.
  * Returns the number of invalid poses (>= 0) or a negative RS_E_* code.
  */

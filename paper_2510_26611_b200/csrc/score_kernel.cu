@@ -330,13 +330,23 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
   if constexpr (G::NS == 1) {
     s[0] = quad_prod(__ldg(r0), __ldg(r1), __ldg(r2));
   } else {
-    // 32-byte loads: two quads per lane and request
+    // 32-byte loads: two quads per lane and request, only the CH quads that hold ranks (the
+    // zero padding up to NS quads contributes s_c = +0 exactly, so it is not read: R = 24
+    // reads 96 of the row's 128 bytes)
 #pragma unroll
     for (int c = 0; c < G::NS; c += 2) {
-      float4 a1, b1, c1;
-      const float4 a0 = ldg256x2(r0 + c, a1), b0 = ldg256x2(r1 + c, b1), c0 = ldg256x2(r2 + c, c1);
-      s[c] = quad_prod(a0, b0, c0);
-      s[c + 1] = quad_prod(a1, b1, c1);
+      if (c + 1 < G::CH) {
+        float4 a1, b1, c1;
+        const float4 a0 = ldg256x2(r0 + c, a1), b0 = ldg256x2(r1 + c, b1), c0 = ldg256x2(r2 + c, c1);
+        s[c] = quad_prod(a0, b0, c0);
+        s[c + 1] = quad_prod(a1, b1, c1);
+      } else if (c < G::CH) {
+        s[c] = quad_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
+        s[c + 1] = 0.0f;
+      } else {
+        s[c] = 0.0f;
+        s[c + 1] = 0.0f;
+      }
     }
   }
 #pragma unroll

@@ -700,3 +700,17 @@ def test_streamed_host_pipeline_bitwise(env, name, k):
     Eh, Dh, invh = prot.score(w.ligand_q, w.ligand_xyz, poses)
     assert invh == invd and np.array_equal(Eh, Ed, equal_nan=True)
     assert np.array_equal(Dh, Dd, equal_nan=True)
+
+
+@pytest.mark.parametrize("R", [12, 24, 16])
+def test_f32_no_window_l2_path(env, R):
+    """The fp32-factor variant without a window (n = 8192, h = 1/256 A: a translation's rows
+    exceed shared memory): H4 reads the binary32 rows from L2, only the quads that hold ranks
+    (R = 12, 24 pad to 4, 8 quads) -- against the O4-f32 oracle."""
+    torch, rsdock, rs_oracle = env
+    w = syn.random_small(seed=95 + R, M=50, L=10, n=8192, b=16.0, R=R, P=300, trans=3.0)
+    prot = build(rsdock, w, flags=rsdock.RS_FLAG_F32_FACTORS)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eo, Do, invo = rs_oracle.score_poses(prot.export_tables(), w.protein_xyz, w.protein_q,
+                                         w.ligand_xyz, w.ligand_q, w.poses, w.dmin_cap, f32=True)
+    compare(Eg, Dg, Eo, Do, inv, invo)
