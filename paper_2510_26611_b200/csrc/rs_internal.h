@@ -48,6 +48,21 @@ struct TuckerRep {           // the long-range part in Tucker format (S5-S6), ke
   std::vector<double> G;     // r0 x r1 x r2, row-major
 };
 
+// S6 on the device (setup_device.cu): accumulates the Tucker core term by term, bitwise equal to
+// the host loop.  ok() is false when the device could not be used (the host loop runs then).
+class CoreDevice {
+ public:
+  CoreDevice(int device, int n, const int* r, const std::vector<int32_t>& cells,
+             const std::vector<double>& z);
+  ~CoreDevice();
+  bool ok() const;
+  bool add_term(double a_k, const std::vector<double> H[3]);   // H_l: n x r_l row-major
+  bool fetch(std::vector<double>& G);
+ private:
+  struct Impl;
+  Impl* p;
+};
+
 // S7: Tucker core -> CP of width rank_R (0: eps mode); returns R
 int core_to_cp(const std::vector<double>& G, int r0, int r1, int r2, int rank_R, double eps,
                int als_sweeps, std::vector<double>& A, std::vector<double>& B,
@@ -65,7 +80,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
                          TuckerRep* tk = nullptr, const int* box_lo = nullptr,
-                         const int* box_hi = nullptr);
+                         const int* box_hi = nullptr, int device = -1);
 
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
                       const std::vector<int32_t>& cells, double rho, double cell_edge,

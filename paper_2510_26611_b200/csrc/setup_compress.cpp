@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -494,7 +495,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
-                         TuckerRep* tk, const int* box_lo, const int* box_hi) {
+                         TuckerRep* tk, const int* box_lo, const int* box_hi, int device) {
   ConvOps ops(n, h, t_long);
   const int RL = ops.RL;
   const int64_t M = (int64_t)z.size();
@@ -509,6 +510,13 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
 
   // S6: core G = sum_k sum_m z_m a_k (U_0^T g_k[.-c_m0]) o (U_1^T ...) o (U_2^T ...)
   std::vector<double> G((size_t)r0 * r1 * r2, 0.0);
+  // on the device when the build has one (bitwise the same core, setup_device.cu)
+  const int rr_[3] = {r0, r1, r2};
+  std::unique_ptr<CoreDevice> cdev;
+  if (device >= 0 && (double)M * r0 * r1 * r2 * RL > 1e8) {
+    cdev.reset(new CoreDevice(device, n, rr_, cells, z));
+    if (!cdev->ok()) cdev.reset();
+  }
   for (int k = 0; k < RL; ++k) {
     std::vector<double> H[3];   // row-major n x r_l
     for (int l = 0; l < 3; ++l) {
@@ -518,6 +526,14 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       H[l].assign((size_t)n * r, 0.0);
       for (int a = 0; a < r; ++a)
         for (int i = 0; i < n; ++i) H[l][(size_t)i * r + a] = tmp[(size_t)a * n + i];
+    }
+    if (cdev) {
+      if (cdev->add_term(a_long[k], H)) continue;
+      // the device failed mid-way: redo the core on the host from scratch
+      cdev.reset();
+      std::fill(G.begin(), G.end(), 0.0);
+      k = -1;
+      continue;
     }
 #pragma omp parallel for schedule(dynamic)
     for (int a = 0; a < r0; ++a) {
@@ -535,6 +551,38 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       }
       double* g = &G[(size_t)a * r1 * r2];
       for (size_t i = 0; i < row.size(); ++i) g[i] += row[i];
+    }
+  }
+  if (cdev && !cdev->fetch(G)) {
+    // could not read the device core back: the host loop (rare; keeps the build working)
+    cdev.reset();
+    std::fill(G.begin(), G.end(), 0.0);
+    for (int k = 0; k < RL; ++k) {
+      std::vector<double> H[3];
+      for (int l = 0; l < 3; ++l) {
+        const int r = mb[l].r;
+        std::vector<double> tmp((size_t)n * r);
+        ops.apply_one(k, mb[l].U.data(), tmp.data(), r);
+        H[l].assign((size_t)n * r, 0.0);
+        for (int a = 0; a < r; ++a)
+          for (int i = 0; i < n; ++i) H[l][(size_t)i * r + a] = tmp[(size_t)a * n + i];
+      }
+      for (int a = 0; a < r0; ++a) {
+        std::vector<double> row((size_t)r1 * r2, 0.0);
+        for (int64_t m = 0; m < M; ++m) {
+          const double w = z[m] * a_long[k] * H[0][(size_t)cells[3 * m] * r0 + a];
+          if (w == 0.0) continue;
+          const double* h1 = &H[1][(size_t)cells[3 * m + 1] * r1];
+          const double* h2 = &H[2][(size_t)cells[3 * m + 2] * r2];
+          for (int b = 0; b < r1; ++b) {
+            const double wb = w * h1[b];
+            double* dst = &row[(size_t)b * r2];
+            for (int c = 0; c < r2; ++c) dst[c] += wb * h2[c];
+          }
+        }
+        double* g = &G[(size_t)a * r1 * r2];
+        for (size_t i = 0; i < row.size(); ++i) g[i] += row[i];
+      }
     }
   }
   if (std::getenv("RS_SETUP_TIMING")) std::fprintf(stderr, "[rs setup]   core done at %.3f\n", std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());

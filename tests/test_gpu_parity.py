@@ -714,3 +714,18 @@ def test_f32_no_window_l2_path(env, R):
     Eo, Do, invo = rs_oracle.score_poses(prot.export_tables(), w.protein_xyz, w.protein_q,
                                          w.ligand_xyz, w.ligand_q, w.poses, w.dmin_cap, f32=True)
     compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_device_core_setup_bitwise(env, name):
+    """S6 on the device (setup_device.cu, N4 part): a handle built with a device forms the Tucker
+    core there with the host loop's exact op sequence, so its exported tables are bitwise the
+    host-only build's."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    dev = build(rsdock, w)
+    host = build(rsdock, w, flags=rsdock.RS_FLAG_HOST_ONLY)
+    td, th = dev.export_tables(), host.export_tables()
+    for k in ("F1", "F2", "F3", "S1", "S2", "S3"):
+        assert np.array_equal(td[k], th[k]), k
+    assert dev.info["cp_core_err"] == host.info["cp_core_err"]
