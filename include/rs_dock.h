@@ -62,6 +62,10 @@ extern "C" {
                                   long-range sum restricted to the box,
                                   instead of scheme (C) from the kept Tucker form            */
 
+#define RS_FLAG_DEVICE_FFT 8u  /* setup: the RHOSVD and core convolutions (S5-S6) with cuFFT on
+                                  the device (tables then differ from a host-only build by
+                                  rounding; without it a device build is bitwise host-equal) */
+
 typedef struct rs_handle rs_handle; /* opaque, immutable after build */
 
 /* Build parameters.  Initialise with rs_params_default() and override fields. */

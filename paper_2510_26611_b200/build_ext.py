@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         out, _ = p.communicate()
         if p.returncode != 0:
             raise RuntimeError("build failed: " + " ".join(cmd) + "\n" + out.decode())
-    link = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
+    link = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fopenmp", "-lgomp",
+            "-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     subprocess.check_call(link)
     return lib
 

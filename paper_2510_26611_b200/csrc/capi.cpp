@@ -380,7 +380,8 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     // S5-S7
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
                             prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep,
-                            &hd->tucker, nullptr, nullptr, host_only ? -1 : prm.device);
+                            &hd->tucker, nullptr, nullptr, host_only ? -1 : prm.device,
+                            (prm.flags & RS_FLAG_DEVICE_FFT) != 0);
     hd->f32 = (prm.flags & RS_FLAG_F32_FACTORS) != 0;
     if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
       set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
@@ -600,7 +601,8 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
         if (h->is_long[k]) { tl.push_back(h->quad.t[k]); al.push_back(h->quad.a[k]); }
       rs::compress_long_range(h->n, h->h, h->cells, h->z, tl, al, rank, h->prm.eps_compress,
                               h->prm.tucker_rank_max, h->prm.als_sweeps, h->prm.seed, hd->F,
-                              &hd->R, &hd->rep, nullptr, lo_, hi_, host_only ? -1 : hd->device);
+                              &hd->R, &hd->rep, nullptr, lo_, hi_, host_only ? -1 : hd->device,
+                              (flags & RS_FLAG_DEVICE_FFT) != 0);
     } else {
       hd->rep.tucker_err = h->rep.tucker_err;
       hd->R = rs::restrict_to_box(h->n, h->tucker, lo_, hi_, rank, h->prm.eps_compress,

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <atomic>
+#include <complex>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -63,6 +64,20 @@ class CoreDevice {
   Impl* p;
 };
 
+// Opt-in (RS_FLAG_DEVICE_FFT): the setup's convolutions y_s = T_k x_s on the device with cuFFT
+// (the same FFT-domain product as ConvOps::apply_one; tables then differ from the host-only
+// build by rounding).  apply() is serialised internally.
+class DeviceConv {
+ public:
+  DeviceConv(int device, int n, int N, const std::vector<std::vector<std::complex<double>>>& FG);
+  ~DeviceConv();
+  bool ok() const;
+  bool apply(int k, const double* X, double* Y, int cols);   // X, Y: n x cols column-major
+ private:
+  struct Impl;
+  Impl* p;
+};
+
 // S7: Tucker core -> CP of width rank_R (0: eps mode); returns R
 int core_to_cp(const std::vector<double>& G, int r0, int r1, int r2, int rank_R, double eps,
                int als_sweeps, std::vector<double>& A, std::vector<double>& B,
@@ -80,7 +95,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
                          TuckerRep* tk = nullptr, const int* box_lo = nullptr,
-                         const int* box_hi = nullptr, int device = -1);
+                         const int* box_hi = nullptr, int device = -1, bool device_fft = false);
 
 void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
                       const std::vector<int32_t>& cells, double rho, double cell_edge,

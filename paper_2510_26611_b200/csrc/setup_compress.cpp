@@ -37,6 +37,7 @@ struct ConvOps {
   std::vector<std::vector<cplx>> FG;      // FFT of the centred kernel, size N
   std::vector<std::vector<double>> nrm;   // windowed column norms N_k(j)
   std::vector<std::vector<double>> pre;   // prefix sums of G^2 over d = -(n-1)..(n-1)
+  DeviceConv* dev = nullptr;              // RS_FLAG_DEVICE_FFT: convolutions on the device
 
   ConvOps(int n_, double h, const std::vector<double>& t_long) : n(n_), RL((int)t_long.size()) {
     N = 1;
@@ -72,6 +73,7 @@ struct ConvOps {
 
   // y_s = T_k x_s for the columns s of X (n x p column-major); Y likewise.
   void apply_one(int k, const double* X, double* Y, int p) const {
+    if (dev && dev->apply(k, X, Y, p)) return;
     std::vector<cplx> buf(N);
     for (int s = 0; s < p; s += 2) {
       std::fill(buf.begin(), buf.end(), cplx(0, 0));
@@ -495,8 +497,14 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
                          const std::vector<double>& a_long, int rank_R, double eps,
                          int tucker_cap, int als_sweeps, uint64_t seed,
                          std::vector<double> F[3], int* R_out, SetupReport* rep,
-                         TuckerRep* tk, const int* box_lo, const int* box_hi, int device) {
+                         TuckerRep* tk, const int* box_lo, const int* box_hi, int device,
+                         bool device_fft) {
   ConvOps ops(n, h, t_long);
+  std::unique_ptr<DeviceConv> dconv;
+  if (device >= 0 && device_fft) {
+    dconv.reset(new DeviceConv(device, n, ops.N, ops.FG));
+    if (dconv->ok()) ops.dev = dconv.get();
+  }
   const int RL = ops.RL;
   const int64_t M = (int64_t)z.size();
   ModeBasis mb[3];

@@ -111,3 +111,136 @@ bool CoreDevice::fetch(std::vector<double>& G) {
 }
 
 }  // namespace rs
+
+// ---- opt-in (RS_FLAG_DEVICE_FFT): the setup's convolutions y = T_k x on the device (cuFFT) ---
+#include <cufft.h>
+#include <mutex>
+
+namespace rs {
+namespace {
+
+__global__ void pack_pairs(const double* X, int n, int N, int p, cufftDoubleComplex* buf) {
+  const int pairs = (p + 1) / 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)pairs * N;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t / N), i = (int)(t % N), s = 2 * q;
+    cufftDoubleComplex v;
+    v.x = i < n ? X[(size_t)s * n + i] : 0.0;
+    v.y = (i < n && s + 1 < p) ? X[(size_t)(s + 1) * n + i] : 0.0;
+    buf[t] = v;
+  }
+}
+
+__global__ void mul_kernel(cufftDoubleComplex* buf, const cufftDoubleComplex* fg, int N, int pairs) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)pairs * N;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const cufftDoubleComplex a = buf[t], b = fg[t % N];
+    cufftDoubleComplex c;
+    c.x = a.x * b.x - a.y * b.y;
+    c.y = a.x * b.y + a.y * b.x;
+    buf[t] = c;
+  }
+}
+
+__global__ void unpack_pairs(const cufftDoubleComplex* buf, int n, int N, int p, double* Y) {
+  const double inv = 1.0 / N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)p * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n), i = (int)(t % n);
+    const cufftDoubleComplex v = buf[(size_t)(s / 2) * N + i + n - 1];
+    Y[t] = ((s & 1) ? v.y : v.x) * inv;
+  }
+}
+
+}  // namespace
+
+struct DeviceConv::Impl {
+  int device = 0, n = 0, N = 0, RL = 0;
+  cufftDoubleComplex* fg = nullptr;
+  cufftDoubleComplex* buf = nullptr;
+  double *X = nullptr, *Y = nullptr;
+  size_t cap_pairs = 0, cap_xy = 0;
+  cufftHandle plan = 0;
+  int plan_batch = 0;
+  bool ok = false;
+  std::mutex mtx;
+};
+
+DeviceConv::DeviceConv(int device, int n, int N, const std::vector<std::vector<std::complex<double>>>& FG)
+    : p(new Impl) {
+  p->device = device;
+  p->n = n;
+  p->N = N;
+  p->RL = (int)FG.size();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return; }
+  bool good = cudaMalloc(&p->fg, (size_t)p->RL * N * sizeof(cufftDoubleComplex)) == cudaSuccess;
+  for (int k = 0; k < p->RL && good; ++k)
+    good = cudaMemcpy(p->fg + (size_t)k * N, FG[k].data(), (size_t)N * sizeof(cufftDoubleComplex),
+                      cudaMemcpyHostToDevice) == cudaSuccess;
+  p->ok = good;
+  if (!good) cudaGetLastError();
+  cudaSetDevice(prev);
+}
+
+DeviceConv::~DeviceConv() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  if (p->plan) cufftDestroy(p->plan);
+  cudaFree(p->fg);
+  cudaFree(p->buf);
+  cudaFree(p->X);
+  cudaFree(p->Y);
+  cudaSetDevice(prev);
+  delete p;
+}
+
+bool DeviceConv::ok() const { return p->ok; }
+
+bool DeviceConv::apply(int k, const double* X, double* Y, int cols) {
+  std::lock_guard<std::mutex> lock(p->mtx);
+  if (!p->ok) return false;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  const int n = p->n, N = p->N, pairs = (cols + 1) / 2;
+  bool good = true;
+  if ((size_t)pairs > p->cap_pairs) {
+    cudaFree(p->buf);
+    good = cudaMalloc(&p->buf, (size_t)pairs * N * sizeof(cufftDoubleComplex)) == cudaSuccess;
+    p->cap_pairs = good ? pairs : 0;
+  }
+  if (good && (size_t)cols * n > p->cap_xy) {
+    cudaFree(p->X);
+    cudaFree(p->Y);
+    good = cudaMalloc(&p->X, (size_t)cols * n * sizeof(double)) == cudaSuccess &&
+           cudaMalloc(&p->Y, (size_t)cols * n * sizeof(double)) == cudaSuccess;
+    p->cap_xy = good ? (size_t)cols * n : 0;
+  }
+  if (good && p->plan_batch != pairs) {
+    if (p->plan) cufftDestroy(p->plan);
+    p->plan = 0;
+    good = cufftPlan1d(&p->plan, N, CUFFT_Z2Z, pairs) == CUFFT_SUCCESS;
+    p->plan_batch = good ? pairs : 0;
+  }
+  good = good && cudaMemcpy(p->X, X, (size_t)cols * n * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (good) {
+    pack_pairs<<<1184, 256>>>(p->X, n, N, cols, p->buf);
+    good = cufftExecZ2Z(p->plan, p->buf, p->buf, CUFFT_FORWARD) == CUFFT_SUCCESS;
+  }
+  if (good) {
+    mul_kernel<<<1184, 256>>>(p->buf, p->fg + (size_t)k * N, N, pairs);
+    good = cufftExecZ2Z(p->plan, p->buf, p->buf, CUFFT_INVERSE) == CUFFT_SUCCESS;
+  }
+  if (good) {
+    unpack_pairs<<<1184, 256>>>(p->buf, n, N, cols, p->Y);
+    good = cudaMemcpy(Y, p->Y, (size_t)cols * n * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  if (!good) { cudaGetLastError(); p->ok = false; }
+  cudaSetDevice(prev);
+  return good;
+}
+
+}  // namespace rs

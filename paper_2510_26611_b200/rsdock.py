@@ -22,6 +22,7 @@ RS_E_INVALID_ARG, RS_E_CUDA, RS_E_NOMEM, RS_E_NO_DEVICE = -1, -2, -3, -4
 RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 RS_FLAG_BOX_SCHEME_B = 4
+RS_FLAG_DEVICE_FFT = 8
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_restrict_box", "rs_score_poses", "rs_score_poses_async",
             "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",

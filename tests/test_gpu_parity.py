@@ -729,3 +729,26 @@ def test_device_core_setup_bitwise(env, name):
     for k in ("F1", "F2", "F3", "S1", "S2", "S3"):
         assert np.array_equal(td[k], th[k]), k
     assert dev.info["cp_core_err"] == host.info["cp_core_err"]
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_device_fft_setup(env, name):
+    """RS_FLAG_DEVICE_FFT (N4 part): the RHOSVD and core convolutions with cuFFT.  The CP it builds
+    agrees with the host-only build's at sampled cells to 1e-6 of their max (the FFT rounding
+    moves the randomized bases, not the accuracy: the same sampled error to 1e-3 relative), and
+    the kernel on its tables matches the oracle as always."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    host = build(rsdock, w, flags=rsdock.RS_FLAG_HOST_ONLY)
+    dev = build(rsdock, w, flags=rsdock.RS_FLAG_DEVICE_FFT)
+    th, td = host.export_tables(), dev.export_tables()
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, w.grid_n, size=(2000, 3))
+    vh = np.einsum("pk,pk,pk->p", th["F1"][idx[:, 0]], th["F2"][idx[:, 1]], th["F3"][idx[:, 2]])
+    vd = np.einsum("pk,pk,pk->p", td["F1"][idx[:, 0]], td["F2"][idx[:, 1]], td["F3"][idx[:, 2]])
+    assert np.max(np.abs(vh - vd)) <= 1e-6 * np.max(np.abs(vh))
+    assert abs(dev.info["sampled_max_err"] - host.info["sampled_max_err"]) <= 1e-3 * host.info["sampled_max_err"]
+    ks, sample = syn.subsample(w.poses, 300)
+    Eg, Dg, inv = gpu_score(torch, rsdock, dev, w, sample)
+    Eo, Do, invo = oracle_score(rs_oracle, dev, w, sample)
+    compare(Eg, Dg, Eo, Do, inv, invo)

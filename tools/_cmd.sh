@@ -1,5 +1,15 @@
 set -u
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "device_core" 2>&1 | tail -3
-RS_SETUP_TIMING=1 timeout 900 python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench 2>&1 >/tmp/c4.json | grep "rs setup"
-python -c "import json;d=json.loads(open('/tmp/c4.json').read().strip().splitlines()[-1]);print(d['setup_seconds'], d['ms_per_step'])"
+timeout 900 python -m pytest tests -m gpu -x -q -k "device_fft or device_core" 2>&1 | tail -15
+python - <<'PY'
+import time, sys
+sys.path.insert(0, ".")
+import torch
+from synth import configs as syn
+from paper_2510_26611_b200 import rsdock
+w = syn.config_c4(n_poses=10)
+for fl in (0, rsdock.RS_FLAG_DEVICE_FFT):
+    t0 = time.time()
+    p = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(), flags=fl)
+    print("C4 setup flags", fl, round(time.time() - t0, 2), p.info["sampled_max_err"], p.info["cp_core_err"])
+PY
