@@ -1,15 +1,8 @@
 set -u
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "device_fft or device_core" 2>&1 | tail -15
-python - <<'PY'
-import time, sys
-sys.path.insert(0, ".")
-import torch
-from synth import configs as syn
-from paper_2510_26611_b200 import rsdock
-w = syn.config_c4(n_poses=10)
-for fl in (0, rsdock.RS_FLAG_DEVICE_FFT):
-    t0 = time.time()
-    p = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(), flags=fl)
-    print("C4 setup flags", fl, round(time.time() - t0, 2), p.info["sampled_max_err"], p.info["cp_core_err"])
-PY
+mkdir -p gpurun_out/r01_final6
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r01_final6/build.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r01_final6/gpu_tests.log 2>&1; echo "tests_rc=$?" >> gpurun_out/r01_final6/gpu_tests.log
+tail -3 gpurun_out/r01_final6/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/r01_final6/bench.json 2> gpurun_out/r01_final6/bench.err; echo bench_rc=$?
+python -c "import json;d=json.loads(open('gpurun_out/r01_final6/bench.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], d['setup_seconds'], d['clocks'])"
