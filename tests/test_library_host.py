@@ -343,3 +343,13 @@ def test_restrict_box_scheme_b_accuracy(oracle, rsd):
     C = rsd.Protein.combine([rsd.Protein(qA, XA, 8.0, **kw), rsd.Protein(qB, XB, 8.0, **kw)],
                            flags=rsd.RS_FLAG_HOST_ONLY)
     assert C.restrict_box([20, 20, 20], [40, 40, 40], 4, flags=fl).info["R"] == 4
+
+
+def test_flag_and_error_constants_match_header(rsd):
+    """The binding's RS_FLAG_* and RS_E_* values are the header's (the ABI is the header)."""
+    hdr = open(os.path.join(ROOT, "include", "rs_dock.h")).read()
+    consts = {m.group(1): int(m.group(2)) for m in
+              re.finditer(r"#define\s+(RS_(?:FLAG|E)_[A-Z0-9_]+)\s+\(?(-?\d+)u?\)?", hdr)}
+    assert len(consts) >= 8, consts
+    for name, value in consts.items():
+        assert getattr(rsd, name) == value, name
