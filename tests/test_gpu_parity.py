@@ -282,9 +282,10 @@ def test_c4_full_size_sampled(env):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("R,mult", [(16, 1), (32, 3)])
+@pytest.mark.parametrize("R,mult", [(R, m) for R in (8, 16, 32) for m in (1, 2, 3)])
 def test_c5_full_size_sampled(env, R, mult):
-    """C5 protein-protein: 5000-atom rigid partner (ligand from global memory), n = 8192."""
+    """C5 protein-protein, the whole R x sigma_s grid (R in {8, 16, 32}, sigma_s in {2, 4, 6} A):
+    5000-atom rigid partner (ligand from global memory), n = 8192."""
     torch, rsdock, rs_oracle = env
     w = syn.config_c5(rank_R=R, sigma_mult=mult)
     prot = build(rsdock, w)
