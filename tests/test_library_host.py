@@ -353,3 +353,44 @@ def test_flag_and_error_constants_match_header(rsd):
     assert len(consts) >= 8, consts
     for name, value in consts.items():
         assert getattr(rsd, name) == value, name
+
+
+def test_c_abi_from_plain_c(rsd, tmp_path):
+    """The boundary is a C ABI: a C99 program that includes only include/rs_dock.h, links
+    librsdock.so, builds a host-only handle, reads its info and tables, and checks the error
+    path (no GPU needed)."""
+    src = tmp_path / "abi.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include <stdlib.h>
+#include "rs_dock.h"
+int main(void) {
+  double q[3] = {0.5, -0.25, 1.0}, xyz[9] = {0, 0, 0, 1.5, 0, 0, 0, 1.5, 0};
+  rs_params p;
+  rs_params_default(&p);
+  p.grid_n = 32; p.rank_R = 4; p.sigma_split = 1.0; p.flags = RS_FLAG_HOST_ONLY;
+  rs_handle* h = rs_build_protein(q, xyz, 3, 8.0, &p);
+  if (!h) { printf("build failed: %s\n", rs_last_error()); return 1; }
+  rs_info info;
+  if (rs_get_info(h, &info) != 0 || info.n != 32 || info.R != 4 || info.n_atoms != 3) return 2;
+  double* F1 = malloc(sizeof(double) * 32 * 4);
+  if (rs_export_tables(h, F1, NULL, NULL, NULL, NULL, NULL) != 0) return 3;
+  double pose[7] = {1, 0, 0, 0, 0, 0, 3}, E, D, ql = 1.0, yl[3] = {0, 0, 0};
+  if (rs_score_poses(h, &ql, yl, 1, pose, 1, &E, &D) != RS_E_NO_DEVICE) return 4;
+  rs_free(h);
+  p.grid_n = 31;
+  if (rs_build_protein(q, xyz, 3, 8.0, &p) != NULL) return 5;
+  printf("ok %d %.3e\n", info.R, F1[0]);
+  free(F1);
+  return 0;
+}
+""")
+    exe = tmp_path / "abi"
+    lib = os.path.dirname(rsd.LIB_PATH)
+    import subprocess
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", str(src), "-I",
+                           os.path.join(ROOT, "include"), "-L", lib, "-lrsdock",
+                           f"-Wl,-rpath,{lib}", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("ok 4")
