@@ -63,7 +63,7 @@ def _worker(rank, world, port, out):
 
 
 def test_sharded_scoring_gloo_world2():
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     port = _free_port()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
@@ -100,7 +100,7 @@ def _ppiem_worker(rank, world, port, out):
 def test_ppiem_sharded_gloo_world2():
     """PPIEM rows split over two ranks (7 positions: 4 + 3), one all-gather: the landscape,
     distances, statuses and minima equal the 1-rank scan bit for bit."""
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     port = _free_port()
     mp.spawn(_ppiem_worker, args=(2, port, out), nprocs=2, join=True)
