@@ -1,3 +1,2 @@
 set -u
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q -k "c5" --durations=3 2>&1 | tail -8
+bash tools/ablate.sh r01_v50 C3 "t768 tile256 chunk2048 taildiv16" 0
