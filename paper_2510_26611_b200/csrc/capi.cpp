@@ -83,7 +83,7 @@ void free_device(rs_handle* h) {
   h->scan_bytes = 0;
   for (void** p : {&h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
                    &h->d_Fw32[0], &h->d_Fw32[1], &h->d_Fw32[2],
-                   &h->d_nb_range}) {
+                   &h->d_nb_range, &h->d_nb_pack}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -140,21 +140,52 @@ int upload_handle(rs_handle* h) {
       prec[4 * k + 3] = h->z[m];
     }
     if (int e = upload(&h->d_prec, prec, &bytes)) return e;
-    std::vector<int32_t> ent(4 * h->cg.idx.size(), 0);
-    for (size_t j = 0; j < h->cg.idx.size(); ++j) {
-      const size_t m = (size_t)h->cg.idx[j];
-      ent[4 * j] = (int32_t)((uint32_t)h->cells[3 * m] | ((uint32_t)h->cells[3 * m + 1] << 16));
-      ent[4 * j + 1] = h->cells[3 * m + 2];
-      ent[4 * j + 2] = rank[m];
-    }
-    if (int e = upload(&h->d_nb_ent, ent, &bytes)) return e;
+    // every list starts at an even entry (a padding entry after odd-length lists), so the
+    // kernel reads its candidates in aligned 32-byte pairs
     const size_t nc = h->cg.off.size() - 1;
     std::vector<int32_t> rng(2 * nc);
+    size_t tot = 0;
     for (size_t c = 0; c < nc; ++c) {
-      rng[2 * c] = h->cg.off[c];
-      rng[2 * c + 1] = h->cg.off[c + 1] - h->cg.off[c];
+      const int32_t cnt = h->cg.off[c + 1] - h->cg.off[c];
+      rng[2 * c] = (int32_t)tot;
+      rng[2 * c + 1] = cnt;
+      tot += (size_t)(cnt + (cnt & 1));
     }
+    if (tot > (size_t)INT32_MAX) { set_err("neighbour lists exceed 2^31 entries"); return RS_E_NOMEM; }
+    {
+      int32_t maxcnt = 0;
+      for (size_t c = 0; c < nc; ++c) maxcnt = std::max(maxcnt, rng[2 * c + 1]);
+      h->loc4 = tot < ((size_t)1 << 24) && maxcnt < 256;
+    }
+    std::vector<int32_t> ent(4 * std::max<size_t>(tot, 2), 0);
+    for (size_t c = 0; c < nc; ++c)
+      for (int32_t u = 0; u < rng[2 * c + 1]; ++u) {
+        const size_t j = (size_t)rng[2 * c] + u;
+        const size_t m = (size_t)h->cg.idx[(size_t)h->cg.off[c] + u];
+        ent[4 * j] = (int32_t)((uint32_t)h->cells[3 * m] | ((uint32_t)h->cells[3 * m + 1] << 16));
+        ent[4 * j + 1] = h->cells[3 * m + 2];
+        ent[4 * j + 2] = rank[m];
+      }
+    if (int e = upload(&h->d_nb_ent, ent, &bytes)) return e;
     if (int e = upload(&h->d_nb_range, rng, &bytes)) return e;
+    if (h->loc4) {
+      // the same ranges packed into 4 bytes, z rows padded to 16 bytes, with rs::kPackPad zero
+      // cells before every axis (a TMA tensor copy takes no negative coordinates): the scoring
+      // kernel copies a tile's box of it into shared memory with one TMA tensor copy
+      const int P = rs::kPackPad;
+      const int d0 = h->cg.dim[0], d1 = h->cg.dim[1], d2 = h->cg.dim[2];
+      const int e0 = d0 + P, e1 = d1 + P;
+      h->nb_dim2p = (d2 + P + 3) / 4 * 4;
+      std::vector<uint32_t> pk((size_t)e0 * e1 * h->nb_dim2p, 0u);
+      for (int x = 0; x < d0; ++x)
+        for (int y = 0; y < d1; ++y)
+          for (int z = 0; z < d2; ++z) {
+            const size_t c = ((size_t)x * d1 + y) * d2 + z;
+            pk[((size_t)(x + P) * e1 + (y + P)) * h->nb_dim2p + (z + P)] =
+                (uint32_t)rng[2 * c] | ((uint32_t)rng[2 * c + 1] << 24);
+          }
+      if (int e = upload(&h->d_nb_pack, pk, &bytes)) return e;
+    }
   }
   if (h->f32) {
     // binary32 copy of the factors (A21), rows as 16-byte quads padded/replicated like Fw
@@ -173,12 +204,18 @@ int upload_handle(rs_handle* h) {
   }
   CUDA_TRY(cudaMalloc(&h->d_work, rs::kWorkSlots * sizeof(int)), RS_E_NOMEM);
   CUDA_TRY(cudaMemset(h->d_work, 0, rs::kWorkSlots * sizeof(int)), RS_E_CUDA);
-  // dense memo of the short-range chain over |D_a| <= n_sigma (filled on the device by the same
-  // O5 op sequence), when it is small enough to stay L2-resident
+  // dense memo of the short-range chain over |D_a| <= n_sigma, filled on the device by the same
+  // O5 op sequence (ascending k; all zeros when R_s = 0); the scoring kernel reads O5 values
+  // only from it (C3: 2.2 MB, C5 at sigma_s = 6 A: 136 MB)
   const double memo_b = 8.0 * std::pow(double(h->n_sigma + 1), 3.0);
-  if (h->Rs > 0 && memo_b <= 64.0 * (1 << 20)) {
-    CUDA_TRY(cudaMalloc(&h->d_memo, (size_t)memo_b), RS_E_NOMEM);
-    bytes += (int64_t)memo_b;
+  if (memo_b > 2.0 * 1024 * 1024 * 1024) {
+    set_err("n_sigma = " + std::to_string(h->n_sigma) + ": the short-range memo ((n_sigma+1)^3 "
+            "doubles) would exceed 2 GiB; use a larger grid step or a smaller sigma_split");
+    return RS_E_NOMEM;
+  }
+  CUDA_TRY(cudaMalloc(&h->d_memo, (size_t)memo_b), RS_E_NOMEM);
+  bytes += (int64_t)memo_b;
+  {
     int e = rs::launch_fill_short_memo((const double*)h->dmem[3], (const double*)h->dmem[4],
                                        (const double*)h->dmem[5], h->Rs, h->n_sigma,
                                        (double*)h->d_memo, nullptr);
@@ -212,8 +249,11 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.t.prec = (const double4*)h->d_prec;
   a.t.short_memo = (const double*)h->d_memo;
   a.t.nb_range = (const int2*)h->d_nb_range;
+  a.t.nb_pack = (const unsigned*)h->d_nb_pack;
+  a.nb_dim2p = h->nb_dim2p;
   a.ns2 = (unsigned)((int64_t)h->n_sigma * h->n_sigma);
   a.f32 = h->f32 ? 1 : 0;
+  a.loc4 = h->loc4 ? 1 : 0;
   {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
     const double t = h->prm.dmin_cap / h->h + std::sqrt(3.0) + 2.0;

@@ -115,6 +115,7 @@ struct DeviceTables {
   const double2* Fw[3] = {nullptr, nullptr, nullptr};  // rows padded/replicated to CHP chunks
   const float4* Fw32[3] = {nullptr, nullptr, nullptr}; // binary32 rows (A21), 16-byte quads
   const int2* nb_range = nullptr;     // per coarse cell: (list begin, count)
+  const unsigned* nb_pack = nullptr;  // loc4 handles: begin | count << 24, z padded to nb_dim2p
   const double* S[3] = {nullptr, nullptr, nullptr};
   const int4* nb_ent = nullptr;       // per list entry: (i0 | i1 << 16, i2, sorted atom, 0)
   const double4* prec = nullptr;      // per sorted protein atom: (x, y, z, q)
@@ -139,6 +140,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
   int f32;                       // long-range part from the binary32 factors (A21)
+  int loc4;                      // every list begin < 2^24 and count < 256: 4-byte local cells
+  int nb_dim2p;                  // z extent of nb_pack (nb_dim[2] rounded up to a multiple of 4)
   // streamed launch (host-buffer pipeline): poses arrive in copy chunks [cb[i], cb[i+1]);
   // arrive[i] != 0 once chunk i landed; the kernel adds finished poses to done[i].  Null: off.
   const unsigned* arrive = nullptr;
@@ -152,7 +155,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
 int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
                            int n_sigma, double* out, void* stream);
 
-constexpr int kWorkSlots = 64;   // concurrent launches per handle with distinct work counters
+constexpr int kWorkSlots = 64;
+constexpr int kPackPad = 24;     // zero cells before each axis of the packed range table (TMA)   // concurrent launches per handle with distinct work counters
 
 // Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
 // (if not null) is incremented by the number of kernels enqueued.
@@ -207,7 +211,10 @@ struct rs_handle {
   void* d_Fw[3] = {nullptr, nullptr, nullptr};
   void* d_Fw32[3] = {nullptr, nullptr, nullptr};
   bool f32 = false;
+  bool loc4 = false;                   // cell ranges fit 24 + 8 bits (kernel's local range table)
   void* d_nb_range = nullptr;
+  void* d_nb_pack = nullptr;           // loc4: packed ranges, the TMA source of the local table
+  int nb_dim2p = 0;
   int* d_work = nullptr;               // kWorkSlots zeroed-per-launch work counters
   void* scan_buf = nullptr;            // rs_ppiem_scan scratch (grow-only)
   size_t scan_bytes = 0;

@@ -5,7 +5,7 @@
 //   H4 long-range CP gather + rank sum (rows of F_0, F_1, F_2 from a shared-memory window
 //      or from L2)                  H5 short-range replicas of nearby protein atoms
 //   H6 vdW min distance over the same cell-list candidates
-//   H7 warp double-double reduction H8 one energy + one min distance per pose
+//   H7 double-double reduction      H8 one energy + one min distance per pose
 //
 // Arithmetic contract (mirrored by oracle/oracle_score.c):
 // every floating-point op of H1-H5 and H7 is an explicit round-to-nearest intrinsic (no FMA
@@ -16,24 +16,30 @@
 // lanes accumulate and the reduction tree are free.  The snap (O3) is finished in integers
 // after the two fp64 ops that define it (ceil of a value in [0, n+1) is exact).
 //
-// Work layout: persistent CTAs (one per SM, 32 warps) take chunks of
-// consecutive poses from a global counter (guided: smaller chunks over the last poses); a warp
-// scores one pose at a time (lanes over ligand atoms), taking poses from a per-tile queue.
-// A tile is the longest run of poses whose rows fit the shared-memory window (a block scan of
+// Work layout: persistent CTAs (one per SM) take chunks of consecutive poses
+// from a global counter (guided: smaller chunks over the last poses).  A tile is the longest
+// run of a chunk's poses whose factor rows fit the shared-memory window (a block scan of
 // per-pose row bounds); the window's rows of the three factor matrices arrive by TMA bulk
-// copies (cp.async.bulk, mbarrier completion) from a row-padded device copy, with slack so that
-// the following tiles usually reuse them.  Rows are 16-byte chunks padded (R=12, 24) or
-// replicated (R=4, 8) to whole 128-byte lines; lane l reads chunk c ^ (l & 7) of its own row in
-// slot c, so the 8 lanes of every quarter-warp hit 8 distinct bank groups whatever rows they
-// gather (conflict-free LDS.128); the halving tree over rank pairs is invariant under that
-// relabelling, so no un-permute is needed.  RS_FLAG_F32_FACTORS (reading A21) runs the same
-// machinery on binary32 rows of rank quads.
+// copies (cp.async.bulk, mbarrier completion) from a row-padded device copy, and the tile's
+// coarse cells of the neighbour lists are copied into a local range table next to it.
+// Warps take UNITS of the tile's poses: G poses (a power of two <= 32, guided so that the
+// warps finish a tile together) with S = 32/G lanes per pose; a lane keeps its pose's R and t
+// in registers and walks the ligand atoms l = sub, sub + S, ... (sub = lane mod S) through
+// H2-H6, so a full unit (G = 32) is one pose per lane and needs no cross-lane reduction.
+// Rows are 16-byte chunks padded (R=12, 24) or replicated (R=4, 8) to whole 128-byte lines;
+// lane l reads chunk c ^ (l & 7) of its own row in slot c, so the 8 lanes of every
+// quarter-warp hit 8 distinct bank groups whatever rows they gather (conflict-free LDS.128);
+// the halving tree over rank pairs is invariant under that relabelling, so no un-permute is
+// needed.  RS_FLAG_F32_FACTORS (reading A21) runs the same machinery on binary32 rank quads.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "rs_internal.h"
@@ -42,20 +48,23 @@ namespace rs {
 namespace {
 
 #ifndef RS_THREADS
-#define RS_THREADS 1024
-#endif
-#ifndef RS_TILE
-#define RS_TILE 512
+#define RS_THREADS 512
 #endif
 #ifndef RS_CHUNK
-#define RS_CHUNK 1024
+#define RS_CHUNK 2048
 #endif
 #ifndef RS_WIN_SLACK
 #define RS_WIN_SLACK 1.5
 #endif
+#ifndef RS_NBR
+#define RS_NBR 2
+#endif
+#ifndef RS_LOC_CELLS
+#define RS_LOC_CELLS 10240
+#endif
 constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = RS_TILE;           // poses per tile (upper bound)
+constexpr int kTile = 2 * kThreads;      // poses per tile (upper bound): two per thread in the scan
 constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 #ifndef RS_TAIL_DIV
 #define RS_TAIL_DIV 8
@@ -64,12 +73,7 @@ constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 #define RS_TAIL_CHUNK 128
 #endif
 constexpr int kTailChunk = RS_TAIL_CHUNK;  // chunk size over the last 1/RS_TAIL_DIV of the poses
-static_assert(kTile <= kThreads, "one thread per pose of a tile");
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef RS_SLOTS
-#define RS_SLOTS 1
-#endif
-constexpr int kSlots = RS_SLOTS;         // candidate slots per lane and flattened round
 
 template <int R>
 struct Geo {
@@ -79,8 +83,6 @@ struct Geo {
   static constexpr int NS = REP ? CH : CHP;                        // loads per row and lane
 };
 
-__device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
-
 // Read-only global loads issued only when pr holds (the predicate is inside the instruction, so
 // the compiler cannot turn a guarded load into an unguarded speculative one: the address may be
 // meaningless when pr is false, and untaken lanes cost no L1 tag lookups).  Result 0 if !pr.
@@ -88,12 +90,6 @@ __device__ __forceinline__ double ldg_if(const double* p, bool pr) {
   double v = 0.0;
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
       : "+d"(v) : "l"(p), "r"((int)pr));
-  return v;
-}
-__device__ __forceinline__ double2 ldg_if(const double2* p, bool pr) {
-  double2 v = make_double2(0.0, 0.0);
-  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.global.nc.v2.f64 {%0, %1}, [%2];\n}"
-      : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((int)pr));
   return v;
 }
 // one 256-bit read-only load (LDG.E.ENL2.256 on sm_100): a whole 32-byte sector per lane
@@ -109,8 +105,6 @@ __device__ __forceinline__ float4 ldg256x2(const float4* p, float4& hi) {
       : "l"(p));
   return v;
 }
-
-// one 256-bit load (LDG.E.ENL2.256 on sm_100): one L1 tag lookup for a 32-byte record
 __device__ __forceinline__ double4 ldg_if(const double4* p, bool pr) {
   double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n}"
@@ -123,10 +117,55 @@ __device__ __forceinline__ int2 ldg_if(const int2* p, bool pr) {
       : "+r"(v.x), "+r"(v.y) : "l"(p), "r"((int)pr));
   return v;
 }
-__device__ __forceinline__ int4 ldg_if(const int4* p, bool pr) {
-  int4 v = make_int4(0, 0, 0, 0);
+// two consecutive 16-byte list entries (a 32-byte aligned pair) in one 256-bit load
+__device__ __forceinline__ void ldg_pair_if(const int4* p, bool pr, int4& e0, int4& e1) {
+  e0 = make_int4(0, 0, 0, 0);
+  e1 = e0;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %9, 0;\n"
+      " @q ld.global.nc.v8.s32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n}"
+      : "+r"(e0.x), "+r"(e0.y), "+r"(e0.z), "+r"(e0.w), "+r"(e1.x), "+r"(e1.y), "+r"(e1.z), "+r"(e1.w)
+      : "l"(p), "r"((int)pr));
+}
+// Predicated loads whose outputs are left undefined when the predicate is off (the caller
+// never reads them then): no zero-initialisation instructions on the hot neighbour path
+__device__ __forceinline__ void ldg_pair_p(const int4* p, bool pr, int4& e0, int4& e1) {
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %9, 0;\n"
+      " @q ld.global.nc.v8.s32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n}"
+      : "=r"(e0.x), "=r"(e0.y), "=r"(e0.z), "=r"(e0.w), "=r"(e1.x), "=r"(e1.y), "=r"(e1.z), "=r"(e1.w)
+      : "l"(p), "r"((int)pr));
+}
+__device__ __forceinline__ int4 ldg_int4_p(const int4* p, bool pr) {
+  int4 v;
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];\n}"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w) : "l"(p), "r"((int)pr));
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "r"((int)pr));
+  return v;
+}
+__device__ __forceinline__ double4 ldg_d4_p(const double4* p, bool pr) {
+  double4 v;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n}"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p), "r"((int)pr));
+  return v;
+}
+__device__ __forceinline__ double ldg_d_p(const double* p, bool pr) {
+  double v;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
+      : "=d"(v) : "l"(p), "r"((int)pr));
+  return v;
+}
+// 16 bytes from shared memory at a 32-bit shared-window address
+__device__ __forceinline__ double2 lds2(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 lds4f(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned addr) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
@@ -172,6 +211,15 @@ __device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, do
   lo = __dadd_rn(lo, __dadd_rn(err, e));
 }
 
+// (hi, lo) += (h2, l2) exactly up to the final lo rounding (TwoSum on the high parts)
+__device__ __forceinline__ void dd_merge(double& hi, double& lo, double h2, double l2) {
+  const double s = __dadd_rn(hi, h2);
+  const double bb = __dsub_rn(s, hi);
+  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
+  hi = s;
+  lo = __dadd_rn(__dadd_rn(lo, l2), e);
+}
+
 // One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
 __device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
   return __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), c.x), __dmul_rn(__dmul_rn(a.y, b.y), c.y));
@@ -188,40 +236,28 @@ __device__ __forceinline__ double halving_tree(double* s) {
   return s[0];
 }
 
-// O4 with compile-time R from the shared-memory window.  rK = byte offset of row K from the
-// window base (a multiple of the row size, the base 256-B aligned).  Slot c reads physical
-// chunk c ^ rho (rho = lane & 7): the 8 lanes of a quarter-warp hit 8 distinct 16-byte bank
-// groups whatever rows they read.  Physical chunk p holds pair p (padded widths: zero beyond CH;
-// replicated widths: pair p mod CH), so slot c holds pair (c ^ rho) mod NS, and the halving
-// tree, which combines c with c ^ m at every level, is bitwise invariant under that relabelling.
-// The halving tree evaluated depth-first: T(c, stride, cnt) = T(c, 2 stride, cnt/2) +
-// T(c + stride, 2 stride, cnt/2), leaves = slot pair sums.  Same pairings as the level-by-level
-// loop (pair c meets c + NS/2 first), but partial sums retire as soon as their chunks arrive,
-// so fewer values are live while the gathers are in flight.
+// O4 with compile-time R from the shared-memory window.  rK = shared address of row K with the
+// lane's XOR offset rho << 4 already in bits 4.. (rows are 128/256-byte aligned, so XOR with
+// c << 4 selects physical chunk c ^ rho of the row).  Physical chunk p holds pair p (padded
+// widths: zero beyond CH; replicated widths: pair p mod CH), so slot c holds pair (c ^ rho)
+// mod NS, and the halving tree, which combines c with c ^ m at every level, is bitwise
+// invariant under that relabelling.  Evaluated depth-first: T(c, stride, cnt) = T(c, 2 stride,
+// cnt/2) + T(c + stride, 2 stride, cnt/2), leaves = slot pair sums (the pairings of the
+// level-by-level loop: pair c meets c + NS/2 first), so partial sums retire as their chunks
+// arrive and fewer values are live while the gathers are in flight.
 template <int C, int STRIDE, int CNT>
 struct SmemTree {
-  static __device__ __forceinline__ double eval(const char* win, unsigned r0, unsigned r1,
-                                                unsigned r2) {
+  static __device__ __forceinline__ double eval(unsigned r0, unsigned r1, unsigned r2) {
     if constexpr (CNT == 1) {
       constexpr unsigned o = (unsigned)C << 4;
-      return pair_prod(*reinterpret_cast<const double2*>(win + (r0 ^ o)),
-                       *reinterpret_cast<const double2*>(win + (r1 ^ o)),
-                       *reinterpret_cast<const double2*>(win + (r2 ^ o)));
+      return pair_prod(lds2(r0 ^ o), lds2(r1 ^ o), lds2(r2 ^ o));
     } else {
-      const double lhs = SmemTree<C, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
-      const double rhs = SmemTree<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      const double lhs = SmemTree<C, 2 * STRIDE, CNT / 2>::eval(r0, r1, r2);
+      const double rhs = SmemTree<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(r0, r1, r2);
       return __dadd_rn(lhs, rhs);
     }
   }
 };
-
-template <int R>
-__device__ __forceinline__ double long_phi_smem(const char* win, unsigned r0, unsigned r1,
-                                                unsigned r2, int rho) {
-  using G = Geo<R>;
-  const unsigned x = (unsigned)rho << 4;
-  return SmemTree<0, 1, G::NS>::eval(win, r0 | x, r1 | x, r2 | x);
-}
 
 // O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
 template <int R>
@@ -303,16 +339,13 @@ __device__ __forceinline__ float quad_prod(float4 a, float4 b, float4 c) {
 // the binary64 path: the tree is invariant under the relabelling)
 template <int C, int STRIDE, int CNT>
 struct SmemTree32 {
-  static __device__ __forceinline__ float eval(const char* win, unsigned r0, unsigned r1,
-                                               unsigned r2) {
+  static __device__ __forceinline__ float eval(unsigned r0, unsigned r1, unsigned r2) {
     if constexpr (CNT == 1) {
       constexpr unsigned o = (unsigned)C << 4;
-      return quad_prod(*reinterpret_cast<const float4*>(win + (r0 ^ o)),
-                       *reinterpret_cast<const float4*>(win + (r1 ^ o)),
-                       *reinterpret_cast<const float4*>(win + (r2 ^ o)));
+      return quad_prod(lds4f(r0 ^ o), lds4f(r1 ^ o), lds4f(r2 ^ o));
     } else {
-      const float lhs = SmemTree32<C, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
-      const float rhs = SmemTree32<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(win, r0, r1, r2);
+      const float lhs = SmemTree32<C, 2 * STRIDE, CNT / 2>::eval(r0, r1, r2);
+      const float rhs = SmemTree32<C + STRIDE, 2 * STRIDE, CNT / 2>::eval(r0, r1, r2);
       return __fadd_rn(lhs, rhs);
     }
   }
@@ -320,7 +353,7 @@ struct SmemTree32 {
 
 // L2 path of O4-f32: rows of the packed binary32 copy, quads in natural order
 template <int R>
-__device__ __noinline__ double long_phi_global32(const float4* F0, const float4* F1,
+__device__ __forceinline__ double long_phi_l2_32(const float4* F0, const float4* F1,
                                                  const float4* F2, int i0, int i1, int i2) {
   using G = Geo32<R>;
   const float4* r0 = F0 + (size_t)i0 * G::CHP;
@@ -356,6 +389,11 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
   }
   return (double)s[0];
 }
+template <int R>
+__device__ __noinline__ double long_phi_global32(const float4* F0, const float4* F1,
+                                                 const float4* F2, int i0, int i1, int i2) {
+  return long_phi_l2_32<R>(F0, F1, F2, i0, i1, i2);
+}
 
 struct ChunkPlan {             // dynamic schedule: nbig chunks of `big` poses, then `tail`-pose chunks
   int64_t nbig;
@@ -365,19 +403,8 @@ struct ChunkPlan {             // dynamic schedule: nbig chunks of `big` poses, 
 struct Window {
   int lo[3], hi[3], off[3];    // staged rows [lo, hi] per axis; smem row of row i = i + off
 };
-
-
-struct __align__(16) PoseRec {  // H1 output of one pose: R (row-major) and t
-  double m[12];
-};
-
-// Per-warp staging of the 32 atoms of one pass for the flattened candidate-pair rounds.
-template <int NA>
-struct __align__(16) PairStage {
-  double2 x01[32 * NA]; // x'_0, x'_1 of slot 32 u + lane (written only for atoms with candidates)
-  double2 x2z[32 * NA]; // x'_2, charge
-  int4 cb[32 * NA];     // i0, i1, i2, (list begin - start of the atom's candidate segment)
-  int map[32 * kSlots]; // candidate slot where an atom's segment starts -> atom slot
+struct LocalBox {              // coarse cells [lo, lo + dim) per axis copied into s_loc; dim 0: none
+  int lo[3], dim[3];
 };
 
 // ---- TMA bulk copy + mbarrier (window staging) ---------------------------------------------
@@ -393,10 +420,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_1d(unsigned dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
+          dst),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
@@ -409,376 +436,160 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
-// O5 value s(D): from the dense memo (filled by the same chain) or the chain itself
-__device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2) {
-  if (a.t.short_memo) {
-    const int d = a.n_sigma + 1;
-    return ldg_if(a.t.short_memo + (abs(e0) * d + abs(e1)) * d + abs(e2), true);
-  }
-  const double* s0 = a.t.S[0] + (size_t)(e0 + a.n_sigma) * a.Rs;
-  const double* s1 = a.t.S[1] + (size_t)(e1 + a.n_sigma) * a.Rs;
-  const double* s2 = a.t.S[2] + (size_t)(e2 + a.n_sigma) * a.Rs;
-  double s = 0.0;
-  for (int k = 0; k < a.Rs; ++k)
-    s = __dadd_rn(s, __dmul_rn(__dmul_rn(__ldg(s0 + k), __ldg(s1 + k)), __ldg(s2 + k)));
-  return s;
+// O5 value s(D) from the dense memo s(|D0|,|D1|,|D2|), which the handle fills on the device with
+// the O5 chain itself (ascending k) for every |D_a| <= n_sigma; loaded only when pr holds
+__device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2, bool pr) {
+  const unsigned d = (unsigned)a.n_sigma + 1u;
+  const unsigned idx = ((unsigned)abs(e0) * d + (unsigned)abs(e1)) * d + (unsigned)abs(e2);
+  return ldg_d_p(reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(a.t.short_memo) +
+                                                 (uint64_t)idx * 8u), pr);
 }
 
-// One candidate pair: an atom of the pass (cell oc, coordinates and charge ox) and a list entry
-// en = (i0 | i1 << 16, i2, sorted atom k).  O7 distance when the integer prefilter admits it,
-// O5 replica term inside the n_sigma ball.  Cells are < 2^15, so the squared integer offsets sum
-// exactly in 32 unsigned bits.
-__device__ __forceinline__ unsigned pair_dd(const int4 oc, const int4 en) {
-  const int e0 = oc.x - (en.x & 0xffff), e1 = oc.y - (int)((unsigned)en.x >> 16), e2 = oc.z - en.y;
+// One candidate list entry en = (i0 | i1 << 16, i2, sorted atom k) against the atom's cell
+// (c0, c1, c2): the squared integer offset (cells are < 2^15, so it sums exactly in 32 bits)
+__device__ __forceinline__ unsigned entry_dd(int c0, int c1, int c2, const int4 en, int& e0, int& e1,
+                                             int& e2) {
+  e0 = c0 - (en.x & 0xffff);
+  e1 = c1 - (int)((unsigned)en.x >> 16);
+  e2 = c2 - en.y;
   return (unsigned)(e0 * e0) + (unsigned)(e1 * e1) + (unsigned)(e2 * e2);
 }
-__device__ __forceinline__ void pair_term(const ScoreArgs& a, const double4 ox, unsigned dd,
-                                          double sv, double2 xy, double2 zq, double& hi, double& lo,
-                                          double& best) {
+
+// H5 + H6 for one candidate whose record r = (x, y, z, q) was loaded: O7 distance when the
+// integer prefilter admits it, O5 replica term inside the n_sigma ball
+__device__ __forceinline__ void pair_term(const ScoreArgs& a, double x0, double x1, double x2,
+                                          double z, unsigned dd, double sv, const double4 r,
+                                          double& hi, double& lo, double& best) {
   if (dd < a.vdw_cells2) {
-    const double dx0 = __dsub_rn(ox.x, xy.x);
-    const double dx1 = __dsub_rn(ox.y, xy.y);
-    const double dx2 = __dsub_rn(ox.z, zq.x);
+    const double dx0 = __dsub_rn(x0, r.x);
+    const double dx1 = __dsub_rn(x1, r.y);
+    const double dx2 = __dsub_rn(x2, r.z);
     const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
-    best = fmin(best, d2);
+    best = d2 < best ? d2 : best;
   }
-  if (dd <= a.ns2) dd_add_prod(hi, lo, ox.w, __dmul_rn(zq.y, sv));
+  if (dd <= a.ns2) dd_add_prod(hi, lo, z, __dmul_rn(r.w, sv));
 }
 
-// O5 value for a pair inside the n_sigma ball (issued as soon as the offset is known)
-__device__ __forceinline__ double pair_short(const ScoreArgs& a, const int4 oc, const int4 en) {
-#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 8)
-  return 1.0;
-#else
-  return short_value(a, oc.x - (en.x & 0xffff), oc.y - (int)((unsigned)en.x >> 16), oc.z - en.y);
+// H6 for one candidate with record r (loaded iff hit): O7 distance, keep the minimum
+__device__ __forceinline__ void pair_hit(double x0, double x1, double x2, const double4 r, bool hit,
+                                         double& best) {
+  const double dx0 = __dsub_rn(x0, r.x);
+  const double dx1 = __dsub_rn(x1, r.y);
+  const double dx2 = __dsub_rn(x2, r.z);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
+  best = (hit && d2 < best) ? d2 : best;
+}
+
+// H5 + H6 for two candidate list entries of one ligand atom (cell c0..c2, coordinates
+// x0..x2, charge z); a0/a1: the entries are real candidates.  The integer prefilter on the
+// cell offset decides whether the protein record (O7 distance) and the memo value (O5 replica
+// term inside the n_sigma ball) are loaded at all.
+__device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x1, double x2,
+                                         double z, int c0, int c1, int c2, const int4 en0,
+                                         const int4 en1, bool a0, bool a1, double& hi, double& lo,
+                                         double& best) {
+  int e00, e01, e02, e10, e11, e12;
+  unsigned dd0 = entry_dd(c0, c1, c2, en0, e00, e01, e02);
+  unsigned dd1 = entry_dd(c0, c1, c2, en1, e10, e11, e12);
+  dd0 = a0 ? dd0 : 0xffffffffu;
+  dd1 = a1 ? dd1 : 0xffffffffu;
+  const bool sr0 = dd0 <= a.ns2, sr1 = dd1 <= a.ns2;
+  const bool v0 = dd0 < a.vdw_cells2, v1 = dd1 < a.vdw_cells2;
+  const double4 rc0 = ldg_d4_p(a.t.prec + en0.z, sr0 || v0);
+  const double4 rc1 = ldg_d4_p(a.t.prec + en1.z, sr1 || v1);
+  const double sv0 = short_value(a, e00, e01, e02, sr0);
+  const double sv1 = short_value(a, e10, e11, e12, sr1);
+  pair_hit(x0, x1, x2, rc0, v0, best);
+  pair_hit(x0, x1, x2, rc1, v1, best);
+  if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(rc0.w, sv0));
+  if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(rc1.w, sv1));
+}
+
+// H5 + H6 for one candidate list entry (see nbr_pair)
+__device__ __forceinline__ void nbr_one(const ScoreArgs& a, double x0, double x1, double x2,
+                                        double z, int c0, int c1, int c2, const int4 en, bool a0,
+                                        double& hi, double& lo, double& best) {
+  int e0, e1, e2;
+  unsigned dd = entry_dd(c0, c1, c2, en, e0, e1, e2);
+  dd = a0 ? dd : 0xffffffffu;
+  const bool sr = dd <= a.ns2, v = dd < a.vdw_cells2;
+  const double4 rc = ldg_d4_p(a.t.prec + en.z, sr || v);
+  const double sv = short_value(a, e0, e1, e2, sr);
+  pair_hit(x0, x1, x2, rc, v, best);
+  if (sr) dd_add_prod(hi, lo, z, __dmul_rn(rc.w, sv));
+}
+
+#ifndef RS_NQ
+#define RS_NQ 3
 #endif
-}
+#ifndef RS_NPAIR
+#define RS_NPAIR 2     // candidates per lane and neighbour pass (1 or 2)
+#endif
+constexpr int kNQ = RS_NQ;   // per-lane stack of atoms waiting for their candidate walk
 
-// Per-atom state of one pass slot (H2/H3 output and the atom's candidate-list range)
-struct AtomState {
-  double x0, x1, x2, z;
-  int i0, i1, i2, beg, cnt;
-  bool go;                     // a real ligand atom (l < L) inside the box
+// Per-warp neighbour queue (RS_NBR == 2): atoms whose candidates a lane has not started yet
+struct __align__(16) NbrQueue {
+  double2 x01[kNQ][32];   // x'_0, x'_1
+  double2 x2z[kNQ][32];   // x'_2, charge
+  int4 cb[kNQ][32];       // i0 | i1 << 16, i2, first entry, end entry
 };
 
-// H2, H3 and the candidate-range lookup for ligand atom l of one pose.  bad is set if the atom
-// leaves the box (O8).  Lanes past the ligand's end (l >= L) run them on atom L-1 and get
-// go = false, z = 0 (branch-free; they contribute nothing).
-template <bool LIG_SMEM>
-__device__ __forceinline__ void atom_stage(const ScoreArgs& a, int l, const double* Rm,
-                                           const double* tv, const double2* s_lig, int lig_n,
-                                           AtomState& st,
-                                           bool& bad) {
-  const bool act = l < a.L;
-  const int lc = act ? l : a.L - 1;
-  double y0, y1, y2, z;
-  if constexpr (LIG_SMEM) {
-    // ligand staged structure-of-arrays: (y0, y1) then (y2, z), conflict-free 16-byte loads
-    const double2 v0 = s_lig[lc], v1 = s_lig[lig_n + lc];
-    y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
-  } else {
-    y0 = __ldg(a.yl + 3 * (int64_t)lc);
-    y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
-    y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
-    z = __ldg(a.zl + lc);
-  }
-  st.z = act ? z : 0.0;
-  // H2 (O2)
-  st.x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
-  st.x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
-  st.x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
-  // H3 (O3): valid iff -b <= x'_a <= b on every axis (false for NaN)
-  const bool ok = fabs(st.x0) <= a.b && fabs(st.x1) <= a.b && fabs(st.x2) <= a.b;
-  bad = bad || (act && !ok);
-  st.go = act && ok;
-  const int nm1 = a.n - 1;
-  st.i0 = snap_dev(st.x0, a.b, a.inv_h, nm1);
-  st.i1 = snap_dev(st.x1, a.b, a.inv_h, nm1);
-  st.i2 = snap_dev(st.x2, a.b, a.inv_h, nm1);
-  st.beg = 0;
-  st.cnt = 0;
-#if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
-  // candidate range of the coarse cell containing i (cell lists cover every protein atom that can
-  // matter to H5/H6 for any point of the cell); loaded before H4 so its latency hides behind it
-  const unsigned cx = (unsigned)((st.i0 >> a.nb_shift) - a.nb_lo[0]);
-  const unsigned cy = (unsigned)((st.i1 >> a.nb_shift) - a.nb_lo[1]);
-  const unsigned cz = (unsigned)((st.i2 >> a.nb_shift) - a.nb_lo[2]);
-  {
-    const bool in = st.go && cx < (unsigned)a.nb_dim[0] && cy < (unsigned)a.nb_dim[1] && cz < (unsigned)a.nb_dim[2];
-    const int2 bc = ldg_if(a.t.nb_range + (cx * a.nb_dim[1] + cy) * a.nb_dim[2] + cz, in);
-    st.beg = bc.x;
-    st.cnt = bc.y;
-  }
-#endif
-}
-
-// H4 (O4) for the NA atoms of a lane: atoms whose rows are staged read the window, real atoms
-// outside it (rare) read L2, lanes past the ligand's end skip it (phi = 0, weight z = 0).
-// F32: O4-f32 from the binary32 rows (A21).
-template <int RT, int NA, bool F32>
-__device__ __forceinline__ void long_range_stage(const ScoreArgs& a, const AtomState* st,
-                                                 bool use_win, const Window& W, const char* win,
-                                                 int rho, double* hi, double* lo) {
-  double phi[NA];
-#pragma unroll
-  for (int u = 0; u < NA; ++u) phi[u] = 0.0;
-  if constexpr (RT > 0) {
-    constexpr int kChp = F32 ? Geo32<RT>::CHP : Geo<RT>::CHP;
-    constexpr unsigned kRow = 16u * kChp;
-    bool l2[NA];
-    unsigned r0[NA], r1[NA], r2[NA];
-#pragma unroll
-    for (int u = 0; u < NA; ++u) {
-      const bool inwin = use_win && (unsigned)(st[u].i0 - W.lo[0]) <= (unsigned)(W.hi[0] - W.lo[0]) &&
-                         (unsigned)(st[u].i1 - W.lo[1]) <= (unsigned)(W.hi[1] - W.lo[1]) &&
-                         (unsigned)(st[u].i2 - W.lo[2]) <= (unsigned)(W.hi[2] - W.lo[2]);
-      l2[u] = st[u].go && !inwin;
-      const bool w = st[u].go && inwin;
-      r0[u] = w ? (unsigned)(st[u].i0 + W.off[0]) * kRow : 0u;
-      r1[u] = w ? (unsigned)(st[u].i1 + W.off[1]) * kRow : 0u;
-      r2[u] = w ? (unsigned)(st[u].i2 + W.off[2]) * kRow : 0u;
-    }
-    if (use_win) {
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
-        phi[u] = st[u].z;
+#if RS_NBR == 2
+constexpr size_t kQueueBytes = sizeof(NbrQueue) * kWarps;   // dynamic shared memory
 #else
-        if (st[u].go && !l2[u]) {
-          if constexpr (F32) {
-            const unsigned x = (unsigned)rho << 4;
-            phi[u] = (double)SmemTree32<0, 1, Geo32<RT>::NS>::eval(win, r0[u] | x, r1[u] | x, r2[u] | x);
-          } else {
-            phi[u] = long_phi_smem<RT>(win, r0[u], r1[u], r2[u], rho);
-          }
-        }
+constexpr size_t kQueueBytes = 0;
 #endif
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < NA; ++u)
-      if (l2[u]) {
-        if constexpr (F32)
-          phi[u] = long_phi_global32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], st[u].i0, st[u].i1, st[u].i2);
-        else
-          phi[u] = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], st[u].i0, st[u].i1, st[u].i2);
-      }
-  } else {
-#pragma unroll
-    for (int u = 0; u < NA; ++u) {
-      if (st[u].go)
-        phi[u] = long_phi_rt(a.t.F[0] + (size_t)st[u].i0 * a.R, a.t.F[1] + (size_t)st[u].i1 * a.R,
-                             a.t.F[2] + (size_t)st[u].i2 * a.R, a.R);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < NA; ++u) dd_add_prod(hi[u], lo[u], st[u].z, phi[u]);
+
+// Per-warp staging of the flattened neighbour rounds (RS_NBR == 1)
+struct __align__(16) NbrStage {
+  double2 x01[32];   // owner's x'_0, x'_1
+  double2 x2z[32];   // owner's x'_2, charge
+  int4 cb[32];       // owner's cell and (list begin - start of its segment)
+  double2 res[32];   // per pair slot: (d^2 or +inf, fl(z_m s) or 0)
+  int map[32];       // slot where an owner's segment starts -> owner lane
+};
+
+__device__ __forceinline__ int pow2_floor(int v) {   // v >= 1
+  return 1 << (31 - __clz(v));
 }
 
-// (hi, lo) += (h2, l2) exactly up to the final lo rounding (TwoSum on the high parts)
-__device__ __forceinline__ void dd_merge(double& hi, double& lo, double h2, double l2) {
-  const double s = __dadd_rn(hi, h2);
-  const double bb = __dsub_rn(s, hi);
-  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
-  hi = s;
-  lo = __dadd_rn(__dadd_rn(lo, l2), e);
-}
-
-__device__ __forceinline__ void load_pose(const PoseRec& pr, double* Rm, double* tv) {
-  const double2* m2 = reinterpret_cast<const double2*>(pr.m);
-#pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    const double2 v = m2[i];
-    const int k0 = 2 * i, k1 = 2 * i + 1;
-    if (k0 < 9) Rm[k0] = v.x; else tv[k0 - 9] = v.x;
-    if (k1 < 9) Rm[k1] = v.y; else tv[k1 - 9] = v.y;
-  }
-}
-
-// Score one pose with one warp: lanes over ligand atoms, NA atoms per lane and pass (NA = 2
-// gives every lane two independent dependency chains and halves the per-pass overheads).
-template <int RT, int NA, bool F32>
-__device__ __forceinline__ void score_pose(const ScoreArgs& a, int64_t p, const PoseRec& pr,
-                                           bool ok, bool use_win, const Window& W,
-                                           const char* win, const double2* s_lig, int lig_smem_n,
-                                           int lane, PairStage<NA>& ps,
-                                           double2& out) {
-  double hi[NA], lo[NA], best = INFINITY;
-#pragma unroll
-  for (int u = 0; u < NA; ++u) hi[u] = lo[u] = 0.0;
-  bool bad = !ok;
-  const int rho = lane & 7;
-  const bool lig_all_smem = a.L <= lig_smem_n;
-  const int L = ok ? a.L : 0;
-  const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
-  for (int l0 = 0; l0 < L; l0 += 32 * NA) {
-    // the pose's R and t, re-read from shared memory (broadcast) each pass: they are live only
-    // during H2, which keeps registers for more resident warps
-    double Rm[9], tv[3];
-    load_pose(pr, Rm, tv);
-    AtomState st[NA];
-#pragma unroll
-    for (int u = 0; u < NA; ++u) {
-      if (lig_all_smem) atom_stage<true>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
-      else atom_stage<false>(a, l0 + 32 * u + lane, Rm, tv, s_lig, lig_smem_n, st[u], bad);
-    }
-    long_range_stage<RT, NA, F32>(a, st, use_win, W, win, rho, hi, lo);
-    if (__any_sync(kFull, bad)) {
-      bad = true;
-      break;                      // the pose is invalid: NaN outputs, skip the rest
-    }
-    // H5 + H6 over the pass's (atom, candidate) pairs, flattened across the warp so every lane
-    // works on some pair in every round (the pose sums are order-free, O6/O7); two slots per
-    // lane and round keep two independent sets of loads in flight
-    int cl = 0;
-#pragma unroll
-    for (int u = 0; u < NA; ++u) cl += st[u].cnt;
-    if (__ballot_sync(kFull, cl > 0) == 0) continue;
-    int inc = cl;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(kFull, inc, o);
-      if (lane >= o) inc += v;
-    }
-    const int total = __shfl_sync(kFull, inc, 31);
-    int seg[NA];
-    {
-      int s0 = inc - cl;
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        seg[u] = s0;
-        if (st[u].cnt > 0) {        // only atoms with candidates are ever read back
-          ps.x01[32 * u + lane] = make_double2(st[u].x0, st[u].x1);
-          ps.x2z[32 * u + lane] = make_double2(st[u].x2, st[u].z);
-          ps.cb[32 * u + lane] = make_int4(st[u].i0, st[u].i1, st[u].i2, st[u].beg - s0);
-        }
-        s0 += st[u].cnt;
-      }
-    }
-    int carry = 0;
-    for (int base = 0; base < total; base += 32 * kSlots) {
-      unsigned m[kSlots];
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q) m[q] = 0;
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < NA; ++u) {
-        const int rel = seg[u] - base;
-        if (st[u].cnt > 0 && rel >= 0 && rel < 32 * kSlots) {
-          ps.map[rel] = 32 * u + lane;
-#pragma unroll
-          for (int q = 0; q < kSlots; ++q)
-            if ((rel >> 5) == q) m[q] |= 1u << (rel & 31);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q) m[q] = __reduce_or_sync(kFull, m[q]);
-      __syncwarp();
-      // owner of slot base + 32 q + lane: the last segment starting at or before it
-      int ow[kSlots];
-      {
-        int prev = carry;
-#pragma unroll
-        for (int q = 0; q < kSlots; ++q) {
-          const unsigned bq = m[q] & lanemask_le;
-          ow[q] = bq ? ps.map[32 * q + 31 - __clz(bq)] : prev;
-          if (q + 1 < kSlots) prev = m[q] ? ps.map[32 * q + 31 - __clz(m[q])] : prev;
-        }
-      }
-      carry = __shfl_sync(kFull, ow[kSlots - 1], 31);
-      int4 oc[kSlots], en[kSlots];
-      unsigned dd[kSlots];
-      bool sr[kSlots], nr[kSlots];
-      double sv[kSlots];
-      double2 xy[kSlots], zq[kSlots];
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q) {
-        const int k = base + 32 * q + lane;
-        oc[q] = make_int4(0, 0, 0, 0);
-        en[q] = oc[q];
-        if (k < total) oc[q] = ps.cb[ow[q]];
-        en[q] = ldg_if(a.t.nb_ent + oc[q].w + k, k < total);
-        dd[q] = k < total ? pair_dd(oc[q], en[q]) : 0xffffffffu;
-        sr[q] = dd[q] <= a.ns2;
-        nr[q] = sr[q] || dd[q] < a.vdw_cells2;
-      }
-      // loads of this round, all independent: memo values, then records
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q) sv[q] = sr[q] ? pair_short(a, oc[q], en[q]) : 0.0;
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q) {
-        xy[q] = make_double2(0.0, 0.0);
-        zq[q] = xy[q];
-        const double4 r4 = ldg_if(a.t.prec + en[q].z, nr[q]);
-        xy[q] = make_double2(r4.x, r4.y);
-        zq[q] = make_double2(r4.z, r4.w);
-      }
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q)
-        if (nr[q]) {
-          const double2 o01 = ps.x01[ow[q]], o2z = ps.x2z[ow[q]];
-          pair_term(a, make_double4(o01.x, o01.y, o2z.x, o2z.y), dd[q], sv[q], xy[q], zq[q],
-                    hi[q % NA], lo[q % NA], best);
-        }
-    }
-    __syncwarp();
-  }
-  // H7: double-double butterfly (TwoSum is exact, so all lanes agree); min of d^2 >= +0 by its
-  // bit pattern (non-negative doubles order like their unsigned bits)
-  bad = __any_sync(kFull, bad);
-  double H = 0.0, Lo = 0.0;
-  unsigned mhi = 0, mlo = 0;
-  if (!bad) {
-    H = hi[0];
-    Lo = lo[0];
-#pragma unroll
-    for (int u = 1; u < NA; ++u) dd_merge(H, Lo, hi[u], lo[u]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double h2 = __shfl_xor_sync(kFull, H, off);
-      const double l2 = __shfl_xor_sync(kFull, Lo, off);
-      dd_merge(H, Lo, h2, l2);
-    }
-    const unsigned long long bb = (unsigned long long)__double_as_longlong(best);
-    const unsigned bhi = (unsigned)(bb >> 32);
-    mhi = __reduce_min_sync(kFull, bhi);
-    mlo = __reduce_min_sync(kFull, bhi == mhi ? (unsigned)bb : 0xffffffffu);
-  }
-  // H8 is finished per tile (one thread per pose, coalesced stores): keep E and min d^2
-  if (lane == 0) {
-    out.x = bad ? NAN : __dadd_rn(H, Lo);
-    out.y = bad ? NAN : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-    if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
-  }
-}
-
-template <int NA>
-__host__ __device__ constexpr size_t win_offset() {
-  return ((sizeof(PoseRec) * kTile + sizeof(PairStage<NA>) * kWarps) + 255) / 256 * 256;
-}
-
-template <int RT, int NA, bool F32>
+// ---- the fused kernel ---------------------------------------------------------------------
+//
+// RT: compiled CP width (0 = runtime width, L2 rows).  F32: binary32 rows (A21).  WIN: the
+// shared-memory window is used (else every atom reads its rows from L2).
+template <int RT, bool F32, bool WIN>
 __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, int cap_rows,
-                                                            int lig_smem_n, const ChunkPlan cp) {
-  // dynamic shared memory (256-B aligned base; every offset but the ligand's is a compile-time
-  // constant, so addresses are immediates rather than recomputed values):
-  //   [PoseRec x kTile][PairStage x warps][factor-row window, 256-B aligned][ligand 2 x double2 x n]
-  extern __shared__ __align__(256) unsigned char smem_raw[];
+                                                            int lig_smem_n, int loc_cap,
+                                                            const ChunkPlan cp,
+                                                            const __grid_constant__ CUtensorMap tmap,
+                                                            int loc_cd) {
+  // dynamic shared memory: [factor-row window, 256-B aligned][local range table][ligand]
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int kChp = F32 ? Geo32<(RT > 0 ? RT : 4)>::CHP : Geo<(RT > 0 ? RT : 2)>::CHP;
-  PoseRec* s_pose = reinterpret_cast<PoseRec*>(smem_raw);
-  PairStage<NA>* s_ps = reinterpret_cast<PairStage<NA>*>(smem_raw + sizeof(PoseRec) * kTile);
-  double2* win = reinterpret_cast<double2*>(smem_raw + win_offset<NA>());
-  double2* s_lig = reinterpret_cast<double2*>(smem_raw + win_offset<NA>() + (size_t)cap_rows * kChp * 16);
-  __shared__ int s_ok[kTile];
-  __shared__ double2 s_out[kTile];    // per pose of the tile: (E, min d^2), NaN if invalid
+  constexpr unsigned kRow = 16u * kChp;
+  const unsigned raw_u32 = smem_u32(smem_raw);
+  const unsigned win_u32 = (raw_u32 + 255u) & ~255u;
+  const unsigned loc_u32 = win_u32 + (unsigned)cap_rows * kRow;
+  unsigned char* loc_g = smem_raw + (loc_u32 - raw_u32);
+  unsigned* s_loc = reinterpret_cast<unsigned*>(loc_g);   // per coarse cell: begin | count << 24
+#if RS_NBR == 2
+  NbrQueue* s_nq = reinterpret_cast<NbrQueue*>(loc_g + (size_t)loc_cap * sizeof(unsigned));
+  double2* s_lig = reinterpret_cast<double2*>(loc_g + (size_t)loc_cap * sizeof(unsigned) + kQueueBytes);
+#else
+  double2* s_lig = reinterpret_cast<double2*>(loc_g + (size_t)loc_cap * sizeof(unsigned));
+#endif
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
+  __shared__ LocalBox s_lb;
   __shared__ int s_next, s_restaged, s_chunk;
   __shared__ double s_rmax2[kWarps];
   __shared__ __align__(8) uint64_t s_bar;
+#if RS_NBR == 1
+  __shared__ NbrStage s_nbr[kWarps];
+#endif
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // ligand radius (body frame) and staging
+  // ligand radius (body frame) and staging: (y0, y1) then (y2, z), structure-of-arrays
   double r2 = 0.0;
   for (int l = tid; l < a.L; l += kThreads) {
     const double y0 = __ldg(a.yl + 3 * (int64_t)l), y1 = __ldg(a.yl + 3 * (int64_t)l + 1),
@@ -796,6 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     s_cur.lo[0] = s_cur.lo[1] = s_cur.lo[2] = 1;
     s_cur.hi[0] = s_cur.hi[1] = s_cur.hi[2] = 0;   // empty
     s_cur.off[0] = s_cur.off[1] = s_cur.off[2] = 0;
+    s_lb.dim[0] = s_lb.dim[1] = s_lb.dim[2] = 0;
+    s_lb.lo[0] = s_lb.lo[1] = s_lb.lo[2] = 0;
     mbar_init(&s_bar);
   }
   __syncthreads();
@@ -803,17 +616,20 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   for (int w = 0; w < kWarps; ++w) rmax2 = fmax(rmax2, s_rmax2[w]);
   // slack: |R y| <= |y| (1 + 1e-15) plus two cells for the snap rounding and the clamp
   const double rb = sqrt(rmax2) * (1.0 + 1e-12) + 2.0 * a.h;
-  const bool window_mode = RT > 0 && cap_rows > 0;
+  const bool window_mode = WIN && RT > 0 && cap_rows > 0;
+  const int L = (int)a.L;
+  const bool lig_all_smem = L <= lig_smem_n;
+  const int nm1 = a.n - 1;
+  const unsigned rho16 = (unsigned)(lane & 7) << 4;
+  const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   unsigned phase = 0;
 
-  // dynamic chunks of kChunk consecutive poses (a global work counter): the neighbour work per
-  // pose varies by an order of magnitude between translations, so static ranges leave the
-  // busiest SM 2-3x behind the mean
+  // dynamic chunks of consecutive poses (a global work counter): the neighbour work per pose
+  // varies by an order of magnitude between translations, so static ranges leave the busiest
+  // SM 2-3x behind the mean
   for (;;) {
     if (tid == 0) s_chunk = atomicAdd(a.work, 1);
     __syncthreads();
-    // guided schedule (host-computed, ChunkPlan): nbig chunks of `big` poses, then chunks of
-    // `tail` poses so that the CTAs finish together
     const int64_t nbig = cp.nbig;
     const int64_t c0 = s_chunk < nbig ? (int64_t)s_chunk * cp.big
                                       : nbig * cp.big + (int64_t)(s_chunk - nbig) * cp.tail;
@@ -840,38 +656,42 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     int64_t p = c0;
     while (p < p_end) {
       int T = (int)(p_end - p < (int64_t)kTile ? p_end - p : (int64_t)kTile);
-      // H1 for the tile: one thread per pose; per-pose window row bounds
-      int wlo[3] = {INT_MAX, INT_MAX, INT_MAX}, whi[3] = {INT_MIN, INT_MIN, INT_MIN}, wbad = 0;
-      if (tid < T) {
-        const double* pq = a.poses + 7 * (p + tid);
-        double qv[7];
-#pragma unroll
-        for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
-        double Rm[9];
-        const bool ok = quat_rot_dev(qv, Rm);
-        PoseRec& pr = s_pose[tid];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) pr.m[i] = Rm[i];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) pr.m[9 + i] = qv[4 + i];
-        s_ok[tid] = ok ? 1 : 0;
-        if (window_mode) {
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            const double t = qv[4 + r];
-            if (!isfinite(t)) wbad = 1;
-            const double f0 = floor((t - rb + a.b) * a.inv_h) - 1.0;
-            const double f1 = floor((t + rb + a.b) * a.inv_h) + 1.0;
-            wlo[r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
-            whi[r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
-          }
-        }
-      }
       bool fits = false;
       if (window_mode) {
-        // inclusive block scan of the row bounds over the tile's poses: the tile becomes the
-        // longest prefix whose cumulative window fits cap_rows
-        if (warp * 32 < T) {             // warps without poses only join the barriers
+        // per-pose window row bounds t +- rb (thread tid: poses 2 tid, 2 tid + 1), then an
+        // inclusive block scan over the tile's poses: the tile becomes the longest prefix whose
+        // cumulative bounds fit cap_rows
+        int blo[2][3], bhi[2][3], bbad[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = 2 * tid + u;
+          bbad[u] = 0;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            blo[u][r] = INT_MAX;
+            bhi[u][r] = INT_MIN;
+          }
+          if (q < T) {
+            const double* pq = a.poses + 7 * (p + q);
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              const double t = __ldg(pq + 4 + r);
+              if (!isfinite(t)) bbad[u] = 1;
+              const double f0 = floor((t - rb + a.b) * a.inv_h) - 1.0;
+              const double f1 = floor((t + rb + a.b) * a.inv_h) + 1.0;
+              blo[u][r] = (int)fmax(0.0, fmin(f0, (double)(a.n - 1)));
+              bhi[u][r] = (int)fmax(0.0, fmin(f1, (double)(a.n - 1)));
+            }
+          }
+        }
+        // the thread's pair combined, then scanned over threads (exclusive prefix kept)
+        int wlo[3], whi[3], wbad = bbad[0] | bbad[1];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          wlo[r] = min(blo[0][r], blo[1][r]);
+          whi[r] = max(bhi[0][r], bhi[1][r]);
+        }
+        if (warp * 64 < T) {             // warps without poses only join the barriers
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             int v[7];
@@ -900,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           }
         }
         __syncthreads();
-        for (int w = 0; w < warp && warp * 32 < T; ++w) {
+        for (int w = 0; w < warp && warp * 64 < T; ++w) {
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
             wlo[r] = min(wlo[r], s_wred[w][r]);
@@ -908,17 +728,67 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           }
           wbad |= s_wred[w][6];
         }
-        int rows = 0;
+        // cumulative bounds through pose 2 tid: the inclusive scan minus this thread's second pose
+        // (exclusive prefix = the previous lane's inclusive value, or the previous warps' total)
+        int plo[3], phi_[3], pbad;
+        {
+          int v[7];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) rows += whi[r] - wlo[r] + 1;
-        const bool fit_me = tid < T && !wbad && rows <= cap_rows;
-        // fit_me is monotone in tid (cumulative bounds), so the first Tfit poses form the tile
-        const int Tfit = __syncthreads_count(fit_me);
+          for (int r = 0; r < 3; ++r) {
+            v[r] = __shfl_up_sync(kFull, wlo[r], 1);
+            v[3 + r] = __shfl_up_sync(kFull, whi[r], 1);
+          }
+          v[6] = __shfl_up_sync(kFull, wbad, 1);
+          if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              v[r] = INT_MAX;
+              v[3 + r] = INT_MIN;
+            }
+            v[6] = 0;
+            for (int w = 0; w < warp && warp * 64 < T; ++w) {
+#pragma unroll
+              for (int r = 0; r < 3; ++r) {
+                v[r] = min(v[r], s_wred[w][r]);
+                v[3 + r] = max(v[3 + r], s_wred[w][3 + r]);
+              }
+              v[6] |= s_wred[w][6];
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            plo[r] = min(v[r], blo[0][r]);
+            phi_[r] = max(v[3 + r], bhi[0][r]);
+          }
+          pbad = v[6] | bbad[0];
+        }
+        int rows0 = 0, rows1 = 0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          rows0 += phi_[r] - plo[r] + 1;
+          rows1 += whi[r] - wlo[r] + 1;
+        }
+        const bool fit0 = 2 * tid < T && !pbad && rows0 <= cap_rows;
+        const bool fit1 = 2 * tid + 1 < T && !wbad && rows1 <= cap_rows;
+        // the fit flags are monotone in the pose index (cumulative bounds), so the first Tfit
+        // poses form the tile
+        const int Tfit = __syncthreads_count(fit0) + __syncthreads_count(fit1);
         fits = Tfit > 0;
         T = fits ? Tfit : 1;         // a single pose whose rows do not fit takes the L2 path
-        // the tile's last thread owns the tile's bounds: it restages the window if needed
-        if (tid == T - 1) {
-          int rs = 0;
+        // the owner of the tile's last pose holds the tile's cumulative bounds
+        const int rows = ((T - 1) & 1) ? rows1 : rows0;
+        if (!((T - 1) & 1)) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            wlo[r] = plo[r];
+            whi[r] = phi_[r];
+          }
+        }
+        // the tile's last thread owns the tile's bounds: it restages the window if needed and
+        // picks the coarse-cell box of the local range table
+        if (tid == (T - 1) >> 1) {
+          int rs = 0, reloc = 0;
+          unsigned win_bytes = 0;
           bool contained = true;
 #pragma unroll
           for (int r = 0; r < 3; ++r) contained = contained && s_cur.lo[r] <= wlo[r] && whi[r] <= s_cur.hi[r];
@@ -927,26 +797,78 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             int row0 = 0;
             unsigned bytes = 0;
             int lo_[3], hi_[3];
-#pragma unroll
             const bool all = cap_rows >= 3 * a.n;     // the whole factor set fits
+#pragma unroll
             for (int r = 0; r < 3; ++r) {
               lo_[r] = all ? 0 : max(0, wlo[r] - extra / 2);
               hi_[r] = all ? a.n - 1 : min(a.n - 1, whi[r] + (extra - extra / 2));
-              bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16;
+              bytes += (unsigned)(hi_[r] - lo_[r] + 1) * kRow;
             }
             // the window was last read through the generic proxy, before the previous barrier
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&s_bar, bytes);
+            win_bytes = bytes;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
               s_cur.lo[r] = lo_[r];
               s_cur.hi[r] = hi_[r];
               s_cur.off[r] = row0 - lo_[r];
-              const void* src = F32 ? (const void*)(a.t.Fw32[r] + (size_t)lo_[r] * kChp)
-                                    : (const void*)(a.t.Fw[r] + (size_t)lo_[r] * kChp);
-              tma_load_1d(win + (size_t)row0 * kChp, src,
-                          (unsigned)(hi_[r] - lo_[r] + 1) * kChp * 16, &s_bar);
               row0 += hi_[r] - lo_[r] + 1;
+            }
+            rs = 1;
+          }
+          if (fits && loc_cd > 0) {
+            // the local range table: a loc_cd x loc_cd x (loc_cd + 4) box of the packed ranges
+            // around the tile's coarse cells (every atom's cell lies within [wlo, whi]), copied
+            // by one TMA tensor copy whose z origin is a multiple of 4 cells (16-byte aligned rows;
+            // cells outside the global grid arrive as zero counts)
+            const int ext[3] = {loc_cd, loc_cd, loc_cd + 4};
+            int clo[3], chi[3];
+            bool inside = s_lb.dim[0] > 0, fit_box = true;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              clo[r] = wlo[r] >> a.nb_shift;
+              chi[r] = whi[r] >> a.nb_shift;
+              inside = inside && s_lb.lo[r] <= clo[r] && chi[r] < s_lb.lo[r] + ext[r];
+              // the packed table starts kPackPad cells below the grid (TMA coordinates are >= 0)
+              fit_box = fit_box && clo[r] - a.nb_lo[r] + kPackPad >= 4;
+            }
+            clo[2] -= (clo[2] - a.nb_lo[2] + kPackPad) & 3;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) fit_box = fit_box && chi[r] - clo[r] < ext[r];
+            if (!inside) {
+              if (fit_box) {
+                if (!rs) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                  s_lb.lo[r] = clo[r];
+                  s_lb.dim[r] = ext[r];
+                }
+                reloc = 1;
+              } else {
+                s_lb.dim[0] = s_lb.dim[1] = s_lb.dim[2] = 0;   // global lookups for this tile
+              }
+            }
+          }
+          if (rs || reloc) {
+            const unsigned tbytes = reloc ? (unsigned)(loc_cd * loc_cd * (loc_cd + 4)) * 4u : 0u;
+            mbar_expect_tx(&s_bar, win_bytes + tbytes);
+            if (win_bytes) {
+#pragma unroll
+              for (int r = 0; r < 3; ++r) {
+                const int lo_r = s_cur.lo[r], len = s_cur.hi[r] - lo_r + 1;
+                const void* src = F32 ? (const void*)(a.t.Fw32[r] + (size_t)lo_r * kChp)
+                                      : (const void*)(a.t.Fw[r] + (size_t)lo_r * kChp);
+                tma_load_1d(win_u32 + (unsigned)(s_cur.off[r] + lo_r) * kRow, src, (unsigned)len * kRow, &s_bar);
+              }
+            }
+            if (reloc) {
+              const int c0 = s_lb.lo[2] - a.nb_lo[2] + kPackPad, c1 = s_lb.lo[1] - a.nb_lo[1] + kPackPad,
+                        c2 = s_lb.lo[0] - a.nb_lo[0] + kPackPad;
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(loc_u32),
+                  "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(&s_bar))
+                  : "memory");
             }
             rs = 1;
           }
@@ -964,22 +886,344 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         mbar_wait(&s_bar, phase);
         phase ^= 1;
       }
-      const Window W = s_cur;
+      const bool use_win = window_mode && fits;
+      // per-lane window row bases (shared addresses, with the lane's XOR offset in bits 4..)
+      unsigned wb0, wb1, wb2;
+      {
+        const Window W = s_cur;
+        wb0 = win_u32 + (unsigned)W.off[0] * kRow + rho16;
+        wb1 = win_u32 + (unsigned)W.off[1] * kRow + rho16;
+        wb2 = win_u32 + (unsigned)W.off[2] * kRow + rho16;
+      }
+      // local range table: address of coarse cell (cx, cy, cz) = loc_org + ((cx d1 + cy) d2 + cz) 4
+      unsigned loc_org = 0;
+      int ld1 = 0, ld2 = 0;
+      bool use_loc = false;
+      {
+        const LocalBox LB = s_lb;
+        use_loc = use_win && LB.dim[0] > 0;
+        ld1 = LB.dim[1];
+        ld2 = LB.dim[2];
+        loc_org = loc_u32 - (unsigned)((LB.lo[0] * ld1 + LB.lo[1]) * ld2 + LB.lo[2]) * 4u;
+      }
+      // ---- units of the tile -----------------------------------------------------------
       for (;;) {
-        int s = 0;
-        if (lane == 0) s = atomicAdd(&s_next, 1);
+        int s = 0, g = 32;
+        if (lane == 0) {
+          const int r = T - *(volatile int*)&s_next;       // a hint only: ranges come from the atomic
+          if (r < 32 * kWarps) g = min(32, pow2_floor(max(1, r / kWarps)));
+          s = atomicAdd(&s_next, g);
+        }
         s = __shfl_sync(kFull, s, 0);
+        g = __shfl_sync(kFull, g, 0);
         if (s >= T) break;
-        score_pose<RT, NA, F32>(a, p + s, s_pose[s], s_ok[s] != 0, fits, W, (const char*)win, s_lig, lig_smem_n,
-                           lane, s_ps[warp], s_out[s]);
+        const int lgS = 5 - (31 - __clz(g));               // S = 32 / g lanes per pose
+        const int S = 1 << lgS;
+        const int sub = lane & (S - 1);
+        const int sp = s + (lane >> lgS);
+        const bool has = sp < T;
+        const int64_t pp = p + (has ? sp : s);
+        // H1 (O1) in registers: each lane holds its pose's R and t
+        double Rm[9], tv[3];
+        bool ok;
+        {
+          double qv[7];
+          const double* pq = a.poses + 7 * pp;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) qv[i] = __ldg(pq + i);
+          ok = quat_rot_dev(qv, Rm);
+          if (!ok) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) Rm[i] = 0.0;   // x' = t: a cell inside the tile's window
+          }
+#pragma unroll
+          for (int i = 0; i < 3; ++i) tv[i] = qv[4 + i];
+        }
+        const bool live = has && ok;
+        bool bad = has && !ok;
+        double hi = 0.0, lo = 0.0, best = INFINITY;
+        const int nsteps = (L + S - 1) >> lgS;
+#if RS_NBR == 2
+        // H5 + H6 as a per-lane queue: a lane walks the candidate list of one atom at a time, two
+        // entries per atom step, while later atoms with candidates wait on its stack; the entry
+        // pair a lane walks next is loaded one atom step ahead, behind that step's H4 gathers
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0, qz = 0.0;
+        int qc01 = 0, qc2 = 0, qpos = 0, qend = 0, qfc = 0;
+        int4 pf0 = make_int4(0, 0, 0, 0), pf1 = pf0;
+        NbrQueue& nq = s_nq[warp];
+        auto nbr_step = [&]() {
+          const bool act = qpos < qend;
+          if (__any_sync(kFull, act)) {
+#if RS_NPAIR == 2
+            nbr_pair(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, pf1, act,
+                     qpos + 1 < qend, hi, lo, best);
+            qpos += 2;
+#else
+            nbr_one(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, act, hi, lo,
+                    best);
+            qpos += 1;
+#endif
+            if (act && qpos >= qend && qfc > 0) {
+              --qfc;
+              const double2 v01 = nq.x01[qfc][lane], v2z = nq.x2z[qfc][lane];
+              const int4 cb = nq.cb[qfc][lane];
+              q0 = v01.x; q1 = v01.y; q2 = v2z.x; qz = v2z.y;
+              qc01 = cb.x; qc2 = cb.y; qpos = cb.z; qend = cb.w;
+            }
+            const bool more = qpos < qend;
+#if RS_NPAIR == 2
+            if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + qpos, more, pf0, pf1);
+#else
+            if (__any_sync(kFull, more)) pf0 = ldg_int4_p(a.t.nb_ent + qpos, more);
+#endif
+          }
+        };
+#endif
+#if RS_NBR == 2
+        // one candidate round per pass; an atom step only when every lane can take its atom
+        // (idle, or room on its stack); after the last atom, walk until every lane is done
+        for (int it = 0;;) {
+          nbr_step();
+          if (__any_sync(kFull, qfc == kNQ && qpos < qend)) continue;
+          if (it >= nsteps) {
+            if (__any_sync(kFull, qpos < qend)) continue;
+            break;
+          }
+          const int l = (it++ << lgS) + sub;
+#else
+        for (int it = 0; it < nsteps; ++it) {
+          const int l = (it << lgS) + sub;
+#endif
+          const bool act = live && l < L;
+          const int lc = l < L ? l : L - 1;
+          double y0, y1, y2, z;
+          if (lig_all_smem) {
+            const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
+            y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
+          } else {
+            y0 = __ldg(a.yl + 3 * (int64_t)lc);
+            y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
+            y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
+            z = __ldg(a.zl + lc);
+          }
+          // H2 (O2)
+          const double x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
+          const double x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
+          const double x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
+          // H3 (O3): valid iff -b <= x'_a <= b on every axis (false for NaN)
+          const bool inb = fabs(x0) <= a.b && fabs(x1) <= a.b && fabs(x2) <= a.b;
+          bad = bad || (act && !inb);
+          const bool go = act && inb;
+          const int i0 = snap_dev(x0, a.b, a.inv_h, nm1);
+          const int i1 = snap_dev(x1, a.b, a.inv_h, nm1);
+          const int i2 = snap_dev(x2, a.b, a.inv_h, nm1);
+          // candidate range of the coarse cell containing i (the lists hold every protein atom
+          // that can matter to H5/H6 for any point of the cell); issued before H4 so its latency
+          // hides behind the gathers
+          int beg = 0, cnt = 0;
+#if !(defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 1))
+          {
+            const int cx = i0 >> a.nb_shift, cy = i1 >> a.nb_shift, cz = i2 >> a.nb_shift;
+            int2 bc;
+            if (use_loc) {
+              // every atom of a fitting tile (and every lane's stand-in atom) has its coarse cell
+              // inside the tile's box (the row bounds t +- rb contain the atom's cell)
+              const unsigned v = lds_u32(loc_org + (unsigned)((cx * ld1 + cy) * ld2 + cz) * 4u);
+              bc = make_int2((int)(v & 0xffffffu), (int)(v >> 24));
+            } else {
+              const unsigned gx = (unsigned)(cx - a.nb_lo[0]), gy = (unsigned)(cy - a.nb_lo[1]),
+                             gz = (unsigned)(cz - a.nb_lo[2]);
+              const bool in = go && gx < (unsigned)a.nb_dim[0] && gy < (unsigned)a.nb_dim[1] &&
+                              gz < (unsigned)a.nb_dim[2];
+              bc = ldg_if(a.t.nb_range + (gx * a.nb_dim[1] + gy) * a.nb_dim[2] + gz, in);
+            }
+            beg = bc.x;
+            cnt = go ? bc.y : 0;
+          }
+#endif
+#if RS_NBR == 0
+          // the atom's first two candidates, loaded before H4 so their latency hides behind it
+          int4 pe0, pe1;
+          ldg_pair_p(a.t.nb_ent + beg, cnt > 0, pe0, pe1);
+#elif RS_NBR == 2
+          // enqueue this atom's candidates: walk them next if the lane is idle, else stack them
+          // (the pass loop guarantees room); the first entry pair loads behind this step's H4
+          if (cnt > 0) {
+            if (qpos >= qend) {
+              q0 = x0; q1 = x1; q2 = x2; qz = z;
+              qc01 = i0 | (i1 << 16); qc2 = i2; qpos = beg; qend = beg + cnt;
+#if RS_NPAIR == 2
+              ldg_pair_p(a.t.nb_ent + beg, true, pf0, pf1);
+#else
+              pf0 = ldg_int4_p(a.t.nb_ent + beg, true);
+#endif
+            } else {
+              nq.x01[qfc][lane] = make_double2(x0, x1);
+              nq.x2z[qfc][lane] = make_double2(x2, z);
+              nq.cb[qfc][lane] = make_int4(i0 | (i1 << 16), i2, beg, beg + cnt);
+              ++qfc;
+            }
+          }
+#endif
+          // H4 (O4)
+          double phi = 0.0;
+          if constexpr (RT > 0) {
+            if (use_win) {
+              // every row of a fitting tile is staged (the tile's bounds contain t +- rb, and
+              // lanes without a real atom stand in with an atom of a pose of the tile)
+              const unsigned r0 = wb0 + (unsigned)i0 * kRow;
+              const unsigned r1 = wb1 + (unsigned)i1 * kRow;
+              const unsigned r2 = wb2 + (unsigned)i2 * kRow;
+#if defined(RS_EXPERIMENT) && (RS_EXPERIMENT & 2)
+              double v = z;
+#else
+              double v;
+              if constexpr (F32) v = (double)SmemTree32<0, 1, Geo32<RT>::NS>::eval(r0, r1, r2);
+              else v = SmemTree<0, 1, Geo<RT>::NS>::eval(r0, r1, r2);
+#endif
+              phi = go ? v : 0.0;
+            } else if (go) {
+              if constexpr (WIN) {       // a single pose whose rows do not fit: out of line
+                if constexpr (F32) phi = long_phi_global32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
+                else phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2);
+              } else if constexpr (F32) {
+                phi = long_phi_l2_32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
+              } else {
+                phi = long_phi_l2<RT>((const double2*)(a.t.F[0] + (size_t)i0 * RT),
+                                      (const double2*)(a.t.F[1] + (size_t)i1 * RT),
+                                      (const double2*)(a.t.F[2] + (size_t)i2 * RT));
+              }
+            }
+          } else {
+            if (go)
+              phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
+                                a.t.F[2] + (size_t)i2 * a.R, a.R);
+          }
+          const double zg = go ? z : 0.0;
+          dd_add_prod(hi, lo, zg, phi);
+#if RS_NBR == 0
+          // H5 + H6 over the atom's candidates, two list entries per round (lists start at even
+          // entries, so a pair is one aligned 32-byte load); the loop runs while any lane of
+          // the warp has candidates left
+          if (__any_sync(kFull, cnt > 0)) {
+            int4 en0 = pe0, en1 = pe1;
+            for (int j = 0;;) {
+              const bool a0 = j < cnt, a1 = j + 1 < cnt;
+              int e00, e01, e02, e10, e11, e12;
+              unsigned dd0 = entry_dd(i0, i1, i2, en0, e00, e01, e02);
+              unsigned dd1 = entry_dd(i0, i1, i2, en1, e10, e11, e12);
+              dd0 = a0 ? dd0 : 0xffffffffu;
+              dd1 = a1 ? dd1 : 0xffffffffu;
+              const bool sr0 = dd0 <= a.ns2, sr1 = dd1 <= a.ns2;
+              const bool v0 = dd0 < a.vdw_cells2, v1 = dd1 < a.vdw_cells2;
+              const double4 rc0 = ldg_d4_p(a.t.prec + en0.z, sr0 || v0);
+              const double4 rc1 = ldg_d4_p(a.t.prec + en1.z, sr1 || v1);
+              const double sv0 = short_value(a, e00, e01, e02, sr0);
+              const double sv1 = short_value(a, e10, e11, e12, sr1);
+              j += 2;
+              const bool more = j < cnt;
+              if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + beg + j, more, en0, en1);
+              pair_hit(x0, x1, x2, rc0, v0, best);
+              pair_hit(x0, x1, x2, rc1, v1, best);
+              if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(rc0.w, sv0));
+              if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(rc1.w, sv1));
+              if (!__any_sync(kFull, more)) break;
+            }
+          }
+#elif RS_NBR == 1
+          // H5 + H6 over the step's (atom, candidate) pairs flattened across the warp: owners
+          // (lanes whose atom has candidates) stage their atom, pair lanes take consecutive
+          // candidates of the concatenated lists, write (d^2, fl(z_m s)) per pair, and each
+          // owner merges its own pairs' results (the pose sums are order-free, O6/O7)
+          if (__any_sync(kFull, cnt > 0)) {
+            NbrStage& ns_ = s_nbr[warp];
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(kFull, incl, o);
+              if (lane >= o) incl += v;
+            }
+            const int total = __shfl_sync(kFull, incl, 31);
+            const int excl = incl - cnt;
+            if (cnt > 0) {
+              ns_.x01[lane] = make_double2(x0, x1);
+              ns_.x2z[lane] = make_double2(x2, z);
+              ns_.cb[lane] = make_int4(i0, i1, i2, beg - excl);
+            }
+            int carry = 0;
+            for (int base = 0; base < total; base += 32) {
+              const int rel = excl - base;
+              const bool starts = cnt > 0 && rel >= 0 && rel < 32;
+              if (starts) ns_.map[rel] = lane;
+              const unsigned M = __reduce_or_sync(kFull, starts ? 1u << (rel & 31) : 0u);
+              __syncwarp();
+              const unsigned mk = M & lanemask_le;
+              const int owner = mk ? ns_.map[31 - __clz(mk)] : carry;
+              carry = __shfl_sync(kFull, owner, 31);
+              const int k = base + lane;
+              const bool act = k < total;
+              const int4 oc = ns_.cb[owner];
+              const int4 en = ldg_int4_p(a.t.nb_ent + oc.w + k, act);
+              int e0, e1, e2;
+              unsigned dd = entry_dd(oc.x, oc.y, oc.z, en, e0, e1, e2);
+              dd = act ? dd : 0xffffffffu;
+              const bool sr = dd <= a.ns2, vr = dd < a.vdw_cells2;
+              const double4 rc = ldg_d4_p(a.t.prec + en.z, sr || vr);
+              const double sv = short_value(a, e0, e1, e2, sr);
+              double d2 = INFINITY;
+              if (vr) {
+                const double2 o01 = ns_.x01[owner], o2z = ns_.x2z[owner];
+                const double dx0 = __dsub_rn(o01.x, rc.x);
+                const double dx1 = __dsub_rn(o01.y, rc.y);
+                const double dx2 = __dsub_rn(o2z.x, rc.z);
+                d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
+              }
+              const double bterm = sr ? __dmul_rn(rc.w, sv) : 0.0;
+              // only pairs below D_cap (they may lower the min) or inside the ball reach the owner
+              const bool keep = sr || d2 < a.dcap2;
+              if (keep) ns_.res[lane] = make_double2(d2, bterm);
+              const unsigned kept = __ballot_sync(kFull, keep);
+              __syncwarp();
+              // each owner merges its kept pairs of this round (slots [excl - base, incl - base))
+              const int jlo = max(excl - base, 0), jhi = min(incl - base, 32);
+              unsigned my = 0;
+              if (jhi > jlo) {
+                const unsigned hiw = jhi >= 32 ? 0xffffffffu : ((1u << jhi) - 1u);
+                my = kept & hiw & ~((1u << jlo) - 1u);
+              }
+              while (__any_sync(kFull, my != 0)) {
+                if (my) {
+                  const int j = __ffs(my) - 1;
+                  my &= my - 1u;
+                  const double2 r = ns_.res[j];
+                  best = r.x < best ? r.x : best;
+                  if (r.y != 0.0) dd_add_prod(hi, lo, z, r.y);
+                }
+              }
+              __syncwarp();
+            }
+          }
+#endif
+        }
+        // H7: merge the S lanes of each pose (xor butterfly within aligned groups of S lanes;
+        // TwoSum is exact, so partners agree); min d^2 and the invalid flag likewise
+        for (int off = S >> 1; off > 0; off >>= 1) {
+          const double h2 = __shfl_xor_sync(kFull, hi, off);
+          const double l2 = __shfl_xor_sync(kFull, lo, off);
+          dd_merge(hi, lo, h2, l2);
+          const double b2 = __shfl_xor_sync(kFull, best, off);
+          best = b2 < best ? b2 : best;
+          const int bo = __shfl_xor_sync(kFull, (int)bad, off);
+          bad = bad || bo != 0;
+        }
+        // H8: E = hi + lo; d = sqrt(min d^2) below D_cap^2, else +inf; NaN if invalid (O8)
+        if (has && sub == 0) {
+          a.E[pp] = bad ? NAN : __dadd_rn(hi, lo);
+          a.D[pp] = bad ? NAN : (best < a.dcap2 ? __dsqrt_rn(best) : INFINITY);
+          if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
+        }
       }
       __syncthreads();
-      // H8: d = sqrt(min d^2) below D_cap^2, else +inf; NaN for invalid poses (O8)
-      if (tid < T) {
-        const double2 o = s_out[tid];
-        a.E[p + tid] = o.x;
-        a.D[p + tid] = isnan(o.y) ? NAN : (o.y < a.dcap2 ? __dsqrt_rn(o.y) : INFINITY);
-      }
       if (a.done) {
         // release the tile's outputs to the copy stream that waits on done[chunk]
         __threadfence();
@@ -1001,51 +1245,119 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   }
 }
 
+// Per-device launch state, set up once (std::call_once: concurrent first launches are safe)
 struct DevCache {
+  std::once_flag once;
   int sms = 0;
   int smem_optin = 0;
-  bool attr_set[24] = {false};
-  int max_dyn[24] = {0};
+  int init_err = 0;
+  std::once_flag attr_once[32];
+  int attr_err[32] = {0};
+  int max_dyn[32] = {0};
 };
 DevCache g_dev[64];
 
-template <int RT, int NA, bool F32>
-int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window_mode) {
+constexpr int kNoWindow = -12345;   // launch_t<.., WIN = true>: use the L2 variant instead
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+PFN_encodeTiled encode_tiled() {
+  static std::once_flag once;
+  static PFN_encodeTiled fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// Tensor map of the packed neighbour ranges (uint32, z fastest) with a cd x cd x (cd + 4) box; false if it
+// cannot be built (the kernel then uses global range lookups)
+bool local_table_map(const ScoreArgs& a, int cd, CUtensorMap* m) {
+  PFN_encodeTiled enc = encode_tiled();
+  if (!enc || !a.t.nb_pack || cd <= 0) return false;
+  const cuuint64_t e1 = (cuuint64_t)a.nb_dim[1] + kPackPad, e0 = (cuuint64_t)a.nb_dim[0] + kPackPad;
+  const cuuint64_t dims[3] = {(cuuint64_t)a.nb_dim2p, e1, e0};
+  const cuuint64_t strides[2] = {(cuuint64_t)a.nb_dim2p * 4u, (cuuint64_t)a.nb_dim2p * e1 * 4u};
+  const cuuint32_t box[3] = {(cuuint32_t)cd + 4u, (cuuint32_t)cd, (cuuint32_t)cd};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)a.t.nb_pack, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int RT, bool F32, bool WIN>
+int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot) {
   DevCache& dc = g_dev[dev & 63];
-  if (!dc.attr_set[slot]) {
+  std::call_once(dc.attr_once[slot], [&] {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT, NA, F32>);
-    if (e != cudaSuccess) return (int)e;
-    dc.max_dyn[slot] = dc.smem_optin - (int)fa.sharedSizeBytes;
-    e = cudaFuncSetAttribute(score_kernel<RT, NA, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dc.max_dyn[slot]);
-    if (e != cudaSuccess) return (int)e;
-    dc.attr_set[slot] = true;
-  }
+    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<RT, F32, WIN>);
+    if (e == cudaSuccess) {
+      const int m = dc.smem_optin - (int)fa.sharedSizeBytes;
+      e = cudaFuncSetAttribute(score_kernel<RT, F32, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+      if (e == cudaSuccess) dc.max_dyn[slot] = m;
+    }
+    dc.attr_err[slot] = (int)e;
+  });
+  if (dc.attr_err[slot]) return dc.attr_err[slot];
   constexpr int kChp = F32 ? Geo32<(RT > 0 ? RT : 4)>::CHP : Geo<(RT > 0 ? RT : 2)>::CHP;
-  const size_t fixed = win_offset<NA>();
+  constexpr size_t kRowB = 16 * (size_t)kChp;
+  const size_t fixed = 256 + kQueueBytes;      // alignment slack of the window base, neighbour queues
   const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
   const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
-  int cap_rows = 0;
-  if (RT > 0 && window_mode && (F32 ? (const void*)a.t.Fw32[0] : (const void*)a.t.Fw[0])) {
-    cap_rows = (int)std::min<size_t>((avail - lig_res) / (16 * kChp), (1u << 20) / (16 * kChp) - 1);
+  int cap_rows = 0, loc_cap = 0, loc_cd = 0;
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if constexpr (RT > 0 && WIN) {
+    if (!(F32 ? (const void*)a.t.Fw32[0] : (const void*)a.t.Fw[0])) return kNoWindow;
+#ifndef RS_NO_TMA_LOC
+    if (a.loc4 && a.t.nb_pack) {
+#else
+    if (false) {
+#endif
+      // local range table: a cd^3 box of coarse cells, cd a multiple of 4 (16-byte TMA rows),
+      // large enough for one translation's atoms when the ligand radius is known
+      int cd = 20;
+      if (a.rmax_hint >= 0) {
+        const double rows = 2.0 * (a.rmax_hint * (1.0 + 1e-12) + 2.0 * a.h) / a.h + 3.0;
+        cd = (int)std::ceil(rows / double(1 << a.nb_shift)) + 1;
+        cd = (cd + 3) / 4 * 4;
+      }
+      if (cd * cd * (cd + 4) <= RS_LOC_CELLS && local_table_map(a, cd, &tmap)) {
+        loc_cd = cd;
+        loc_cap = cd * cd * (cd + 4);
+      }
+    }
+    const size_t loc_b = (size_t)loc_cap * sizeof(unsigned);
+    cap_rows = (int)std::min<size_t>((avail - lig_res - std::min(avail - lig_res, loc_b)) / kRowB,
+                                     (1u << 20) / kRowB - 1);
     if (3 * a.n <= cap_rows) {
       // the whole factor set fits (small grids, e.g. C1): stage it once, every tile fits
       cap_rows = 3 * a.n;
     } else if (a.rmax_hint >= 0) {
-      // leave the rest of the 228 KB to L1 (cell lists, records, memo): what one
-      // translation's window needs plus RS_WIN_SLACK; no window at all when even one
-      // translation's rows do not fit (every pose would be its own tile with its own restage:
-      // the L2 path is faster then)
+      // what one translation's window needs plus RS_WIN_SLACK (the rest of the 228 KB is L1
+      // for the candidate lists, records and the short-range memo); no window at all when even
+      // one translation's rows do not fit (every pose would be its own tile with its own
+      // restage: the L2 variant is faster then)
       const double need = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 8.0);
-      if (need > cap_rows) cap_rows = 0;
-      else cap_rows = std::min(cap_rows, (int)std::max(64.0, RS_WIN_SLACK * need));
+      if (need > cap_rows) return kNoWindow;
+      cap_rows = std::min(cap_rows, (int)std::max(64.0, RS_WIN_SLACK * need));
     }
+    if (cap_rows <= 0) return kNoWindow;
   }
-  const size_t win_b = (size_t)cap_rows * 16 * kChp;
-  const int64_t lig_fit = (int64_t)((avail - std::min(avail, win_b)) / sizeof(double4));
+  const size_t win_b = (size_t)cap_rows * kRowB;
+  const size_t loc_b = (size_t)loc_cap * sizeof(unsigned);
+  const size_t used = std::min(avail, win_b + loc_b);
+  const int64_t lig_fit = (int64_t)((avail - used) / sizeof(double4));
   const int lig_n = (int)std::min<int64_t>(a.L, cap_rows > 0 ? std::min<int64_t>(lig_fit, 256) : lig_fit);
-  const size_t dyn = fixed + win_b + (size_t)lig_n * sizeof(double4);
+  const size_t dyn = fixed + win_b + loc_b + (size_t)lig_n * sizeof(double4);
   // chunk plan: big chunks for the first (1 - 1/RS_TAIL_DIV) of the poses, then tail chunks of
   // at most kTailChunk poses, small enough that every SM gets work when P is small
   // (big chunks also shrink with P: at least ~4 per SM, so one chunk never dominates a launch)
@@ -1057,7 +1369,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool window
   const int64_t chunks = cp.nbig + (rest + cp.tail - 1) / cp.tail;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
-  score_kernel<RT, NA, F32><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n, cp);
+  score_kernel<RT, F32, WIN><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n, loc_cap, cp, tmap, loc_cd);
   return (int)cudaGetLastError();
 }
 
@@ -1086,13 +1398,13 @@ int launch_fill_short_memo(const double* S0, const double* S1, const double* S2,
 
 const char* score_kernel_variant(int R) {
   switch (R) {
-    case 4: return "score_kernel<4, NA>";
-    case 8: return "score_kernel<8, NA>";
-    case 12: return "score_kernel<12, NA>";
-    case 16: return "score_kernel<16, NA>";
-    case 24: return "score_kernel<24, NA>";
-    case 32: return "score_kernel<32, NA>";
-    default: return "score_kernel<0, NA> (runtime R)";
+    case 4: return "score_kernel<4>";
+    case 8: return "score_kernel<8>";
+    case 12: return "score_kernel<12>";
+    case 16: return "score_kernel<16>";
+    case 24: return "score_kernel<24>";
+    case 32: return "score_kernel<32>";
+    default: return "score_kernel<0> (runtime R)";
   }
 }
 
@@ -1151,58 +1463,41 @@ void pack_window_rows32(const std::vector<double>& F, int n, int R, std::vector<
 
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   if (a.P <= 0) return 0;
+  if (a.L > (int64_t)1 << 30) return (int)cudaErrorInvalidValue;   // the kernel indexes atoms in int
   DevCache& dc = g_dev[device & 63];
-  if (dc.sms == 0) {
-    cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, device);
-    cudaDeviceGetAttribute(&dc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  }
+  std::call_once(dc.once, [&] {
+    cudaError_t e = cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&dc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    dc.init_err = (int)e;
+  });
+  if (dc.init_err) return dc.init_err;
   cudaStream_t st = (cudaStream_t)stream;
-  // window mode unless the ligand alone spans more rows than the window can hold
-  bool window_mode = true;
-  if (a.rmax_hint >= 0) {
-    const double rows = 3.0 * (2.0 * (a.rmax_hint + 2.0 * a.h) / a.h + 4.0);
-    const double row_b = a.f32 ? 128.0 : 16.0 * (a.R <= 8 ? 8 : ((a.R / 2 + 7) / 8) * 8);
-    window_mode = rows * row_b <= 0.75 * double(dc.smem_optin);
-  }
-  // one atom per lane and pass (NA = 2, two independent chains per lane, needs the registers
-  // of a 512-thread CTA and measured slower than 32 resident warps with NA = 1)
-#ifdef RS_FORCE_NA
-  const int na = RS_FORCE_NA, sl = na == 2 ? 8 : 0;
-#else
-  const int na = (kThreads <= 512 && a.L > 32) ? 2 : 1, sl = na == 2 ? 8 : 0;
-#endif
   int e;
   if (a.f32) {
     // binary32 factors (A21): compiled widths only (the build refuses others)
+#define RS_F32_CASE(RR, SLOT)                                                               \
+  case RR:                                                                                 \
+    e = launch_t<RR, true, true>(a, st, device, SLOT);                                     \
+    if (e == kNoWindow) e = launch_t<RR, true, false>(a, st, device, SLOT + 1);            \
+    break;
     switch (a.R) {
-      case 4: e = launch_t<4, 1, true>(a, st, device, 17, window_mode); break;
-      case 8: e = launch_t<8, 1, true>(a, st, device, 18, window_mode); break;
-      case 12: e = launch_t<12, 1, true>(a, st, device, 19, window_mode); break;
-      case 16: e = launch_t<16, 1, true>(a, st, device, 20, window_mode); break;
-      case 24: e = launch_t<24, 1, true>(a, st, device, 21, window_mode); break;
-      case 32: e = launch_t<32, 1, true>(a, st, device, 22, window_mode); break;
+      RS_F32_CASE(4, 20) RS_F32_CASE(8, 22) RS_F32_CASE(12, 24) RS_F32_CASE(16, 26)
+      RS_F32_CASE(24, 28) RS_F32_CASE(32, 30)
       default: return (int)cudaErrorInvalidValue;
     }
-  } else if (kThreads <= 512 && na == 2) {
-    switch (a.R) {
-      case 4: e = launch_t<4, 2, false>(a, st, device, 9, window_mode); break;
-      case 8: e = launch_t<8, 2, false>(a, st, device, 10, window_mode); break;
-      case 12: e = launch_t<12, 2, false>(a, st, device, 11, window_mode); break;
-      case 16: e = launch_t<16, 2, false>(a, st, device, 12, window_mode); break;
-      case 24: e = launch_t<24, 2, false>(a, st, device, 13, window_mode); break;
-      case 32: e = launch_t<32, 2, false>(a, st, device, 14, window_mode); break;
-      default: e = launch_t<0, 2, false>(a, st, device, 8, false); break;
-    }
+#undef RS_F32_CASE
   } else {
+#define RS_F64_CASE(RR, SLOT)                                                               \
+  case RR:                                                                                 \
+    e = launch_t<RR, false, true>(a, st, device, SLOT);                                    \
+    if (e == kNoWindow) e = launch_t<RR, false, false>(a, st, device, SLOT + 1);           \
+    break;
     switch (a.R) {
-      case 4: e = launch_t<4, 1, false>(a, st, device, 1, window_mode); break;
-      case 8: e = launch_t<8, 1, false>(a, st, device, 2, window_mode); break;
-      case 12: e = launch_t<12, 1, false>(a, st, device, 3, window_mode); break;
-      case 16: e = launch_t<16, 1, false>(a, st, device, 4, window_mode); break;
-      case 24: e = launch_t<24, 1, false>(a, st, device, 5, window_mode); break;
-      case 32: e = launch_t<32, 1, false>(a, st, device, 6, window_mode); break;
-      default: e = launch_t<0, 1, false>(a, st, device, 0, false); break;
+      RS_F64_CASE(4, 2) RS_F64_CASE(8, 4) RS_F64_CASE(12, 6) RS_F64_CASE(16, 8)
+      RS_F64_CASE(24, 10) RS_F64_CASE(32, 12)
+      default: e = launch_t<0, false, false>(a, st, device, 0); break;
     }
+#undef RS_F64_CASE
   }
   if (launches) *launches += 1;
   return e;

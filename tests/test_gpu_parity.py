@@ -643,10 +643,10 @@ def test_shards_concatenate_bitwise(env):
 
 # ----------------------------------------------------------------------------- maximum sizes
 
-def test_max_grid_no_memo_no_window(env):
+def test_max_grid_no_window(env):
     """n = 32768 (the largest grid; cells need all 15 bits of the packed entries), h = 1/256 A:
-    n_sigma = 256, so the dense short-range memo would exceed its budget and every O5 value
-    runs the explicit chain; a translation's rows exceed shared memory, so H4 reads L2."""
+    n_sigma = 256 (a 136 MB short-range memo); a translation's rows exceed shared memory, so
+    H4 reads L2."""
     torch, rsdock, rs_oracle = env
     w = syn.random_small(seed=90, M=60, L=12, n=32768, b=64.0, R=8, P=200, protein_radius=4.0,
                          trans=3.0)
