@@ -113,9 +113,74 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def load_workload(name):
+def load_workload(name, pose_stream=0):
     from synth import configs as syn
-    return syn.make(name)
+    return syn.make(name, pose_stream=pose_stream)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside a launcher: re-run this command under torch.distributed.run
+    with N processes on this node (one per GPU, rendezvous on 127.0.0.1); rank 0 prints the
+    line.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # communicator init lines (nranks) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
+def rank_batch(args, world, rank):
+    """This rank's poses: weak scaling -- an independent batch of the config's size per rank
+    (pose_stream = rank; rank 0 holds the canonical batch); strong scaling -- the contiguous
+    slice shard_bounds(P, world, rank) of the one canonical batch (translation tiles stay
+    compact).  Returns (workload, lo, hi, global P)."""
+    from paper_2510_26611_b200.shard import shard_bounds
+    if args.scaling == "weak":
+        w = load_workload(args.config, pose_stream=rank)
+        return w, 0, w.P, w.P * world
+    w = load_workload(args.config)
+    lo, hi = shard_bounds(w.P, world, rank)
+    return w, lo, hi, w.P
+
+
+def bench_dry_run(args):
+    """The multi-rank plumbing of the bench without a GPU (gloo): per-rank batches, barrier,
+    max-over-ranks step time, rank-0 line.  For the CPU tests of the launcher."""
+    import hashlib
+    import torch
+    world, rank = _env_int("WORLD_SIZE", 1), _env_int("RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    w, lo, hi, Pg = rank_batch(args, world, rank)
+    digest = int(hashlib.sha1(np.ascontiguousarray(w.poses[lo:hi]).tobytes()).hexdigest()[:12], 16)
+    ms = torch.tensor([1.0 + 0.25 * rank], dtype=torch.float64)      # stand-in per-rank times
+    digests = [torch.tensor([digest], dtype=torch.int64) for _ in range(world)]
+    if dist:
+        dist.barrier()
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_gather(digests, torch.tensor([digest], dtype=torch.int64))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": args.scaling,
+                          "ms_per_step": float(ms.item()),
+                          "value": Pg / (float(ms.item()) * 1e-3), "poses_per_rank": hi - lo,
+                          "global_poses": Pg, "rank_digests": [int(d.item()) for d in digests]}),
+              flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
 
 
 def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7, f32=False):
@@ -186,7 +251,10 @@ def config_dict(w, args):
                         f"box b={w.box_half_width}, R={w.rank_R}, P={w.P} poses",
             "config": args.config, "M": w.M, "L": w.L, "n": w.grid_n, "R": w.rank_R,
             "poses": w.P, "sigma_split": w.sigma_split, "sigma_vdw": w.sigma_vdw,
-            "parallelism": f"pose-shard x{args.gpus} (replicated handle)",
+            "parallelism": (f"dp{_env_int('WORLD_SIZE', 1)}: " +
+                            ("an independent pose batch per rank" if getattr(args, "scaling", "weak") == "weak"
+                             else "the batch split into contiguous slices") +
+                            ", replicated handle, no data-path collective"),
             "mode": ("forces (rs_score_forces, N1)" if getattr(args, "forces", False) else "energy + mindist")
                     + (", fp32 factors (A21)" if getattr(args, "f32", False) else "")
                     + (", Eq. (23) complex: 2 proteins x R/2, rank-concatenated (A24)"
@@ -298,7 +366,17 @@ def main():
                     help="the fp32-factor variant (RS_FLAG_F32_FACTORS, DESIGN.md reading A21)")
     ap.add_argument("--nbr-cell", type=float, default=0.0,
                     help="edge [A] of the neighbour-list cells (0 = the library's automatic choice)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: an independent batch of the config's size per rank; strong: the "
+                         "one batch split into contiguous slices over the ranks")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="the multi-rank plumbing only (gloo, no GPU): per-rank batches, max-over-"
+                         "ranks timing, rank-0 line (used by the CPU tests)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if args.dry_run:
+        return bench_dry_run(args)
     if args.impl == "reference":
         return impl_reference(args)
     if args.ppiem:
@@ -323,7 +401,10 @@ def main():
         dist.barrier()
     from paper_2510_26611_b200 import rsdock
 
-    w = load_workload(args.config)
+    w, lo, hi, P_global = rank_batch(args, world, rank)
+    if rank == 0 and dist:
+        print(f"bench: NCCL communicator initialised, nranks={world}, scaling={args.scaling}",
+              file=sys.stderr, flush=True)
     ncpu = os.cpu_count() or 1
     t0 = time.perf_counter()
     fl = rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0
@@ -372,8 +453,8 @@ def main():
 
     q = torch.tensor(w.ligand_q, device=dev)
     y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
-    poses = torch.tensor(w.poses, device=dev).contiguous()
-    P, L = w.P, w.L
+    poses = torch.tensor(w.poses[lo:hi], device=dev).contiguous()
+    P, L = hi - lo, w.L
     E = torch.empty(P, dtype=torch.float64, device=dev)
     D = torch.empty(P, dtype=torch.float64, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -413,13 +494,13 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     ms = total_ms / args.steps
-    value = world * P / (ms * 1e-3)
+    value = P_global / (ms * 1e-3)           # every rank's poses / the slowest rank's time
     invalid = int(cnt.item())
 
     # end to end through the same C ABI with pinned HOST buffers (copies inside the call)
     e2e = None
     if not args.no_e2e:
-        hp = torch.from_numpy(w.poses).pin_memory()
+        hp = torch.from_numpy(np.ascontiguousarray(w.poses[lo:hi])).pin_memory()
         hq = torch.from_numpy(w.ligand_q).pin_memory()
         hy = torch.from_numpy(np.ascontiguousarray(w.ligand_xyz)).pin_memory()
         hE = torch.empty(P, dtype=torch.float64).pin_memory()
@@ -447,7 +528,7 @@ def main():
             hts.append(ev0.elapsed_time(ev1) * 1e-3)
         h2d_gbs = hp.numel() * 8 / min(hts) / 1e9
         del dbuf
-        e2e = {"value": world * P / te, "unit": "poses/s",
+        e2e = {"value": P_global / te, "unit": "poses/s",
                "h2d_bytes_per_step": int(P * 7 * 8 + L * 4 * 8), "d2h_bytes_per_step": int(P * 2 * 8),
                "h2d_pinned_gbs": h2d_gbs,
                "upload_bound_poses_per_s": world * h2d_gbs * 1e9 / 56.0,
@@ -501,7 +582,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32-factors/f64" if args.f32 else "f64",
         "data": "synthetic", "atom_evals_per_s": value * L,
         "config": config_dict(w, args),

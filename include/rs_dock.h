@@ -260,7 +260,10 @@ int rs_export_setup(const rs_handle* h, double* t, double* a, int32_t* is_long,
  *     d = +inf (no protein atom within D_cap):  s <- s - (D_cap - sigma_vdw)
  *     d - sigma_vdw <= tol:                      converged (vdW contact)
  *     otherwise:                                 s <- s - (d - sigma_vdw) * 0.999
- * all poses advancing together, one batched scoring launch per iteration (at most max_iter).
+ * (a later d below sigma_vdw can only come from rounding: contact); all poses advance
+ * together, one batched scoring launch per iteration (at most max_iter).  Every dirs[j] must be
+ * a unit vector to within 1e-9 (else RS_E_INVALID_ARG: a longer direction could step past the
+ * clearance).
  * Outputs (host arrays, row j, column k, m_P x m_L): energy at the final position (A4-A5; NaN
  * unless status is 0 or 4), the final s and a status: 0 contact reached, 1 a ligand atom left
  * the box, 2 clash at s_start, 3 passed the centre without contact (s < 0), 4 max_iter reached

@@ -54,7 +54,8 @@ def scan(tables, X, qM, Y, zL, centre, dirs, quats, s_start, sigma, dcap, tol=1e
                 else:
                     delta = d - sigma
                     if delta < 0.0:
-                        status[j, k] = 2 if it == 0 else 1
+                        # later only rounding puts d below sigma: contact (A23)
+                        status[j, k] = 2 if it == 0 else 0
                         continue
                     if delta <= tol:
                         status[j, k] = 0

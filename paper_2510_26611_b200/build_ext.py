@@ -22,7 +22,7 @@ def _stale():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(PKG, "csrc", "*.h")) + \
+    deps = sources() + glob.glob(os.path.join(PKG, "csrc", "*.h")) + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + \
         [os.path.join(ROOT, "include", "rs_dock.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 

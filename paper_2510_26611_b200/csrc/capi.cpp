@@ -78,6 +78,10 @@ void free_device(rs_handle* h) {
   }
   if (h->d_work) cudaFree(h->d_work);
   h->d_work = nullptr;
+  for (void*& ev : h->work_ev) {
+    if (ev) cudaEventDestroy((cudaEvent_t)ev);
+    ev = nullptr;
+  }
   if (h->scan_buf) cudaFree(h->scan_buf);
   h->scan_buf = nullptr;
   h->scan_bytes = 0;
@@ -202,8 +206,6 @@ int upload_handle(rs_handle* h) {
       if (int e = upload(&h->d_Fw[a], packed, &bytes)) return e;
     }
   }
-  CUDA_TRY(cudaMalloc(&h->d_work, rs::kWorkSlots * sizeof(int)), RS_E_NOMEM);
-  CUDA_TRY(cudaMemset(h->d_work, 0, rs::kWorkSlots * sizeof(int)), RS_E_CUDA);
   // dense memo of the short-range chain over |D_a| <= n_sigma, filled on the device by the same
   // O5 op sequence (ascending k; all zeros when R_s = 0); the scoring kernel reads O5 values
   // only from it (C3: 2.2 MB, C5 at sigma_s = 6 A: 136 MB)
@@ -213,6 +215,9 @@ int upload_handle(rs_handle* h) {
             "doubles) would exceed 2 GiB; use a larger grid step or a smaller sigma_split");
     return RS_E_NOMEM;
   }
+  CUDA_TRY(cudaMalloc(&h->d_work, rs::kWorkSlots * sizeof(int)), RS_E_NOMEM);
+  for (int k = 0; k < rs::kWorkSlots; ++k)
+    CUDA_TRY(cudaEventCreateWithFlags((cudaEvent_t*)&h->work_ev[k], cudaEventDisableTiming), RS_E_CUDA);
   CUDA_TRY(cudaMalloc(&h->d_memo, (size_t)memo_b), RS_E_NOMEM);
   bytes += (int64_t)memo_b;
   {
@@ -275,16 +280,24 @@ int pointer_kind(const void* p) {
 }
 
 // Ligand radius max |y_l| (body frame).  Only steers the launch shape (shared-memory window
-// or not); correctness never depends on it (the kernel recomputes it).  Device ligands are
-// read back once per (pointer, L) and cached on the handle.
-double ligand_rmax(rs_handle* h, const double* yl, int64_t L, bool dev) {
+// or not, local-table box); correctness never depends on it (the kernel recomputes it).  Device
+// ligands are read back once per (pointer, L) with a copy ordered on the caller's stream and
+// cached on the handle (a reused buffer keeps the old shape hint: at worst a slower launch);
+// under stream capture no readback happens and the launch sizes itself without the hint.
+double ligand_rmax(rs_handle* h, const double* yl, int64_t L, bool dev, cudaStream_t st) {
   if (L <= 0) return 0.0;
   std::vector<double> tmp;
   const double* y = yl;
   if (dev) {
     if (h->rmax_key == (const void*)yl && h->rmax_L == L) return h->rmax_val;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return -1.0;
+    }
     tmp.resize(3 * (size_t)L);
-    if (cudaMemcpy(tmp.data(), yl, 3 * (size_t)L * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    if (cudaMemcpyAsync(tmp.data(), yl, 3 * (size_t)L * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
       cudaGetLastError();
       return -1.0;
     }
@@ -300,6 +313,27 @@ double ligand_rmax(rs_handle* h, const double* yl, int64_t L, bool dev) {
     h->rmax_val = r;
   }
   return r;
+}
+
+// One scoring launch with a dynamic-schedule work counter that no other launch in flight holds:
+// a ring of kWorkSlots counters on the handle, each reused only after the event recorded behind
+// its previous launch (the stream waits on it; a per-slot lock keeps the wait-reset-launch-record
+// sequence of one caller together), so launches on different streams never share a counter
+int launch_with_counter(rs_handle* h, rs::ScoreArgs& a, cudaStream_t st) {
+  const unsigned k = h->work_slot.fetch_add(1) % rs::kWorkSlots;
+  std::lock_guard<std::mutex> lock(h->work_mtx[k]);
+  // (under stream capture the graph's own order stands in for the event: no cross-capture wait)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return (int)cudaGetLastError();
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  cudaError_t e = capturing ? cudaSuccess : cudaStreamWaitEvent(st, (cudaEvent_t)h->work_ev[k], 0);
+  if (e != cudaSuccess) return (int)e;
+  a.work = h->d_work + k;
+  e = cudaMemsetAsync(a.work, 0, sizeof(int), st);
+  if (e != cudaSuccess) return (int)e;
+  const int r = rs::launch_score(a, st, h->device, nullptr);
+  if (r != 0 || capturing) return r;
+  return (int)cudaEventRecord((cudaEvent_t)h->work_ev[k], st);
 }
 
 }  // namespace
@@ -764,11 +798,9 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
   a.invalid = (unsigned long long*)invalid_count_dev;
   {
     std::lock_guard<std::mutex> lock(h->mtx);
-    a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, true);
+    a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, true, st);
   }
-  a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
-  CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st), RS_E_CUDA);
-  int e = rs::launch_score(a, st, h->device, nullptr);
+  int e = launch_with_counter(h, a, st);
   if (e != 0) {
     set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
     return RS_E_CUDA;
@@ -815,6 +847,7 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
   if (P > 0 && (!poses || !energies_out || !mindist_out)) { set_err("null pose/output pointer"); return RS_E_INVALID_ARG; }
   if (n_lig > 0 && (!q_lig || !xyz_lig)) { set_err("null ligand pointer"); return RS_E_INVALID_ARG; }
+  if (n_lig > (int64_t)1 << 30) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
   if (P == 0) return 0;
   std::lock_guard<std::mutex> lock(h->mtx);
   CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
@@ -870,7 +903,7 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   a.zl = zl;
   a.yl = yl;
   a.L = n_lig;
-  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
+  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev, st[0]);
   static const bool streamed_off = std::getenv("RS_NO_STREAMED") != nullptr;
   // streamed only for large batches: below ~4e5 poses (C2: 1e5) the per-chunk stream waits cost
   // more than the launch ramps they save (measured: C2 all-host 0.40 ms streamed, 0.36 chunked)
@@ -923,8 +956,6 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     }
     CUDA_TRY(cudaMemsetAsync(d_arrive, 0, (2 * kMaxCb + 2) * sizeof(unsigned), st[0]), RS_E_CUDA);
     CUDA_TRY(cudaMemcpyAsync(d_cb, cb, (n_cb + 1) * sizeof(long long), cudaMemcpyHostToDevice, st[0]), RS_E_CUDA);
-    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
-    CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st[0]), RS_E_CUDA);
     cudaEvent_t armed;
     CUDA_TRY(cudaEventCreateWithFlags(&armed, cudaEventDisableTiming), RS_E_CUDA);
     CUDA_TRY(cudaEventRecord(armed, st[0]), RS_E_CUDA);
@@ -946,7 +977,7 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     a.cb = d_cb;
     a.n_cb = n_cb;
     a.stall = d_stall;
-    int e = rs::launch_score(a, st[0], h->device, nullptr);
+    int e = launch_with_counter(h, a, st[0]);
     if (e != 0) {
       set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
       return RS_E_CUDA;
@@ -987,9 +1018,7 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     a.E = e_dev ? energies_out + off : d_E + off;
     a.D = d_dev ? mindist_out + off : d_D + off;
     a.invalid = d_cnt + s;
-    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
-    CUDA_TRY(cudaMemsetAsync(a.work, 0, sizeof(int), st[s]), RS_E_CUDA);
-    int e = rs::launch_score(a, st[s], h->device, nullptr);
+    int e = launch_with_counter(h, a, st[s]);
     if (e != 0) {
       set_err(std::string("kernel launch failed: ") + cudaGetErrorString((cudaError_t)e));
       return RS_E_CUDA;
@@ -1049,6 +1078,16 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
     set_err("rs_ppiem_scan needs dmin_cap > sigma_vdw (the sphere-tracing step)");
     return RS_E_INVALID_ARG;
   }
+  if (n_lig > ((int64_t)1 << 30)) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
+  for (int32_t j = 0; j < m_P; ++j) {
+    // the sphere-tracing step never exceeds the clearance only along unit directions
+    const double* u = dirs + 3 * (size_t)j;
+    const double nn = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    if (!(std::fabs(nn - 1.0) <= 1e-9)) {
+      set_err("rs_ppiem_scan: dirs[" + std::to_string(j) + "] is not a unit vector");
+      return RS_E_INVALID_ARG;
+    }
+  }
   std::lock_guard<std::mutex> lock(h->mtx);
   CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
   const int64_t P = (int64_t)m_P * m_L;
@@ -1098,7 +1137,7 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   a.zl = zl;
   a.yl = yl;
   a.L = n_lig;
-  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev);
+  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev, nullptr);
   a.E = d_Ec;
   a.D = d_Dc;
   a.invalid = d_inv;
@@ -1106,15 +1145,13 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   auto score = [&](const double* poses_cur, int64_t n) -> int {
     a.poses = poses_cur;
     a.P = n;
-    a.work = h->d_work + (h->work_slot.fetch_add(1) % rs::kWorkSlots);
-    if (cudaMemsetAsync(a.work, 0, sizeof(int), st) != cudaSuccess) return 1;
-    return rs::launch_score(a, st, h->device, nullptr);
+    return launch_with_counter(h, a, st);
   };
   int cur = 0;
   int64_t n_cur = P;
   for (int it = 0; it < max_iter && n_cur > 0; ++it) {
     // score the poses still moving (compacted), then step them and compact the next list
-    if (score(d_pose[cur], n_cur) != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+    if (int e = score(d_pose[cur], n_cur)) { set_err("scan scoring launch failed: " + std::to_string(e)); return RS_E_CUDA; }
     CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int), st), RS_E_CUDA);
     if (int e = rs::launch_scan_update(d_c, d_dirs, d_q, m_P, m_L, d_Dc, d_Ec, sigma, dcap, tol,
                                        it == 0, d_E, d_s, d_st, d_slot, d_pose[1 - cur], d_count, st)) {
@@ -1129,7 +1166,7 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
   // poses still moving after max_iter were stepped after their last scoring: score them where
   // they stand (feasible by construction) and report status 4
   if (n_cur > 0) {
-    if (score(d_pose[cur], n_cur) != 0) { set_err("scan scoring launch failed"); return RS_E_CUDA; }
+    if (int e = score(d_pose[cur], n_cur)) { set_err("scan scoring launch failed: " + std::to_string(e)); return RS_E_CUDA; }
     if (int e = rs::launch_scan_gather(P, d_st, d_slot, d_Ec, d_E, st)) {
       set_err(std::string("scan gather failed: ") + cudaGetErrorString((cudaError_t)e));
       return RS_E_CUDA;

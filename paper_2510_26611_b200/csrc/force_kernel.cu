@@ -17,37 +17,18 @@
 #include <cstdint>
 
 #include "rs_internal.h"
+#include "rs_device.cuh"
 
 namespace rs {
 namespace {
+
+using namespace dev;
 
 constexpr int kForceThreads = 256;
 #ifndef RS_FORCE_MINB
 #define RS_FORCE_MINB 1          // resident blocks per SM the register budget must allow
 #endif
 constexpr unsigned kAll = 0xffffffffu;
-
-__device__ __forceinline__ bool quat_rot(const double* q, double* R) {
-  const double w = q[0], x = q[1], y = q[2], z = q[3];
-  const double nn = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)),
-                              __dmul_rn(z, z));
-  if (!(nn > 0.0) || !isfinite(nn)) return false;
-  const double s = __ddiv_rn(2.0, nn);
-  const double xs = __dmul_rn(x, s), ys = __dmul_rn(y, s), zs = __dmul_rn(z, s);
-  const double wx = __dmul_rn(w, xs), wy = __dmul_rn(w, ys), wz = __dmul_rn(w, zs);
-  const double xx = __dmul_rn(x, xs), xy = __dmul_rn(x, ys), xz = __dmul_rn(x, zs);
-  const double yy = __dmul_rn(y, ys), yz = __dmul_rn(y, zs), zz = __dmul_rn(z, zs);
-  R[0] = __dsub_rn(1.0, __dadd_rn(yy, zz));
-  R[1] = __dsub_rn(xy, wz);
-  R[2] = __dadd_rn(xz, wy);
-  R[3] = __dadd_rn(xy, wz);
-  R[4] = __dsub_rn(1.0, __dadd_rn(xx, zz));
-  R[5] = __dsub_rn(yz, wx);
-  R[6] = __dsub_rn(xz, wy);
-  R[7] = __dadd_rn(yz, wx);
-  R[8] = __dsub_rn(1.0, __dadd_rn(xx, yy));
-  return true;
-}
 
 // O4: rank pairs, then the pairwise halving tree (reading A20), rows from L2
 template <int R>
@@ -201,29 +182,6 @@ __device__ __forceinline__ double phi_at(const ScoreArgs& a, int i0, int i1, int
   else return phi_rows_rt(f0, f1, f2, r);
 }
 
-__device__ __forceinline__ void dd_acc(double& hi, double& lo, double p) {
-  const double s = __dadd_rn(hi, p);
-  const double bb = __dsub_rn(s, hi);
-  const double err = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(p, bb));
-  hi = s;
-  lo = __dadd_rn(lo, err);
-}
-
-__device__ __forceinline__ void dd_join(double& hi, double& lo, double h2, double l2) {
-  const double s = __dadd_rn(hi, h2);
-  const double bb = __dsub_rn(s, hi);
-  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
-  hi = s;
-  lo = __dadd_rn(__dadd_rn(lo, l2), e);
-}
-
-__device__ __forceinline__ int snap_cell(double x, double b, double inv_h, int nm1) {
-  const double u = __dmul_rn(__dadd_rn(x, b), inv_h);
-  int c;
-  asm("cvt.rpi.s32.f64 %0, %1;" : "=r"(c) : "d"(u));
-  return min(max(c - 1, 0), nm1);
-}
-
 template <int R>
 __global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(const ScoreArgs a,
                                                                              double* out) {
@@ -241,7 +199,7 @@ __global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(con
 #pragma unroll
     for (int i = 0; i < 7; ++i) q[i] = __ldg(pq + i);
     double Rm[9];
-    bool ok = quat_rot(q, Rm);
+    bool ok = quat_rot_dev(q, Rm);
     double hi[9], lo[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) hi[j] = lo[j] = 0.0;
@@ -262,7 +220,7 @@ __global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(con
         } else {
           int i[3];
 #pragma unroll
-          for (int r = 0; r < 3; ++r) i[r] = snap_cell(xp[r], a.b, a.inv_h, nm1);
+          for (int r = 0; r < 3; ++r) i[r] = snap_dev(xp[r], a.b, a.inv_h, nm1);
           // backward neighbours (forward at the lower edge)
           int sh[3];
 #pragma unroll
@@ -314,7 +272,7 @@ __global__ void __launch_bounds__(kForceThreads, RS_FORCE_MINB) force_kernel(con
     for (int j = 0; j < 9; ++j) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1)
-        dd_join(hi[j], lo[j], __shfl_xor_sync(kAll, hi[j], off), __shfl_xor_sync(kAll, lo[j], off));
+        dd_merge(hi[j], lo[j], __shfl_xor_sync(kAll, hi[j], off), __shfl_xor_sync(kAll, lo[j], off));
       res[j] = ok ? __dadd_rn(hi[j], lo[j]) : NAN;
     }
     // lanes 0..8 write one component each (coalesced 72-byte row)
@@ -492,7 +450,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) force_window_kernel(const Scor
 #pragma unroll
       for (int i = 0; i < 7; ++i) q[i] = __ldg(pq + i);
       double Rm[9];
-      bool ok = quat_rot(q, Rm);
+      bool ok = quat_rot_dev(q, Rm);
       double hi[9], lo[9];
 #pragma unroll
       for (int j = 0; j < 9; ++j) hi[j] = lo[j] = 0.0;
@@ -515,7 +473,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) force_window_kernel(const Scor
             bool inwin = true;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              i[r] = snap_cell(xp[r], a.b, a.inv_h, nm1);
+              i[r] = snap_dev(xp[r], a.b, a.inv_h, nm1);
               sh[r] = i[r] > 0 ? i[r] - 1 : i[r] + 1;
               inwin = inwin && min(i[r], sh[r]) >= org[r] && max(i[r], sh[r]) < org[r] + len[r];
             }
@@ -567,7 +525,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) force_window_kernel(const Scor
       for (int j = 0; j < 9; ++j) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1)
-          dd_join(hi[j], lo[j], __shfl_xor_sync(kAll, hi[j], off), __shfl_xor_sync(kAll, lo[j], off));
+          dd_merge(hi[j], lo[j], __shfl_xor_sync(kAll, hi[j], off), __shfl_xor_sync(kAll, lo[j], off));
         res[j] = ok ? __dadd_rn(hi[j], lo[j]) : NAN;
       }
       double mine = res[0];

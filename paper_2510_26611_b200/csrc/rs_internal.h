@@ -135,7 +135,7 @@ struct ScoreArgs {               // one launch of the scoring kernel
   double* E;
   double* D;
   unsigned long long* invalid;   // may be null
-  int* work;                     // zeroed work counter (dynamic pose chunks), stream-ordered
+  int* work;                     // this launch's zeroed work counter (dynamic pose chunks)
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
@@ -155,8 +155,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
 int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
                            int n_sigma, double* out, void* stream);
 
-constexpr int kWorkSlots = 64;
-constexpr int kPackPad = 24;     // zero cells before each axis of the packed range table (TMA)   // concurrent launches per handle with distinct work counters
+constexpr int kWorkSlots = 64;   // work counters per handle, each reused behind its last launch
+constexpr int kPackPad = 24;     // zero cells before each axis of the packed range table (TMA)
 
 // Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
 // (if not null) is incremented by the number of kernels enqueued.
@@ -215,10 +215,12 @@ struct rs_handle {
   void* d_nb_range = nullptr;
   void* d_nb_pack = nullptr;           // loc4: packed ranges, the TMA source of the local table
   int nb_dim2p = 0;
-  int* d_work = nullptr;               // kWorkSlots zeroed-per-launch work counters
+  int* d_work = nullptr;               // kWorkSlots dynamic-schedule work counters
+  void* work_ev[rs::kWorkSlots] = {};  // cudaEvent_t recorded behind each counter's last launch
+  std::mutex work_mtx[rs::kWorkSlots];
+  std::atomic<unsigned> work_slot{0};
   void* scan_buf = nullptr;            // rs_ppiem_scan scratch (grow-only)
   size_t scan_bytes = 0;
-  std::atomic<unsigned> work_slot{0};
   int64_t device_bytes = 0;
   // staging for host-pointer calls
   std::mutex mtx;

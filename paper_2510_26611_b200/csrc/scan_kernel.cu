@@ -38,7 +38,9 @@ __global__ void scan_init_kernel(const double* centre, const double* dirs, const
 
 // One sphere-tracing step from the scored minimum distances Dc (+inf at or beyond D_cap, NaN
 // for an invalid pose) and energies Ec of the current list (pose p at slot[p]).  Status: -1
-// active, 0 contact, 1 left the box, 2 clash at the start, 3 passed the centre.  Poses that
+// active, 0 contact, 1 left the box (an invalid pose), 2 clash at the start, 3 passed the
+// centre.  The directions are unit vectors (the host checks), so a step of at most the
+// clearance d - sigma never jumps the first contact on the line.  Poses that
 // move are appended to the next list (poses_next, slot[p], *count).
 __global__ void scan_update_kernel(const double* centre, const double* dirs, const double* quats,
                                    int m_P, int m_L, const double* Dc, const double* Ec,
@@ -61,8 +63,10 @@ __global__ void scan_update_kernel(const double* centre, const double* dirs, con
       sn = __dsub_rn(s[p], __dsub_rn(dcap, sigma));
     } else {
       const double delta = __dsub_rn(d, sigma);
-      if (delta < 0.0) {                               // only possible at the start
-        status[p] = first ? 2 : 1;
+      if (delta < 0.0) {
+        // at the start: a clash; later the steps never close more than the clearance, so only
+        // rounding can put d below sigma: that is contact (reading A23)
+        status[p] = first ? 2 : 0;
         continue;
       }
       if (delta <= tol) {

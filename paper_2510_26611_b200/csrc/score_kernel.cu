@@ -43,9 +43,12 @@
 #include <vector>
 
 #include "rs_internal.h"
+#include "rs_device.cuh"
 
 namespace rs {
 namespace {
+
+using namespace dev;
 
 #ifndef RS_THREADS
 #define RS_THREADS 512
@@ -167,73 +170,6 @@ __device__ __forceinline__ unsigned lds_u32(unsigned addr) {
   unsigned v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
-}
-
-// O3 cell of a valid coordinate: u = (x + b) * inv_h in [0, n(1+eps)]; i = clamp(ceil(u)-1)
-__device__ __forceinline__ int snap_dev(double x, double b, double inv_h, int nm1) {
-  const double u = __dmul_rn(__dadd_rn(x, b), inv_h);
-  int c;
-  asm("cvt.rpi.s32.f64 %0, %1;" : "=r"(c) : "d"(u));
-  return min(max(c - 1, 0), nm1);
-}
-
-// O1: quaternion (w,x,y,z) -> R (row-major); false if |q|^2 is 0 or not finite
-__device__ __forceinline__ bool quat_rot_dev(const double* q, double* R) {
-  const double w = q[0], x = q[1], y = q[2], z = q[3];
-  const double nn = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)),
-                              __dmul_rn(z, z));
-  if (!(nn > 0.0) || !isfinite(nn)) return false;
-  const double s = __ddiv_rn(2.0, nn);
-  const double xs = __dmul_rn(x, s), ys = __dmul_rn(y, s), zs = __dmul_rn(z, s);
-  const double wx = __dmul_rn(w, xs), wy = __dmul_rn(w, ys), wz = __dmul_rn(w, zs);
-  const double xx = __dmul_rn(x, xs), xy = __dmul_rn(x, ys), xz = __dmul_rn(x, zs);
-  const double yy = __dmul_rn(y, ys), yz = __dmul_rn(y, zs), zz = __dmul_rn(z, zs);
-  R[0] = __dsub_rn(1.0, __dadd_rn(yy, zz));
-  R[1] = __dsub_rn(xy, wz);
-  R[2] = __dadd_rn(xz, wy);
-  R[3] = __dadd_rn(xy, wz);
-  R[4] = __dsub_rn(1.0, __dadd_rn(xx, zz));
-  R[5] = __dsub_rn(yz, wx);
-  R[6] = __dsub_rn(xz, wy);
-  R[7] = __dadd_rn(yz, wx);
-  R[8] = __dsub_rn(1.0, __dadd_rn(xx, yy));
-  return true;
-}
-
-// O6 accumulate the exact product a*b into (hi, lo)
-__device__ __forceinline__ void dd_add_prod(double& hi, double& lo, double a, double b) {
-  const double p = __dmul_rn(a, b);
-  const double e = __fma_rn(a, b, -p);
-  const double s = __dadd_rn(hi, p);
-  const double bb = __dsub_rn(s, hi);
-  const double err = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(p, bb));
-  hi = s;
-  lo = __dadd_rn(lo, __dadd_rn(err, e));
-}
-
-// (hi, lo) += (h2, l2) exactly up to the final lo rounding (TwoSum on the high parts)
-__device__ __forceinline__ void dd_merge(double& hi, double& lo, double h2, double l2) {
-  const double s = __dadd_rn(hi, h2);
-  const double bb = __dsub_rn(s, hi);
-  const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(h2, bb));
-  hi = s;
-  lo = __dadd_rn(__dadd_rn(lo, l2), e);
-}
-
-// One rank pair: s_c = (a0 b0) c0 + (a1 b1) c1
-__device__ __forceinline__ double pair_prod(double2 a, double2 b, double2 c) {
-  return __dadd_rn(__dmul_rn(__dmul_rn(a.x, b.x), c.x), __dmul_rn(__dmul_rn(a.y, b.y), c.y));
-}
-
-// O4 halving tree over NS pair sums (A20): s_c = s_c + s_{c+m}, m = NS/2 .. 1
-template <int NS>
-__device__ __forceinline__ double halving_tree(double* s) {
-#pragma unroll
-  for (int m = NS / 2; m >= 1; m /= 2) {
-#pragma unroll
-    for (int c = 0; c < m; ++c) s[c] = __dadd_rn(s[c], s[c + m]);
-  }
-  return s[0];
 }
 
 // O4 with compile-time R from the shared-memory window.  rK = shared address of row K with the

@@ -119,13 +119,33 @@ def rs_last_error() -> str:
     return load().rs_last_error().decode()
 
 
-def _ptr(x):
-    """data pointer of a numpy array or torch tensor (contiguous fp64 expected)."""
+def _ptr(x, name="array", count=None, dtype="float64", cuda=None):
+    """Data pointer of a numpy array or torch tensor after checking what the C ABI reads from
+    it: the element type, C-contiguity, at least `count` elements and (cuda=True/False) where
+    it lives.  Marshalling only: nothing is converted or copied; a mismatch raises."""
     if x is None:
         return None
     if isinstance(x, np.ndarray):
-        return x.ctypes.data
-    return x.data_ptr()
+        if x.dtype != np.dtype(dtype):
+            raise TypeError(f"{name}: expected {dtype}, got {x.dtype}")
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: must be C-contiguous")
+        if cuda:
+            raise ValueError(f"{name}: must be a CUDA tensor (a numpy array is host memory)")
+        n, ptr = x.size, x.ctypes.data
+    else:
+        import torch
+        want = {"float64": torch.float64, "int32": torch.int32, "int64": torch.int64}[dtype]
+        if x.dtype != want:
+            raise TypeError(f"{name}: expected torch.{dtype}, got {x.dtype}")
+        if not x.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+        if cuda is not None and bool(x.is_cuda) != bool(cuda):
+            raise ValueError(f"{name}: must be a {'CUDA' if cuda else 'host'} tensor")
+        n, ptr = x.numel(), x.data_ptr()
+    if count is not None and n < count:
+        raise ValueError(f"{name}: needs at least {count} elements, has {n}")
+    return ptr
 
 
 def rs_build_protein(q, xyz, box_half_width, params: rs_params | None = None):
@@ -158,8 +178,10 @@ def rs_restrict_box(h, lo, hi, rank, flags=0):
 
 
 def rs_score_poses(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out) -> int:
-    r = load().rs_score_poses(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
-                              _ptr(energies_out), _ptr(mindist_out))
+    n_lig, P = int(n_lig), int(P)
+    r = load().rs_score_poses(h, _ptr(q_lig, "q_lig", n_lig), _ptr(xyz_lig, "xyz_lig", 3 * n_lig),
+                              n_lig, _ptr(poses, "poses", 7 * P), P,
+                              _ptr(energies_out, "energies_out", P), _ptr(mindist_out, "mindist_out", P))
     if r < 0:
         raise RuntimeError(f"rs_score_poses ({r}): " + rs_last_error())
     return int(r)
@@ -167,8 +189,13 @@ def rs_score_poses(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out
 
 def rs_score_poses_async(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindist_out,
                          invalid_count=None, stream=None) -> int:
-    r = load().rs_score_poses_async(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
-                                    _ptr(energies_out), _ptr(mindist_out), _ptr(invalid_count),
+    n_lig, P = int(n_lig), int(P)
+    r = load().rs_score_poses_async(h, _ptr(q_lig, "q_lig", n_lig, cuda=True),
+                                    _ptr(xyz_lig, "xyz_lig", 3 * n_lig, cuda=True), n_lig,
+                                    _ptr(poses, "poses", 7 * P, cuda=True), P,
+                                    _ptr(energies_out, "energies_out", P, cuda=True),
+                                    _ptr(mindist_out, "mindist_out", P, cuda=True),
+                                    _ptr(invalid_count, "invalid_count", 1, "int64", cuda=True),
                                     stream)
     if r < 0:
         raise RuntimeError(f"rs_score_poses_async ({r}): " + rs_last_error())
@@ -177,8 +204,12 @@ def rs_score_poses_async(h, q_lig, xyz_lig, n_lig, poses, P, energies_out, mindi
 
 def rs_score_forces(h, q_lig, xyz_lig, n_lig, poses, P, forces_out, invalid_count=None,
                     stream=None) -> int:
-    r = load().rs_score_forces(h, _ptr(q_lig), _ptr(xyz_lig), int(n_lig), _ptr(poses), int(P),
-                               _ptr(forces_out), _ptr(invalid_count), stream)
+    n_lig, P = int(n_lig), int(P)
+    r = load().rs_score_forces(h, _ptr(q_lig, "q_lig", n_lig, cuda=True),
+                               _ptr(xyz_lig, "xyz_lig", 3 * n_lig, cuda=True), n_lig,
+                               _ptr(poses, "poses", 7 * P, cuda=True), P,
+                               _ptr(forces_out, "forces_out", 9 * P, cuda=True),
+                               _ptr(invalid_count, "invalid_count", 1, "int64", cuda=True), stream)
     if r < 0:
         raise RuntimeError(f"rs_score_forces ({r}): " + rs_last_error())
     return int(r)
@@ -196,9 +227,10 @@ def rs_ppiem_scan(h, q_lig, xyz_lig, centre, dirs, quats, s_start, tol=1e-3, max
     s = np.empty((m_P, m_L))
     st = np.empty((m_P, m_L), dtype=np.int32)
     n_lig = int(q_lig.shape[0])
-    r = load().rs_ppiem_scan(h, _ptr(q_lig), _ptr(xyz_lig), n_lig, _ptr(centre), _ptr(dirs), m_P,
-                             _ptr(quats), m_L, float(s_start), float(tol), int(max_iter), _ptr(E),
-                             _ptr(s), _ptr(st))
+    r = load().rs_ppiem_scan(h, _ptr(q_lig, "q_lig", n_lig), _ptr(xyz_lig, "xyz_lig", 3 * n_lig),
+                             n_lig, _ptr(centre, "centre", 3), _ptr(dirs, "dirs", 3 * m_P), m_P,
+                             _ptr(quats, "quats", 4 * m_L), m_L, float(s_start), float(tol),
+                             int(max_iter), _ptr(E), _ptr(s), _ptr(st, "status", dtype="int32"))
     if r < 0:
         raise RuntimeError(f"rs_ppiem_scan ({r}): " + rs_last_error())
     return E, s, st
@@ -208,7 +240,8 @@ def rs_landscape_minima(E, top_k):
     """PPIEM step A6: flat indices j*m_L + k of up to top_k local minima, by energy."""
     E = np.ascontiguousarray(E, dtype=np.float64)
     out = np.empty(max(int(top_k), 1), dtype=np.int32)
-    r = load().rs_landscape_minima(_ptr(E), E.shape[0], E.shape[1], int(top_k), _ptr(out))
+    r = load().rs_landscape_minima(_ptr(E), E.shape[0], E.shape[1], int(top_k),
+                                   _ptr(out, "idx_out", dtype="int32"))
     if r < 0:
         raise RuntimeError("rs_landscape_minima: " + rs_last_error())
     return out[:r].copy()

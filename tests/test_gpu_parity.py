@@ -225,6 +225,47 @@ def test_repeated_and_concurrent_streams(env):
         assert sum(int(o[2].item()) for o in outs) == inv0
 
 
+def test_many_unsynchronised_launches_on_streams(env):
+    """100 launches in flight at once on three streams, none synchronised with another (more
+    than any fixed pool of work counters): every launch has its own counter, so every output
+    equals the one-call result bit for bit."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1()
+    prot = build(rsdock, w)
+    E0, D0, inv0 = gpu_score(torch, rsdock, prot, w, w.poses)
+    dev = torch.device("cuda:0")
+    q = torch.tensor(w.ligand_q, device=dev)
+    y = torch.tensor(w.ligand_xyz, device=dev).contiguous()
+    ps = torch.tensor(w.poses, device=dev).contiguous()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for st in streams:
+        st.wait_stream(torch.cuda.current_stream())
+    outs = []
+    for k in range(100):
+        st = streams[k % 3]
+        E = torch.empty(w.P, dtype=torch.float64, device=dev)
+        D = torch.empty(w.P, dtype=torch.float64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        with torch.cuda.stream(st):
+            prot.score_async(q, y, ps, E, D, cnt, stream=st)
+        outs.append((E, D, cnt))
+    torch.cuda.synchronize()
+    for E, D, cnt in outs:
+        assert np.array_equal(E.cpu().numpy(), E0) and np.array_equal(D.cpu().numpy(), D0)
+        assert int(cnt.item()) == inv0
+
+
+def test_ppiem_rejects_non_unit_directions(env):
+    """A direction longer than 1 would let a step exceed the clearance: refused."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1(n_poses=4)
+    prot = build(rsdock, w, dmin_cap=4.5)
+    dirs, quats = syn.planar_scan(4, 2)
+    centre = w.protein_xyz.mean(0)
+    with pytest.raises(RuntimeError, match="unit vector"):
+        rsdock.rs_ppiem_scan(prot.handle, w.ligand_q, w.ligand_xyz, centre, 1.5 * dirs, quats, 15.0)
+
+
 # ----------------------------------------------------------------------------- physics on GPU
 
 def test_tolerance_mode_gpu_vs_coulomb(env):

@@ -82,6 +82,33 @@ def test_no_cpu_fallback(rsd):
         p.score(w.ligand_q, w.ligand_xyz, w.poses)
 
 
+def test_binding_checks_what_it_marshals(rsd):
+    """The binding passes raw pointers, so it refuses arrays the C ABI would misread: another
+    element type, a strided view, too few elements (no conversion, no copy)."""
+    w = _small()
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=64, rank_R=8,
+                    sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    P, L = w.P, w.L
+    E, D = np.empty(P), np.empty(P)
+    with pytest.raises(TypeError, match="poses"):
+        rsd.rs_score_poses(p.handle, w.ligand_q, w.ligand_xyz, L, w.poses.astype(np.float32), P, E, D)
+    with pytest.raises(ValueError, match="contiguous"):
+        rsd.rs_score_poses(p.handle, w.ligand_q, w.ligand_xyz, L, np.asfortranarray(w.poses), P, E, D)
+    with pytest.raises(ValueError, match="energies_out"):
+        rsd.rs_score_poses(p.handle, w.ligand_q, w.ligand_xyz, L, w.poses, P, E[:-1], D)
+    with pytest.raises(ValueError, match="CUDA"):
+        rsd.rs_score_poses_async(p.handle, w.ligand_q, w.ligand_xyz, L, w.poses, P, E, D)
+    torch = pytest.importorskip("torch")
+    with pytest.raises(TypeError, match="q_lig"):
+        rsd.rs_score_poses(p.handle, torch.tensor(w.ligand_q, dtype=torch.float32),
+                           w.ligand_xyz, L, w.poses, P, E, D)
+    with pytest.raises(ValueError, match="contiguous"):
+        rsd.rs_score_poses(p.handle, w.ligand_q, torch.tensor(w.ligand_xyz).t(), L, w.poses, P, E, D)
+    # well-formed host arrays pass the binding and reach the library (which has no device here)
+    with pytest.raises(RuntimeError, match="no device tables"):
+        rsd.rs_score_poses(p.handle, w.ligand_q, w.ligand_xyz, L, w.poses, P, E, D)
+
+
 @pytest.fixture(scope="module")
 def c1_host(rsd):
     w = syn.config_c1()

@@ -105,3 +105,40 @@ def test_ppiem_sharded_gloo_world2():
     port = _free_port()
     mp.spawn(_ppiem_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] and out[1]
+
+
+def _run_bench(*extra):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env.pop("RANK", None)
+    env.pop("LOCAL_RANK", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", *extra],
+                         capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import json
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_launcher_weak_scaling_spawns_ranks():
+    """`bench.py --gpus 2` outside a launcher re-runs itself under torch.distributed.run with 2
+    ranks (gloo here): each rank scores an independent batch of the config's size, the step
+    time is the max over ranks, the value counts every rank's poses, one line from rank 0."""
+    d = _run_bench("--gpus", "2", "--config", "C1")
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["ms_per_step"] == 1.25                       # max of the ranks' stand-in times
+    assert d["global_poses"] == 2 * d["poses_per_rank"] == 2000
+    assert len(set(d["rank_digests"])) == 2               # independent batches
+
+
+def test_bench_launcher_strong_scaling_splits_one_batch():
+    d = _run_bench("--gpus", "2", "--config", "C1", "--scaling", "strong")
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["global_poses"] == 1000 and d["poses_per_rank"] == 500
+    assert len(set(d["rank_digests"])) == 2
+    one = _run_bench("--config", "C1", "--scaling", "strong")
+    assert one["n_gpus"] == 1 and one["global_poses"] == 1000
