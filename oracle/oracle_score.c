@@ -176,6 +176,9 @@ double oracle_short_value(const double *S1, const double *S2, const double *S3, 
  *   mode                   : bit 0 = long_only: skip O5 and O7 (Lemma 3.2's cost alone; the CPU
  *                            like-for-like rate); bit 1 = fp32 factors (O4-f32 instead of O4)
  * Outputs E (P), dmin (P).  Returns the number of invalid poses (O8: NaN outputs).
+ * asum (P, may be NULL): sum over the pose's addends of |addend| (the M8 report's condition
+ * number kappa = asum / |E|); NaN for invalid poses.  Report only: E never
+ * reads it.
  * Protein cells are recomputed here with oracle_snap (never taken from the library).
  */
 int64_t oracle_score_poses(int n, double b, int R, const double *F1, const double *F2,
@@ -183,7 +186,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
                            const double *S2, const double *S3, int64_t M, const double *X,
                            const double *zM, int64_t L, const double *Y, const double *zL,
                            int64_t P, const double *poses, double dcap, int mode,
-                           double *E, double *dmin)
+                           double *E, double *dmin, double *asum)
 {
     int long_only = mode & 1, f32 = (mode >> 1) & 1;
     double inv_h = (double)n / (2.0 * b);
@@ -200,7 +203,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
         double Rm[9];
         int ok = oracle_quat_to_rot(pq, Rm);
         dd_t acc = {0.0, 0.0};
-        double best = INFINITY;
+        double best = INFINITY, abs_sum = 0.0;
         for (int64_t l = 0; l < L && ok; ++l) {
             double xp[3];
             int il[3];
@@ -214,6 +217,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
             double phi = f32 ? oracle_long_value_f32(F1, F2, F3, R, il[0], il[1], il[2])
                              : oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
             dd_add_product(&acc, zL[l], phi);
+            abs_sum += fabs(zL[l] * phi);
             if (long_only) continue;
             for (int64_t m = 0; m < M; ++m) {
                 /* O7: distance between continuous coordinates */
@@ -231,6 +235,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
                                                   (int)e2);
                     double w = zM[m] * s;
                     dd_add_product(&acc, zL[l], w);
+                    abs_sum += fabs(zL[l] * w);
                 }
             }
         }
@@ -242,6 +247,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
             E[p] = acc.hi + acc.lo;
             dmin[p] = (best < dcap2) ? sqrt(best) : INFINITY;
         }
+        if (asum) asum[p] = ok ? abs_sum : NAN;
     }
     free(iM);
     return invalid;

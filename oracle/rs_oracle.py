@@ -58,7 +58,7 @@ def lib():
         L.oracle_score_poses.argtypes = [
             ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, dp, ctypes.c_int, ctypes.c_int,
             dp, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp,
-            ctypes.c_double, ctypes.c_int, dp, dp]
+            ctypes.c_double, ctypes.c_int, dp, dp, dp]
         L.oracle_score_poses.restype = ctypes.c_int64
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_score_forces.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, dp,
@@ -317,8 +317,11 @@ def K_h(delta, h, order=12):
 # O1-O8 scorer (C) wrapper
 # ------------------------------------------------------------------------------------------
 
-def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=False):
+def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=False,
+                abs_sum=False):
     """Per-pose (E, dmin, n_invalid) from exported tables (f32: the O4-f32 long-range part).
+    abs_sum: also return sum_addends |addend| per pose (E, dmin, n_invalid, asum), the M8
+    report's kappa = asum / |E|.
 
     tables: n, b, R, F1, F2, F3 (n x R), n_sigma, Rs, S1, S2, S3 ((2 n_sigma+1) x Rs)."""
     n, b = int(tables["n"]), float(tables["b"])
@@ -332,11 +335,15 @@ def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=Fa
     E = np.empty(P)
     d = np.empty(P)
     dummy = np.zeros(1)
+    asum = np.empty(P) if abs_sum else None
     inv = lib().oracle_score_poses(
         n, b, R, _p(F1), _p(F2), _p(F3), ns, Rs, _p(S1 if S1.size else dummy),
         _p(S2 if S2.size else dummy), _p(S3 if S3.size else dummy), X.shape[0], _p(X), _p(qM),
         Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap),
-        (1 if long_only else 0) | (2 if f32 else 0), _p(E), _p(d))
+        (1 if long_only else 0) | (2 if f32 else 0), _p(E), _p(d),
+        _p(asum) if abs_sum else None)
+    if abs_sum:
+        return E, d, int(inv), asum
     return E, d, int(inv)
 
 

@@ -293,47 +293,141 @@ def test_tolerance_mode_gpu_vs_coulomb(env):
 
 # ----------------------------------------------------------------------------- full sizes
 
-@pytest.mark.parametrize("name,k", [("C2", 2000), ("C3", 400)])
-def test_full_size_sampled(env, name, k):
+def record(report, key, Eg, Dg, Eo, Do, asum, sigma):
+    """M8 report row: sample size, bitwise-equal fraction of the energies,
+    max relative difference, the condition number kappa = sum|addends| / |E| (oracle side)
+    distribution, and the clash counts (d < sigma_vdW; none within 1e-9 A of sigma unless a
+    test puts them there)."""
+    ok = ~np.isnan(Eo)
+    rel = np.abs(Eg[ok] - Eo[ok]) / np.maximum(np.abs(Eo[ok]), 1e-300)
+    kap = asum[ok] / np.maximum(np.abs(Eo[ok]), 1e-300)
+    q = (lambda a, f: float(np.quantile(a, f)) if a.size else None)
+    report[key] = {
+        "n": int(Eo.size), "valid": int(ok.sum()),
+        "bitwise_frac": float(np.mean(Eg[ok] == Eo[ok])) if ok.any() else 1.0,
+        "max_rel": float(rel.max()) if rel.size else 0.0,
+        "kappa": {"median": q(kap, 0.5), "p99": q(kap, 0.99), "p999": q(kap, 0.999),
+                  "max": float(kap.max()) if kap.size else None},
+        "clash": int(np.sum(Do[ok] < sigma)),
+        "near_sigma_1e9": int(np.sum(np.abs(Do[ok] - sigma) <= 1e-9)),
+    }
+    return report[key]
+
+
+def sampled_parity(env, report, key, w, prot, k, seed):
+    """The whole batch through the async API in the bench launch configuration; the oracle
+    re-scores a seeded sample of k poses one by one (with its kappa)."""
+    torch, rsdock, rs_oracle = env
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
+    idx, _ = syn.subsample(w.poses, k, seed=seed)
+    tb = prot.export_tables()
+    Eo, Do, invo, asum = rs_oracle.score_poses(tb, w.protein_xyz, w.protein_q, w.ligand_xyz,
+                                               w.ligand_q, w.poses[idx], w.dmin_cap, abs_sum=True)
+    compare(Eg[idx], Dg[idx], Eo, Do)
+    assert inv == int(np.isnan(Eg).sum())
+    return record(report, key, Eg[idx], Dg[idx], Eo, Do, asum, w.sigma_vdw)
+
+
+@pytest.mark.parametrize("name,k", [("C2", 10000), ("C3", 10000)])
+def test_full_size_sampled(env, parity_report, name, k):
     """Whole batch on the GPU in the bench launch configuration (async API, device tensors);
-    the oracle re-scores a seeded sample of poses."""
+    the oracle re-scores a seeded sample of poses (M8 sizes: 10^4)."""
     torch, rsdock, rs_oracle = env
     w = syn.make(name)
     prot = build(rsdock, w)
-    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
-    idx, _ = syn.subsample(w.poses, k, seed=3)
-    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
-    compare(Eg[idx], Dg[idx], Eo, Do)
-    assert inv == int(np.isnan(Eg).sum())
+    row = sampled_parity(env, parity_report, name, w, prot, k, 3)
+    assert row["clash"] > 0 and row["valid"] > 0.9 * k
 
 
 @pytest.mark.slow
-def test_c4_full_size_sampled(env):
+def test_c4_full_size_sampled(env, parity_report):
     """C4: n = 16384, 50,000 atoms, R = 24 (L2 path: the ligand spans more rows than fit in
-    shared memory), 10^7 poses on the GPU, 64 sampled poses re-scored by the oracle."""
+    shared memory), 10^7 poses on the GPU, 10^4 sampled poses re-scored by the oracle; the
+    sample holds hundreds of clashing poses (C4's ~5% clash rate) on the L2 path."""
     torch, rsdock, rs_oracle = env
     w = syn.make("C4")
     prot = build(rsdock, w)
     assert prot.info["R"] == 24
-    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
-    idx, _ = syn.subsample(w.poses, 64, seed=4)
-    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
-    compare(Eg[idx], Dg[idx], Eo, Do)
-    assert inv == int(np.isnan(Eg).sum())
+    row = sampled_parity(env, parity_report, "C4", w, prot, 10000, 4)
+    assert row["clash"] >= 100
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("R,mult", [(R, m) for R in (8, 16, 32) for m in (1, 2, 3)])
-def test_c5_full_size_sampled(env, R, mult):
+def test_c5_full_size_sampled(env, parity_report, R, mult):
     """C5 protein-protein, the whole R x sigma_s grid (R in {8, 16, 32}, sigma_s in {2, 4, 6} A):
-    5000-atom rigid partner (ligand from global memory), n = 8192."""
+    5000-atom rigid partner (ligand from global memory), n = 8192; 10^3 sampled poses per point."""
     torch, rsdock, rs_oracle = env
     w = syn.config_c5(rank_R=R, sigma_mult=mult)
     prot = build(rsdock, w)
-    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses, async_api=True)
-    idx, _ = syn.subsample(w.poses, 24, seed=5)
-    Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses, idx)
-    compare(Eg[idx], Dg[idx], Eo, Do)
+    sampled_parity(env, parity_report, f"C5_R{R}_s{2 * mult}", w, prot, 1000, 5)
+
+
+def test_snap_ties_on_cell_boundaries(env, parity_report):
+    """H3/O3 ties: protein atoms, ligand atoms and translations on exact multiples of h, so
+    with the identity and the axis half-turns (exact rotation matrices, O1) every transformed
+    ligand coordinate falls exactly on a cell boundary (u = (x + b)/h an integer); the
+    protein's cells (S4) tie too.  The kernel and the oracle must take the same side of every
+    tie (A3: cell = ceil(u) - 1 clamped), so the results are compared element by element."""
+    torch, rsdock, rs_oracle = env
+    w0 = syn.random_small(seed=21, M=40, L=9, n=64, b=8.0, R=8, P=1)
+    h = 2.0 * w0.box_half_width / w0.grid_n
+    X = np.round(w0.protein_xyz / h) * h
+    X = X[np.unique(X, axis=0, return_index=True)[1]]
+    Y = np.round(w0.ligand_xyz / h) * h
+    g = np.random.default_rng(5)
+    halfturns = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]], float)
+    q = halfturns[g.integers(0, 4, 600)]
+    t = np.round(g.uniform(-3.0, 3.0, (600, 3)) / h) * h
+    poses = np.concatenate([q, t], axis=1)
+    w = syn.Workload("ties", X, w0.protein_q[:X.shape[0]], Y, w0.ligand_q, poses, w0.grid_n,
+                     w0.box_half_width, w0.rank_R, w0.sigma_split, w0.sigma_vdw, w0.dmin_cap)
+    u = (w.protein_xyz + w.box_half_width) / h
+    assert np.all(u == np.round(u))                       # protein atoms on boundaries
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, poses)
+    tb = prot.export_tables()
+    Eo, Do, invo, asum = rs_oracle.score_poses(tb, X, w.protein_q, Y, w.ligand_q, poses,
+                                               w.dmin_cap, abs_sum=True)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    row = record(parity_report, "snap_ties", Eg, Dg, Eo, Do, asum, w.sigma_vdw)
+    assert row["valid"] > 500
+
+
+def test_poses_at_vdw_and_cap_thresholds(env, parity_report):
+    """H6 thresholds: poses whose closest ligand-protein pair sits at sigma_vdW +- 1e-9 A (the
+    clash flag's edge, M8) and at D_cap +- 1e-9 A (the edge of the reported distance: +inf
+    beyond, reading A11; this test builds with D_cap = 4 A so the two edges differ).  A one-atom ligand is placed along the outward radial
+    direction of each of the 12 outermost protein atoms at the chosen distance (for the
+    outermost atom no other atom is closer, so its poses sit exactly at the edge); the kernel
+    must report the same distance bit for bit and the same inf/finite split."""
+    torch, rsdock, rs_oracle = env
+    w0 = syn.random_small(seed=31, M=40, L=3, n=64, b=8.0, R=8, P=1, protein_radius=2.5)
+    X = w0.protein_xyz
+    c = X.mean(0)
+    Y = np.zeros((1, 3))                  # one atom: the pose's distance is the placed one
+    eps = 1e-9
+    dists = []
+    for base in (w0.sigma_vdw, 4.0):
+        dists += [base - eps, base, base + eps, base - 4 * eps, base + 4 * eps]
+    poses = []
+    for m in np.argsort(-np.linalg.norm(X - c, axis=1))[:12]:     # the outermost atoms
+        u = (X[m] - c) / np.linalg.norm(X[m] - c)
+        for d in dists:
+            poses.append([1.0, 0.0, 0.0, 0.0, *(X[m] + d * u)])   # identity: x'_0 = t
+    poses = np.array(poses)
+    w = syn.Workload("thresholds", X, w0.protein_q, Y, w0.ligand_q[:1], poses, w0.grid_n,
+                     w0.box_half_width, w0.rank_R, w0.sigma_split, w0.sigma_vdw, 4.0)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, poses)
+    tb = prot.export_tables()
+    Eo, Do, invo, asum = rs_oracle.score_poses(tb, X, w.protein_q, Y, w.ligand_q, poses,
+                                               w.dmin_cap, abs_sum=True)
+    compare(Eg, Dg, Eo, Do, inv, invo)
+    row = record(parity_report, "vdw_cap_thresholds", Eg, Dg, Eo, Do, asum, w.sigma_vdw)
+    assert row["near_sigma_1e9"] >= 3                       # poses really sit at the edge
+    top = Do[len(dists) // 2:len(dists)]                    # outermost atom, at D_cap +- eps
+    assert np.isfinite(top[[0, 3]]).all() and np.isinf(top[[2, 4]]).all()
 
 
 # ----------------------------------------------------------------------------- fp32 factors (N5)

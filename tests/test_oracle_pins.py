@@ -277,6 +277,14 @@ def test_scorer_long_range_equals_dense_materialisation(oracle):
     E2, _, _ = oracle.score_poses(_tables(F, b=b), np.zeros((0, 3)), np.zeros(0), Y, 4.0 * z,
                                   poses, 1.0, long_only=True)
     assert np.array_equal(E2, 4.0 * E)
+    # M8's addend magnitude sum: sum_l |z_l T[i_l]| from the same dense tensor, so kappa >= 1
+    _, _, _, asum = oracle.score_poses(_tables(F, b=b), np.zeros((0, 3)), np.zeros(0), Y, z,
+                                       poses, 1.0, long_only=True, abs_sum=True)
+    for p in range(40):
+        R_ = Rotation.from_quat(poses[p, [1, 2, 3, 0]]).as_matrix()
+        idx = oracle.snap_np(Y @ R_.T + poses[p, 4:], b, n)
+        ref = math.fsum(abs(z[l] * T[tuple(idx[l])]) for l in range(6))
+        assert abs(asum[p] - ref) <= 1e-13 * ref and asum[p] >= abs(E[p]) * (1 - 1e-15)
 
 
 # ---------------------------------------------------------------------------------- O7/O8
