@@ -16,6 +16,8 @@ Contents (each function cites the passage it follows):
   * brute-force Coulomb binding energy     -- Eq. (13)
   * cell average of the Newton kernel K_h  -- Eq. (1) with p = 1/r
   * ctypes wrappers around oracle_score.c  -- O1-O8 (per-pose energy + min distance)
+  * compression-error certificates         -- TEP step 4 PAPER.md:1184-1209, SPEC.md:80:
+    dense CP, Gram-identity norms/inner products, unfolding tails, dense HOSVD, dense CP-ALS
 
 Parity status: every function here is pinned by tests/test_oracle_pins.py against closed
 forms, library routines (scipy quad / Rotation / cdist, fractions) or brute force.
@@ -397,3 +399,107 @@ def score_forces(tables: dict, Y, zL, poses):
 
 def num_threads():
     return int(lib().oracle_num_threads())
+
+
+# ------------------------------------------------------------------------------------------
+# Compression-error certificates for TEP step 4 (the rank bound
+# PAPER.md:472-484; SPEC.md:77-80 frobenius_norm by the Gram identity).  A CP tensor is a
+# triple (F1, F2, F3) of n x K side matrices (weights folded in), T = sum_k F1_k o F2_k o F3_k.
+# ------------------------------------------------------------------------------------------
+
+def cp_dense(F1, F2, F3):
+    """The dense n1 x n2 x n3 tensor sum_k F1[:, k] o F2[:, k] o F3[:, k], one mode-3 slice at a
+    time: T[:, :, l] = (F1 * F3[l]) F2^T."""
+    F1, F2, F3 = _c(F1), _c(F2), _c(F3)
+    T = np.empty((F1.shape[0], F2.shape[0], F3.shape[0]))
+    for l in range(F3.shape[0]):
+        T[:, :, l] = (F1 * F3[l][None, :]) @ F2.T
+    return T
+
+
+def cp_inner(A, B, block=2048):
+    """<A, B> of two CP tensors on one grid by the Gram identity:
+    sum_{k, k'} prod_a (A_a^T B_a)[k, k'], never forming the dense tensors (blocks of A's
+    columns), summed with math.fsum over the blocks."""
+    K = A[0].shape[1]
+    parts = []
+    for s in range(0, K, block):
+        e = min(K, s + block)
+        G = np.ones((e - s, B[0].shape[1]))
+        for a in range(3):
+            G *= A[a][:, s:e].T @ B[a]
+        parts.append(float(G.sum()))
+    return math.fsum(parts)
+
+
+def cp_norm2(F, block=2048):
+    """||T||_F^2 of a CP tensor by the Gram identity, symmetric in (k, k'): the diagonal
+    column blocks once, the blocks above it twice."""
+    K = F[0].shape[1]
+    parts = []
+    for s in range(0, K, block):
+        e = min(K, s + block)
+        G = np.ones((e - s, K - s))
+        for a in range(3):
+            G *= F[a][:, s:e].T @ F[a][:, s:]
+        parts.append(float(G[:, :e - s].sum()) + 2.0 * float(G[:, e - s:].sum()))
+    return math.fsum(parts)
+
+
+def certified_rel_error(F_exact, F_approx):
+    """||T - T~||_F / ||T||_F from the factors only: ||T||^2 + ||T~||^2 - 2 <T, T~> (SPEC.md:80,
+    certification of the compression error)."""
+    n2 = cp_norm2(F_exact)
+    d2 = n2 + cp_norm2(F_approx) - 2.0 * cp_inner(F_exact, F_approx)
+    return math.sqrt(max(d2, 0.0) / n2)
+
+
+def unfolding_tails(F, R):
+    """Per mode a: the sum of the squared singular values of the mode-a unfolding T_(a) beyond
+    the R largest, from T_(a) T_(a)^T = F_a (o_{b != a} F_b^T F_b) F_a^T (Hadamard product of
+    the other modes' Grams).  Any approximation of multilinear rank <= R in mode a (every CP
+    tensor of width R) is at least sqrt(tail_a) away from T (Eckart-Young on the unfolding)."""
+    Gs = [F[a].T @ F[a] for a in range(3)]
+    tails = []
+    for a in range(3):
+        H = np.ones_like(Gs[0])
+        for b in range(3):
+            if b != a:
+                H *= Gs[b]
+        lam = np.linalg.eigvalsh(F[a] @ H @ F[a].T)[::-1]
+        tails.append(float(np.clip(lam[R:], 0.0, None).sum()))
+    return tails
+
+
+def hosvd_dense(T, R):
+    """Truncated HOSVD of a dense tensor (De Lathauwer et al.): U_a = the R dominant left
+    singular vectors of the mode-a unfolding, core = T x_1 U_1^T x_2 U_2^T x_3 U_3^T.  Returns
+    (U1, U2, U3, core, relative error) with error^2 = ||T||^2 - ||core||^2 (orthogonal
+    projection).  Quasi-optimal: its error is at most sqrt(3) x the best Tucker(R) error."""
+    U = []
+    for a in range(3):
+        Ta = np.moveaxis(T, a, 0).reshape(T.shape[a], -1)
+        w, V = np.linalg.eigh(Ta @ Ta.T)
+        U.append(V[:, ::-1][:, :R])
+    core = np.einsum("ijl,ia,jb,lc->abc", T, U[0], U[1], U[2], optimize=True)
+    n2 = float(np.sum(T * T))
+    return U[0], U[1], U[2], core, math.sqrt(max(n2 - float(np.sum(core * core)), 0.0) / n2)
+
+
+def cp_als_dense(T, R, iters=100, init=None, seed=0):
+    """CP-ALS on a dense tensor (Carroll-Chang / Harshman; Kolda-Bader Alg. 1): each sweep
+    solves the three linear least-squares problems F_a = T_(a) KR(others) (o_{b != a} G_b)^+
+    in turn.  init: three n x R starting matrices (default: seeded normal).  Returns
+    (F1, F2, F3, relative Frobenius error)."""
+    rng = np.random.default_rng(seed)
+    F = [np.array(f, dtype=np.float64) for f in init] if init is not None else \
+        [rng.normal(size=(T.shape[a], R)) for a in range(3)]
+    subs = ["ijl,jr,lr->ir", "ijl,ir,lr->jr", "ijl,ir,jr->lr"]
+    for _ in range(iters):
+        for a in range(3):
+            o = [b for b in range(3) if b != a]
+            mttkrp = np.einsum(subs[a], T, F[o[0]], F[o[1]], optimize=True)
+            V = (F[o[0]].T @ F[o[0]]) * (F[o[1]].T @ F[o[1]])
+            F[a] = mttkrp @ np.linalg.pinv(V)
+    D = T - cp_dense(*F)
+    return F[0], F[1], F[2], math.sqrt(float(np.sum(D * D)) / float(np.sum(T * T)))

@@ -421,3 +421,58 @@ int main(void) {
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok 4")
+
+
+def _exact_long_factors(oracle, w, st):
+    """The protein's uncompressed long-range CP factors (rank M x R_l, Eq. (6)), from the
+    oracle's own quadrature, split and snapping (only (s, K, L_s) are read from the build)."""
+    t, a = oracle.quadrature(st["s"], st["K"], st["Ls"])
+    lm = oracle.split_long(t, w.sigma_split, w.eps_split)
+    h = 2 * w.box_half_width / w.grid_n
+    iM = oracle.snap_np(w.protein_xyz, w.box_half_width, w.grid_n)
+    return oracle.uncompressed_long_factors(iM, w.protein_q, t, a, lm, w.grid_n, h)
+
+
+def test_setup_fixed_R_absolute_pin_c1(oracle, c1_host):
+    """Fixed-R TEP (S5-S7) pinned against dense references, not its own report (C1: n = 256,
+    R = 8, the exact long-range tensor has CP rank 200 x 18 = 3600 and fits densely):
+      * the library's F is within 1.5x of the error of a dense CP-ALS(R) of the exact tensor
+        (60 sweeps from its dense HOSVD(R) factors);
+      * it cannot beat the rank bound: its error is >= every unfolding's Eckart-Young tail at R
+        and >= HOSVD(R)'s error / sqrt(3) (HOSVD quasi-optimality);
+      * the certified error by the Gram identity equals the dense one."""
+    w, p = c1_host
+    Fx = _exact_long_factors(oracle, w, p.export_setup())
+    tb = p.export_tables()
+    Fl = [tb["F1"], tb["F2"], tb["F3"]]
+    T = oracle.cp_dense(*Fx)
+    D = T - oracle.cp_dense(*Fl)
+    n2 = float(np.sum(T * T))
+    e_lib = math.sqrt(float(np.sum(D * D)) / n2)
+    del D
+    e_cert = oracle.certified_rel_error(Fx, Fl)
+    assert abs(e_cert - e_lib) <= 1e-9
+    R = w.rank_R
+    tails = oracle.unfolding_tails(Fx, R)
+    U1, U2, U3, core, e_hosvd = oracle.hosvd_dense(T, R)
+    e_als = oracle.cp_als_dense(T, R, iters=60, init=[U1, U2, U3])[3]
+    assert e_lib >= math.sqrt(max(tails) / n2) and e_lib >= e_hosvd / math.sqrt(3.0)
+    assert e_lib <= 1.5 * e_als, (e_lib, e_als, e_hosvd)
+
+
+@pytest.mark.slow
+def test_setup_fixed_R_certified_error_c2(oracle, rsd):
+    """C2 (n = 1024, R = 12, exact CP rank 2000 x 20 = 40,000): the whole-grid relative
+    Frobenius error of the library's long-range F, certified from the factors by the Gram
+    identity (no dense tensor), agrees with the error the build reports for its two
+    steps (Tucker projection, then CP of the core: orthogonal parts, so their squares add) to
+    within 10%: the report is neither optimistic nor vacuous."""
+    w = syn.make("C2")
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, grid_n=w.grid_n,
+                    rank_R=w.rank_R, sigma_split=w.sigma_split, eps_quad=w.eps_quad,
+                    eps_split=w.eps_split, flags=rsd.RS_FLAG_HOST_ONLY)
+    Fx = _exact_long_factors(oracle, w, p.export_setup())
+    tb = p.export_tables()
+    e_cert = oracle.certified_rel_error(Fx, [tb["F1"], tb["F2"], tb["F3"]])
+    e_rep = math.hypot(p.info["tucker_err"], p.info["cp_core_err"])
+    assert 0.9 * e_rep <= e_cert <= 1.1 * e_rep, (e_cert, e_rep)

@@ -799,3 +799,59 @@ def test_complex_vs_brute_force_coulomb_of_both_proteins(oracle):
         n_checked += 1
     assert n_checked >= P // 2
     assert n_missing_A == n_checked and n_missing_B == n_checked
+
+
+# ------------------------------------------------------- compression certificates (TEP step 4)
+def _rand_cp(rng, n, K):
+    return [rng.normal(size=(n, K)) for _ in range(3)]
+
+
+def test_cp_norm_and_inner_gram_identity_vs_dense(oracle):
+    """SPEC.md:77-85 frobenius_norm examples: all-ones rank-1 on n = 4 has norm 8; the Gram
+    identity equals the dense norm / inner product (numpy on the materialised tensors) on
+    random rank-6 and rank-5 tensors, n = 8, to 1e-12; certified error 0 for an exact copy and
+    1 against the zero-rank tensor."""
+    ones = [np.ones((4, 1))] * 3
+    assert abs(math.sqrt(oracle.cp_norm2(ones)) - 8.0) < 1e-14
+    rng = np.random.default_rng(41)
+    A, B = _rand_cp(rng, 8, 6), _rand_cp(rng, 8, 5)
+    TA = np.einsum("ik,jk,lk->ijl", *A)
+    TB = np.einsum("ik,jk,lk->ijl", *B)
+    assert abs(oracle.cp_norm2(A, block=4) - np.sum(TA * TA)) <= 1e-12 * np.sum(TA * TA)
+    assert abs(oracle.cp_inner(A, B, block=4) - np.sum(TA * TB)) <= 1e-12 * np.sum(np.abs(TA * TB))
+    assert np.allclose(oracle.cp_dense(*A), TA, rtol=0, atol=1e-12)
+    assert oracle.certified_rel_error(A, A) <= 1e-7
+    zero = [np.zeros((8, 1))] * 3
+    assert abs(oracle.certified_rel_error(A, zero) - 1.0) <= 1e-14
+    D = TA - TB
+    ref = math.sqrt(np.sum(D * D) / np.sum(TA * TA))
+    assert abs(oracle.certified_rel_error(A, B) - ref) <= 1e-10 * ref
+
+
+def test_unfolding_tails_and_hosvd_vs_numpy_svd(oracle):
+    """Unfolding tails from the Grams equal the tail singular values of numpy's SVD of the dense
+    unfoldings; HOSVD's error sits between the largest tail and the root sum of the tails
+    (the De Lathauwer bounds) and vanishes for a tensor of multilinear rank <= R."""
+    rng = np.random.default_rng(42)
+    F = _rand_cp(rng, 10, 7)
+    T = np.einsum("ik,jk,lk->ijl", *F)
+    n2 = float(np.sum(T * T))
+    tails = oracle.unfolding_tails(F, 3)
+    for a in range(3):
+        s = np.linalg.svd(np.moveaxis(T, a, 0).reshape(10, -1), compute_uv=False)
+        assert abs(tails[a] - np.sum(s[3:] ** 2)) <= 1e-10 * n2
+    e = oracle.hosvd_dense(T, 3)[4]
+    assert math.sqrt(max(tails) / n2) - 1e-12 <= e <= math.sqrt(sum(tails) / n2) + 1e-12
+    assert oracle.hosvd_dense(T, 7)[4] <= 1e-6
+
+
+def test_cp_als_recovers_exact_low_rank(oracle):
+    """Dense CP-ALS recovers a generic rank-3 tensor (relative error < 1e-8) and its error is
+    never below the unfolding lower bound at a smaller width."""
+    rng = np.random.default_rng(43)
+    F = _rand_cp(rng, 9, 3)
+    T = np.einsum("ik,jk,lk->ijl", *F)
+    assert oracle.cp_als_dense(T, 3, iters=300, seed=1)[3] < 1e-8
+    tails = oracle.unfolding_tails(F, 2)
+    e2 = oracle.cp_als_dense(T, 2, iters=100, seed=1)[3]
+    assert e2 >= math.sqrt(max(tails) / float(np.sum(T * T))) - 1e-12
