@@ -546,8 +546,9 @@ int launch_forces_window(const ScoreArgs& a, double* out, cudaStream_t st, int s
   const int row_bytes = R * 8;
   const int cap = std::min(a.n, (smem_max - 1024) / (3 * row_bytes));
   const size_t bytes = (size_t)3 * cap * row_bytes;
-  cudaFuncSetAttribute(force_window_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)bytes);
+  const cudaError_t ae = cudaFuncSetAttribute(force_window_kernel<R>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (ae != cudaSuccess) return (int)ae;
   const int64_t blocks = std::min<int64_t>((a.P + kWinTile - 1) / kWinTile, sms);
   force_window_kernel<R><<<(int)std::max<int64_t>(blocks, 1), kWinThreads, bytes, st>>>(a, out, cap);
   return (int)cudaGetLastError();
