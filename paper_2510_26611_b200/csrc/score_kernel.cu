@@ -59,9 +59,6 @@ using namespace dev;
 #ifndef RS_WIN_SLACK
 #define RS_WIN_SLACK 1.5
 #endif
-#ifndef RS_NBR
-#define RS_NBR 2
-#endif
 #ifndef RS_LOC_CELLS
 #define RS_LOC_CELLS 10240
 #endif
@@ -441,49 +438,20 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(rc1.w, sv1));
 }
 
-// H5 + H6 for one candidate list entry (see nbr_pair)
-__device__ __forceinline__ void nbr_one(const ScoreArgs& a, double x0, double x1, double x2,
-                                        double z, int c0, int c1, int c2, const int4 en, bool a0,
-                                        double& hi, double& lo, double& best) {
-  int e0, e1, e2;
-  unsigned dd = entry_dd(c0, c1, c2, en, e0, e1, e2);
-  dd = a0 ? dd : 0xffffffffu;
-  const bool sr = dd <= a.ns2, v = dd < a.vdw_cells2;
-  const double4 rc = ldg_d4_p(a.t.prec + en.z, sr || v);
-  const double sv = short_value(a, e0, e1, e2, sr);
-  pair_hit(x0, x1, x2, rc, v, best);
-  if (sr) dd_add_prod(hi, lo, z, __dmul_rn(rc.w, sv));
-}
-
 #ifndef RS_NQ
 #define RS_NQ 3
 #endif
-#ifndef RS_NPAIR
-#define RS_NPAIR 2     // candidates per lane and neighbour pass (1 or 2)
-#endif
 constexpr int kNQ = RS_NQ;   // per-lane stack of atoms waiting for their candidate walk
 
-// Per-warp neighbour queue (RS_NBR == 2): atoms whose candidates a lane has not started yet
+// Per-warp neighbour queues: atoms whose candidates a lane has not started yet
 struct __align__(16) NbrQueue {
   double2 x01[kNQ][32];   // x'_0, x'_1
   double2 x2z[kNQ][32];   // x'_2, charge
   int4 cb[kNQ][32];       // i0 | i1 << 16, i2, first entry, end entry
 };
 
-#if RS_NBR == 2
-constexpr size_t kQueueBytes = sizeof(NbrQueue) * kWarps;   // dynamic shared memory
-#else
-constexpr size_t kQueueBytes = 0;
-#endif
 
-// Per-warp staging of the flattened neighbour rounds (RS_NBR == 1)
-struct __align__(16) NbrStage {
-  double2 x01[32];   // owner's x'_0, x'_1
-  double2 x2z[32];   // owner's x'_2, charge
-  int4 cb[32];       // owner's cell and (list begin - start of its segment)
-  double2 res[32];   // per pair slot: (d^2 or +inf, fl(z_m s) or 0)
-  int map[32];       // slot where an owner's segment starts -> owner lane
-};
+constexpr size_t kQueueBytes = sizeof(NbrQueue) * kWarps;   // dynamic shared memory
 
 __device__ __forceinline__ int pow2_floor(int v) {   // v >= 1
   return 1 << (31 - __clz(v));
@@ -508,21 +476,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   const unsigned loc_u32 = win_u32 + (unsigned)cap_rows * kRow;
   unsigned char* loc_g = smem_raw + (loc_u32 - raw_u32);
   unsigned* s_loc = reinterpret_cast<unsigned*>(loc_g);   // per coarse cell: begin | count << 24
-#if RS_NBR == 2
   NbrQueue* s_nq = reinterpret_cast<NbrQueue*>(loc_g + (size_t)loc_cap * sizeof(unsigned));
   double2* s_lig = reinterpret_cast<double2*>(loc_g + (size_t)loc_cap * sizeof(unsigned) + kQueueBytes);
-#else
-  double2* s_lig = reinterpret_cast<double2*>(loc_g + (size_t)loc_cap * sizeof(unsigned));
-#endif
   __shared__ int s_wred[kWarps][8];
   __shared__ Window s_cur;
   __shared__ LocalBox s_lb;
   __shared__ int s_next, s_restaged, s_chunk;
   __shared__ double s_rmax2[kWarps];
   __shared__ __align__(8) uint64_t s_bar;
-#if RS_NBR == 1
-  __shared__ NbrStage s_nbr[kWarps];
-#endif
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ligand radius (body frame) and staging: (y0, y1) then (y2, z), structure-of-arrays
@@ -557,7 +518,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   const bool lig_all_smem = L <= lig_smem_n;
   const int nm1 = a.n - 1;
   const unsigned rho16 = (unsigned)(lane & 7) << 4;
-  const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
   unsigned phase = 0;
 
   // dynamic chunks of consecutive poses (a global work counter): the neighbour work per pose
@@ -879,7 +839,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         bool bad = has && !ok;
         double hi = 0.0, lo = 0.0, best = INFINITY;
         const int nsteps = (L + S - 1) >> lgS;
-#if RS_NBR == 2
         // H5 + H6 as a per-lane queue: a lane walks the candidate list of one atom at a time, two
         // entries per atom step, while later atoms with candidates wait on its stack; the entry
         // pair a lane walks next is loaded one atom step ahead, behind that step's H4 gathers
@@ -890,15 +849,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         auto nbr_step = [&]() {
           const bool act = qpos < qend;
           if (__any_sync(kFull, act)) {
-#if RS_NPAIR == 2
             nbr_pair(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, pf1, act,
                      qpos + 1 < qend, hi, lo, best);
             qpos += 2;
-#else
-            nbr_one(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, act, hi, lo,
-                    best);
-            qpos += 1;
-#endif
             if (act && qpos >= qend && qfc > 0) {
               --qfc;
               const double2 v01 = nq.x01[qfc][lane], v2z = nq.x2z[qfc][lane];
@@ -907,15 +860,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               qc01 = cb.x; qc2 = cb.y; qpos = cb.z; qend = cb.w;
             }
             const bool more = qpos < qend;
-#if RS_NPAIR == 2
             if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + qpos, more, pf0, pf1);
-#else
-            if (__any_sync(kFull, more)) pf0 = ldg_int4_p(a.t.nb_ent + qpos, more);
-#endif
           }
         };
-#endif
-#if RS_NBR == 2
         // one candidate round per pass; an atom step only when every lane can take its atom
         // (idle, or room on its stack); after the last atom, walk until every lane is done
         for (int it = 0;;) {
@@ -926,10 +873,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             break;
           }
           const int l = (it++ << lgS) + sub;
-#else
-        for (int it = 0; it < nsteps; ++it) {
-          const int l = (it << lgS) + sub;
-#endif
           const bool act = live && l < L;
           const int lc = l < L ? l : L - 1;
           double y0, y1, y2, z;
@@ -977,22 +920,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             cnt = go ? bc.y : 0;
           }
 #endif
-#if RS_NBR == 0
-          // the atom's first two candidates, loaded before H4 so their latency hides behind it
-          int4 pe0, pe1;
-          ldg_pair_p(a.t.nb_ent + beg, cnt > 0, pe0, pe1);
-#elif RS_NBR == 2
           // enqueue this atom's candidates: walk them next if the lane is idle, else stack them
           // (the pass loop guarantees room); the first entry pair loads behind this step's H4
           if (cnt > 0) {
             if (qpos >= qend) {
               q0 = x0; q1 = x1; q2 = x2; qz = z;
               qc01 = i0 | (i1 << 16); qc2 = i2; qpos = beg; qend = beg + cnt;
-#if RS_NPAIR == 2
               ldg_pair_p(a.t.nb_ent + beg, true, pf0, pf1);
-#else
-              pf0 = ldg_int4_p(a.t.nb_ent + beg, true);
-#endif
             } else {
               nq.x01[qfc][lane] = make_double2(x0, x1);
               nq.x2z[qfc][lane] = make_double2(x2, z);
@@ -1000,7 +934,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               ++qfc;
             }
           }
-#endif
           // H4 (O4)
           double phi = 0.0;
           if constexpr (RT > 0) {
@@ -1037,109 +970,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           }
           const double zg = go ? z : 0.0;
           dd_add_prod(hi, lo, zg, phi);
-#if RS_NBR == 0
-          // H5 + H6 over the atom's candidates, two list entries per round (lists start at even
-          // entries, so a pair is one aligned 32-byte load); the loop runs while any lane of
-          // the warp has candidates left
-          if (__any_sync(kFull, cnt > 0)) {
-            int4 en0 = pe0, en1 = pe1;
-            for (int j = 0;;) {
-              const bool a0 = j < cnt, a1 = j + 1 < cnt;
-              int e00, e01, e02, e10, e11, e12;
-              unsigned dd0 = entry_dd(i0, i1, i2, en0, e00, e01, e02);
-              unsigned dd1 = entry_dd(i0, i1, i2, en1, e10, e11, e12);
-              dd0 = a0 ? dd0 : 0xffffffffu;
-              dd1 = a1 ? dd1 : 0xffffffffu;
-              const bool sr0 = dd0 <= a.ns2, sr1 = dd1 <= a.ns2;
-              const bool v0 = dd0 < a.vdw_cells2, v1 = dd1 < a.vdw_cells2;
-              const double4 rc0 = ldg_d4_p(a.t.prec + en0.z, sr0 || v0);
-              const double4 rc1 = ldg_d4_p(a.t.prec + en1.z, sr1 || v1);
-              const double sv0 = short_value(a, e00, e01, e02, sr0);
-              const double sv1 = short_value(a, e10, e11, e12, sr1);
-              j += 2;
-              const bool more = j < cnt;
-              if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + beg + j, more, en0, en1);
-              pair_hit(x0, x1, x2, rc0, v0, best);
-              pair_hit(x0, x1, x2, rc1, v1, best);
-              if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(rc0.w, sv0));
-              if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(rc1.w, sv1));
-              if (!__any_sync(kFull, more)) break;
-            }
-          }
-#elif RS_NBR == 1
-          // H5 + H6 over the step's (atom, candidate) pairs flattened across the warp: owners
-          // (lanes whose atom has candidates) stage their atom, pair lanes take consecutive
-          // candidates of the concatenated lists, write (d^2, fl(z_m s)) per pair, and each
-          // owner merges its own pairs' results (the pose sums are order-free, O6/O7)
-          if (__any_sync(kFull, cnt > 0)) {
-            NbrStage& ns_ = s_nbr[warp];
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int v = __shfl_up_sync(kFull, incl, o);
-              if (lane >= o) incl += v;
-            }
-            const int total = __shfl_sync(kFull, incl, 31);
-            const int excl = incl - cnt;
-            if (cnt > 0) {
-              ns_.x01[lane] = make_double2(x0, x1);
-              ns_.x2z[lane] = make_double2(x2, z);
-              ns_.cb[lane] = make_int4(i0, i1, i2, beg - excl);
-            }
-            int carry = 0;
-            for (int base = 0; base < total; base += 32) {
-              const int rel = excl - base;
-              const bool starts = cnt > 0 && rel >= 0 && rel < 32;
-              if (starts) ns_.map[rel] = lane;
-              const unsigned M = __reduce_or_sync(kFull, starts ? 1u << (rel & 31) : 0u);
-              __syncwarp();
-              const unsigned mk = M & lanemask_le;
-              const int owner = mk ? ns_.map[31 - __clz(mk)] : carry;
-              carry = __shfl_sync(kFull, owner, 31);
-              const int k = base + lane;
-              const bool act = k < total;
-              const int4 oc = ns_.cb[owner];
-              const int4 en = ldg_int4_p(a.t.nb_ent + oc.w + k, act);
-              int e0, e1, e2;
-              unsigned dd = entry_dd(oc.x, oc.y, oc.z, en, e0, e1, e2);
-              dd = act ? dd : 0xffffffffu;
-              const bool sr = dd <= a.ns2, vr = dd < a.vdw_cells2;
-              const double4 rc = ldg_d4_p(a.t.prec + en.z, sr || vr);
-              const double sv = short_value(a, e0, e1, e2, sr);
-              double d2 = INFINITY;
-              if (vr) {
-                const double2 o01 = ns_.x01[owner], o2z = ns_.x2z[owner];
-                const double dx0 = __dsub_rn(o01.x, rc.x);
-                const double dx1 = __dsub_rn(o01.y, rc.y);
-                const double dx2 = __dsub_rn(o2z.x, rc.z);
-                d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
-              }
-              const double bterm = sr ? __dmul_rn(rc.w, sv) : 0.0;
-              // only pairs below D_cap (they may lower the min) or inside the ball reach the owner
-              const bool keep = sr || d2 < a.dcap2;
-              if (keep) ns_.res[lane] = make_double2(d2, bterm);
-              const unsigned kept = __ballot_sync(kFull, keep);
-              __syncwarp();
-              // each owner merges its kept pairs of this round (slots [excl - base, incl - base))
-              const int jlo = max(excl - base, 0), jhi = min(incl - base, 32);
-              unsigned my = 0;
-              if (jhi > jlo) {
-                const unsigned hiw = jhi >= 32 ? 0xffffffffu : ((1u << jhi) - 1u);
-                my = kept & hiw & ~((1u << jlo) - 1u);
-              }
-              while (__any_sync(kFull, my != 0)) {
-                if (my) {
-                  const int j = __ffs(my) - 1;
-                  my &= my - 1u;
-                  const double2 r = ns_.res[j];
-                  best = r.x < best ? r.x : best;
-                  if (r.y != 0.0) dd_add_prod(hi, lo, z, r.y);
-                }
-              }
-              __syncwarp();
-            }
-          }
-#endif
         }
         // H7: merge the S lanes of each pose (xor butterfly within aligned groups of S lanes;
         // TwoSum is exact, so partners agree); min d^2 and the invalid flag likewise
