@@ -113,9 +113,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def load_workload(name, pose_stream=0):
+def load_workload(name, pose_stream=0, **kw):
     from synth import configs as syn
-    return syn.make(name, pose_stream=pose_stream)
+    return syn.make(name, pose_stream=pose_stream, **kw)
+
+
+def workload_kw(args):
+    """C5's sweep point (BASELINE: R in {8, 16, 32} x short-range cutoff {1, 2, 3} x default)."""
+    if args.config == "C5":
+        return {"rank_R": args.c5_rank, "sigma_mult": args.c5_sigma_mult}
+    return {}
 
 
 def _free_port():
@@ -147,9 +154,9 @@ def rank_batch(args, world, rank):
     compact).  Returns (workload, lo, hi, global P)."""
     from paper_2510_26611_b200.shard import shard_bounds
     if args.scaling == "weak":
-        w = load_workload(args.config, pose_stream=rank)
+        w = load_workload(args.config, pose_stream=rank, **workload_kw(args))
         return w, 0, w.P, w.P * world
-    w = load_workload(args.config)
+    w = load_workload(args.config, **workload_kw(args))
     lo, hi = shard_bounds(w.P, world, rank)
     return w, lo, hi, w.P
 
@@ -205,7 +212,7 @@ def impl_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
-    w = load_workload(args.config)
+    w = load_workload(args.config, **workload_kw(args))
     from paper_2510_26611_b200 import rsdock
     flags = 0
     try:
@@ -290,7 +297,7 @@ def bench_ppiem(args):
         __graft_entry__.build_library()
     if dist:
         dist.barrier()
-    w = load_workload(args.config)
+    w = load_workload(args.config, **workload_kw(args))
     prm = dict(w.params())
     prm["dmin_cap"] = w.sigma_vdw + 2.0
     prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **prm, device=local)
@@ -344,6 +351,10 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--c5-rank", type=int, default=16, choices=[8, 16, 32],
+                    help="C5 sweep: CP width R")
+    ap.add_argument("--c5-sigma-mult", type=int, default=1, choices=[1, 2, 3],
+                    help="C5 sweep: short-range cutoff sigma_s = k x 2 A")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-poses", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -432,13 +443,13 @@ def main():
         tr = w.poses[:, 4:]
         inv_h = w.grid_n / (2 * w.box_half_width)
         cell = lambda x: np.clip(np.ceil((x + w.box_half_width) * inv_h) - 1, 0, w.grid_n - 1)
-        lo = cell(tr.min(0) - rl - 0.5).astype(np.int32)
-        hi = cell(tr.max(0) + rl + 0.5).astype(np.int32)
+        blo = cell(tr.min(0) - rl - 0.5).astype(np.int32)
+        bhi = cell(tr.max(0) + rl + 0.5).astype(np.int32)
         t1 = time.perf_counter()
-        prot = parent.restrict_box(lo, hi, args.box,
+        prot = parent.restrict_box(blo, bhi, args.box,
                                    flags=fl | (rsdock.RS_FLAG_BOX_SCHEME_B if scheme_b else 0))
         box_info = {"scheme": args.box_scheme.upper(), "restrict_seconds": time.perf_counter() - t1,
-                    "lo": lo.tolist(), "hi": hi.tolist(), "R_pi": args.box,
+                    "lo": blo.tolist(), "hi": bhi.tolist(), "R_pi": args.box,
                     "box_cp_core_err": prot.info["cp_core_err"],
                     "parent_cp_core_err": parent.info["cp_core_err"],
                     "parent_sampled_max_err": parent.info["sampled_max_err"],
@@ -549,11 +560,17 @@ def main():
     t_s = ms * 1e-3
     achieved = gather_bytes / t_s / 1e9
     smem_peak = mb.get("lds128_random_row_rotated_gbs") if mb else None
-    l2_peak = mb.get("l2_gather_1p5MB_gbs") if mb else None
+    l2_peak = mb.get("l2_gather_cg_9p4MB_gbs") if mb else None          # L2 service rate, C4 size
+    l2_peak_c3 = mb.get("l2_gather_cg_1p6MB_gbs") if mb else None       # the same at C3's size
     fp64_rate = mb.get("dfma_instr_per_s") if mb else None
     dp_instr = ((0.0 if args.f32 else 3.0 * R) + 25.0) * P * L   # 2R DMUL + R DADD + ~25 per atom
     if args.forces:
         dp_instr = (12.0 * R + 80.0) * P * L      # four values (8R DMUL + 4R DADD) + resultants
+    # the variant the library runs for this ligand: a shared-memory window of the tile's rows
+    # (bound: shared-memory bandwidth) or rows from L2 (bound: L2 gather bandwidth)
+    path = rsdock.RS_PATH_WINDOW if args.forces else rsdock.rs_score_path(prot.handle, w.ligand_xyz)
+    on_l2 = path != rsdock.RS_PATH_WINDOW
+    peak = l2_peak if on_l2 else smem_peak
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tfile):
@@ -562,15 +579,17 @@ def main():
         except Exception:
             traffic = None
     roofline = {
-        "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-        "frac": (achieved / smem_peak) if smem_peak else None, "traffic": traffic,
+        "bound": "l2" if on_l2 else "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": (achieved / peak) if peak else None, "traffic": traffic,
         "kernel": (f"force_window_kernel<{R}>" if R in (4, 8, 16, 32) else f"force_kernel<{R}>")
-                  if args.forces else f"score_kernel<{R}>",
-        "peak_source": "tools/microbench (same run): conflict-free random-row LDS.128 "
-                       "(lane-rotated chunks), 148 SMs",
+                  if args.forces else f"score_kernel<{R}>" + (" (L2 rows)" if on_l2 else " (smem window)"),
+        "peak_source": ("tools/microbench (same run): random 32-byte-sector row gathers with "
+                        "ld.global.cg (L2 only) over a 9.4 MB table, 148 SMs" if on_l2 else
+                        "tools/microbench (same run): conflict-free random-row LDS.128 "
+                        "(lane-rotated chunks), 148 SMs"),
         "algorithmic_bytes_per_launch": gather_bytes,
         "fp64_frac": (dp_instr / t_s / fp64_rate) if fp64_rate else None,
-        "l2_literal_frac": (achieved / l2_peak) if l2_peak else None,
+        "l2_literal_frac": (achieved / (l2_peak if on_l2 else l2_peak_c3)) if (l2_peak and l2_peak_c3) else None,
         "hbm_peak_measured_gbs": peaks.get("hbm_gbs"),
     }
     cpu = None

@@ -232,6 +232,32 @@ int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig
                         const double* poses, int64_t P, double* forces_out,
                         int64_t* invalid_count_dev, void* cuda_stream);
 
+/*
+ * Which variant of the fused scoring kernel rs_score_poses[_async] runs for this handle and a
+ * ligand (host pointer, n_lig x 3 body-frame coordinates; only its radius matters), without
+ * launching anything: RS_PATH_WINDOW (H4 rows staged in a shared-memory window per pose tile:
+ * the roofline is shared-memory bandwidth), RS_PATH_L2 (rows gathered from L2 with 32-byte
+ * loads: the window of one translation does not fit) or RS_PATH_L2_RUNTIME (a width without a
+ * compiled kernel, L2 rows).  The measurement (bench.py) picks its roofline from this.  Returns
+ * the path (> 0) or a negative RS_E_* code.
+ */
+#define RS_PATH_WINDOW     1
+#define RS_PATH_L2         2
+#define RS_PATH_L2_RUNTIME 3
+int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig);
+
+/*
+ * Handle cache (SPEC.md:207's kernel cache): rs_save_handle writes every host-side table of the
+ * handle (parameters, quadrature, split, CP factors, short-range rows, protein atoms and cells,
+ * cell lists, Tucker form, setup report) to one binary file with a 64-bit checksum;
+ * rs_load_handle reads it back bit for bit and uploads it to `device` (< 0: the saved ordinal),
+ * skipping the setup (S1-S9).  flags may hold RS_FLAG_HOST_ONLY.  The file is tied to this
+ * library's layout of the rs_params struct; a mismatch is refused.  rs_save_handle returns 0
+ * or a negative RS_E_* code; rs_load_handle returns NULL on error (rs_last_error()).
+ */
+int rs_save_handle(const rs_handle* h, const char* path);
+rs_handle* rs_load_handle(const char* path, int32_t device, int32_t flags);
+
 /* Fill *out.  Returns 0 or RS_E_INVALID_ARG. */
 int rs_get_info(const rs_handle* h, rs_info* out);
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -363,6 +364,7 @@ const char* rs_last_error(void) { return g_err.c_str(); }
 
 rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
                             double box_half_width, const rs_params* params) {
+  rs::NvtxRange nvtx_("rs_build_protein");
   g_err.clear();
   auto t0 = std::chrono::steady_clock::now();
   rs_params prm;
@@ -444,6 +446,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     hd->Rs = (int)ts.size();
     hd->n_sigma = (int)std::ceil(prm.sigma_split / h);
     auto lap = [&](const char* what) {
+      nvtxMarkA(what);                    // end of a setup phase on the NVTX timeline
       static const bool on = std::getenv("RS_SETUP_TIMING") != nullptr;
       if (on)
         std::fprintf(stderr, "[rs setup] %-22s %8.3f s (at %.3f)\n", what,
@@ -509,6 +512,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
 // long-range CP factors concatenate along the rank (R = sum R_p, no recompression), and the
 // short-range part and the vdW distance run over the union of the atoms.
 rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, int32_t flags) {
+  rs::NvtxRange nvtx_("rs_combine_proteins");
   g_err.clear();
   auto t0 = std::chrono::steady_clock::now();
   if (!parts || n_parts < 1) { set_err("need n_parts >= 1 handles"); return nullptr; }
@@ -617,6 +621,7 @@ rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, i
 
 rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t* hi, int32_t rank,
                            int32_t flags) {
+  rs::NvtxRange nvtx_("rs_restrict_box");
   g_err.clear();
   auto t0 = std::chrono::steady_clock::now();
   if (!h || !lo || !hi) { set_err("null argument"); return nullptr; }
@@ -705,6 +710,24 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
   return H.release();
 }
 
+int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig) {
+  if (!h || (n_lig > 0 && !xyz_lig) || n_lig < 0) { set_err("null or invalid argument"); return RS_E_INVALID_ARG; }
+  if (n_lig > (int64_t)1 << 30) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
+  if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
+  if (pointer_kind(xyz_lig) != 0) { set_err("rs_score_path needs a host ligand"); return RS_E_INVALID_ARG; }
+  CUDA_TRY(cudaSetDevice(h->device), RS_E_CUDA);
+  rs::ScoreArgs a = base_args(h);
+  a.L = n_lig;
+  a.P = 0;
+  a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, false, nullptr);
+  const int e = rs::plan_score(a, h->device);
+  if (e < rs::kPathWindow || e > rs::kPathL2Runtime) {
+    set_err(std::string("launch plan failed: ") + cudaGetErrorString((cudaError_t)e));
+    return RS_E_CUDA;
+  }
+  return e;
+}
+
 int rs_get_info(const rs_handle* h, rs_info* out) {
   if (!h || !out) { set_err("null argument"); return RS_E_INVALID_ARG; }
   std::memset(out, 0, sizeof(*out));
@@ -773,6 +796,7 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
                              int64_t n_lig, const double* poses, int64_t P,
                              double* energies_out, double* mindist_out,
                              int64_t* invalid_count_dev, void* cuda_stream) {
+  rs::NvtxRange nvtx_("rs_score_poses_async");
   if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
   if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
   if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
@@ -811,6 +835,7 @@ int64_t rs_score_poses_async(rs_handle* h, const double* q_lig, const double* xy
 int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
                         const double* poses, int64_t P, double* forces_out,
                         int64_t* invalid_count_dev, void* cuda_stream) {
+  rs::NvtxRange nvtx_("rs_score_forces");
   if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
   if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
   if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
@@ -842,6 +867,7 @@ int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig
 
 int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig, int64_t n_lig,
                        const double* poses, int64_t P, double* energies_out, double* mindist_out) {
+  rs::NvtxRange nvtx_("rs_score_poses");
   if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
   if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
   if (n_lig < 0 || P < 0) { set_err("negative size"); return RS_E_INVALID_ARG; }
@@ -906,8 +932,15 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, lig_dev, st[0]);
   static const bool streamed_off = std::getenv("RS_NO_STREAMED") != nullptr;
   // streamed only for large batches: below ~4e5 poses (C2: 1e5) the per-chunk stream waits cost
-  // more than the launch ramps they save (measured: C2 all-host 0.40 ms streamed, 0.36 chunked)
-  if (!pose_dev && !e_dev && !d_dev && P >= 400000 && wait_value32() && !streamed_off) {
+  // more than the launch ramps they save (measured: C2 all-host 0.40 ms streamed, 0.36 chunked).
+  // RS_STREAM_MIN_POSES moves the threshold (the sanitizer runs use it on small batches).
+  static const int64_t stream_min = [] {
+    const char* v = std::getenv("RS_STREAM_MIN_POSES");
+    return v ? std::max<int64_t>(1, std::atoll(v)) : (int64_t)400000;
+  }();
+  static std::atomic<bool> stream_broken{false};   // a streamed launch stalled once: no more
+  if (!pose_dev && !e_dev && !d_dev && P >= stream_min && wait_value32() && !streamed_off &&
+      !stream_broken.load()) {
     // Streamed pipeline: ONE launch over all P poses on stream 0 while stream 1 copies the
     // poses in geometrically growing chunks, each followed by its arrival flag; the kernel
     // waits for a chunk's flag before it scores poses from it and counts finished poses per
@@ -962,10 +995,13 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     CUDA_TRY(cudaStreamWaitEvent(st[1], armed, 0), RS_E_CUDA);
     CUDA_TRY(cudaStreamWaitEvent(st[2], armed, 0), RS_E_CUDA);
     cudaEventDestroy(armed);
+    // fault injection for the stall path's test: arrival flags never sent
+    static const bool drop_flags = std::getenv("RS_STREAM_FAULT_DROP_FLAGS") != nullptr;
     for (int i = 0; i < n_cb; ++i) {
       CUDA_TRY(cudaMemcpyAsync(d_pose + 7 * cb[i], poses + 7 * cb[i], (cb[i + 1] - cb[i]) * 7 * sizeof(double),
                                cudaMemcpyHostToDevice, st[1]), RS_E_CUDA);
-      CUDA_TRY(cudaMemcpyAsync(d_arrive + i, h->h_ones + i, sizeof(unsigned), cudaMemcpyHostToDevice, st[1]), RS_E_CUDA);
+      if (!drop_flags)
+        CUDA_TRY(cudaMemcpyAsync(d_arrive + i, h->h_ones + i, sizeof(unsigned), cudaMemcpyHostToDevice, st[1]), RS_E_CUDA);
     }
     a.poses = d_pose;
     a.P = P;
@@ -997,8 +1033,13 @@ int64_t rs_score_poses(rs_handle* h, const double* q_lig, const double* xyz_lig,
     unsigned stall = 0;
     CUDA_TRY(cudaMemcpy(&cnt0, d_cnt, sizeof(cnt0), cudaMemcpyDeviceToHost), RS_E_CUDA);
     CUDA_TRY(cudaMemcpy(&stall, d_stall, sizeof(stall), cudaMemcpyDeviceToHost), RS_E_CUDA);
-    if (stall) { set_err("streamed pipeline: a pose chunk never arrived"); return RS_E_CUDA; }
-    return (int64_t)cnt0;
+    if (!stall) return (int64_t)cnt0;
+    // the copies did not run beside the kernel: its results are void; recompute the batch with
+    // the chunked launches below (every later call skips streaming)
+    stream_broken.store(true);
+    CUDA_TRY(cudaMemset(d_cnt, 0, kStreams * sizeof(unsigned long long)), RS_E_CUDA);
+    std::fprintf(stderr, "[rsdock] streamed pipeline stalled (copy engine not concurrent with the kernel); "
+                         "recomputing with chunked launches\n");
   }
   int chunk = 0;
   // first chunk P/16 (measured at C3 on pinned host buffers: P/64 2.185 ms, P/16 2.147 ms; the
@@ -1066,6 +1107,7 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
                       const double* centre, const double* dirs, int32_t m_P, const double* quats,
                       int32_t m_L, double s_start, double tol, int32_t max_iter,
                       double* energies_out, double* s_out, int32_t* status_out) {
+  rs::NvtxRange nvtx_("rs_ppiem_scan");
   if (!h) { set_err("null handle"); return RS_E_INVALID_ARG; }
   if (!h->on_device) { set_err("handle has no device tables"); return RS_E_NO_DEVICE; }
   if (!centre || !dirs || !quats || !energies_out || !s_out || !status_out || m_P <= 0 || m_L <= 0 ||
@@ -1183,6 +1225,155 @@ int64_t rs_ppiem_scan(rs_handle* h, const double* q_lig, const double* xyz_lig, 
     if (sv != 0 && sv != 4) energies_out[p] = NAN;
   }
   return 0;
+}
+
+}  // extern "C"
+
+// ---- handle save / load (SPEC.md:207's kernel cache) ---------------------------
+// One binary file: "RSDOCK02", then every host-side field of the handle in a fixed order (PODs
+// raw, vectors as a u64 count + elements), then a 64-bit FNV-1a hash of everything before it.
+// Loading restores the host tables bit for bit and uploads them like a build (S10).
+namespace {
+struct Writer {
+  std::vector<unsigned char> buf;
+  template <class T> void pod(const T& v) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+    buf.insert(buf.end(), p, p + sizeof(T));
+  }
+  template <class T> void vec(const std::vector<T>& v) {
+    pod<uint64_t>(v.size());
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(v.data());
+    buf.insert(buf.end(), p, p + v.size() * sizeof(T));
+  }
+};
+struct Reader {
+  const unsigned char* p;
+  size_t left;
+  bool ok = true;
+  template <class T> void pod(T& v) {
+    if (!ok || left < sizeof(T)) { ok = false; return; }
+    std::memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    left -= sizeof(T);
+  }
+  template <class T> void vec(std::vector<T>& v) {
+    uint64_t n = 0;
+    pod(n);
+    if (!ok || n > left / sizeof(T)) { ok = false; return; }
+    v.assign(reinterpret_cast<const T*>(p), reinterpret_cast<const T*>(p) + n);
+    p += n * sizeof(T);
+    left -= n * sizeof(T);
+  }
+};
+uint64_t fnv1a(const unsigned char* p, size_t n) {
+  uint64_t x = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) x = (x ^ p[i]) * 1099511628211ull;
+  return x;
+}
+constexpr char kMagic[8] = {'R', 'S', 'D', 'O', 'C', 'K', '0', '2'};
+
+// the handle's host fields in file order (Archive = Writer or Reader)
+template <class A, class H>
+void archive_handle(A& ar, H& h) {
+  ar.pod(h.prm);
+  ar.pod(h.n); ar.pod(h.b); ar.pod(h.h); ar.pod(h.inv_h);
+  ar.pod(h.quad.s); ar.pod(h.quad.Ls); ar.pod(h.quad.err); ar.pod(h.quad.K);
+  ar.vec(h.quad.t); ar.vec(h.quad.a);
+  ar.vec(h.is_long);
+  ar.pod(h.R); ar.pod(h.Rs); ar.pod(h.n_sigma); ar.pod(h.R_long_ref);
+  for (int a = 0; a < 3; ++a) ar.vec(h.F[a]);
+  for (int a = 0; a < 3; ++a) ar.vec(h.S[a]);
+  ar.pod(h.M);
+  ar.vec(h.xyz); ar.vec(h.z); ar.vec(h.cells);
+  ar.pod(h.cg.shift); ar.pod(h.cg.lo); ar.pod(h.cg.dim); ar.vec(h.cg.off); ar.vec(h.cg.idx);
+  ar.pod(h.rep);
+  ar.pod(h.tucker.r);
+  for (int a = 0; a < 3; ++a) ar.vec(h.tucker.U[a]);
+  ar.vec(h.tucker.G);
+  ar.pod(h.box_lo); ar.pod(h.box_hi);
+  ar.pod(h.setup_seconds);
+  ar.pod(h.f32);
+}
+}  // namespace
+
+extern "C" {
+
+int rs_save_handle(const rs_handle* h, const char* path) {
+  if (!h || !path) { set_err("null argument"); return RS_E_INVALID_ARG; }
+  rs::NvtxRange nvtx_("rs_save_handle");
+  Writer w;
+  try {
+    w.buf.insert(w.buf.end(), kMagic, kMagic + 8);
+    w.pod<uint32_t>(sizeof(rs_params));
+    archive_handle(w, *h);
+    w.pod(fnv1a(w.buf.data(), w.buf.size()));
+  } catch (const std::bad_alloc&) {
+    set_err("out of host memory");
+    return RS_E_NOMEM;
+  }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) { set_err(std::string("cannot open ") + path + " for writing"); return RS_E_INVALID_ARG; }
+  const size_t n = std::fwrite(w.buf.data(), 1, w.buf.size(), f);
+  const int cl = std::fclose(f);
+  if (n != w.buf.size() || cl != 0) { set_err(std::string("short write to ") + path); return RS_E_INVALID_ARG; }
+  return 0;
+}
+
+rs_handle* rs_load_handle(const char* path, int32_t device, int32_t flags) {
+  if (!path) { set_err("null argument"); return nullptr; }
+  rs::NvtxRange nvtx_("rs_load_handle");
+  std::vector<unsigned char> buf;
+  {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) { set_err(std::string("cannot open ") + path); return nullptr; }
+    unsigned char tmp[1 << 16];
+    size_t k;
+    while ((k = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + k);
+    std::fclose(f);
+  }
+  if (buf.size() < 8 + 4 + 8 || std::memcmp(buf.data(), kMagic, 8) != 0) {
+    set_err(std::string(path) + ": not an rsdock handle file (magic)");
+    return nullptr;
+  }
+  uint64_t stored = 0;
+  std::memcpy(&stored, buf.data() + buf.size() - 8, 8);
+  if (fnv1a(buf.data(), buf.size() - 8) != stored) {
+    set_err(std::string(path) + ": checksum mismatch (truncated or corrupted)");
+    return nullptr;
+  }
+  Reader r{buf.data() + 8, buf.size() - 16};
+  uint32_t psz = 0;
+  r.pod(psz);
+  if (psz != sizeof(rs_params)) { set_err("handle file from an incompatible library version"); return nullptr; }
+  std::unique_ptr<rs_handle> H;
+  try {
+    H.reset(new rs_handle());
+    archive_handle(r, *H);
+  } catch (const std::bad_alloc&) {
+    set_err("out of host memory");
+    return nullptr;
+  }
+  if (!r.ok || r.left != 0) { set_err(std::string(path) + ": malformed handle file"); return nullptr; }
+  rs_handle* hd = H.get();
+  const bool host_only = (flags & RS_FLAG_HOST_ONLY) != 0;
+  hd->prm.device = device >= 0 ? device : hd->prm.device;
+  hd->prm.flags = (hd->prm.flags & ~RS_FLAG_HOST_ONLY) | (flags & RS_FLAG_HOST_ONLY);
+  hd->device = hd->prm.device;
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= hd->device || hd->device < 0) {
+      cudaGetLastError();
+      set_err("no CUDA device (there is no CPU fallback; use RS_FLAG_HOST_ONLY for host-only tables)");
+      return nullptr;
+    }
+    if (upload_handle(hd) != 0) {
+      std::string msg = g_err;
+      free_device(hd);
+      set_err(msg.empty() ? "upload failed" : msg);
+      return nullptr;
+    }
+  }
+  return H.release();
 }
 
 }  // extern "C"

@@ -1,6 +1,8 @@
 // Internal declarations of librsdock (not part of the C ABI; see include/rs_dock.h).
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>   // NVTX v3, header-only: ranges cost nothing without a profiler
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -13,6 +15,15 @@
 #include "../../include/rs_dock.h"
 
 namespace rs {
+
+// NVTX range over a C-ABI call or a setup phase (visible in nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 // ---- host setup (Algorithm TEP) --------------------------------------
 
@@ -161,6 +172,10 @@ constexpr int kPackPad = 24;     // zero cells before each axis of the packed ra
 // Launch the fused scoring kernel (H1-H8).  Returns a cudaError_t as int.  *launches
 // (if not null) is incremented by the number of kernels enqueued.
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
+// which variant launch_score would run for these arguments (no launch): a kPath* value, or a
+// positive CUDA error code
+constexpr int kPathWindow = 1, kPathL2 = 2, kPathL2Runtime = 3;
+int plan_score(const ScoreArgs& a, int device);
 const char* score_kernel_variant(int R);
 // NEXT row N2: PPIEM scan kernels (scan_kernel.cu)
 int launch_scan_init(const double* centre, const double* dirs, const double* quats, int m_P,

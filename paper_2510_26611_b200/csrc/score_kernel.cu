@@ -539,11 +539,18 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
       if (tid == 0) {
         int c = 0;
         while (c + 1 < a.n_cb && a.cb[c + 1] <= p_end - 1) ++c;
+        // bounded by wall time (%globaltimer, ns): if the copy engine does not run beside the
+        // kernel (MPS, a sanitizer, a busy engine) the launch gives up once, flags the stall
+        // and the host recomputes the batch without streaming
         unsigned v = 0;
-        for (long long spin = 0;; ++spin) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.arrive + c) : "memory");
           if (v != 0) break;
-          if (spin > (1ll << 26)) { atomicExch(a.stall, 1u); break; }
+          if (*(volatile const unsigned*)a.stall != 0u) break;   // another CTA gave up already
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 2000000000ull) { atomicExch(a.stall, 1u); break; }
           __nanosleep(256);
         }
       }
@@ -1059,8 +1066,9 @@ bool local_table_map(const ScoreArgs& a, int cd, CUtensorMap* m) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+constexpr int kPlanned = -12346;    // launch_t in plan-only mode: the variant would launch
 template <int RT, bool F32, bool WIN>
-int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot) {
+int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool plan_only = false) {
   DevCache& dc = g_dev[dev & 63];
   std::call_once(dc.attr_once[slot], [&] {
     cudaFuncAttributes fa;
@@ -1135,6 +1143,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot) {
   const int64_t chunks = cp.nbig + (rest + cp.tail - 1) / cp.tail;
   int grid = (int)std::min<int64_t>(chunks, (int64_t)dc.sms);
   if (grid < 1) grid = 1;
+  if (plan_only) return kPlanned;
   score_kernel<RT, F32, WIN><<<grid, kThreads, dyn, st>>>(a, cap_rows, lig_n, loc_cap, cp, tmap, loc_cd);
   return (int)cudaGetLastError();
 }
@@ -1227,8 +1236,11 @@ void pack_window_rows32(const std::vector<double>& F, int n, int R, std::vector<
       }
 }
 
-int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
-  if (a.P <= 0) return 0;
+// Dispatch of one scoring launch: the compiled width's shared-memory window variant, else its
+// L2 variant, else the runtime-width kernel.  plan_only: decide without launching and return
+// the path (kPathWindow / kPathL2 / kPathL2Runtime) or a CUDA error code.
+int launch_or_plan(const ScoreArgs& a, void* stream, int device, int* launches, bool plan_only) {
+  if (a.P <= 0 && !plan_only) return 0;
   if (a.L > (int64_t)1 << 30) return (int)cudaErrorInvalidValue;   // the kernel indexes atoms in int
   DevCache& dc = g_dev[device & 63];
   std::call_once(dc.once, [&] {
@@ -1243,8 +1255,10 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
     // binary32 factors (A21): compiled widths only (the build refuses others)
 #define RS_F32_CASE(RR, SLOT)                                                               \
   case RR:                                                                                 \
-    e = launch_t<RR, true, true>(a, st, device, SLOT);                                     \
-    if (e == kNoWindow) e = launch_t<RR, true, false>(a, st, device, SLOT + 1);            \
+    e = launch_t<RR, true, true>(a, st, device, SLOT, plan_only);                          \
+    if (e == kPlanned) return kPathWindow;                                                 \
+    if (e == kNoWindow) e = launch_t<RR, true, false>(a, st, device, SLOT + 1, plan_only); \
+    if (e == kPlanned) return kPathL2;                                                     \
     break;
     switch (a.R) {
       RS_F32_CASE(4, 20) RS_F32_CASE(8, 22) RS_F32_CASE(12, 24) RS_F32_CASE(16, 26)
@@ -1255,18 +1269,29 @@ int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
   } else {
 #define RS_F64_CASE(RR, SLOT)                                                               \
   case RR:                                                                                 \
-    e = launch_t<RR, false, true>(a, st, device, SLOT);                                    \
-    if (e == kNoWindow) e = launch_t<RR, false, false>(a, st, device, SLOT + 1);           \
+    e = launch_t<RR, false, true>(a, st, device, SLOT, plan_only);                         \
+    if (e == kPlanned) return kPathWindow;                                                 \
+    if (e == kNoWindow) e = launch_t<RR, false, false>(a, st, device, SLOT + 1, plan_only); \
+    if (e == kPlanned) return kPathL2;                                                     \
     break;
     switch (a.R) {
       RS_F64_CASE(4, 2) RS_F64_CASE(8, 4) RS_F64_CASE(12, 6) RS_F64_CASE(16, 8)
       RS_F64_CASE(24, 10) RS_F64_CASE(32, 12)
-      default: e = launch_t<0, false, false>(a, st, device, 0); break;
+      default:
+        e = launch_t<0, false, false>(a, st, device, 0, plan_only);
+        if (e == kPlanned) return kPathL2Runtime;
+        break;
     }
 #undef RS_F64_CASE
   }
   if (launches) *launches += 1;
   return e;
 }
+
+int launch_score(const ScoreArgs& a, void* stream, int device, int* launches) {
+  return launch_or_plan(a, stream, device, launches, false);
+}
+
+int plan_score(const ScoreArgs& a, int device) { return launch_or_plan(a, nullptr, device, nullptr, true); }
 
 }  // namespace rs

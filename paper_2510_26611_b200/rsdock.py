@@ -23,10 +23,11 @@ RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 RS_FLAG_BOX_SCHEME_B = 4
 RS_FLAG_DEVICE_FFT = 8
+RS_PATH_WINDOW, RS_PATH_L2, RS_PATH_L2_RUNTIME = 1, 2, 3
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_restrict_box", "rs_score_poses", "rs_score_poses_async",
             "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",
-            "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
+            "rs_score_path", "rs_save_handle", "rs_load_handle", "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
 
 class rs_params(ctypes.Structure):
@@ -93,6 +94,12 @@ def load():
     L.rs_ppiem_scan.restype = ctypes.c_int64
     L.rs_landscape_minima.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp]
     L.rs_landscape_minima.restype = ctypes.c_int32
+    L.rs_save_handle.argtypes = [_vp, ctypes.c_char_p]
+    L.rs_save_handle.restype = ctypes.c_int
+    L.rs_load_handle.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]
+    L.rs_load_handle.restype = _vp
+    L.rs_score_path.argtypes = [_vp, _vp, ctypes.c_int64]
+    L.rs_score_path.restype = ctypes.c_int
     L.rs_get_info.argtypes = [_vp, ctypes.POINTER(rs_info)]
     L.rs_get_info.restype = ctypes.c_int
     L.rs_export_tables.argtypes = [_vp] + [_vp] * 6
@@ -247,6 +254,17 @@ def rs_landscape_minima(E, top_k):
     return out[:r].copy()
 
 
+def rs_score_path(h, xyz_lig) -> int:
+    """Kernel variant rs_score_poses runs for this ligand (RS_PATH_WINDOW / _L2 / _L2_RUNTIME)."""
+    if isinstance(xyz_lig, np.ndarray):
+        xyz_lig = np.ascontiguousarray(xyz_lig, dtype=np.float64).reshape(-1, 3)
+    n = xyz_lig.shape[0] if xyz_lig.ndim == 2 else xyz_lig.shape[0] // 3
+    r = load().rs_score_path(h, _ptr(xyz_lig, "xyz_lig", count=3 * n, cuda=False), n)
+    if r < 0:
+        raise RuntimeError("rs_score_path: " + rs_last_error())
+    return int(r)
+
+
 def rs_get_info(h) -> dict:
     info = rs_info()
     if load().rs_get_info(h, ctypes.byref(info)) != 0:
@@ -284,6 +302,18 @@ def rs_export_setup(h) -> dict:
                 K=info["quad_K"], Ls=info["quad_Ls"])
 
 
+def rs_save_handle(h, path) -> None:
+    if load().rs_save_handle(h, os.fsencode(path)) != 0:
+        raise RuntimeError("rs_save_handle: " + rs_last_error())
+
+
+def rs_load_handle(path, device=-1, flags=0):
+    h = load().rs_load_handle(os.fsencode(path), int(device), int(flags))
+    if not h:
+        raise RuntimeError("rs_load_handle: " + rs_last_error())
+    return h
+
+
 def rs_free(h) -> None:
     if h:
         load().rs_free(h)
@@ -319,6 +349,20 @@ class Protein:
         self.params = parts[0].params
         self._h = rs_combine_proteins([p.handle for p in parts], flags)
         self.info = rs_get_info(self._h)
+        return self
+
+    def save(self, path):
+        """Write the handle's tables to `path` (rs_save_handle: SPEC's kernel cache)."""
+        rs_save_handle(self._h, path)
+
+    @classmethod
+    def load(cls, path, device=-1, flags=0):
+        """A Protein from a file written by save(), uploaded to `device` without a setup."""
+        self = cls.__new__(cls)
+        self._h = None
+        self._h = rs_load_handle(path, device, flags)
+        self.info = rs_get_info(self._h)
+        self.params = None
         return self
 
     @property

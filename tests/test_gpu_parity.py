@@ -5,11 +5,15 @@ bitwise), min distance bitwise, identical NaN (invalid-pose) pattern and count. 
 compare every pose; full-size configs run the whole batch in the launch configuration
 bench.py times and compare a seeded sample of poses the oracle scores one by one."""
 import math
+import os
+import sys
 
 import numpy as np
 import pytest
 
 from synth import configs as syn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -84,6 +88,79 @@ def test_small_random_all_widths(env, R):
     Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, w.poses)
     Eo, Do, invo = oracle_score(rs_oracle, prot, w, w.poses)
     compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+def test_score_path_plan(env):
+    """rs_score_path reports the variant the launcher picks: the shared-memory window when the
+    whole factor set fits (C1), L2 rows when one translation's rows do not (C5: a 5,000-atom
+    partner at n = 8192), the runtime-width kernel for an uncompiled width; scoring agrees with
+    the oracle on each."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c1(n_poses=64)
+    prot = build(rsdock, w)
+    assert rsdock.rs_score_path(prot.handle, w.ligand_xyz) == rsdock.RS_PATH_WINDOW
+    w10 = syn.random_small(seed=3, M=40, L=9, n=64, b=8.0, R=10, P=40)
+    p10 = build(rsdock, w10)
+    assert rsdock.rs_score_path(p10.handle, w10.ligand_xyz) == rsdock.RS_PATH_L2_RUNTIME
+    w5 = syn.config_c5(rank_R=8, sigma_mult=1, n_poses=64)
+    p5 = build(rsdock, w5)
+    assert rsdock.rs_score_path(p5.handle, w5.ligand_xyz) == rsdock.RS_PATH_L2
+    # a small ligand on the same handle fits the window again
+    assert rsdock.rs_score_path(p5.handle, w5.ligand_xyz[:20] * 0.1) == rsdock.RS_PATH_WINDOW
+    with pytest.raises(ValueError):      # the plan reads a host ligand
+        rsdock.rs_score_path(p5.handle, torch.tensor(w5.ligand_xyz, device="cuda:0"))
+
+
+_STALL_SCRIPT = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2510_26611_b200 import rsdock
+from synth import configs as syn
+w = syn.config_c1(n_poses=1000)
+prot = rsdock.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params())
+poses = np.ascontiguousarray(np.tile(w.poses, (3, 1)))
+E = np.empty(len(poses)); D = np.empty(len(poses))
+inv = rsdock.rs_score_poses(prot.handle, w.ligand_q, w.ligand_xyz, w.L, poses, len(poses), E, D)
+np.save(sys.argv[2], np.stack([E, D]))
+print("invalid", inv)
+'''
+
+
+@pytest.mark.parametrize("fault", [False, True])
+def test_streamed_pipeline_stall_falls_back(env, tmp_path, fault):
+    """The streamed host pipeline (one launch waiting on copy-engine arrival flags) on a small
+    batch (RS_STREAM_MIN_POSES): bitwise the device-resident results; with the arrival flags
+    withheld (fault injection: the copies never run beside the kernel) the launch gives up after
+    its wall-time bound and the call recomputes with chunked launches, still bitwise equal."""
+    import subprocess
+    torch, rsdock, rs_oracle = env
+    envv = dict(os.environ, RS_STREAM_MIN_POSES="1000")
+    if fault:
+        envv["RS_STREAM_FAULT_DROP_FLAGS"] = "1"
+    out = tmp_path / "ed.npy"
+    r = subprocess.run([sys.executable, "-c", _STALL_SCRIPT, ROOT, str(out)], env=envv,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert ("stalled" in r.stderr) == fault
+    Eh, Dh = np.load(out)
+    w = syn.config_c1(n_poses=1000)
+    prot = build(rsdock, w)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, np.tile(w.poses, (3, 1)))
+    assert np.array_equal(Eh, Eg, equal_nan=True) and np.array_equal(Dh, Dg, equal_nan=True)
+
+
+def test_loaded_handle_scores_identically(env, tmp_path):
+    """A handle written by rs_save_handle and read back by rs_load_handle scores every pose
+    bit for bit like the handle it came from (the setup is skipped, S10 runs)."""
+    torch, rsdock, rs_oracle = env
+    w = syn.config_c2(n_rot=2)
+    prot = build(rsdock, w)
+    path = tmp_path / "c2.rsh"
+    prot.save(path)
+    again = rsdock.Protein.load(path, device=0)
+    Ea, Da, ia = gpu_score(torch, rsdock, prot, w, w.poses)
+    Eb, Db, ib = gpu_score(torch, rsdock, again, w, w.poses)
+    assert ia == ib and np.array_equal(Ea, Eb, equal_nan=True) and np.array_equal(Da, Db, equal_nan=True)
 
 
 def test_c1_all_poses(env):

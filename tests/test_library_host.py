@@ -476,3 +476,34 @@ def test_setup_fixed_R_certified_error_c2(oracle, rsd):
     e_cert = oracle.certified_rel_error(Fx, [tb["F1"], tb["F2"], tb["F3"]])
     e_rep = math.hypot(p.info["tucker_err"], p.info["cp_core_err"])
     assert 0.9 * e_rep <= e_cert <= 1.1 * e_rep, (e_cert, e_rep)
+
+
+def test_handle_save_load_roundtrip(rsd, tmp_path):
+    """rs_save_handle / rs_load_handle (SPEC.md:207's kernel cache): every exported table,
+    the setup data and the info of a loaded host-only handle equal the original's bit for bit;
+    a truncated or corrupted file, or a file that is not a handle, is refused with a message."""
+    w = syn.config_c1(n_poses=8)
+    p = rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                    flags=rsd.RS_FLAG_HOST_ONLY)
+    path = tmp_path / "c1.rsh"
+    p.save(path)
+    q = rsd.Protein.load(path, flags=rsd.RS_FLAG_HOST_ONLY)
+    ta, tb = p.export_tables(), q.export_tables()
+    assert ta.keys() == tb.keys()
+    for k in ta:
+        assert np.array_equal(ta[k], tb[k]), k
+    sa, sb = rsd.rs_export_setup(p.handle), rsd.rs_export_setup(q.handle)
+    for k in ("t", "a", "is_long", "cells"):
+        assert np.array_equal(sa[k], sb[k]), k
+    ia, ib = dict(p.info), dict(q.info)
+    for k in ia:
+        if k not in ("setup_seconds",):
+            assert ia[k] == ib[k], k
+    raw = path.read_bytes()
+    bad = tmp_path / "bad.rsh"
+    for blob in (raw[:-9], raw[:100] + bytes([raw[100] ^ 1]) + raw[101:], b"not a handle file at all"):
+        bad.write_bytes(blob)
+        with pytest.raises(RuntimeError, match="checksum|magic|malformed"):
+            rsd.Protein.load(bad, flags=rsd.RS_FLAG_HOST_ONLY)
+    with pytest.raises(RuntimeError, match="cannot open"):
+        rsd.Protein.load(tmp_path / "missing.rsh", flags=rsd.RS_FLAG_HOST_ONLY)

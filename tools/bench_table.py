@@ -19,9 +19,9 @@ for f in sorted(glob.glob(os.path.join(sys.argv[1], "*.json"))):
     e2e = d.get("e2e") or {}
     rows.append((name, f"{d['ms_per_step']:.4f} ms / step ({d['config']['poses']} poses)",
                  f"{d['value']:.3g} poses/s", f"{d.get('atom_evals_per_s', 0):.3g}",
-                 f"{rf.get('frac') or 0:.3f} / {rf.get('l2_literal_frac') or 0:.3f}",
+                 f"{rf.get('bound', '-')} {rf.get('frac') or 0:.3f} / {rf.get('l2_literal_frac') or 0:.3f}",
                  f"{e2e.get('value', 0):.3g}" if e2e else "-"))
-print("| run | time | throughput | atom-evals/s | roofline frac (smem / L2-literal) | e2e poses/s |")
+print("| run | time | throughput | atom-evals/s | roofline: bound, frac (serving level / L2-literal) | e2e poses/s |")
 print("|---|---|---|---|---|---|")
 for r in rows:
     print("| " + " | ".join(r) + " |")

@@ -15,6 +15,10 @@ KEYS = {
     "dram_read_bytes": ("dram__bytes_read.sum", 1.0),
     "dram_write_bytes": ("dram__bytes_write.sum", 1.0),
     "lts_bytes": ("lts__t_bytes.sum", 1.0),
+    "l1_hit_rate_pct": ("l1tex__t_sector_hit_rate.pct", 1.0),
+    "l2_hit_rate_pct": ("lts__t_sector_hit_rate.pct", 1.0),
+    "global_ld_sectors": ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 1.0),
+    "l1tex_data_pipe_wavefronts_pct": ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed", 1.0),
     "smem_ld_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", 1.0),
     "smem_ld_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", 1.0),
     "smem_wavefront_pct_of_peak": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 1.0),
