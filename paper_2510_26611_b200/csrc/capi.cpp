@@ -172,6 +172,7 @@ int upload_handle(rs_handle* h) {
         ent[4 * j + 2] = rank[m];
       }
     if (int e = upload(&h->d_nb_ent, ent, &bytes)) return e;
+    h->n_ent = (int64_t)(ent.size() / 4);
     if (int e = upload(&h->d_nb_range, rng, &bytes)) return e;
     if (h->loc4) {
       // the same ranges packed into 4 bytes, z rows padded to 16 bytes, with rs::kPackPad zero
@@ -253,6 +254,8 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   }
   a.t.nb_ent = (const int4*)h->d_nb_ent;
   a.t.prec = (const double4*)h->d_prec;
+  a.n_ent = h->n_ent;
+  a.n_prot = h->M;
   a.t.short_memo = (const double*)h->d_memo;
   a.t.nb_range = (const int2*)h->d_nb_range;
   a.t.nb_pack = (const unsigned*)h->d_nb_pack;

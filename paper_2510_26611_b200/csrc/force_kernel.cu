@@ -478,6 +478,9 @@ __global__ void __launch_bounds__(kWinThreads, 1) force_window_kernel(const Scor
               inwin = inwin && min(i[r], sh[r]) >= org[r] && max(i[r], sh[r]) < org[r] + len[r];
             }
             Phi4 f;
+            RS_DCHECK(i[0] >= 0 && i[0] < a.n && i[1] >= 0 && i[1] < a.n && i[2] >= 0 && i[2] < a.n &&
+                      sh[0] >= 0 && sh[0] < a.n && sh[1] >= 0 && sh[1] < a.n && sh[2] >= 0 && sh[2] < a.n);
+            RS_DCHECK(!inwin || (len[0] <= cap && len[1] <= cap && len[2] <= cap));
             if (inwin) {
               f = phi4_win<R>(W[0], W[1], W[2], org, i, sh, lane);
             } else {      // rows outside the window: depth-first tree on 16-byte L2 loads
@@ -532,6 +535,7 @@ __global__ void __launch_bounds__(kWinThreads, 1) force_window_kernel(const Scor
 #pragma unroll
       for (int j = 1; j < 9; ++j)
         if (lane == j) mine = res[j];
+      RS_DCHECK(p >= 0 && p < a.P);
       if (lane < 9) out[9 * p + lane] = mine;
       if (!ok && lane == 0 && a.invalid) atomicAdd(a.invalid, 1ull);
     }

@@ -11,6 +11,18 @@
 
 #include <cuda_runtime.h>
 
+// Bounds-checked build (-DRS_DEVICE_CHECKS; tools/build_variants.py checked=-DRS_DEVICE_CHECKS):
+// every shared-memory window row, local-table cell, queue slot, list entry, record, memo
+// value, TMA box and output index is asserted in range (device assert: the failing
+// expression, block and thread are printed and the launch fails).  The substitute for
+// compute-sanitizer, which this pool does not run.
+#ifdef RS_DEVICE_CHECKS
+#include <cassert>
+#define RS_DCHECK(x) assert(x)
+#else
+#define RS_DCHECK(x) ((void)0)
+#endif
+
 namespace rs {
 namespace dev {
 

@@ -148,6 +148,7 @@ struct ScoreArgs {               // one launch of the scoring kernel
   unsigned long long* invalid;   // may be null
   int* work;                     // this launch's zeroed work counter (dynamic pose chunks)
   double rmax_hint;              // ligand radius if known on the host (< 0: unknown)
+  int64_t n_ent = 0, n_prot = 0;  // list entries and protein records (bounds for checked builds)
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
   int f32;                       // long-range part from the binary32 factors (A21)
@@ -221,6 +222,7 @@ struct rs_handle {
   int device = 0;
   void* dmem[6] = {nullptr};           // F1..3, S1..3
   void* d_nb_ent = nullptr;
+  int64_t n_ent = 0;                   // list entries uploaded (incl. padding)
   void* d_prec = nullptr;
   void* d_memo = nullptr;
   void* d_Fw[3] = {nullptr, nullptr, nullptr};

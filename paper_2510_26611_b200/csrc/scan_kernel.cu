@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "rs_internal.h"
+#include "rs_device.cuh"
 
 namespace rs {
 namespace {
@@ -52,6 +53,7 @@ __global__ void scan_update_kernel(const double* centre, const double* dirs, con
        p += (int64_t)gridDim.x * blockDim.x) {
     if (status[p] != -1) continue;
     const int sl = slot[p];
+    RS_DCHECK(sl >= 0 && sl < P);
     const double d = Dc[sl];
     E[p] = Ec[sl];
     double sn;
@@ -82,6 +84,7 @@ __global__ void scan_update_kernel(const double* centre, const double* dirs, con
     s[p] = sn;
     const int j = (int)(p / m_L), k = (int)(p % m_L);
     const int ns = atomicAdd(count, 1);
+    RS_DCHECK(ns >= 0 && ns < P);
     slot[p] = ns;
     write_pose(poses_next + 7 * (int64_t)ns, centre, dirs + 3 * j, quats + 4 * k, sn);
   }

@@ -374,6 +374,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1, int e2, bool pr) {
   const unsigned d = (unsigned)a.n_sigma + 1u;
   const unsigned idx = ((unsigned)abs(e0) * d + (unsigned)abs(e1)) * d + (unsigned)abs(e2);
+  RS_DCHECK(!pr || (abs(e0) <= a.n_sigma && abs(e1) <= a.n_sigma && abs(e2) <= a.n_sigma && idx < d * d * d));
   return ldg_d_p(reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(a.t.short_memo) +
                                                  (uint64_t)idx * 8u), pr);
 }
@@ -428,6 +429,8 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   dd1 = a1 ? dd1 : 0xffffffffu;
   const bool sr0 = dd0 <= a.ns2, sr1 = dd1 <= a.ns2;
   const bool v0 = dd0 < a.vdw_cells2, v1 = dd1 < a.vdw_cells2;
+  RS_DCHECK(!(sr0 || v0) || (en0.z >= 0 && en0.z < a.n_prot));
+  RS_DCHECK(!(sr1 || v1) || (en1.z >= 0 && en1.z < a.n_prot));
   const double4 rc0 = ldg_d4_p(a.t.prec + en0.z, sr0 || v0);
   const double4 rc1 = ldg_d4_p(a.t.prec + en1.z, sr1 || v1);
   const double sv0 = short_value(a, e00, e01, e02, sr0);
@@ -759,6 +762,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 #pragma unroll
               for (int r = 0; r < 3; ++r) {
                 const int lo_r = s_cur.lo[r], len = s_cur.hi[r] - lo_r + 1;
+                RS_DCHECK(lo_r >= 0 && len > 0 && lo_r + len <= a.n && s_cur.off[r] + lo_r >= 0 &&
+                          s_cur.off[r] + lo_r + len <= cap_rows);
                 const void* src = F32 ? (const void*)(a.t.Fw32[r] + (size_t)lo_r * kChp)
                                       : (const void*)(a.t.Fw[r] + (size_t)lo_r * kChp);
                 tma_load_1d(win_u32 + (unsigned)(s_cur.off[r] + lo_r) * kRow, src, (unsigned)len * kRow, &s_bar);
@@ -767,6 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             if (reloc) {
               const int c0 = s_lb.lo[2] - a.nb_lo[2] + kPackPad, c1 = s_lb.lo[1] - a.nb_lo[1] + kPackPad,
                         c2 = s_lb.lo[0] - a.nb_lo[0] + kPackPad;
+              RS_DCHECK(c0 >= 0 && c1 >= 0 && c2 >= 0 && (c0 & 3) == 0);
               asm volatile(
                   "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
                   " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(loc_u32),
@@ -867,6 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               qc01 = cb.x; qc2 = cb.y; qpos = cb.z; qend = cb.w;
             }
             const bool more = qpos < qend;
+            RS_DCHECK(!more || (qpos >= 0 && qpos + 2 <= a.n_ent));
             if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + qpos, more, pf0, pf1);
           }
         };
@@ -884,6 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           const int lc = l < L ? l : L - 1;
           double y0, y1, y2, z;
           if (lig_all_smem) {
+            RS_DCHECK(lc >= 0 && lc < lig_smem_n);
             const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
             y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
           } else {
@@ -914,6 +922,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             if (use_loc) {
               // every atom of a fitting tile (and every lane's stand-in atom) has its coarse cell
               // inside the tile's box (the row bounds t +- rb contain the atom's cell)
+              RS_DCHECK(cx >= s_lb.lo[0] && cx < s_lb.lo[0] + s_lb.dim[0] && cy >= s_lb.lo[1] &&
+                        cy < s_lb.lo[1] + s_lb.dim[1] && cz >= s_lb.lo[2] && cz < s_lb.lo[2] + s_lb.dim[2]);
               const unsigned v = lds_u32(loc_org + (unsigned)((cx * ld1 + cy) * ld2 + cz) * 4u);
               bc = make_int2((int)(v & 0xffffffu), (int)(v >> 24));
             } else {
@@ -929,12 +939,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 #endif
           // enqueue this atom's candidates: walk them next if the lane is idle, else stack them
           // (the pass loop guarantees room); the first entry pair loads behind this step's H4
+          RS_DCHECK(cnt <= 0 || (beg >= 0 && beg + cnt <= a.n_ent));
           if (cnt > 0) {
             if (qpos >= qend) {
               q0 = x0; q1 = x1; q2 = x2; qz = z;
               qc01 = i0 | (i1 << 16); qc2 = i2; qpos = beg; qend = beg + cnt;
               ldg_pair_p(a.t.nb_ent + beg, true, pf0, pf1);
             } else {
+              RS_DCHECK(qfc < kNQ);
               nq.x01[qfc][lane] = make_double2(x0, x1);
               nq.x2z[qfc][lane] = make_double2(x2, z);
               nq.cb[qfc][lane] = make_int4(i0 | (i1 << 16), i2, beg, beg + cnt);
@@ -947,6 +959,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             if (use_win) {
               // every row of a fitting tile is staged (the tile's bounds contain t +- rb, and
               // lanes without a real atom stand in with an atom of a pose of the tile)
+              RS_DCHECK(i0 >= s_cur.lo[0] && i0 <= s_cur.hi[0] && i1 >= s_cur.lo[1] && i1 <= s_cur.hi[1] &&
+                        i2 >= s_cur.lo[2] && i2 <= s_cur.hi[2]);
               const unsigned r0 = wb0 + (unsigned)i0 * kRow;
               const unsigned r1 = wb1 + (unsigned)i1 * kRow;
               const unsigned r2 = wb2 + (unsigned)i2 * kRow;
@@ -959,6 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 #endif
               phi = go ? v : 0.0;
             } else if (go) {
+              RS_DCHECK(i0 >= 0 && i0 < a.n && i1 >= 0 && i1 < a.n && i2 >= 0 && i2 < a.n);
               if constexpr (WIN) {       // a single pose whose rows do not fit: out of line
                 if constexpr (F32) phi = long_phi_global32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
                 else phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2);
@@ -991,6 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         }
         // H8: E = hi + lo; d = sqrt(min d^2) below D_cap^2, else +inf; NaN if invalid (O8)
         if (has && sub == 0) {
+          RS_DCHECK(pp >= 0 && pp < a.P);
           a.E[pp] = bad ? NAN : __dadd_rn(hi, lo);
           a.D[pp] = bad ? NAN : (best < a.dcap2 ? __dsqrt_rn(best) : INFINITY);
           if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
