@@ -63,8 +63,11 @@ extern "C" {
                                   instead of scheme (C) from the kept Tucker form            */
 
 #define RS_FLAG_DEVICE_FFT 8u  /* setup: the RHOSVD and core convolutions (S5-S6) with cuFFT on
-                                  the device (tables then differ from a host-only build by
-                                  rounding; without it a device build is bitwise host-equal) */
+                                  the device -- the default of every device build (kept as an
+                                  explicit request); its tables differ from a host-only build's
+                                  by rounding                                                */
+#define RS_FLAG_HOST_FFT 16u   /* setup: the S5-S6 convolutions on the host even with a device
+                                  (tables bitwise equal to a RS_FLAG_HOST_ONLY build's)       */
 
 typedef struct rs_handle rs_handle; /* opaque, immutable after build */
 

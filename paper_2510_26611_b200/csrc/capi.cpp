@@ -461,7 +461,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     rs::compress_long_range(n, h, hd->cells, hd->z, tl, al, prm.rank_R, prm.eps_compress,
                             prm.tucker_rank_max, prm.als_sweeps, prm.seed, hd->F, &hd->R, &hd->rep,
                             &hd->tucker, nullptr, nullptr, host_only ? -1 : prm.device,
-                            (prm.flags & RS_FLAG_DEVICE_FFT) != 0);
+                            (prm.flags & RS_FLAG_HOST_FFT) == 0);
     hd->f32 = (prm.flags & RS_FLAG_F32_FACTORS) != 0;
     if (hd->f32 && rs::window_row_chunks32(hd->R) == 0) {
       set_err("RS_FLAG_F32_FACTORS needs a compiled CP width R in {4, 8, 12, 16, 24, 32}, got " +
@@ -492,7 +492,8 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
     const double work = double(n_atoms) * double(tl.size());
     const int nsamp = (int)std::max(100.0, std::min(2000.0, 4e9 / std::max(work, 1.0)));
     rs::sample_compression_error(n, b, h, hd->xyz, hd->cells, hd->z, tl, al, hd->F, hd->R,
-                                 std::max(prm.sigma_vdw, h), hd->cg, nsamp, prm.seed, &hd->rep);
+                                 std::max(prm.sigma_vdw, h), hd->cg, nsamp, prm.seed, &hd->rep,
+                                 host_only ? -1 : prm.device);
     lap("error samples");
   } catch (const std::bad_alloc&) {
     set_err("out of host memory during setup");
@@ -684,7 +685,7 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
       rs::compress_long_range(h->n, h->h, h->cells, h->z, tl, al, rank, h->prm.eps_compress,
                               h->prm.tucker_rank_max, h->prm.als_sweeps, h->prm.seed, hd->F,
                               &hd->R, &hd->rep, nullptr, lo_, hi_, host_only ? -1 : hd->device,
-                              (flags & RS_FLAG_DEVICE_FFT) != 0);
+                              (flags & RS_FLAG_HOST_FFT) == 0);
     } else {
       hd->rep.tucker_err = h->rep.tucker_err;
       hd->R = rs::restrict_to_box(h->n, h->tucker, lo_, hi_, rank, h->prm.eps_compress,

@@ -117,7 +117,12 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
                               const std::vector<double>& t_long, const std::vector<double>& a_long,
                               const std::vector<double> F[3], int R, double r_excl,
                               const CoarseGrid& cg, int n_samples, uint64_t seed,
-                              SetupReport* rep);
+                              SetupReport* rep, int device = -1);
+// the uncompressed long-range values at sample cells on the device (false: no device / error)
+bool exact_long_values_device(int device, int n, const std::vector<double>& G,
+                              const std::vector<double>& a_long, const std::vector<int32_t>& cells,
+                              const std::vector<double>& z, const std::vector<int>& pts,
+                              std::vector<double>& out);
 
 // ---- device side -------------------------------------------------------------------------
 

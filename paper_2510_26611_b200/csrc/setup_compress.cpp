@@ -92,8 +92,76 @@ struct ConvOps {
   }
 };
 
-// Thin orthonormal basis of the columns of Y (n x p) in place.
+// RS_SETUP_TIMING: per-phase wall times of the range finder (stderr)
+struct PhaseClock {
+  bool on = std::getenv("RS_SETUP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(int mode, const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rs setup]     mode %d %-14s %7.3f s\n", mode, what,
+                 std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+
+// Thin orthonormal basis of the columns of Y (n x p) in place: CholeskyQR2 (the Gram matrix
+// Y^T Y, its Cholesky factor R, Y <- Y R^-1, twice; the second pass restores orthogonality to
+// rounding), OpenMP over rows; a Householder QR when a Cholesky pivot vanishes (rank-deficient
+// Y, e.g. rows clipped to a box).  The result spans the same space (one basis of it).
+namespace {
+bool cholesky_qr_pass(std::vector<double>& Y, int n, int p) {
+  // Gram matrix over 64 fixed row blocks summed in block order: bitwise independent of the
+  // thread count (the setup is deterministic)
+  constexpr int kBlocks = 64;
+  std::vector<std::vector<double>> part(kBlocks);
+#pragma omp parallel for schedule(dynamic)
+  for (int blk = 0; blk < kBlocks; ++blk) {
+    std::vector<double> g((size_t)p * p, 0.0);
+    const int i0 = (int)((int64_t)n * blk / kBlocks), i1 = (int)((int64_t)n * (blk + 1) / kBlocks);
+    for (int i = i0; i < i1; ++i)
+      for (int a = 0; a < p; ++a) {
+        const double ya = Y[(size_t)a * n + i];
+        if (ya == 0.0) continue;
+        for (int b = a; b < p; ++b) g[(size_t)a * p + b] += ya * Y[(size_t)b * n + i];
+      }
+    part[blk].swap(g);
+  }
+  std::vector<double> G((size_t)p * p, 0.0);
+  for (int blk = 0; blk < kBlocks; ++blk)
+    for (size_t t = 0; t < G.size(); ++t) G[t] += part[blk][t];
+  // G = R^T R, R upper triangular (row-major R[a][b], a <= b)
+  std::vector<double> R((size_t)p * p, 0.0);
+  double dmax = 0.0;
+  for (int a = 0; a < p; ++a) dmax = std::max(dmax, G[(size_t)a * p + a]);
+  for (int a = 0; a < p; ++a) {
+    double d = G[(size_t)a * p + a];
+    for (int k = 0; k < a; ++k) d -= R[(size_t)k * p + a] * R[(size_t)k * p + a];
+    if (!(d > 1e-24 * dmax)) return false;
+    const double r = std::sqrt(d);
+    R[(size_t)a * p + a] = r;
+    for (int b = a + 1; b < p; ++b) {
+      double v = G[(size_t)a * p + b];
+      for (int k = 0; k < a; ++k) v -= R[(size_t)k * p + a] * R[(size_t)k * p + b];
+      R[(size_t)a * p + b] = v / r;
+    }
+  }
+  // each row y of Y: x R = y (forward substitution over the columns)
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i)
+    for (int b = 0; b < p; ++b) {
+      double v = Y[(size_t)b * n + i];
+      for (int a = 0; a < b; ++a) v -= Y[(size_t)a * n + i] * R[(size_t)a * p + b];
+      Y[(size_t)b * n + i] = v / R[(size_t)b * p + b];
+    }
+  return true;
+}
+}  // namespace
+
 void orthonormalise(std::vector<double>& Y, int n, int p) {
+  std::vector<double> keep = Y;
+  if (n >= p && cholesky_qr_pass(Y, n, p) && cholesky_qr_pass(Y, n, p)) return;
+  Y.swap(keep);
   std::vector<double> tau;
   std::vector<double> A = Y;
   la::householder_qr(A.data(), n, p, tau);
@@ -151,6 +219,8 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
                                : (tucker_cap > 0 ? tucker_cap : n);
   int p = (rank_R > 0) ? std::min(pmax, std::max(2 * r_cap + 16, 48)) : std::min(pmax, 64);
   ModeBasis out;
+  PhaseClock pc;
+  pc.lap(mode, "weights");
   for (;;) {
     // range finder: Y = sum_k T_k (sqrt(c_k) .* Xi_k).  Per-k results are summed in k order
     // so the setup is bitwise independent of the thread count.
@@ -174,9 +244,11 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       for (size_t i = 0; i < Y.size(); ++i) Y[i] += Yk[k][i];
       std::vector<double>().swap(Yk[k]);
     }
+    pc.lap(mode, "sketch");
     clip_rows(Y, p);
     orthonormalise(Y, n, p);
     clip_rows(Y, p);
+    pc.lap(mode, "qr1");
     // one power iteration: Y = sum_k T_k (c_k .* (T_k Q))
     {
       std::vector<double> Y2((size_t)n * p, 0.0);
@@ -197,13 +269,13 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
         std::vector<double>().swap(Yk[k]);
       }
       Y.swap(Y2);
+      pc.lap(mode, "power");
       clip_rows(Y, p);
       orthonormalise(Y, n, p);
       clip_rows(Y, p);
+      pc.lap(mode, "qr2");
     }
-    // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :]; streaming QR.
-    std::vector<double> Rt((size_t)p * p, 0.0);
-    bool have_R = false;
+    // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :]
     const int nocc = (int)occj.size();
     std::vector<std::vector<double>> Zk(RL);   // (T_k Q) at the occupied rows, nocc x p
 #pragma omp parallel
@@ -217,40 +289,42 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
           for (int s = 0; s < p; ++s) Zk[k][(size_t)jj * p + s] = Z[(size_t)s * n + occj[jj]];
       }
     }
-    const int blk_rows = std::max(4 * p, 2048);
-    std::vector<double> B;
-    int rows = 0;
-    auto flush = [&]() {
-      if (rows == 0) return;
-      const int m = std::max(rows + (have_R ? p : 0), p);   // zero rows pad a short block
-      std::vector<double> A((size_t)m * p, 0.0);
-      for (int s = 0; s < p; ++s) {
-        int off = 0;
-        if (have_R)
-          for (int i = 0; i < p; ++i) A[(size_t)s * m + i] = Rt[(size_t)s * p + i];
-        off = have_R ? p : 0;
-        for (int i = 0; i < rows; ++i) A[(size_t)s * m + off + i] = B[(size_t)i * p + s];
-      }
-      std::vector<double> tau;
-      la::householder_qr(A.data(), m, p, tau);
-      std::fill(Rt.begin(), Rt.end(), 0.0);
-      for (int s = 0; s < p; ++s)
-        for (int i = 0; i <= std::min(s, m - 1); ++i) Rt[(size_t)s * p + i] = A[(size_t)s * m + i];
-      have_R = true;
-      rows = 0;
-      B.clear();
-    };
+    pc.lap(mode, "WtQ apply");
+    // the singular values and right vectors of the stacked W^T Q from its p x p Gram matrix
+    // sum_k sum_j c_k[j] Z_k[j,:]^T Z_k[j,:] (per k in parallel, summed in k order: bitwise
+    // independent of the thread count), by the Jacobi eigensolver; sigma = sqrt(lambda)
+    // descending.  (Squaring costs accuracy only below ~1e-8 sigma_0, far under the ranks kept.)
+    std::vector<std::vector<double>> Gk(RL);
+#pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < RL; ++k) {
+      std::vector<double> g((size_t)p * p, 0.0);
       for (int jj = 0; jj < nocc; ++jj) {
-        const int j = occj[jj];
-        const double w = std::sqrt(c[k][j]);
-        for (int s = 0; s < p; ++s) B.push_back(w * Zk[k][(size_t)jj * p + s]);
-        if (++rows >= blk_rows) flush();
+        const double cw = c[k][occj[jj]];
+        if (cw == 0.0) continue;
+        const double* zr = Zk[k].data() + (size_t)jj * p;
+        for (int s_ = 0; s_ < p; ++s_) {
+          const double v = cw * zr[s_];
+          for (int t = s_; t < p; ++t) g[(size_t)s_ * p + t] += v * zr[t];
+        }
       }
+      Gk[k].swap(g);
+      std::vector<double>().swap(Zk[k]);
     }
-    flush();
+    std::vector<double> Gm((size_t)p * p, 0.0);
+    for (int k = 0; k < RL; ++k)
+      for (size_t t = 0; t < Gm.size(); ++t) Gm[t] += Gk[k][t];
+    for (int s_ = 0; s_ < p; ++s_)
+      for (int t = s_ + 1; t < p; ++t) Gm[(size_t)t * p + s_] = Gm[(size_t)s_ * p + t];
+    pc.lap(mode, "WtQ gram");
+    std::vector<double> lam(p), Ve((size_t)p * p);
+    la::sym_eig(Gm.data(), p, lam.data(), Ve.data());   // ascending
     std::vector<double> sv(p), V((size_t)p * p);
-    la::jacobi_svd(Rt.data(), p, p, sv.data(), V.data(), nullptr);
+    for (int i = 0; i < p; ++i) {
+      const int src = p - 1 - i;
+      sv[i] = std::sqrt(std::max(lam[src], 0.0));
+      for (int s_ = 0; s_ < p; ++s_) V[(size_t)i * p + s_] = Ve[(size_t)src * p + s_];
+    }
+    pc.lap(mode, "svd");
     double tot = 0;
     for (double v : sv) tot += v * v;
     // rank for the tolerance
@@ -782,7 +856,7 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
                               const std::vector<double>& t_long, const std::vector<double>& a_long,
                               const std::vector<double> F[3], int R, double r_excl,
                               const CoarseGrid& cg, int n_samples, uint64_t seed,
-                              SetupReport* rep) {
+                              SetupReport* rep, int device) {
   const int64_t M = (int64_t)z.size();
   const int RL = (int)t_long.size();
   if (M == 0 || n_samples <= 0) return;
@@ -837,11 +911,13 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
   }
   const int ns = (int)pts.size() / 3;
   std::vector<double> ex(ns), cp(ns);
+  // the uncompressed values: on the device when the build has one (the O(ns M R_l) sum)
+  const bool on_dev = device >= 0 && exact_long_values_device(device, n, G, a_long, cells, z, pts, ex);
 #pragma omp parallel for schedule(dynamic)
   for (int s = 0; s < ns; ++s) {
     const int* c = &pts[3 * s];
     double v = 0;
-    for (int64_t m = 0; m < M; ++m) {
+    for (int64_t m = 0; m < M && !on_dev; ++m) {
       const int d0 = std::abs(c[0] - cells[3 * m]), d1 = std::abs(c[1] - cells[3 * m + 1]),
                 d2 = std::abs(c[2] - cells[3 * m + 2]);
       double acc = 0;
@@ -849,7 +925,7 @@ void sample_compression_error(int n, double b, double h, const std::vector<doubl
         acc += a_long[k] * G[(size_t)k * n + d0] * G[(size_t)k * n + d1] * G[(size_t)k * n + d2];
       v += z[m] * acc;
     }
-    ex[s] = v;
+    if (!on_dev) ex[s] = v;
     double w = 0;
     for (int q = 0; q < R; ++q)
       w += F[0][(size_t)c[0] * R + q] * F[1][(size_t)c[1] * R + q] * F[2][(size_t)c[2] * R + q];

@@ -244,3 +244,80 @@ bool DeviceConv::apply(int k, const double* X, double* Y, int cols) {
 }
 
 }  // namespace rs
+
+// ---- sampled compression error (setup report) on the device ----------------------------
+// The uncompressed long-range value at each sample cell c: sum_m z_m sum_k a_k g_k[|c0 - i_m0|]
+// g_k[|c1 - i_m1|] g_k[|c2 - i_m2|] (Eq. (6)); one block per sample, threads over the protein
+// atoms, a fixed shared-memory tree per block (deterministic).  Only the reported error uses it.
+namespace rs {
+namespace {
+
+__global__ void exact_long_kernel(int n, int RL, int64_t M, const double* __restrict__ G,
+                                  const double* __restrict__ a, const int* __restrict__ cells,
+                                  const double* __restrict__ z, const int* __restrict__ pts,
+                                  double* __restrict__ out) {
+  __shared__ double red[256];
+  const int s = blockIdx.x;
+  const int c0 = pts[3 * s], c1 = pts[3 * s + 1], c2 = pts[3 * s + 2];
+  double v = 0.0;
+  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+    const int d0 = abs(c0 - cells[3 * m]), d1 = abs(c1 - cells[3 * m + 1]), d2 = abs(c2 - cells[3 * m + 2]);
+    double acc = 0.0;
+    for (int k = 0; k < RL; ++k) {
+      const double* g = G + (size_t)k * n;
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(a[k], __ldg(g + d0)), __ldg(g + d1)), __ldg(g + d2)));
+    }
+    v = __dadd_rn(v, __dmul_rn(z[m], acc));
+  }
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[s] = red[0];
+}
+
+}  // namespace
+
+bool exact_long_values_device(int device, int n, const std::vector<double>& G,
+                              const std::vector<double>& a_long, const std::vector<int32_t>& cells,
+                              const std::vector<double>& z, const std::vector<int>& pts,
+                              std::vector<double>& out) {
+  const int RL = (int)a_long.size();
+  const int64_t M = (int64_t)z.size();
+  const int ns = (int)pts.size() / 3;
+  out.assign(ns, 0.0);
+  if (ns == 0) return true;
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  double *dG = nullptr, *da = nullptr, *dz = nullptr, *dout = nullptr;
+  int *dc = nullptr, *dp = nullptr;
+  bool ok = cudaMalloc(&dG, G.size() * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&da, RL * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&dz, M * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&dout, ns * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&dc, cells.size() * sizeof(int)) == cudaSuccess &&
+            cudaMalloc(&dp, pts.size() * sizeof(int)) == cudaSuccess;
+  ok = ok && cudaMemcpy(dG, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(da, a_long.data(), RL * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(dz, z.data(), M * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(dc, cells.data(), cells.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(dp, pts.data(), pts.size() * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok) {
+    exact_long_kernel<<<ns, 256>>>(n, RL, M, dG, da, dc, dz, dp, dout);
+    ok = cudaGetLastError() == cudaSuccess &&
+         cudaMemcpy(out.data(), dout, ns * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  for (void* q : {(void*)dG, (void*)da, (void*)dz, (void*)dout, (void*)dc, (void*)dp})
+    if (q) cudaFree(q);
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  return ok;
+}
+
+}  // namespace rs
+

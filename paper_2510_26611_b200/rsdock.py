@@ -23,6 +23,7 @@ RS_FLAG_HOST_ONLY = 1
 RS_FLAG_F32_FACTORS = 2
 RS_FLAG_BOX_SCHEME_B = 4
 RS_FLAG_DEVICE_FFT = 8
+RS_FLAG_HOST_FFT = 16
 RS_PATH_WINDOW, RS_PATH_L2, RS_PATH_L2_RUNTIME = 1, 2, 3
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_restrict_box", "rs_score_poses", "rs_score_poses_async",

@@ -931,12 +931,12 @@ def test_f32_no_window_l2_path(env, R):
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_device_core_setup_bitwise(env, name):
-    """S6 on the device (setup_device.cu, N4 part): a handle built with a device forms the Tucker
-    core there with the host loop's exact op sequence, so its exported tables are bitwise the
-    host-only build's."""
+    """S6 on the device (setup_device.cu, N4 part): a handle built with a device and the host
+    convolutions (RS_FLAG_HOST_FFT) forms the Tucker core there with the host loop's exact op
+    sequence, so its exported tables are bitwise the host-only build's."""
     torch, rsdock, rs_oracle = env
     w = syn.make(name)
-    dev = build(rsdock, w)
+    dev = build(rsdock, w, flags=rsdock.RS_FLAG_HOST_FFT)
     host = build(rsdock, w, flags=rsdock.RS_FLAG_HOST_ONLY)
     td, th = dev.export_tables(), host.export_tables()
     for k in ("F1", "F2", "F3", "S1", "S2", "S3"):
@@ -946,14 +946,14 @@ def test_device_core_setup_bitwise(env, name):
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_device_fft_setup(env, name):
-    """RS_FLAG_DEVICE_FFT (N4 part): the RHOSVD and core convolutions with cuFFT.  The CP it builds
+    """The default device build (N4 part): the RHOSVD and core convolutions with cuFFT.  The CP it builds
     agrees with the host-only build's at sampled cells to 1e-6 of their max (the FFT rounding
     moves the randomized bases, not the accuracy: the same sampled error to 1e-3 relative), and
     the kernel on its tables matches the oracle as always."""
     torch, rsdock, rs_oracle = env
     w = syn.make(name)
     host = build(rsdock, w, flags=rsdock.RS_FLAG_HOST_ONLY)
-    dev = build(rsdock, w, flags=rsdock.RS_FLAG_DEVICE_FFT)
+    dev = build(rsdock, w)
     th, td = host.export_tables(), dev.export_tables()
     rng = np.random.default_rng(3)
     idx = rng.integers(0, w.grid_n, size=(2000, 3))
