@@ -154,6 +154,44 @@ double oracle_long_value_f32(const double *F1, const double *F2, const double *F
     return (double)s[0];
 }
 
+/* ---- O4-T: the long-range value from the Tucker form (NEXT row N5, "Tucker-format
+ * evaluation"; the Tucker rank bound PAPER.md:472-484; reading A26).  With the rows
+ * u_l = U_l[i_l, :] (U_l: n x r_l, row-major) of the RHOSVD bases and the core G (r0 x r1 x r2,
+ * row-major, charges and quadrature weights folded in):
+ *   v_ab = sum_c G[a][b][c] * u2[c]          (ascending c, each product rounded, then added)
+ *   t_a  = sum_b u1[b] * v_ab                (ascending b)
+ *   phi  = sum_a u0[a] * t_a                 (ascending a)
+ * each chain starting from +0, no fused multiply-add. */
+double oracle_tucker_value(const double *U0, const double *U1, const double *U2, int r0, int r1,
+                           int r2, const double *G, int i0, int i1, int i2)
+{
+    const double *u0 = U0 + (int64_t)i0 * r0, *u1 = U1 + (int64_t)i1 * r1, *u2 = U2 + (int64_t)i2 * r2;
+    double phi = 0.0;
+    for (int a = 0; a < r0; ++a) {
+        double t = 0.0;
+        for (int b = 0; b < r1; ++b) {
+            const double *g = G + ((int64_t)a * r1 + b) * r2;
+            double v = 0.0;
+            for (int c = 0; c < r2; ++c) v = v + g[c] * u2[c];
+            t = t + u1[b] * v;
+        }
+        phi = phi + u0[a] * t;
+    }
+    return phi;
+}
+
+/* Tucker tables for mode bit 2 of oracle_score_poses (set before the call; test
+ * infrastructure, one scoring call at a time) */
+static const double *g_tU[3], *g_tG;
+static int g_tr[3];
+void oracle_set_tucker(const double *U0, const double *U1, const double *U2, int r0, int r1, int r2,
+                       const double *G)
+{
+    g_tU[0] = U0; g_tU[1] = U1; g_tU[2] = U2;
+    g_tr[0] = r0; g_tr[1] = r1; g_tr[2] = r2;
+    g_tG = G;
+}
+
 /* ---- O5: short-range reference value S(Delta) for |Delta|_2 <= n_sigma (Def. 2.1) ---- */
 double oracle_short_value(const double *S1, const double *S2, const double *S3, int Rs,
                           int n_sigma, int d0, int d1, int d2)
@@ -174,7 +212,8 @@ double oracle_short_value(const double *S1, const double *S2, const double *S3, 
  *   Y (L x 3), zL (L)      : ligand body coordinates (centred) and charges
  *   poses (P x 7)          : w,x,y,z,tx,ty,tz
  *   mode                   : bit 0 = long_only: skip O5 and O7 (Lemma 3.2's cost alone; the CPU
- *                            like-for-like rate); bit 1 = fp32 factors (O4-f32 instead of O4)
+ *                            like-for-like rate); bit 1 = fp32 factors (O4-f32 instead of O4);
+ *                            bit 2 = Tucker form (O4-T instead of O4; oracle_set_tucker first)
  * Outputs E (P), dmin (P).  Returns the number of invalid poses (O8: NaN outputs).
  * asum (P, may be NULL): sum over the pose's addends of |addend| (the M8 report's condition
  * number kappa = asum / |E|); NaN for invalid poses.  Report only: E never
@@ -188,7 +227,7 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
                            int64_t P, const double *poses, double dcap, int mode,
                            double *E, double *dmin, double *asum)
 {
-    int long_only = mode & 1, f32 = (mode >> 1) & 1;
+    int long_only = mode & 1, f32 = (mode >> 1) & 1, tucker = (mode >> 2) & 1;
     double inv_h = (double)n / (2.0 * b);
     int *iM = (int *)malloc(sizeof(int) * 3 * (size_t)(M > 0 ? M : 1));
     for (int64_t m = 0; m < M; ++m)
@@ -214,8 +253,10 @@ int64_t oracle_score_poses(int n, double b, int R, const double *F1, const doubl
             }
             if (!ok) break;
             /* O4 */
-            double phi = f32 ? oracle_long_value_f32(F1, F2, F3, R, il[0], il[1], il[2])
-                             : oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
+            double phi = tucker ? oracle_tucker_value(g_tU[0], g_tU[1], g_tU[2], g_tr[0], g_tr[1],
+                                                      g_tr[2], g_tG, il[0], il[1], il[2])
+                         : f32 ? oracle_long_value_f32(F1, F2, F3, R, il[0], il[1], il[2])
+                               : oracle_long_value(F1, F2, F3, R, il[0], il[1], il[2]);
             dd_add_product(&acc, zL[l], phi);
             abs_sum += fabs(zL[l] * phi);
             if (long_only) continue;

@@ -62,6 +62,10 @@ def lib():
             dp, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp, dp, ctypes.c_int64, dp,
             ctypes.c_double, ctypes.c_int, dp, dp, dp]
         L.oracle_score_poses.restype = ctypes.c_int64
+        L.oracle_tucker_value.argtypes = [dp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.oracle_tucker_value.restype = ctypes.c_double
+        L.oracle_set_tucker.argtypes = [dp, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_score_forces.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, dp,
                                           ctypes.c_int64, dp, dp, ctypes.c_int64, dp, dp]
@@ -319,8 +323,18 @@ def K_h(delta, h, order=12):
 # O1-O8 scorer (C) wrapper
 # ------------------------------------------------------------------------------------------
 
+def tucker_value(tk: dict, i0, i1, i2) -> float:
+    """O4-T at one cell: the long-range value from the Tucker form tk = (U0, U1, U2: n x r_l
+    row-major, G: r0 x r1 x r2), the contraction order of oracle_tucker_value (reading A26)."""
+    U = [_c(tk[k]) for k in ("U0", "U1", "U2")]
+    G = _c(tk["G"])
+    r = [u.shape[1] for u in U]
+    return lib().oracle_tucker_value(_p(U[0]), _p(U[1]), _p(U[2]), r[0], r[1], r[2], _p(G),
+                                     int(i0), int(i1), int(i2))
+
+
 def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=False,
-                abs_sum=False):
+                abs_sum=False, tucker=None):
     """Per-pose (E, dmin, n_invalid) from exported tables (f32: the O4-f32 long-range part).
     abs_sum: also return sum_addends |addend| per pose (E, dmin, n_invalid, asum), the M8
     report's kappa = asum / |E|.
@@ -338,11 +352,18 @@ def score_poses(tables: dict, X, qM, Y, zL, poses, dcap, long_only=False, f32=Fa
     d = np.empty(P)
     dummy = np.zeros(1)
     asum = np.empty(P) if abs_sum else None
+    mode = (1 if long_only else 0) | (2 if f32 else 0)
+    if tucker is not None:
+        # O4-T (N5): the long range from the Tucker form instead of the CP factors
+        U = [_c(tucker[k]) for k in ("U0", "U1", "U2")]
+        G = _c(tucker["G"])
+        lib().oracle_set_tucker(_p(U[0]), _p(U[1]), _p(U[2]), U[0].shape[1], U[1].shape[1],
+                                U[2].shape[1], _p(G))
+        mode |= 4
     inv = lib().oracle_score_poses(
         n, b, R, _p(F1), _p(F2), _p(F3), ns, Rs, _p(S1 if S1.size else dummy),
         _p(S2 if S2.size else dummy), _p(S3 if S3.size else dummy), X.shape[0], _p(X), _p(qM),
-        Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap),
-        (1 if long_only else 0) | (2 if f32 else 0), _p(E), _p(d),
+        Y.shape[0], _p(Y), _p(zL), P, _p(poses), float(dcap), mode, _p(E), _p(d),
         _p(asum) if abs_sum else None)
     if abs_sum:
         return E, d, int(inv), asum

@@ -855,3 +855,63 @@ def test_cp_als_recovers_exact_low_rank(oracle):
     tails = oracle.unfolding_tails(F, 2)
     e2 = oracle.cp_als_dense(T, 2, iters=100, seed=1)[3]
     assert e2 >= math.sqrt(max(tails) / float(np.sum(T * T))) - 1e-12
+
+
+# ----------------------------------------------------------------------------- O4-T (N5)
+
+def _tucker(rng, n, r):
+    return {"U0": rng.standard_normal((n, r[0])), "U1": rng.standard_normal((n, r[1])),
+            "U2": rng.standard_normal((n, r[2])), "G": rng.standard_normal(tuple(r))}
+
+
+def test_tucker_value_rank_one_closed_form(oracle):
+    """O4-T with r = (1, 1, 1) is u0 (u1 (g u2)): exact in binary64 for small integers."""
+    tk = {"U0": np.array([[3.0], [5.0]]), "U1": np.array([[-2.0], [7.0]]),
+          "U2": np.array([[4.0], [11.0]]), "G": np.array([[[-6.0]]])}
+    for i0 in range(2):
+        for i1 in range(2):
+            for i2 in range(2):
+                want = tk["U0"][i0, 0] * (tk["U1"][i1, 0] * (tk["G"][0, 0, 0] * tk["U2"][i2, 0]))
+                assert oracle.tucker_value(tk, i0, i1, i2) == want
+
+
+def test_tucker_value_dense_materialisation(oracle):
+    """O4-T equals the dense Tucker tensor sum_abc G_abc U0[i,a] U1[j,b] U2[k,c] (numpy einsum)
+    at every cell of a small grid with unequal ranks, to rounding."""
+    rng = np.random.default_rng(11)
+    n, r = 6, (2, 3, 4)
+    tk = _tucker(rng, n, r)
+    T = np.einsum("abc,ia,jb,kc->ijk", tk["G"], tk["U0"], tk["U1"], tk["U2"])
+    got = np.array([[[oracle.tucker_value(tk, i, j, k) for k in range(n)] for j in range(n)]
+                    for i in range(n)])
+    assert np.max(np.abs(got - T)) <= 1e-13 * np.max(np.abs(T))
+
+
+def test_tucker_value_order_hand_worked(oracle):
+    """The contraction order of reading A26, by hand: with G[0,0,:] = (1e16, 1, -1e16) and
+    u2 = (1, 1, 1) the innermost chain is ((0 + 1e16) + 1) + (-1e16) = 0 in binary64 (the exact
+    value is 1; a chain in the other order, (-1e16 + 1) + 1e16, also gives 0, and the tree
+    (1e16 + -1e16) + 1 gives 1): O4-T is the ascending chain."""
+    tk = {"U0": np.array([[1.0]]), "U1": np.array([[1.0]]), "U2": np.array([[1.0, 1.0, 1.0]]),
+          "G": np.array([[[1e16, 1.0, -1e16]]])}
+    assert oracle.tucker_value(tk, 0, 0, 0) == 0.0
+    tk["G"] = np.array([[[1e16, -1e16, 1.0]]])
+    assert oracle.tucker_value(tk, 0, 0, 0) == 1.0
+
+
+def test_tucker_scorer_is_zL_weighted_sum(oracle):
+    """The scorer's long-range part with a Tucker form (mode bit 2) is the double-double sum of
+    z_l O4-T(i_l) over the ligand atoms: one atom at the identity pose reproduces the cell value."""
+    rng = np.random.default_rng(5)
+    n, b = 16, 4.0
+    tk = _tucker(rng, n, (2, 2, 3))
+    tb = {"n": n, "b": b, "R": 1, "F1": np.zeros((n, 1)), "F2": np.zeros((n, 1)),
+          "F3": np.zeros((n, 1)), "n_sigma": 0, "S1": np.zeros((1, 0)), "S2": np.zeros((1, 0)),
+          "S3": np.zeros((1, 0))}
+    Y = np.array([[0.3, -1.1, 2.2]])
+    zL = np.array([0.75])
+    poses = np.array([[1.0, 0, 0, 0, 0.0, 0.0, 0.0]])
+    E, d, inv = oracle.score_poses(tb, np.zeros((0, 3)), np.zeros(0), Y, zL, poses, 2.5,
+                                   long_only=True, tucker=tk)
+    c = [oracle.snap_np(Y[0], b, n)[a] for a in range(3)]
+    assert inv == 0 and E[0] == 0.75 * oracle.tucker_value(tk, *c)
