@@ -190,20 +190,20 @@ def bench_dry_run(args):
     return 0
 
 
-def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7, f32=False):
+def cpu_reference_rate(w, tables, budget_s=12.0, max_poses=200000, seed=7, f32=False, tucker=None):
     """Time the oracle (as it stands) on a bounded seeded sample of the workload's poses."""
     from oracle import rs_oracle
     from synth import configs as syn
     _, probe = syn.subsample(w.poses, 64, seed=seed)
     t0 = time.perf_counter()
     rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, probe,
-                          w.dmin_cap, f32=f32)
+                          w.dmin_cap, f32=f32, tucker=tucker)
     dt = time.perf_counter() - t0
     k = int(min(max_poses, max(64, 64 * budget_s / max(dt, 1e-6))))
     idx, sample = syn.subsample(w.poses, k, seed=seed + 1)
     t0 = time.perf_counter()
     rs_oracle.score_poses(tables, w.protein_xyz, w.protein_q, w.ligand_xyz, w.ligand_q, sample,
-                          w.dmin_cap, f32=f32)
+                          w.dmin_cap, f32=f32, tucker=tucker)
     dt = time.perf_counter() - t0
     return k, dt, rs_oracle.num_threads()
 
@@ -264,6 +264,7 @@ def config_dict(w, args):
                             ", replicated handle, no data-path collective"),
             "mode": ("forces (rs_score_forces, N1)" if getattr(args, "forces", False) else "energy + mindist")
                     + (", fp32 factors (A21)" if getattr(args, "f32", False) else "")
+                    + (", Tucker-format evaluation (N5, A26)" if getattr(args, "tucker", False) else "")
                     + (", Eq. (23) complex: 2 proteins x R/2, rank-concatenated (A24)"
                        if getattr(args, "complex", False) else "")
                     + (f", box-restricted width {args.box}, scheme "
@@ -373,6 +374,8 @@ def main():
     ap.add_argument("--complex", action="store_true",
                     help="build the config's protein as a two-protein complex (Eq. (23), N4): "
                          "one RS tensor of width R/2 per protein, rank-concatenated")
+    ap.add_argument("--tucker", action="store_true",
+                    help="Tucker-format evaluation of the long range (RS_FLAG_TUCKER_EVAL, NEXT row N5)")
     ap.add_argument("--f32", action="store_true",
                     help="the fp32-factor variant (RS_FLAG_F32_FACTORS, DESIGN.md reading A21)")
     ap.add_argument("--nbr-cell", type=float, default=0.0,
@@ -418,7 +421,7 @@ def main():
               file=sys.stderr, flush=True)
     ncpu = os.cpu_count() or 1
     t0 = time.perf_counter()
-    fl = rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0
+    fl = (rsdock.RS_FLAG_F32_FACTORS if args.f32 else 0) | (rsdock.RS_FLAG_TUCKER_EVAL if args.tucker else 0)
     box_info = None
     if args.complex:
         # NEXT row N4 (Eq. (23)): one RS tensor per protein (R/2 each), combined on the device
@@ -578,6 +581,10 @@ def main():
             traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    if args.tucker:
+        # N5: the Tucker contraction is FP64 issue (2 r0 r1 r2 + 2 r0 r1 + 2 r0 DMUL/DADD per atom)
+        tr = info["tucker_r"]
+        dp_instr = (2.0 * tr[0] * tr[1] * tr[2] + 2.0 * tr[0] * tr[1] + 2.0 * tr[0] + 25.0) * P * L
     roofline = {
         "bound": "l2" if on_l2 else "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if peak else None, "traffic": traffic,
@@ -592,9 +599,17 @@ def main():
         "l2_literal_frac": (achieved / (l2_peak if on_l2 else l2_peak_c3)) if (l2_peak and l2_peak_c3) else None,
         "hbm_peak_measured_gbs": peaks.get("hbm_gbs"),
     }
+    if args.tucker:
+        roofline.update({"bound": "fp64", "achieved": dp_instr / t_s / 1e9,
+                         "peak": fp64_rate / 1e9 if fp64_rate else None, "unit": "G DP instr/s",
+                         "frac": (dp_instr / t_s / fp64_rate) if fp64_rate else None,
+                         "kernel": "score_kernel<Tucker>",
+                         "peak_source": "tools/microbench (same run): DFMA issue rate, 148 SMs",
+                         "algorithmic_dp_instr_per_launch": dp_instr})
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        k, dt, cores = cpu_reference_rate(w, prot.export_tables(), f32=args.f32)
+        k, dt, cores = cpu_reference_rate(w, prot.export_tables(), f32=args.f32,
+                                          tucker=prot.export_tucker() if args.tucker else None)
         cpu = {"value": k / dt, "unit": "poses/s", "cores": cores, "kind": "oracle",
                "sample": f"{k} seeded poses of {w.name} ({dt:.1f} s; brute-force short-range/vdW "
                          f"over all {w.M} protein atoms)"}

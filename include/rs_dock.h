@@ -66,6 +66,11 @@ extern "C" {
                                   the device -- the default of every device build (kept as an
                                   explicit request); its tables differ from a host-only build's
                                   by rounding                                                */
+#define RS_FLAG_TUCKER_EVAL 32u /* scoring evaluates the long range from the Tucker form of
+                                  S5-S6 (RHOSVD bases U_l, core G) instead of the CP factors:
+                                  NEXT row N5, r0 r1 r2 multiply-adds per atom instead of 3R
+                                  products (reading A26); needs r_l <= 32 and a core
+                                  of at most 16384 entries; not for combined/box handles       */
 #define RS_FLAG_HOST_FFT 16u   /* setup: the S5-S6 convolutions on the host even with a device
                                   (tables bitwise equal to a RS_FLAG_HOST_ONLY build's)       */
 
@@ -240,13 +245,14 @@ int64_t rs_score_forces(rs_handle* h, const double* q_lig, const double* xyz_lig
  * ligand (host pointer, n_lig x 3 body-frame coordinates; only its radius matters), without
  * launching anything: RS_PATH_WINDOW (H4 rows staged in a shared-memory window per pose tile:
  * the roofline is shared-memory bandwidth), RS_PATH_L2 (rows gathered from L2 with 32-byte
- * loads: the window of one translation does not fit) or RS_PATH_L2_RUNTIME (a width without a
- * compiled kernel, L2 rows).  The measurement (bench.py) picks its roofline from this.  Returns
+ * loads: the window of one translation does not fit), RS_PATH_L2_RUNTIME (a width without a
+ * compiled kernel, L2 rows) or RS_PATH_TUCKER (RS_FLAG_TUCKER_EVAL: the Tucker form).  The measurement (bench.py) picks its roofline from this.  Returns
  * the path (> 0) or a negative RS_E_* code.
  */
 #define RS_PATH_WINDOW     1
 #define RS_PATH_L2         2
 #define RS_PATH_L2_RUNTIME 3
+#define RS_PATH_TUCKER     4
 int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig);
 
 /*
@@ -260,6 +266,15 @@ int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig);
  */
 int rs_save_handle(const rs_handle* h, const char* path);
 rs_handle* rs_load_handle(const char* path, int32_t device, int32_t flags);
+
+/*
+ * Copy the handle's Tucker form of the long-range part (S5-S6; what RS_FLAG_TUCKER_EVAL scores
+ * from) to caller buffers (host): r[3] the Tucker ranks; U0, U1, U2 n x r_l each (row-major:
+ * row i holds U_l[i, :]); G r0 x r1 x r2 (row-major), charges and quadrature weights folded in.
+ * Pass NULL buffers to query r only.  Returns 0 or a negative code (RS_E_INVALID_ARG when the
+ * handle keeps no Tucker form, e.g. a combined handle).
+ */
+int rs_export_tucker(const rs_handle* h, int32_t* r, double* U0, double* U1, double* U2, double* G);
 
 /* Fill *out.  Returns 0 or RS_E_INVALID_ARG. */
 int rs_get_info(const rs_handle* h, rs_info* out);

@@ -86,7 +86,7 @@ void free_device(rs_handle* h) {
   if (h->scan_buf) cudaFree(h->scan_buf);
   h->scan_buf = nullptr;
   h->scan_bytes = 0;
-  for (void** p : {&h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
+  for (void** p : {&h->d_Ut[0], &h->d_Ut[1], &h->d_Ut[2], &h->d_TG, &h->d_prec, &h->d_nb_ent, &h->d_memo, &h->d_Fw[0], &h->d_Fw[1], &h->d_Fw[2],
                    &h->d_Fw32[0], &h->d_Fw32[1], &h->d_Fw32[2],
                    &h->d_nb_range, &h->d_nb_pack}) {
     if (*p) cudaFree(*p);
@@ -193,6 +193,17 @@ int upload_handle(rs_handle* h) {
       if (int e = upload(&h->d_nb_pack, pk, &bytes)) return e;
     }
   }
+  if (h->prm.flags & RS_FLAG_TUCKER_EVAL) {
+    // the Tucker form for the scoring kernel (N5): bases row-major (row i = U_l[i, :]), core
+    const rs::TuckerRep& tk = h->tucker;
+    for (int l = 0; l < 3; ++l) {
+      std::vector<double> rows((size_t)h->n * tk.r[l]);
+      for (int i = 0; i < h->n; ++i)
+        for (int a = 0; a < tk.r[l]; ++a) rows[(size_t)i * tk.r[l] + a] = tk.U[l][(size_t)a * h->n + i];
+      if (int e = upload(&h->d_Ut[l], rows, &bytes)) return e;
+    }
+    if (int e = upload(&h->d_TG, tk.G, &bytes)) return e;
+  }
   if (h->f32) {
     // binary32 copy of the factors (A21), rows as 16-byte quads padded/replicated like Fw
     std::vector<float> packed;
@@ -262,6 +273,14 @@ rs::ScoreArgs base_args(const rs_handle* h) {
   a.nb_dim2p = h->nb_dim2p;
   a.ns2 = (unsigned)((int64_t)h->n_sigma * h->n_sigma);
   a.f32 = h->f32 ? 1 : 0;
+  if (h->d_TG) {
+    a.tk = 1;
+    for (int l = 0; l < 3; ++l) {
+      a.tr[l] = h->tucker.r[l];
+      a.t.Ut[l] = (const double*)h->d_Ut[l];
+    }
+    a.t.TG = (const double*)h->d_TG;
+  }
   a.loc4 = h->loc4 ? 1 : 0;
   {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
@@ -468,6 +487,16 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
               std::to_string(hd->R));
       return nullptr;
     }
+    if (prm.flags & RS_FLAG_TUCKER_EVAL) {
+      const int* r = hd->tucker.r;
+      if (hd->f32 || r[0] < 1 || r[0] > 32 || r[1] < 1 || r[1] > 32 || r[2] < 1 || r[2] > 32 ||
+          (int64_t)r[0] * r[1] * r[2] > 16384) {
+        set_err("RS_FLAG_TUCKER_EVAL needs Tucker ranks r_l <= 32 with r0 r1 r2 <= 16384 (and no "
+                "RS_FLAG_F32_FACTORS); got " + std::to_string(r[0]) + " x " + std::to_string(r[1]) +
+                " x " + std::to_string(r[2]));
+        return nullptr;
+      }
+    }
     if (hd->R > (1 << 20)) {
       set_err("compressed CP width " + std::to_string(hd->R) + " exceeds 2^20 (raise eps_compress or fix rank_R)");
       return nullptr;
@@ -541,6 +570,7 @@ rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, i
   if (R > (1 << 20)) { set_err("combined CP width exceeds 2^20"); return nullptr; }
   rs_params prm = p0->prm;
   prm.flags = flags;
+  if (flags & RS_FLAG_TUCKER_EVAL) { set_err("RS_FLAG_TUCKER_EVAL: a combined handle has no Tucker form"); return nullptr; }
   const bool host_only = (flags & RS_FLAG_HOST_ONLY) != 0;
   if (!host_only) {
     int ndev = 0;
@@ -630,6 +660,7 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
   auto t0 = std::chrono::steady_clock::now();
   if (!h || !lo || !hi) { set_err("null argument"); return nullptr; }
   if (rank < 0) { set_err("rank must be >= 0"); return nullptr; }
+  if (flags & RS_FLAG_TUCKER_EVAL) { set_err("RS_FLAG_TUCKER_EVAL: a box handle scores its box CP"); return nullptr; }
   for (int a = 0; a < 3; ++a)
     if (lo[a] < 0 || hi[a] >= h->n || lo[a] > hi[a]) {
       set_err("need 0 <= lo <= hi < n on every axis");
@@ -714,6 +745,20 @@ rs_handle* rs_restrict_box(const rs_handle* h, const int32_t* lo, const int32_t*
   return H.release();
 }
 
+int rs_export_tucker(const rs_handle* h, int32_t* r, double* U0, double* U1, double* U2, double* G) {
+  if (!h || !r) { set_err("null argument"); return RS_E_INVALID_ARG; }
+  const rs::TuckerRep& tk = h->tucker;
+  if (tk.G.empty()) { set_err("this handle keeps no Tucker form (combined or box handle)"); return RS_E_INVALID_ARG; }
+  for (int l = 0; l < 3; ++l) r[l] = tk.r[l];
+  double* U[3] = {U0, U1, U2};
+  for (int l = 0; l < 3; ++l)
+    if (U[l])
+      for (int i = 0; i < h->n; ++i)
+        for (int a = 0; a < tk.r[l]; ++a) U[l][(size_t)i * tk.r[l] + a] = tk.U[l][(size_t)a * h->n + i];
+  if (G) std::memcpy(G, tk.G.data(), tk.G.size() * sizeof(double));
+  return 0;
+}
+
 int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig) {
   if (!h || (n_lig > 0 && !xyz_lig) || n_lig < 0) { set_err("null or invalid argument"); return RS_E_INVALID_ARG; }
   if (n_lig > (int64_t)1 << 30) { set_err("n_lig too large"); return RS_E_INVALID_ARG; }
@@ -725,7 +770,7 @@ int rs_score_path(rs_handle* h, const double* xyz_lig, int64_t n_lig) {
   a.P = 0;
   a.rmax_hint = ligand_rmax(h, xyz_lig, n_lig, false, nullptr);
   const int e = rs::plan_score(a, h->device);
-  if (e < rs::kPathWindow || e > rs::kPathL2Runtime) {
+  if (e < rs::kPathWindow || e > rs::kPathTucker) {
     set_err(std::string("launch plan failed: ") + cudaGetErrorString((cudaError_t)e));
     return RS_E_CUDA;
   }

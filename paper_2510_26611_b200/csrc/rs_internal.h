@@ -136,6 +136,8 @@ struct DeviceTables {
   const int4* nb_ent = nullptr;       // per list entry: (i0 | i1 << 16, i2, sorted atom, 0)
   const double4* prec = nullptr;      // per sorted protein atom: (x, y, z, q)
   const double* short_memo = nullptr; // s(|D0|,|D1|,|D2|) for |D_a| <= n_sigma, or null
+  const double* Ut[3] = {nullptr, nullptr, nullptr};  // Tucker bases n x r_l, row-major (N5)
+  const double* TG = nullptr;         // Tucker core r0 x r1 x r2 (N5)
 };
 
 struct ScoreArgs {               // one launch of the scoring kernel
@@ -157,6 +159,8 @@ struct ScoreArgs {               // one launch of the scoring kernel
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
   int f32;                       // long-range part from the binary32 factors (A21)
+  int tk = 0;                    // long-range part from the Tucker form (N5, reading A26)
+  int tr[3] = {0, 0, 0};         // its ranks
   int loc4;                      // every list begin < 2^24 and count < 256: 4-byte local cells
   int nb_dim2p;                  // z extent of nb_pack (nb_dim[2] rounded up to a multiple of 4)
   // streamed launch (host-buffer pipeline): poses arrive in copy chunks [cb[i], cb[i+1]);
@@ -180,7 +184,7 @@ constexpr int kPackPad = 24;     // zero cells before each axis of the packed ra
 int launch_score(const ScoreArgs& a, void* stream, int device, int* launches);
 // which variant launch_score would run for these arguments (no launch): a kPath* value, or a
 // positive CUDA error code
-constexpr int kPathWindow = 1, kPathL2 = 2, kPathL2Runtime = 3;
+constexpr int kPathWindow = 1, kPathL2 = 2, kPathL2Runtime = 3, kPathTucker = 4;
 int plan_score(const ScoreArgs& a, int device);
 const char* score_kernel_variant(int R);
 // NEXT row N2: PPIEM scan kernels (scan_kernel.cu)
@@ -230,6 +234,8 @@ struct rs_handle {
   int64_t n_ent = 0;                   // list entries uploaded (incl. padding)
   void* d_prec = nullptr;
   void* d_memo = nullptr;
+  void* d_Ut[3] = {nullptr, nullptr, nullptr};   // RS_FLAG_TUCKER_EVAL: bases, row-major
+  void* d_TG = nullptr;                          //                      core
   void* d_Fw[3] = {nullptr, nullptr, nullptr};
   void* d_Fw32[3] = {nullptr, nullptr, nullptr};
   bool f32 = false;

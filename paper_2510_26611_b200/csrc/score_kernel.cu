@@ -328,6 +328,35 @@ __device__ __noinline__ double long_phi_global32(const float4* F0, const float4*
   return long_phi_l2_32<R>(F0, F1, F2, i0, i1, i2);
 }
 
+// O4-T (NEXT row N5, reading A26): phi = sum_a u0[a] (sum_b u1[b] (sum_c G[a][b][c] u2[c])),
+// each sum an ascending chain of rounded products and sums (the oracle's order), u_l the rows
+// of the RHOSVD bases at the atom's cells (from L2), G from shared memory; r_l <= 32 (u2 held
+// in registers, the c loop unrolled and predicated)
+constexpr int kTkMax = 32;
+__device__ __noinline__ double tucker_phi(const ScoreArgs& a, int i0, int i1, int i2, const double* G) {
+  const int r0 = a.tr[0], r1 = a.tr[1], r2 = a.tr[2];
+  const double* u0 = a.t.Ut[0] + (size_t)i0 * r0;
+  const double* u1 = a.t.Ut[1] + (size_t)i1 * r1;
+  const double* u2 = a.t.Ut[2] + (size_t)i2 * r2;
+  double w[kTkMax];
+#pragma unroll
+  for (int c = 0; c < kTkMax; ++c) w[c] = c < r2 ? __ldg(u2 + c) : 0.0;
+  double phi = 0.0;
+  for (int x = 0; x < r0; ++x) {
+    double t = 0.0;
+    for (int y = 0; y < r1; ++y) {
+      const double* g = G + ((size_t)x * r1 + y) * r2;
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < kTkMax; ++c)
+        if (c < r2) v = __dadd_rn(v, __dmul_rn(g[c], w[c]));
+      t = __dadd_rn(t, __dmul_rn(__ldg(u1 + y), v));
+    }
+    phi = __dadd_rn(phi, __dmul_rn(__ldg(u0 + x), t));
+  }
+  return phi;
+}
+
 struct ChunkPlan {             // dynamic schedule: nbig chunks of `big` poses, then `tail`-pose chunks
   int64_t nbig;
   int big, tail;
@@ -510,6 +539,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
     s_lb.dim[0] = s_lb.dim[1] = s_lb.dim[2] = 0;
     s_lb.lo[0] = s_lb.lo[1] = s_lb.lo[2] = 0;
     mbar_init(&s_bar);
+  }
+  // N5 (RT < 0): the Tucker core in shared memory behind the ligand (every lane reads the same
+  // core entry at the same step: broadcast loads)
+  double* s_tg = reinterpret_cast<double*>(s_lig + 2 * (size_t)lig_smem_n);
+  if constexpr (RT < 0) {
+    const int ng = a.tr[0] * a.tr[1] * a.tr[2];
+    for (int t = tid; t < ng; t += kThreads) s_tg[t] = __ldg(a.t.TG + t);
   }
   __syncthreads();
   double rmax2 = 0.0;
@@ -985,10 +1021,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
                                       (const double2*)(a.t.F[2] + (size_t)i2 * RT));
               }
             }
-          } else {
+          } else if constexpr (RT == 0) {
             if (go)
               phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
                                 a.t.F[2] + (size_t)i2 * a.R, a.R);
+          } else {
+            // N5: the long range from the Tucker form, core staged in shared memory
+            if (go) phi = tucker_phi(a, i0, i1, i2, s_tg);
           }
           const double zg = go ? z : 0.0;
           dd_add_prod(hi, lo, zg, phi);
@@ -1099,7 +1138,8 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool plan_o
   if (dc.attr_err[slot]) return dc.attr_err[slot];
   constexpr int kChp = F32 ? Geo32<(RT > 0 ? RT : 4)>::CHP : Geo<(RT > 0 ? RT : 2)>::CHP;
   constexpr size_t kRowB = 16 * (size_t)kChp;
-  const size_t fixed = 256 + kQueueBytes;      // alignment slack of the window base, neighbour queues
+  // alignment slack of the window base, neighbour queues, and (N5) the Tucker core
+  const size_t fixed = 256 + kQueueBytes + (RT < 0 ? (size_t)a.tr[0] * a.tr[1] * a.tr[2] * sizeof(double) : 0);
   const size_t avail = (size_t)dc.max_dyn[slot] > fixed ? (size_t)dc.max_dyn[slot] - fixed : 0;
   const size_t lig_res = std::min<size_t>(avail, (size_t)std::min<int64_t>(a.L, 256) * sizeof(double4));
   int cap_rows = 0, loc_cap = 0, loc_cd = 0;
@@ -1267,6 +1307,13 @@ int launch_or_plan(const ScoreArgs& a, void* stream, int device, int* launches, 
   if (dc.init_err) return dc.init_err;
   cudaStream_t st = (cudaStream_t)stream;
   int e;
+  if (a.tk) {
+    // N5: Tucker-format evaluation (rows from L2, the core in shared memory)
+    e = launch_t<-1, false, false>(a, st, device, 14, plan_only);
+    if (e == kPlanned) return kPathTucker;
+    if (launches) *launches += 1;
+    return e;
+  }
   if (a.f32) {
     // binary32 factors (A21): compiled widths only (the build refuses others)
 #define RS_F32_CASE(RR, SLOT)                                                               \

@@ -24,11 +24,12 @@ RS_FLAG_F32_FACTORS = 2
 RS_FLAG_BOX_SCHEME_B = 4
 RS_FLAG_DEVICE_FFT = 8
 RS_FLAG_HOST_FFT = 16
-RS_PATH_WINDOW, RS_PATH_L2, RS_PATH_L2_RUNTIME = 1, 2, 3
+RS_FLAG_TUCKER_EVAL = 32
+RS_PATH_WINDOW, RS_PATH_L2, RS_PATH_L2_RUNTIME, RS_PATH_TUCKER = 1, 2, 3, 4
 
 EXPORTED = ["rs_params_default", "rs_build_protein", "rs_combine_proteins", "rs_restrict_box", "rs_score_poses", "rs_score_poses_async",
             "rs_score_forces", "rs_ppiem_scan", "rs_landscape_minima",
-            "rs_score_path", "rs_save_handle", "rs_load_handle", "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
+            "rs_score_path", "rs_export_tucker", "rs_save_handle", "rs_load_handle", "rs_get_info", "rs_export_tables", "rs_export_setup", "rs_last_error", "rs_free"]
 
 
 class rs_params(ctypes.Structure):
@@ -95,6 +96,8 @@ def load():
     L.rs_ppiem_scan.restype = ctypes.c_int64
     L.rs_landscape_minima.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp]
     L.rs_landscape_minima.restype = ctypes.c_int32
+    L.rs_export_tucker.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+    L.rs_export_tucker.restype = ctypes.c_int
     L.rs_save_handle.argtypes = [_vp, ctypes.c_char_p]
     L.rs_save_handle.restype = ctypes.c_int
     L.rs_load_handle.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]
@@ -303,6 +306,20 @@ def rs_export_setup(h) -> dict:
                 K=info["quad_K"], Ls=info["quad_Ls"])
 
 
+def rs_export_tucker(h) -> dict:
+    """The handle's Tucker form (N5): U0, U1, U2 (n x r_l, row i = U_l[i, :]) and G."""
+    r = np.zeros(3, dtype=np.int32)
+    if load().rs_export_tucker(h, r.ctypes.data, None, None, None, None) != 0:
+        raise RuntimeError("rs_export_tucker: " + rs_last_error())
+    n = rs_get_info(h)["n"]
+    U = [np.empty((n, int(r[l]))) for l in range(3)]
+    G = np.empty(tuple(int(x) for x in r))
+    if load().rs_export_tucker(h, r.ctypes.data, U[0].ctypes.data, U[1].ctypes.data,
+                               U[2].ctypes.data, G.ctypes.data) != 0:
+        raise RuntimeError("rs_export_tucker: " + rs_last_error())
+    return {"U0": U[0], "U1": U[1], "U2": U[2], "G": G}
+
+
 def rs_save_handle(h, path) -> None:
     if load().rs_save_handle(h, os.fsencode(path)) != 0:
         raise RuntimeError("rs_save_handle: " + rs_last_error())
@@ -351,6 +368,9 @@ class Protein:
         self._h = rs_combine_proteins([p.handle for p in parts], flags)
         self.info = rs_get_info(self._h)
         return self
+
+    def export_tucker(self) -> dict:
+        return rs_export_tucker(self._h)
 
     def save(self, path):
         """Write the handle's tables to `path` (rs_save_handle: SPEC's kernel cache)."""

@@ -965,3 +965,22 @@ def test_device_fft_setup(env, name):
     Eg, Dg, inv = gpu_score(torch, rsdock, dev, w, sample)
     Eo, Do, invo = oracle_score(rs_oracle, dev, w, sample)
     compare(Eg, Dg, Eo, Do, inv, invo)
+
+
+@pytest.mark.parametrize("name,k", [("C1", 1000), ("C2", 2000)])
+def test_tucker_eval_matches_oracle(env, name, k):
+    """RS_FLAG_TUCKER_EVAL (NEXT row N5, reading A26): the fused kernel with the long range from
+    the Tucker form (rows of the RHOSVD bases from L2, core in shared memory) matches the
+    oracle's O4-T scorer pose by pose (1e-12, distances bitwise), the plan reports the Tucker
+    path, and a saved / reloaded handle keeps scoring the same."""
+    torch, rsdock, rs_oracle = env
+    w = syn.make(name)
+    prot = build(rsdock, w, flags=rsdock.RS_FLAG_TUCKER_EVAL)
+    assert rsdock.rs_score_path(prot.handle, w.ligand_xyz) == rsdock.RS_PATH_TUCKER
+    _, sample = syn.subsample(w.poses, k)
+    Eg, Dg, inv = gpu_score(torch, rsdock, prot, w, sample)
+    Eo, Do, invo = rs_oracle.score_poses(prot.export_tables(), w.protein_xyz, w.protein_q,
+                                         w.ligand_xyz, w.ligand_q, sample, w.dmin_cap,
+                                         tucker=prot.export_tucker())
+    compare(Eg, Dg, Eo, Do, inv, invo)
+

@@ -507,3 +507,36 @@ def test_handle_save_load_roundtrip(rsd, tmp_path):
             rsd.Protein.load(bad, flags=rsd.RS_FLAG_HOST_ONLY)
     with pytest.raises(RuntimeError, match="cannot open"):
         rsd.Protein.load(tmp_path / "missing.rsh", flags=rsd.RS_FLAG_HOST_ONLY)
+
+
+def test_tucker_form_pins(oracle, rsd, c1_host):
+    """The Tucker form a handle keeps (S5-S6), evaluated by the oracle's O4-T (N5, reading A26):
+    (i) at exterior cells of C1 it is closer to the oracle's uncompressed long-range sum than the
+    width-8 CP derived from it (the CP compresses the Tucker core further); (ii) in tolerance
+    mode (eps = 1e-7), where the CP is the core's slice expansion truncated at eps, the two agree
+    to that tolerance; (iii) the flag is refused where no Tucker form exists or with fp32
+    factors."""
+    w, p = c1_host
+    st = p.export_setup()
+    tk = p.export_tucker()
+    tb = p.export_tables()
+    pts = _exterior_cells(oracle, w, 60, seed=7)
+    ref = _uncompressed_long(oracle, w, st, st["cells"], pts)
+    tv = np.array([oracle.tucker_value(tk, *c) for c in pts])
+    cp = np.einsum("pk,pk,pk->p", tb["F1"][pts[:, 0]], tb["F2"][pts[:, 1]], tb["F3"][pts[:, 2]])
+    e_t = np.max(np.abs(tv - ref)) / np.max(np.abs(ref))
+    e_cp = np.max(np.abs(cp - ref)) / np.max(np.abs(ref))
+    assert e_t < 0.5 * e_cp, (e_t, e_cp)
+    ws = syn.random_small(seed=5, M=60, L=5, n=64, b=8.0)
+    pt = rsd.Protein(ws.protein_q, ws.protein_xyz, ws.box_half_width, grid_n=64, rank_R=0,
+                     eps_compress=1e-7, sigma_split=1.0, flags=rsd.RS_FLAG_HOST_ONLY)
+    tk2, tb2 = pt.export_tucker(), pt.export_tables()
+    cells = np.random.default_rng(2).integers(0, 64, size=(200, 3))
+    tv2 = np.array([oracle.tucker_value(tk2, *c) for c in cells])
+    cp2 = np.einsum("pk,pk,pk->p", tb2["F1"][cells[:, 0]], tb2["F2"][cells[:, 1]], tb2["F3"][cells[:, 2]])
+    assert np.max(np.abs(tv2 - cp2)) <= 1e-6 * np.max(np.abs(tv2))
+    with pytest.raises(RuntimeError):
+        rsd.Protein(w.protein_q, w.protein_xyz, w.box_half_width, **w.params(),
+                    flags=rsd.RS_FLAG_HOST_ONLY | rsd.RS_FLAG_TUCKER_EVAL | rsd.RS_FLAG_F32_FACTORS)
+    with pytest.raises(RuntimeError):
+        rsd.Protein.combine([p], flags=rsd.RS_FLAG_HOST_ONLY | rsd.RS_FLAG_TUCKER_EVAL)
