@@ -69,6 +69,10 @@ class CoreDevice {
   ~CoreDevice();
   bool ok() const;
   bool add_term(double a_k, const std::vector<double> H[3]);   // H_l: n x r_l row-major
+  // every term k on the device: H_l = (T_k U_l) from the device convolutions straight into the
+  // accumulation (U_l: n x r_l column-major, uploaded once; no host round trip per term)
+  bool add_terms_device(class DeviceConv& conv, const std::vector<double> U[3],
+                        const std::vector<double>& a_long);
   bool fetch(std::vector<double>& G);
  private:
   struct Impl;
@@ -85,6 +89,7 @@ class DeviceConv {
   bool ok() const;
   bool apply(int k, const double* X, double* Y, int cols);   // X, Y: n x cols column-major
  private:
+  friend class CoreDevice;
   struct Impl;
   Impl* p;
 };

@@ -599,8 +599,19 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
     cdev.reset(new CoreDevice(device, n, rr_, cells, z));
     if (!cdev->ok()) cdev.reset();
   }
-  for (int k = 0; k < RL; ++k) {
+  double t_conv = 0, t_add = 0;
+  const bool timing = std::getenv("RS_SETUP_TIMING") != nullptr;
+  // device convolutions and device accumulation: every term without leaving the device (the
+  // same cuFFT calls and the same accumulation as the per-term loop below, so bitwise the same)
+  int k0 = 0;
+  if (cdev && ops.dev) {
+    std::vector<double> U3[3] = {mb[0].U, mb[1].U, mb[2].U};
+    if (cdev->add_terms_device(*ops.dev, U3, a_long)) k0 = RL;
+    else cdev.reset();
+  }
+  for (int k = k0; k < RL; ++k) {
     std::vector<double> H[3];   // row-major n x r_l
+    auto tc = std::chrono::steady_clock::now();
     for (int l = 0; l < 3; ++l) {
       const int r = mb[l].r;
       std::vector<double> tmp((size_t)n * r);
@@ -609,8 +620,12 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       for (int a = 0; a < r; ++a)
         for (int i = 0; i < n; ++i) H[l][(size_t)i * r + a] = tmp[(size_t)a * n + i];
     }
+    if (timing) t_conv += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
     if (cdev) {
-      if (cdev->add_term(a_long[k], H)) continue;
+      tc = std::chrono::steady_clock::now();
+      const bool ok_add = cdev->add_term(a_long[k], H);
+      if (timing) t_add += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
+      if (ok_add) continue;
       // the device failed mid-way: redo the core on the host from scratch
       cdev.reset();
       std::fill(G.begin(), G.end(), 0.0);
@@ -667,6 +682,7 @@ void compress_long_range(int n, double h, const std::vector<int32_t>& cells,
       }
     }
   }
+  if (timing) std::fprintf(stderr, "[rs setup]     core: convolutions %.3f s, device accumulation %.3f s\n", t_conv, t_add);
   if (std::getenv("RS_SETUP_TIMING")) std::fprintf(stderr, "[rs setup]   core done at %.3f\n", std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
   // S7: core -> CP of width R
   std::vector<double> A, B, C;

@@ -5,6 +5,8 @@
 // row += wb H2; then G += row), compiled with -fmad=false like the host's -ffp-contract=off,
 // so the core -- and every table built from it -- is bitwise the host-only build's.
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cstdint>
@@ -149,6 +151,78 @@ __global__ void unpack_pairs(const cufftDoubleComplex* buf, int n, int N, int p,
     const int s = (int)(t / n), i = (int)(t % n);
     const cufftDoubleComplex v = buf[(size_t)(s / 2) * N + i + n - 1];
     Y[t] = ((s & 1) ? v.y : v.x) * inv;
+  }
+}
+
+// S6 accumulation for the device-FFT path, split over atoms: block (a, chunk) adds
+// sum_{m in chunk} (z_m a_k H0[m,a]) H1[m,b] H2[m,c] for all (b, c) into its partial; atoms in
+// ascending order, the chunks' partials summed in ascending order by core_reduce_kernel, so the
+// core is deterministic (not bitwise the per-entry loop's order: device-FFT builds are
+// validated by their accuracy)
+constexpr int kCoreChunk = 512, kCoreSub = 64;
+__global__ void core_chunk_kernel(int r0, int r1, int r2, int64_t M, const int* __restrict__ cells,
+                                  const double* __restrict__ z, double ak, const double* __restrict__ H0,
+                                  const double* __restrict__ H1, const double* __restrict__ H2,
+                                  double* __restrict__ part) {
+  extern __shared__ double sm[];
+  double* sw = sm;                         // kCoreSub weights
+  double* s1 = sm + kCoreSub;              // kCoreSub x r1
+  double* s2 = s1 + (size_t)kCoreSub * r1; // kCoreSub x r2
+  const int a = blockIdx.x % r0, chunk = blockIdx.x / r0;
+  const int64_t m0 = (int64_t)chunk * kCoreChunk, m1 = min(M, m0 + kCoreChunk);
+  const int nout = r1 * r2;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t mb = m0; mb < m1; mb += kCoreSub) {
+    const int cnt = (int)min((int64_t)kCoreSub, m1 - mb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int64_t m = mb + t;
+      sw[t] = __dmul_rn(__dmul_rn(z[m], ak), H0[(size_t)cells[3 * m] * r0 + a]);
+    }
+    for (int t = threadIdx.x; t < cnt * r1; t += blockDim.x) {
+      const int u = t / r1, b = t % r1;
+      s1[t] = H1[(size_t)cells[3 * (mb + u) + 1] * r1 + b];
+    }
+    for (int t = threadIdx.x; t < cnt * r2; t += blockDim.x) {
+      const int u = t / r2, c = t % r2;
+      s2[t] = H2[(size_t)cells[3 * (mb + u) + 2] * r2 + c];
+    }
+    __syncthreads();
+    for (int u = 0; u < cnt; ++u) {
+      const double w = sw[u];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = threadIdx.x + j * blockDim.x;
+        if (idx < nout) {
+          const int b = idx / r2, c = idx % r2;
+          acc[j] = __dadd_rn(acc[j], __dmul_rn(__dmul_rn(w, s1[u * r1 + b]), s2[u * r2 + c]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int idx = threadIdx.x + j * blockDim.x;
+    if (idx < nout) part[((size_t)chunk * r0 + a) * nout + idx] = acc[j];
+  }
+}
+
+__global__ void core_reduce_kernel(int nchunk, int64_t ng, const double* __restrict__ part, double* G) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ng; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s = __dadd_rn(s, part[(size_t)c * ng + t]);
+    G[t] = __dadd_rn(G[t], s);
+  }
+}
+
+// the same values transposed: Yr row-major n x p (row i holds the p columns at i)
+__global__ void unpack_pairs_rows(const cufftDoubleComplex* buf, int n, int N, int p, double* Yr) {
+  const double inv = 1.0 / N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)p * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / p), s = (int)(t % p);
+    const cufftDoubleComplex v = buf[(size_t)(s / 2) * N + i + n - 1];
+    Yr[t] = ((s & 1) ? v.y : v.x) * inv;
   }
 }
 
@@ -317,6 +391,92 @@ bool exact_long_values_device(int device, int n, const std::vector<double>& G,
   cudaGetLastError();
   cudaSetDevice(prev);
   return ok;
+}
+
+}  // namespace rs
+
+// ---- S6 end to end on the device ------------------------------------------------------------
+namespace rs {
+
+bool CoreDevice::add_terms_device(DeviceConv& conv, const std::vector<double> U[3],
+                                  const std::vector<double>& a_long) {
+  if (!p->ok || !conv.p->ok || conv.p->device != p->device || conv.p->n != p->n) return false;
+  std::lock_guard<std::mutex> lock(conv.p->mtx);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  const int n = p->n, N = conv.p->N;
+  int maxr = std::max(p->r[0], std::max(p->r[1], p->r[2]));
+  const int maxpairs = (maxr + 1) / 2;
+  double* dU[3] = {nullptr, nullptr, nullptr};
+  cufftDoubleComplex* buf = nullptr;
+  cufftHandle plans[3] = {0, 0, 0};
+  const int64_t ng = (int64_t)p->r[0] * p->r[1] * p->r[2];
+  double* part = nullptr;
+  bool good = p->r[1] * p->r[2] <= 1024 &&
+              cudaMalloc(&buf, (size_t)maxpairs * N * sizeof(cufftDoubleComplex)) == cudaSuccess &&
+              cudaMalloc(&part, (size_t)((p->M + kCoreChunk - 1) / kCoreChunk) * ng * sizeof(double)) == cudaSuccess;
+  for (int l = 0; l < 3 && good; ++l) {
+    good = cudaMalloc(&dU[l], (size_t)n * p->r[l] * sizeof(double)) == cudaSuccess &&
+           cudaMemcpy(dU[l], U[l].data(), (size_t)n * p->r[l] * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+           cufftPlan1d(&plans[l], N, CUFFT_Z2Z, (p->r[l] + 1) / 2) == CUFFT_SUCCESS;
+  }
+  const bool timing = std::getenv("RS_SETUP_TIMING") != nullptr;
+  cudaEvent_t ev[2];
+  float t_conv = 0.f, t_acc = 0.f;
+  if (timing) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); }
+  for (int k = 0; k < (int)a_long.size() && good; ++k) {
+    if (timing) cudaEventRecord(ev[0]);
+    for (int l = 0; l < 3 && good; ++l) {
+      const int r = p->r[l], pairs = (r + 1) / 2;
+      pack_pairs<<<1184, 256>>>(dU[l], n, N, r, buf);
+      good = cufftExecZ2Z(plans[l], buf, buf, CUFFT_FORWARD) == CUFFT_SUCCESS;
+      if (good) {
+        mul_kernel<<<1184, 256>>>(buf, conv.p->fg + (size_t)k * N, N, pairs);
+        good = cufftExecZ2Z(plans[l], buf, buf, CUFFT_INVERSE) == CUFFT_SUCCESS;
+      }
+      if (good) unpack_pairs_rows<<<1184, 256>>>(buf, n, N, r, p->H[l]);
+    }
+    if (timing) {
+      float ms = 0.f;
+      cudaEventRecord(ev[1]);
+      cudaEventSynchronize(ev[1]);
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      t_conv += ms;
+      cudaEventRecord(ev[0]);
+    }
+    if (good) {
+      const int nchunk = (int)((p->M + kCoreChunk - 1) / kCoreChunk);
+      const size_t shm = (size_t)kCoreSub * (1 + p->r[1] + p->r[2]) * sizeof(double);
+      core_chunk_kernel<<<nchunk * p->r[0], 256, shm>>>(p->r[0], p->r[1], p->r[2], p->M, p->cells, p->z,
+                                                        a_long[k], p->H[0], p->H[1], p->H[2], part);
+      core_reduce_kernel<<<256, 256>>>(nchunk, ng, part, p->G);
+      good = cudaGetLastError() == cudaSuccess;
+    }
+    if (timing) {
+      float ms = 0.f;
+      cudaEventRecord(ev[1]);
+      cudaEventSynchronize(ev[1]);
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      t_acc += ms;
+    }
+  }
+  if (timing) {
+    std::fprintf(stderr, "[rs setup]     core on the device: convolutions %.3f s, accumulation %.3f s\n",
+                 t_conv * 1e-3, t_acc * 1e-3);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  good = good && cudaDeviceSynchronize() == cudaSuccess;
+  for (int l = 0; l < 3; ++l) {
+    if (plans[l]) cufftDestroy(plans[l]);
+    cudaFree(dU[l]);
+  }
+  cudaFree(buf);
+  cudaFree(part);
+  if (!good) { cudaGetLastError(); p->ok = false; }
+  cudaSetDevice(prev);
+  return good;
 }
 
 }  // namespace rs
