@@ -163,7 +163,8 @@ int upload_handle(rs_handle* h) {
       h->loc4 = tot < ((size_t)1 << 24) && maxcnt < 256;
     }
     std::vector<int32_t> ent(4 * std::max<size_t>(tot, 2), 0);
-    for (size_t c = 0; c < nc; ++c)
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t c = 0; c < (int64_t)nc; ++c)
       for (int32_t u = 0; u < rng[2 * c + 1]; ++u) {
         const size_t j = (size_t)rng[2 * c] + u;
         const size_t m = (size_t)h->cg.idx[(size_t)h->cg.off[c] + u];
@@ -183,6 +184,7 @@ int upload_handle(rs_handle* h) {
       const int e0 = d0 + P, e1 = d1 + P;
       h->nb_dim2p = (d2 + P + 3) / 4 * 4;
       std::vector<uint32_t> pk((size_t)e0 * e1 * h->nb_dim2p, 0u);
+#pragma omp parallel for schedule(static)
       for (int x = 0; x < d0; ++x)
         for (int y = 0; y < d1; ++y)
           for (int z = 0; z < d2; ++z) {

@@ -90,11 +90,32 @@ class DeviceConv {
   bool apply(int k, const double* X, double* Y, int cols);   // X, Y: n x cols column-major
  private:
   friend class CoreDevice;
+  friend class RangeFinderDevice;
   struct Impl;
   Impl* p;
 };
 
 // S7: Tucker core -> CP of width rank_R (0: eps mode); returns R
+// The RHOSVD range finder of one mode with every convolution on the device (device-FFT builds,
+// no box): the sketch sum_k T_k (sqrt(c_k) .* Xi_k) (the host's counter-based normal draws,
+// generated on the device), the power step sum_k T_k (c_k .* (T_k Q)) and the p x p Gram matrix
+// sum_k sum_j c_k[j] (T_k Q)[j,:]^T (T_k Q)[j,:], each sum in k order; the orthonormalisations
+// stay on the host (small).  Any failure returns false and the caller runs the host path.
+class RangeFinderDevice {
+ public:
+  RangeFinderDevice(DeviceConv& conv, const std::vector<std::vector<double>>& c, int n);
+  ~RangeFinderDevice();
+  bool ok() const;
+  bool sketch(int p, uint64_t seed, int mode, const std::vector<int>& occj, std::vector<double>& Y);
+  bool power(const std::vector<double>& Q, int p, std::vector<double>& Y);
+  bool gram(const std::vector<double>& Q, int p, std::vector<double>& Gm);
+ private:
+  bool reserve(int p);
+  bool apply(int k, const double* dX, double* dY, int p);   // device buffers, n x p col-major
+  struct Impl;
+  Impl* q;
+};
+
 int core_to_cp(const std::vector<double>& G, int r0, int r1, int r2, int rank_R, double eps,
                int als_sweeps, std::vector<double>& A, std::vector<double>& B,
                std::vector<double>& C, int* R_exact, double* rel_err);

@@ -219,13 +219,22 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
                                : (tucker_cap > 0 ? tucker_cap : n);
   int p = (rank_R > 0) ? std::min(pmax, std::max(2 * r_cap + 16, 48)) : std::min(pmax, 64);
   ModeBasis out;
+  std::unique_ptr<RangeFinderDevice> rf;
+  if (ops.dev && !box_lo) {
+    rf.reset(new RangeFinderDevice(*ops.dev, c, n));
+    if (!rf->ok()) rf.reset();
+  }
   PhaseClock pc;
   pc.lap(mode, "weights");
   for (;;) {
     // range finder: Y = sum_k T_k (sqrt(c_k) .* Xi_k).  Per-k results are summed in k order
-    // so the setup is bitwise independent of the thread count.
+    // so the setup is bitwise independent of the thread count.  Device-FFT builds (no box) run
+    // the sums on the device (RangeFinderDevice), the host path below otherwise.
     std::vector<double> Y((size_t)n * p, 0.0);
     std::vector<std::vector<double>> Yk(RL);
+    if (!(rf && rf->sketch(p, seed, mode, occj, Y))) {
+    rf.reset();
+    std::fill(Y.begin(), Y.end(), 0.0);
 #pragma omp parallel
     {
       std::vector<double> X((size_t)n * p);
@@ -244,6 +253,7 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       for (size_t i = 0; i < Y.size(); ++i) Y[i] += Yk[k][i];
       std::vector<double>().swap(Yk[k]);
     }
+    }
     pc.lap(mode, "sketch");
     clip_rows(Y, p);
     orthonormalise(Y, n, p);
@@ -252,6 +262,9 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
     // one power iteration: Y = sum_k T_k (c_k .* (T_k Q))
     {
       std::vector<double> Y2((size_t)n * p, 0.0);
+      if (!(rf && rf->power(Y, p, Y2))) {
+      rf.reset();
+      std::fill(Y2.begin(), Y2.end(), 0.0);
 #pragma omp parallel
       {
         std::vector<double> Z((size_t)n * p);
@@ -268,6 +281,7 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
         for (size_t i = 0; i < Y2.size(); ++i) Y2[i] += Yk[k][i];
         std::vector<double>().swap(Yk[k]);
       }
+      }
       Y.swap(Y2);
       pc.lap(mode, "power");
       clip_rows(Y, p);
@@ -275,7 +289,15 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       clip_rows(Y, p);
       pc.lap(mode, "qr2");
     }
-    // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :]
+    // W^T Q, stacked over (k, occupied j): rows sqrt(c_k[j]) (T_k Q)[j, :].  Its singular values
+    // and right vectors from the p x p Gram matrix sum_k sum_j c_k[j] Z_k[j,:]^T Z_k[j,:]
+    // (Z_k = T_k Q; per k in parallel, summed in k order: bitwise independent of the thread
+    // count), by the Jacobi eigensolver; sigma = sqrt(lambda) descending.  (Squaring costs
+    // accuracy only below ~1e-8 sigma_0, far under the ranks kept.)
+    std::vector<double> Gm((size_t)p * p, 0.0);
+    if (!(rf && rf->gram(Y, p, Gm))) {
+    rf.reset();
+    std::fill(Gm.begin(), Gm.end(), 0.0);
     const int nocc = (int)occj.size();
     std::vector<std::vector<double>> Zk(RL);   // (T_k Q) at the occupied rows, nocc x p
 #pragma omp parallel
@@ -290,10 +312,6 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       }
     }
     pc.lap(mode, "WtQ apply");
-    // the singular values and right vectors of the stacked W^T Q from its p x p Gram matrix
-    // sum_k sum_j c_k[j] Z_k[j,:]^T Z_k[j,:] (per k in parallel, summed in k order: bitwise
-    // independent of the thread count), by the Jacobi eigensolver; sigma = sqrt(lambda)
-    // descending.  (Squaring costs accuracy only below ~1e-8 sigma_0, far under the ranks kept.)
     std::vector<std::vector<double>> Gk(RL);
 #pragma omp parallel for schedule(dynamic)
     for (int k = 0; k < RL; ++k) {
@@ -310,11 +328,11 @@ ModeBasis mode_basis(const ConvOps& ops, int mode, const std::vector<int32_t>& c
       Gk[k].swap(g);
       std::vector<double>().swap(Zk[k]);
     }
-    std::vector<double> Gm((size_t)p * p, 0.0);
     for (int k = 0; k < RL; ++k)
       for (size_t t = 0; t < Gm.size(); ++t) Gm[t] += Gk[k][t];
     for (int s_ = 0; s_ < p; ++s_)
       for (int t = s_ + 1; t < p; ++t) Gm[(size_t)t * p + s_] = Gm[(size_t)s_ * p + t];
+    }
     pc.lap(mode, "WtQ gram");
     std::vector<double> lam(p), Ve((size_t)p * p);
     la::sym_eig(Gm.data(), p, lam.data(), Ve.data());   // ascending
@@ -858,12 +876,29 @@ void build_cell_lists(int n, double b, double h, const std::vector<double>& xyz,
       }
     }
   };
-  for (int64_t m = 0; m < M; ++m) visit(m, [&](int64_t c) { cnt[c + 1]++; });
+  // counts and fill over the atoms in parallel (atomic slots), then every cell's list sorted
+  // back to ascending atom index: the same lists as a serial pass over the atoms
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t m = 0; m < M; ++m)
+    visit(m, [&](int64_t c) {
+#pragma omp atomic
+      cnt[c + 1]++;
+    });
   for (int64_t c = 0; c < ncell; ++c) cnt[c + 1] += cnt[c];
   cg->off = cnt;
   cg->idx.assign(cnt[ncell], 0);
   std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
-  for (int64_t m = 0; m < M; ++m) visit(m, [&](int64_t c) { cg->idx[pos[c]++] = (int32_t)m; });
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t m = 0; m < M; ++m)
+    visit(m, [&](int64_t c) {
+      int32_t slot;
+#pragma omp atomic capture
+      slot = pos[c]++;
+      cg->idx[slot] = (int32_t)m;
+    });
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t c = 0; c < ncell; ++c)
+    if (cnt[c + 1] - cnt[c] > 1) std::sort(cg->idx.begin() + cnt[c], cg->idx.begin() + cnt[c + 1]);
 }
 
 // ---- sampled compression error (reported; O11(iii) re-checks it independently) ---------------

@@ -481,3 +481,224 @@ bool CoreDevice::add_terms_device(DeviceConv& conv, const std::vector<double> U[
 
 }  // namespace rs
 
+// ---- the RHOSVD range finder's convolutions on the device ------------------------------------
+namespace rs {
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix_dev(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// la::normal (setup_linalg.cpp) on the device: the same counter-based draws (Box-Muller of two
+// splitmix64 uniforms; device log/cos, so the last bits may differ from the host's libm)
+__device__ __forceinline__ double normal_dev(uint64_t seed, uint64_t i) {
+  const uint64_t a = splitmix_dev(seed * 0x100000001B3ull + 2 * i);
+  const uint64_t b = splitmix_dev(seed * 0x100000001B3ull + 2 * i + 1);
+  const double u1 = (double((a >> 11) + 1)) * (1.0 / 9007199254740993.0);
+  const double u2 = double(b >> 11) * (1.0 / 9007199254740992.0);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+// X (n x p column-major) = sqrt(c_k[j]) xi_{k,j,s} at occupied rows j, 0 elsewhere
+__global__ void sketch_kernel(int n, int p, int k, const double* __restrict__ c, const unsigned char* __restrict__ occ,
+                              uint64_t seed, double* __restrict__ X) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * p;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n), j = (int)(t % n);
+    X[t] = occ[j] ? sqrt(c[j]) * normal_dev(seed, ((uint64_t)k * n + j) * 4096u + s) : 0.0;
+  }
+}
+__global__ void add_kernel(int64_t len, const double* __restrict__ A, double* __restrict__ Y) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x)
+    Y[t] += A[t];
+}
+__global__ void scale_rows_kernel(int n, int p, const double* __restrict__ c, double* __restrict__ Z) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * p;
+       t += (int64_t)gridDim.x * blockDim.x)
+    Z[t] *= c[t % n];
+}
+// partial weighted Gram of Z (n x p column-major) over a fixed row block: G[s][t] (s <= t) =
+// sum_{j in block} c[j] Z[s][j] Z[t][j]; blocks summed in order on the host
+__global__ void wgram_kernel(int n, int p, int nblk, const double* __restrict__ c, const double* __restrict__ Z,
+                             double* __restrict__ part) {
+  const int blk = blockIdx.y;
+  const int j0 = (int)((int64_t)n * blk / nblk), j1 = (int)((int64_t)n * (blk + 1) / nblk);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < p * p; e += gridDim.x * blockDim.x) {
+    const int s = e / p, t = e % p;
+    double g = 0.0;
+    if (s <= t)
+      for (int j = j0; j < j1; ++j) {
+        const double w = c[j];
+        if (w != 0.0) g += w * Z[(size_t)s * n + j] * Z[(size_t)t * n + j];
+      }
+    part[(size_t)blk * p * p + e] = g;
+  }
+}
+
+}  // namespace
+
+struct RangeFinderDevice::Impl {
+  DeviceConv* conv = nullptr;
+  int n = 0, RL = 0, cap = 0;
+  double *c = nullptr, *X = nullptr, *Y = nullptr, *Z = nullptr, *W = nullptr, *part = nullptr;
+  unsigned char* occ = nullptr;
+  cufftDoubleComplex* buf = nullptr;
+  cufftHandle plan = 0;
+  int plan_pairs = 0;
+  bool ok = false;
+};
+
+RangeFinderDevice::RangeFinderDevice(DeviceConv& conv, const std::vector<std::vector<double>>& c, int n)
+    : q(new Impl) {
+  q->conv = &conv;
+  q->n = n;
+  q->RL = (int)c.size();
+  if (!conv.p->ok || conv.p->n != n) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(conv.p->device) != cudaSuccess) { cudaGetLastError(); return; }
+  bool good = cudaMalloc(&q->c, (size_t)q->RL * n * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&q->occ, n) == cudaSuccess;
+  for (int k = 0; k < q->RL && good; ++k)
+    good = cudaMemcpy(q->c + (size_t)k * n, c[k].data(), n * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  q->ok = good;
+  if (!good) cudaGetLastError();
+  cudaSetDevice(prev);
+}
+
+RangeFinderDevice::~RangeFinderDevice() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(q->conv->p->device);
+  if (q->plan) cufftDestroy(q->plan);
+  for (void* x : {(void*)q->c, (void*)q->X, (void*)q->Y, (void*)q->Z, (void*)q->W, (void*)q->part,
+                  (void*)q->occ, (void*)q->buf})
+    if (x) cudaFree(x);
+  cudaSetDevice(prev);
+  delete q;
+}
+
+bool RangeFinderDevice::ok() const { return q->ok; }
+
+bool RangeFinderDevice::reserve(int p) {
+  const int n = q->n, N = q->conv->p->N, pairs = (p + 1) / 2;
+  if (p > q->cap) {
+    for (double** b : {&q->X, &q->Y, &q->Z, &q->W}) {
+      cudaFree(*b);
+      *b = nullptr;
+      if (cudaMalloc(b, (size_t)n * p * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return false; }
+    }
+    cudaFree(q->buf);
+    q->buf = nullptr;
+    if (cudaMalloc(&q->buf, (size_t)pairs * N * sizeof(cufftDoubleComplex)) != cudaSuccess) { cudaGetLastError(); return false; }
+    cudaFree(q->part);
+    q->part = nullptr;
+    if (cudaMalloc(&q->part, (size_t)64 * p * p * sizeof(double)) != cudaSuccess) { cudaGetLastError(); return false; }
+    q->cap = p;
+  }
+  if (q->plan_pairs != pairs) {
+    if (q->plan) cufftDestroy(q->plan);
+    q->plan = 0;
+    if (cufftPlan1d(&q->plan, N, CUFFT_Z2Z, pairs) != CUFFT_SUCCESS) { q->plan_pairs = 0; return false; }
+    q->plan_pairs = pairs;
+  }
+  return true;
+}
+
+// dY = T_k dX with the same kernels and FFT-domain product as DeviceConv::apply
+bool RangeFinderDevice::apply(int k, const double* dX, double* dY, int p) {
+  const int n = q->n, N = q->conv->p->N, pairs = (p + 1) / 2;
+  pack_pairs<<<1184, 256>>>(dX, n, N, p, q->buf);
+  if (cufftExecZ2Z(q->plan, q->buf, q->buf, CUFFT_FORWARD) != CUFFT_SUCCESS) return false;
+  mul_kernel<<<1184, 256>>>(q->buf, q->conv->p->fg + (size_t)k * N, N, pairs);
+  if (cufftExecZ2Z(q->plan, q->buf, q->buf, CUFFT_INVERSE) != CUFFT_SUCCESS) return false;
+  unpack_pairs<<<1184, 256>>>(q->buf, n, N, p, dY);
+  return cudaGetLastError() == cudaSuccess;
+}
+
+bool RangeFinderDevice::sketch(int p, uint64_t seed, int mode, const std::vector<int>& occj, std::vector<double>& Y) {
+  if (!q->ok) return false;
+  std::lock_guard<std::mutex> lock(q->conv->p->mtx);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(q->conv->p->device);
+  const int n = q->n;
+  bool good = reserve(p);
+  if (good) {
+    std::vector<unsigned char> occ(n, 0);
+    for (int j : occj) occ[j] = 1;
+    good = cudaMemcpy(q->occ, occ.data(), n, cudaMemcpyHostToDevice) == cudaSuccess &&
+           cudaMemset(q->Y, 0, (size_t)n * p * sizeof(double)) == cudaSuccess;
+  }
+  const uint64_t s = seed + 0x51ED27ull * (mode + 1);   // mode_basis's stream
+  for (int k = 0; k < q->RL && good; ++k) {
+    sketch_kernel<<<1184, 256>>>(n, p, k, q->c + (size_t)k * n, q->occ, s, q->X);
+    good = apply(k, q->X, q->Z, p);
+    if (good) add_kernel<<<1184, 256>>>((int64_t)n * p, q->Z, q->Y);
+  }
+  Y.resize((size_t)n * p);
+  good = good && cudaMemcpy(Y.data(), q->Y, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+  if (!good) { cudaGetLastError(); q->ok = false; }
+  cudaSetDevice(prev);
+  return good;
+}
+
+bool RangeFinderDevice::power(const std::vector<double>& Q, int p, std::vector<double>& Y) {
+  if (!q->ok) return false;
+  std::lock_guard<std::mutex> lock(q->conv->p->mtx);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(q->conv->p->device);
+  const int n = q->n;
+  bool good = reserve(p) &&
+              cudaMemcpy(q->X, Q.data(), (size_t)n * p * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemset(q->Y, 0, (size_t)n * p * sizeof(double)) == cudaSuccess;
+  for (int k = 0; k < q->RL && good; ++k) {
+    good = apply(k, q->X, q->Z, p);
+    if (good) {
+      scale_rows_kernel<<<1184, 256>>>(n, p, q->c + (size_t)k * n, q->Z);
+      good = apply(k, q->Z, q->W, p);
+    }
+    if (good) add_kernel<<<1184, 256>>>((int64_t)n * p, q->W, q->Y);
+  }
+  Y.resize((size_t)n * p);
+  good = good && cudaMemcpy(Y.data(), q->Y, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+  if (!good) { cudaGetLastError(); q->ok = false; }
+  cudaSetDevice(prev);
+  return good;
+}
+
+bool RangeFinderDevice::gram(const std::vector<double>& Q, int p, std::vector<double>& Gm) {
+  if (!q->ok) return false;
+  std::lock_guard<std::mutex> lock(q->conv->p->mtx);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(q->conv->p->device);
+  const int n = q->n;
+  constexpr int kBlk = 64;
+  bool good = reserve(p) &&
+              cudaMemcpy(q->X, Q.data(), (size_t)n * p * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  Gm.assign((size_t)p * p, 0.0);
+  std::vector<double> part((size_t)kBlk * p * p);
+  for (int k = 0; k < q->RL && good; ++k) {
+    good = apply(k, q->X, q->Z, p);
+    if (good) {
+      wgram_kernel<<<dim3((p * p + 255) / 256, kBlk), 256>>>(n, p, kBlk, q->c + (size_t)k * n, q->Z, q->part);
+      good = cudaGetLastError() == cudaSuccess &&
+             cudaMemcpy(part.data(), q->part, part.size() * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    // per-k Gram: blocks in order, then added to the total in k order (deterministic)
+    for (int blk = 0; blk < kBlk && good; ++blk)
+      for (size_t e = 0; e < (size_t)p * p; ++e) Gm[e] += part[(size_t)blk * p * p + e];
+  }
+  for (int s_ = 0; s_ < p; ++s_)
+    for (int t = s_ + 1; t < p; ++t) Gm[(size_t)t * p + s_] = Gm[(size_t)s_ * p + t];
+  if (!good) { cudaGetLastError(); q->ok = false; }
+  cudaSetDevice(prev);
+  return good;
+}
+
+}  // namespace rs
+
