@@ -62,6 +62,9 @@ using namespace dev;
 #ifndef RS_LOC_CELLS
 #define RS_LOC_CELLS 10240
 #endif
+#ifndef RS_L2_CG
+#define RS_L2_CG 1     // L2-path launches gather rows with ld.global.cg (L2 only)
+#endif
 constexpr int kThreads = RS_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = 2 * kThreads;      // poses per tile (upper bound): two per thread in the scan
@@ -92,17 +95,46 @@ __device__ __forceinline__ double ldg_if(const double* p, bool pr) {
       : "+d"(v) : "l"(p), "r"((int)pr));
   return v;
 }
-// one 256-bit read-only load (LDG.E.ENL2.256 on sm_100): a whole 32-byte sector per lane
+// one 256-bit load of a factor row sector on the L2 path (a whole 32-byte sector per lane).
+// CG: ld.global.cg, cached in L2 only (rows of random cells miss L1 anyway: 1-4 % hit rate at
+// C4/C5; the L2-only gather measures 13 % faster, tools/microbench); else ld.global.nc
+// (LDG.E.ENL2.256.CONSTANT, L1-allocating: the window kernels' rare out-of-window poses)
+template <bool CG>
 __device__ __forceinline__ double4 ldg256(const double4* p) {
   double4 v;
-  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  if constexpr (CG)
+    asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  else
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
   return v;
 }
+template <bool CG = false>
 __device__ __forceinline__ float4 ldg256x2(const float4* p, float4& hi) {
   float4 v;
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
-      : "l"(p));
+  if constexpr (CG)
+    asm("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+        : "l"(p));
+  else
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+        : "l"(p));
+  return v;
+}
+// a scalar / 16-byte L2-path load: ld.global.cg when CG (L2 only), else the read-only path
+template <bool CG>
+__device__ __forceinline__ double ldg_l2(const double* p) {
+  double v;
+  if constexpr (CG) asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else v = __ldg(p);
+  return v;
+}
+template <bool CG>
+__device__ __forceinline__ float4 ldg_l2(const float4* p) {
+  float4 v;
+  if constexpr (CG)
+    asm("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else v = __ldg(p);
   return v;
 }
 __device__ __forceinline__ double4 ldg_if(const double4* p, bool pr) {
@@ -193,7 +225,7 @@ struct SmemTree {
 };
 
 // O4 with compile-time R from L2 (unpadded n x R rows); slot c = pair c (no bank structure)
-template <int R>
+template <int R, bool CG = false>
 __device__ __forceinline__ double long_phi_l2(const double2* r0, const double2* r1, const double2* r2) {
   // 32-byte loads (two rank pairs, LDG.E.ENL2.256): a whole L2 sector per lane and request,
   // twice the useful bytes per sector of 16-byte loads when every lane reads its own row
@@ -211,7 +243,7 @@ __device__ __forceinline__ double long_phi_l2(const double2* r0, const double2* 
     const double4* q2 = reinterpret_cast<const double4*>(r2);
 #pragma unroll
     for (int c = 0; c < G::CH / 2; ++c) {
-      const double4 a = ldg256(q0 + c), b = ldg256(q1 + c), cc = ldg256(q2 + c);
+      const double4 a = ldg256<CG>(q0 + c), b = ldg256<CG>(q1 + c), cc = ldg256<CG>(q2 + c);
       s[2 * c] = pair_prod(make_double2(a.x, a.y), make_double2(b.x, b.y), make_double2(cc.x, cc.y));
       s[2 * c + 1] = pair_prod(make_double2(a.z, a.w), make_double2(b.z, b.w), make_double2(cc.z, cc.w));
     }
@@ -222,6 +254,7 @@ __device__ __forceinline__ double long_phi_l2(const double2* r0, const double2* 
 // O4 with a runtime R (generic widths, e.g. tolerance-mode builds): rows from L2, the same
 // pairwise halving tree over rank pairs.  The tree is walked depth-first: its leaves in order
 // are the pairs c = bitrev(j), j = 0..C-1, merged with a binary-counter stack (depth log2 C).
+template <bool CG = false>
 __device__ __forceinline__ double long_phi_rt(const double* r0, const double* r1, const double* r2,
                                               int R) {
   int lg = 0;
@@ -232,9 +265,10 @@ __device__ __forceinline__ double long_phi_rt(const double* r0, const double* r1
   for (int j = 0; j < C; ++j) {
     const int c = lg ? (int)(__brev((unsigned)j) >> (32 - lg)) : 0;
     double q0 = 0.0, q1 = 0.0;
-    if (2 * c < R) q0 = __dmul_rn(__dmul_rn(__ldg(r0 + 2 * c), __ldg(r1 + 2 * c)), __ldg(r2 + 2 * c));
+    if (2 * c < R)
+      q0 = __dmul_rn(__dmul_rn(ldg_l2<CG>(r0 + 2 * c), ldg_l2<CG>(r1 + 2 * c)), ldg_l2<CG>(r2 + 2 * c));
     if (2 * c + 1 < R)
-      q1 = __dmul_rn(__dmul_rn(__ldg(r0 + 2 * c + 1), __ldg(r1 + 2 * c + 1)), __ldg(r2 + 2 * c + 1));
+      q1 = __dmul_rn(__dmul_rn(ldg_l2<CG>(r0 + 2 * c + 1), ldg_l2<CG>(r1 + 2 * c + 1)), ldg_l2<CG>(r2 + 2 * c + 1));
     double v = __dadd_rn(q0, q1);
     for (int t = j; t & 1; t >>= 1) v = __dadd_rn(st[--top], v);
     st[top++] = v;
@@ -285,7 +319,7 @@ struct SmemTree32 {
 };
 
 // L2 path of O4-f32: rows of the packed binary32 copy, quads in natural order
-template <int R>
+template <int R, bool CG = false>
 __device__ __forceinline__ double long_phi_l2_32(const float4* F0, const float4* F1,
                                                  const float4* F2, int i0, int i1, int i2) {
   using G = Geo32<R>;
@@ -303,11 +337,11 @@ __device__ __forceinline__ double long_phi_l2_32(const float4* F0, const float4*
     for (int c = 0; c < G::NS; c += 2) {
       if (c + 1 < G::CH) {
         float4 a1, b1, c1;
-        const float4 a0 = ldg256x2(r0 + c, a1), b0 = ldg256x2(r1 + c, b1), c0 = ldg256x2(r2 + c, c1);
+        const float4 a0 = ldg256x2<CG>(r0 + c, a1), b0 = ldg256x2<CG>(r1 + c, b1), c0 = ldg256x2<CG>(r2 + c, c1);
         s[c] = quad_prod(a0, b0, c0);
         s[c + 1] = quad_prod(a1, b1, c1);
       } else if (c < G::CH) {
-        s[c] = quad_prod(__ldg(r0 + c), __ldg(r1 + c), __ldg(r2 + c));
+        s[c] = quad_prod(ldg_l2<CG>(r0 + c), ldg_l2<CG>(r1 + c), ldg_l2<CG>(r2 + c));
         s[c + 1] = 0.0f;
       } else {
         s[c] = 0.0f;
@@ -1014,16 +1048,16 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
                 if constexpr (F32) phi = long_phi_global32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
                 else phi = long_phi_global<RT>(a.t.F[0], a.t.F[1], a.t.F[2], i0, i1, i2);
               } else if constexpr (F32) {
-                phi = long_phi_l2_32<RT>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
+                phi = long_phi_l2_32<RT, RS_L2_CG != 0>(a.t.Fw32[0], a.t.Fw32[1], a.t.Fw32[2], i0, i1, i2);
               } else {
-                phi = long_phi_l2<RT>((const double2*)(a.t.F[0] + (size_t)i0 * RT),
+                phi = long_phi_l2<RT, RS_L2_CG != 0>((const double2*)(a.t.F[0] + (size_t)i0 * RT),
                                       (const double2*)(a.t.F[1] + (size_t)i1 * RT),
                                       (const double2*)(a.t.F[2] + (size_t)i2 * RT));
               }
             }
           } else if constexpr (RT == 0) {
             if (go)
-              phi = long_phi_rt(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
+              phi = long_phi_rt<RS_L2_CG != 0>(a.t.F[0] + (size_t)i0 * a.R, a.t.F[1] + (size_t)i1 * a.R,
                                 a.t.F[2] + (size_t)i2 * a.R, a.R);
           } else {
             // N5: the long range from the Tucker form, core staged in shared memory
