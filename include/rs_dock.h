@@ -146,8 +146,9 @@ void rs_params_default(rs_params* p);
  * side matrices of the rank-(M x R_l) long-range sum (Eq. (6)), S6 Tucker core, S7 core ->
  * CP of width R (exact canonical-Tucker-canonical when it fits, else CP-ALS), S8 short-range
  * reference rows (Def. 2.1), S9 cell lists for the short-range / vdW pass, S10 upload.
- * Returns NULL on error (invalid argument, atom outside the box, odd n, sigma_split < h,
- * sigma_vdw > dmin_cap, no CUDA device unless RS_FLAG_HOST_ONLY, CUDA or allocation failure).
+ * Returns NULL on error (invalid argument, more than 524,288 atoms (a neighbour-list entry holds
+ * a 19-bit atom index), atom outside the box, odd n, sigma_split < h, sigma_vdw > dmin_cap, no
+ * CUDA device unless RS_FLAG_HOST_ONLY, CUDA or allocation failure).
  */
 rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
                             double box_half_width, const rs_params* params);

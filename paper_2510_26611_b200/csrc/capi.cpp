@@ -125,9 +125,15 @@ int upload_handle(rs_handle* h) {
     // so the few atoms near one pose tile share cache lines); each list entry carries the
     // atom's fine cell (for the integer prefilter) and its sorted index:
     //   nb_range[c] = (first entry, count)       int2 per coarse cell
-    //   nb_ent[j]   = (i0 | i1 << 16, i2, k, 0)  int4 per list entry
-    //   prec[k]     = (x, y, z, q)               double4 per protein atom
+    //   nb_ent[j]   = (i0 | i1 << 15 | (k & 3) << 30, i2 | (k >> 2) << 15, q)  16 bytes per
+    //                 list entry: the fine cell (15 bits per axis, n <= 32768), the sorted
+    //                 index k (19 bits) and the charge (8 bytes), so the H5 term needs no record
+    //   prec[k]     = (x, y, z, q)               double4 per protein atom (the H6 distance)
     const int64_t M = h->M;
+    if (M > rs::kMaxPackedAtoms) {
+      set_err("protein too large for the packed neighbour lists (max 524288 atoms)");
+      return RS_E_INVALID_ARG;
+    }
     std::vector<int64_t> key(M);
     std::vector<int32_t> order(M), rank(M);
     for (int64_t m = 0; m < M; ++m) {
@@ -163,15 +169,37 @@ int upload_handle(rs_handle* h) {
       h->loc4 = tot < ((size_t)1 << 24) && maxcnt < 256;
     }
     std::vector<int32_t> ent(4 * std::max<size_t>(tot, 2), 0);
+    // each list in ascending distance of the atom's fine cell from the coarse cell's centre
+    // (key = |2 i_m - C|^2 in half cells, C = 2^(s+1) c + 2^s - 1; ties by atom index), so the
+    // kernel can end a walk at the first entry too far from the centre to matter
+    const int sh = h->cg.shift;
+    const int cd1 = h->cg.dim[1], cd2 = h->cg.dim[2];
 #pragma omp parallel for schedule(dynamic, 4096)
-    for (int64_t c = 0; c < (int64_t)nc; ++c)
-      for (int32_t u = 0; u < rng[2 * c + 1]; ++u) {
-        const size_t j = (size_t)rng[2 * c] + u;
-        const size_t m = (size_t)h->cg.idx[(size_t)h->cg.off[c] + u];
-        ent[4 * j] = (int32_t)((uint32_t)h->cells[3 * m] | ((uint32_t)h->cells[3 * m + 1] << 16));
-        ent[4 * j + 1] = h->cells[3 * m + 2];
-        ent[4 * j + 2] = rank[m];
+    for (int64_t c = 0; c < (int64_t)nc; ++c) {
+      const int32_t cnt = rng[2 * c + 1];
+      if (cnt == 0) continue;
+      const int64_t cc[3] = {c / ((int64_t)cd1 * cd2) + h->cg.lo[0], (c / cd2) % cd1 + h->cg.lo[1],
+                             c % cd2 + h->cg.lo[2]};
+      std::vector<std::pair<int64_t, int32_t>> lk((size_t)cnt);
+      for (int32_t u = 0; u < cnt; ++u) {
+        const int32_t m = h->cg.idx[(size_t)h->cg.off[c] + u];
+        int64_t key = 0;
+        for (int ax = 0; ax < 3; ++ax) {
+          const int64_t d = 2 * (int64_t)h->cells[3 * (size_t)m + ax] - (cc[ax] * (2 << sh) + (1 << sh) - 1);
+          key += d * d;
+        }
+        lk[(size_t)u] = {key, m};
       }
+      std::sort(lk.begin(), lk.end());
+      for (int32_t u = 0; u < cnt; ++u) {
+        const size_t j = (size_t)rng[2 * c] + u;
+        const size_t m = (size_t)lk[(size_t)u].second;
+        const uint32_t k = (uint32_t)rank[m];
+        ent[4 * j] = (int32_t)((uint32_t)h->cells[3 * m] | ((uint32_t)h->cells[3 * m + 1] << 15) | ((k & 3u) << 30));
+        ent[4 * j + 1] = (int32_t)((uint32_t)h->cells[3 * m + 2] | ((k >> 2) << 15));
+        std::memcpy(&ent[4 * j + 2], &h->z[m], sizeof(double));
+      }
+    }
     if (int e = upload(&h->d_nb_ent, ent, &bytes)) return e;
     h->n_ent = (int64_t)(ent.size() / 4);
     if (int e = upload(&h->d_nb_range, rng, &bytes)) return e;
@@ -395,6 +423,7 @@ rs_handle* rs_build_protein(const double* q, const double* xyz, int64_t n_atoms,
   if (params) prm = *params; else rs_params_default(&prm);
   if (!q || !xyz) { set_err("null input pointer"); return nullptr; }
   if (n_atoms <= 0) { set_err("n_atoms must be > 0"); return nullptr; }
+  if (n_atoms > rs::kMaxPackedAtoms) { set_err("n_atoms exceeds 524288 (19-bit atom index of a list entry)"); return nullptr; }
   if (!(box_half_width > 0) || !std::isfinite(box_half_width)) { set_err("box_half_width must be finite and > 0"); return nullptr; }
   if (prm.grid_n < 2 || (prm.grid_n & 1)) { set_err("grid_n must be even and >= 2"); return nullptr; }
   if (prm.grid_n > 32768) { set_err("grid_n too large (max 32768)"); return nullptr; }
@@ -570,6 +599,7 @@ rs_handle* rs_combine_proteins(const rs_handle* const* parts, int32_t n_parts, i
   int64_t R = 0, M = 0;
   for (int32_t p = 0; p < n_parts; ++p) { R += parts[p]->R; M += parts[p]->M; }
   if (R > (1 << 20)) { set_err("combined CP width exceeds 2^20"); return nullptr; }
+  if (M > rs::kMaxPackedAtoms) { set_err("combined protein exceeds 524288 atoms"); return nullptr; }
   rs_params prm = p0->prm;
   prm.flags = flags;
   if (flags & RS_FLAG_TUCKER_EVAL) { set_err("RS_FLAG_TUCKER_EVAL: a combined handle has no Tucker form"); return nullptr; }

@@ -159,7 +159,7 @@ struct DeviceTables {
   const int2* nb_range = nullptr;     // per coarse cell: (list begin, count)
   const unsigned* nb_pack = nullptr;  // loc4 handles: begin | count << 24, z padded to nb_dim2p
   const double* S[3] = {nullptr, nullptr, nullptr};
-  const int4* nb_ent = nullptr;       // per list entry: (i0 | i1 << 16, i2, sorted atom, 0)
+  const int4* nb_ent = nullptr;       // per list entry: fine cell + sorted atom (packed), charge
   const double4* prec = nullptr;      // per sorted protein atom: (x, y, z, q)
   const double* short_memo = nullptr; // s(|D0|,|D1|,|D2|) for |D_a| <= n_sigma, or null
   const double* Ut[3] = {nullptr, nullptr, nullptr};  // Tucker bases n x r_l, row-major (N5)
@@ -202,6 +202,7 @@ struct ScoreArgs {               // one launch of the scoring kernel
 int launch_fill_short_memo(const double* S0, const double* S1, const double* S2, int Rs,
                            int n_sigma, double* out, void* stream);
 
+constexpr int64_t kMaxPackedAtoms = (int64_t)1 << 19;   // sorted atom index: 19 bits of a list entry
 constexpr int kWorkSlots = 64;   // work counters per handle, each reused behind its last launch
 constexpr int kPackPad = 24;     // zero cells before each axis of the packed range table (TMA)
 

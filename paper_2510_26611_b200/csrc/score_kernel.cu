@@ -468,29 +468,21 @@ __device__ __forceinline__ double short_value(const ScoreArgs& a, int e0, int e1
                                                  (uint64_t)idx * 8u), pr);
 }
 
-// One candidate list entry en = (i0 | i1 << 16, i2, sorted atom k) against the atom's cell
-// (c0, c1, c2): the squared integer offset (cells are < 2^15, so it sums exactly in 32 bits)
+// One candidate list entry en = (i0 | i1 << 15 | (k & 3) << 30, i2 | (k >> 2) << 15, q) against
+// the atom's cell (c0, c1, c2): the squared integer offset (cells are < 2^15, so it sums
+// exactly in 32 bits)
 __device__ __forceinline__ unsigned entry_dd(int c0, int c1, int c2, const int4 en, int& e0, int& e1,
                                              int& e2) {
-  e0 = c0 - (en.x & 0xffff);
-  e1 = c1 - (int)((unsigned)en.x >> 16);
-  e2 = c2 - en.y;
+  e0 = c0 - (en.x & 0x7fff);
+  e1 = c1 - (int)(((unsigned)en.x >> 15) & 0x7fffu);
+  e2 = c2 - (en.y & 0x7fff);
   return (unsigned)(e0 * e0) + (unsigned)(e1 * e1) + (unsigned)(e2 * e2);
 }
-
-// H5 + H6 for one candidate whose record r = (x, y, z, q) was loaded: O7 distance when the
-// integer prefilter admits it, O5 replica term inside the n_sigma ball
-__device__ __forceinline__ void pair_term(const ScoreArgs& a, double x0, double x1, double x2,
-                                          double z, unsigned dd, double sv, const double4 r,
-                                          double& hi, double& lo, double& best) {
-  if (dd < a.vdw_cells2) {
-    const double dx0 = __dsub_rn(x0, r.x);
-    const double dx1 = __dsub_rn(x1, r.y);
-    const double dx2 = __dsub_rn(x2, r.z);
-    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx0, dx0), __dmul_rn(dx1, dx1)), __dmul_rn(dx2, dx2));
-    best = d2 < best ? d2 : best;
-  }
-  if (dd <= a.ns2) dd_add_prod(hi, lo, z, __dmul_rn(r.w, sv));
+__device__ __forceinline__ unsigned entry_k(const int4 en) {   // the sorted atom index
+  return (((unsigned)en.y >> 15) << 2) | ((unsigned)en.x >> 30);
+}
+__device__ __forceinline__ double entry_q(const int4 en) {     // the atom's charge z_m
+  return __hiloint2double(en.w, en.z);
 }
 
 // H6 for one candidate with record r (loaded iff hit): O7 distance, keep the minimum
@@ -503,31 +495,85 @@ __device__ __forceinline__ void pair_hit(double x0, double x1, double x2, const 
   best = (hit && d2 < best) ? d2 : best;
 }
 
+// The integer prefilter of H6 tightened to the lane's running minimum: a pair with
+// |x_l - x_m|^2 < best has |D| <= |x_l - x_m| inv_h + sqrt 3 cells, so only entries with
+// |D|^2 below ceil((sqrt(best) inv_h + sqrt 3 + 2)^2) (the static bound's 2-cell margin) can
+// lower it; capped at the static bound vdw_cells2 (D_cap).  The minimum is order-free (O7), so
+// skipping the others changes no result.
+#ifndef RS_DYN_THR
+#define RS_DYN_THR 2   // 0: static D_cap bound only; 1: fp64 sqrt; 2: binary32 bound (rounded up)
+#endif
+__device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
+#if RS_DYN_THR == 1
+  const double t = __dadd_rn(__dmul_rn(__dsqrt_rn(best), a.inv_h), 3.7320508075688772);
+  const double t2 = __dmul_rn(t, t);
+  return t2 < (double)a.vdw_cells2 ? (unsigned)ceil(t2) + 1u : a.vdw_cells2;
+#else
+  // every binary32 step rounded up: t >= sqrt(best) inv_h + sqrt 3 + 2, so the bound stays
+  // conservative (the 2-cell margin is far above binary32 rounding anyway)
+  const float bf = __double2float_ru(best);
+  const float t = __fadd_ru(__fmul_ru(__fsqrt_ru(bf), __double2float_ru(a.inv_h)), 3.7320509f);
+  const float t2 = __fmul_ru(t, t);
+  return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
+#endif
+}
+
+#ifndef RS_EARLY_STOP
+#define RS_EARLY_STOP 1
+#endif
+// Early end of a candidate walk.  Every list is sorted by key = |2 i_m - C|^2 (half cells, C
+// the coarse cell's centre; rs_build_protein).  The atom's cell a lies within (2^s - 1) sqrt 3
+// half cells of C, so an entry the walk still needs (|i_m - a|^2 <= max(ns2, vthr)) has
+// key <= (2 sqrt(max(ns2, vthr)) + (2^s - 1) sqrt 3)^2: the first entry above that bound ends
+// the walk (binary32, every step rounded up, plus 2).
+__device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) {
+  const float T = (float)max(a.ns2, vthr);
+  const float r = __fadd_ru(__fmul_ru(2.0f, __fsqrt_ru(T)),
+                            __fmul_ru((float)((1 << a.nb_shift) - 1), 1.7320509f));
+  const float r2 = __fmul_ru(r, r);
+  return r2 < 4.0e9f ? (unsigned)r2 + 2u : 0xffffffffu;
+}
+// the key of entry en for an atom in cell (c0, c1, c2) whose offsets to the entry are e
+__device__ __forceinline__ unsigned entry_key(const ScoreArgs& a, int c0, int c1, int c2, int e0, int e1,
+                                              int e2) {
+  const int s = a.nb_shift, off = (1 << s) - 1;
+  const int k0 = 2 * (c0 - e0) - ((c0 >> s) * (2 << s) + off);
+  const int k1 = 2 * (c1 - e1) - ((c1 >> s) * (2 << s) + off);
+  const int k2 = 2 * (c2 - e2) - ((c2 >> s) * (2 << s) + off);
+  return (unsigned)(k0 * k0) + (unsigned)(k1 * k1) + (unsigned)(k2 * k2);
+}
+
 // H5 + H6 for two candidate list entries of one ligand atom (cell c0..c2, coordinates
 // x0..x2, charge z); a0/a1: the entries are real candidates.  The integer prefilter on the
-// cell offset decides whether the protein record (O7 distance) and the memo value (O5 replica
-// term inside the n_sigma ball) are loaded at all.
+// cell offset decides whether the memo value (O5 replica term inside the n_sigma ball, with
+// the charge from the entry) and the protein record (O7 distance, only while the pair can
+// still lower the lane's minimum: vthr) are loaded at all.
 __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x1, double x2,
                                          double z, int c0, int c1, int c2, const int4 en0,
                                          const int4 en1, bool a0, bool a1, double& hi, double& lo,
-                                         double& best) {
+                                         double& best, unsigned vthr, unsigned stopk, bool& end) {
   int e00, e01, e02, e10, e11, e12;
   unsigned dd0 = entry_dd(c0, c1, c2, en0, e00, e01, e02);
   unsigned dd1 = entry_dd(c0, c1, c2, en1, e10, e11, e12);
+#if RS_EARLY_STOP
+  end = a1 && entry_key(a, c0, c1, c2, e10, e11, e12) > stopk;
+#else
+  end = false;
+#endif
   dd0 = a0 ? dd0 : 0xffffffffu;
   dd1 = a1 ? dd1 : 0xffffffffu;
   const bool sr0 = dd0 <= a.ns2, sr1 = dd1 <= a.ns2;
-  const bool v0 = dd0 < a.vdw_cells2, v1 = dd1 < a.vdw_cells2;
-  RS_DCHECK(!(sr0 || v0) || (en0.z >= 0 && en0.z < a.n_prot));
-  RS_DCHECK(!(sr1 || v1) || (en1.z >= 0 && en1.z < a.n_prot));
-  const double4 rc0 = ldg_d4_p(a.t.prec + en0.z, sr0 || v0);
-  const double4 rc1 = ldg_d4_p(a.t.prec + en1.z, sr1 || v1);
+  const bool v0 = dd0 < vthr, v1 = dd1 < vthr;
+  RS_DCHECK(!v0 || entry_k(en0) < (unsigned)a.n_prot);
+  RS_DCHECK(!v1 || entry_k(en1) < (unsigned)a.n_prot);
+  const double4 rc0 = ldg_d4_p(a.t.prec + entry_k(en0), v0);
+  const double4 rc1 = ldg_d4_p(a.t.prec + entry_k(en1), v1);
   const double sv0 = short_value(a, e00, e01, e02, sr0);
   const double sv1 = short_value(a, e10, e11, e12, sr1);
   pair_hit(x0, x1, x2, rc0, v0, best);
   pair_hit(x0, x1, x2, rc1, v1, best);
-  if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(rc0.w, sv0));
-  if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(rc1.w, sv1));
+  if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(entry_q(en0), sv0));
+  if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(entry_q(en1), sv1));
 }
 
 #ifndef RS_NQ
@@ -535,12 +581,26 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
 #endif
 constexpr int kNQ = RS_NQ;   // per-lane stack of atoms waiting for their candidate walk
 
+#ifndef RS_QCOMPACT
+#define RS_QCOMPACT 0
+#endif
+#ifndef RS_LIG_OUTER
+#define RS_LIG_OUTER 1
+#endif
 // Per-warp neighbour queues: atoms whose candidates a lane has not started yet
+#if RS_QCOMPACT
+// (atom, first entry, end entry): x' and the cell are recomputed from the lane's pose when the
+// atom is popped (the same H2/H3 op sequence, so bitwise the values the atom step had)
+struct __align__(16) NbrQueue {
+  int4 cb[kNQ][32];
+};
+#else
 struct __align__(16) NbrQueue {
   double2 x01[kNQ][32];   // x'_0, x'_1
   double2 x2z[kNQ][32];   // x'_2, charge
   int4 cb[kNQ][32];       // i0 | i1 << 16, i2, first entry, end entry
 };
+#endif
 
 
 constexpr size_t kQueueBytes = sizeof(NbrQueue) * kWarps;   // dynamic shared memory
@@ -592,6 +652,32 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) r2 = fmax(r2, __shfl_xor_sync(kFull, r2, off));
   if (lane == 0) s_rmax2[warp] = r2;
+#if RS_LIG_OUTER
+  // atoms in descending |y| (ties: lower index first): the outer atoms, which meet the protein,
+  // come first, so their queued candidate walks overlap the inner atoms' steps instead of a
+  // drain after the last atom (the O6 sums are order-free)
+  if (a.L > 1 && a.L <= lig_smem_n && a.L <= kThreads) {
+    __syncthreads();
+    double4* tmp = reinterpret_cast<double4*>(s_nq);   // the queues are unused until the units
+    if (tid < a.L) {
+      const double2 v0 = s_lig[tid], v1 = s_lig[lig_smem_n + tid];
+      const double r = v0.x * v0.x + v0.y * v0.y + v1.x * v1.x;
+      int rk = 0;
+      for (int j = 0; j < (int)a.L; ++j) {
+        const double2 w0 = s_lig[j], w1 = s_lig[lig_smem_n + j];
+        const double rj = w0.x * w0.x + w0.y * w0.y + w1.x * w1.x;
+        rk += (rj > r || (rj == r && j < tid)) ? 1 : 0;
+      }
+      tmp[rk] = make_double4(v0.x, v0.y, v1.x, v1.y);
+    }
+    __syncthreads();
+    if (tid < a.L) {
+      const double4 v = tmp[tid];
+      s_lig[tid] = make_double2(v.x, v.y);
+      s_lig[lig_smem_n + tid] = make_double2(v.z, v.w);
+    }
+  }
+#endif
   if (tid == 0) {
     s_cur.lo[0] = s_cur.lo[1] = s_cur.lo[2] = 1;
     s_cur.hi[0] = s_cur.hi[1] = s_cur.hi[2] = 0;   // empty
@@ -947,6 +1033,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         const bool live = has && ok;
         bool bad = has && !ok;
         double hi = 0.0, lo = 0.0, best = INFINITY;
+        unsigned vthr = a.vdw_cells2;
+        unsigned stopk = stop_key(a, vthr);
+        double bthr = INFINITY;   // the minimum the bounds were computed from
         const int nsteps = (L + S - 1) >> lgS;
         // H5 + H6 as a per-lane queue: a lane walks the candidate list of one atom at a time, two
         // entries per atom step, while later atoms with candidates wait on its stack; the entry
@@ -955,18 +1044,58 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         int qc01 = 0, qc2 = 0, qpos = 0, qend = 0, qfc = 0;
         int4 pf0 = make_int4(0, 0, 0, 0), pf1 = pf0;
         NbrQueue& nq = s_nq[warp];
+        // the ligand atom lc (body frame y, charge z), from shared memory when staged
+        auto lig_atom = [&](int lc, double& y0, double& y1, double& y2, double& z) {
+          if (lig_all_smem) {
+            RS_DCHECK(lc >= 0 && lc < lig_smem_n);
+            const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
+            y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
+          } else {
+            y0 = __ldg(a.yl + 3 * (int64_t)lc);
+            y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
+            y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
+            z = __ldg(a.zl + lc);
+          }
+        };
+        // H2 (O2): x' = R y + t, the pose's R and t in registers
+        auto h2 = [&](double y0, double y1, double y2, double& x0, double& x1, double& x2) {
+          x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
+          x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
+          x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
+        };
         auto nbr_step = [&]() {
           const bool act = qpos < qend;
           if (__any_sync(kFull, act)) {
+#if RS_DYN_THR
+            // the bounds follow the lane's minimum lazily: it may have moved in the previous
+            // round, whose record loads have landed behind the atom step since (a branch on this
+            // round's records would stall the warp before its H4 gathers)
+            if (best < bthr) {
+              bthr = best;
+              vthr = vdw_thr(a, best);
+              stopk = stop_key(a, vthr);
+            }
+#endif
+            bool end;
             nbr_pair(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, pf1, act,
-                     qpos + 1 < qend, hi, lo, best);
-            qpos += 2;
+                     qpos + 1 < qend, hi, lo, best, vthr, stopk, end);
+            qpos = end ? qend : qpos + 2;
             if (act && qpos >= qend && qfc > 0) {
               --qfc;
+#if RS_QCOMPACT
+              const int4 cb = nq.cb[qfc][lane];
+              double y0, y1, y2;
+              lig_atom(cb.x, y0, y1, y2, qz);
+              h2(y0, y1, y2, q0, q1, q2);
+              qc01 = snap_dev(q0, a.b, a.inv_h, nm1) | (snap_dev(q1, a.b, a.inv_h, nm1) << 16);
+              qc2 = snap_dev(q2, a.b, a.inv_h, nm1);
+              qpos = cb.y; qend = cb.z;
+#else
               const double2 v01 = nq.x01[qfc][lane], v2z = nq.x2z[qfc][lane];
               const int4 cb = nq.cb[qfc][lane];
               q0 = v01.x; q1 = v01.y; q2 = v2z.x; qz = v2z.y;
               qc01 = cb.x; qc2 = cb.y; qpos = cb.z; qend = cb.w;
+#endif
             }
             const bool more = qpos < qend;
             RS_DCHECK(!more || (qpos >= 0 && qpos + 2 <= a.n_ent));
@@ -986,20 +1115,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           const bool act = live && l < L;
           const int lc = l < L ? l : L - 1;
           double y0, y1, y2, z;
-          if (lig_all_smem) {
-            RS_DCHECK(lc >= 0 && lc < lig_smem_n);
-            const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
-            y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
-          } else {
-            y0 = __ldg(a.yl + 3 * (int64_t)lc);
-            y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
-            y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
-            z = __ldg(a.zl + lc);
-          }
+          lig_atom(lc, y0, y1, y2, z);
           // H2 (O2)
-          const double x0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[0], y0), __dmul_rn(Rm[1], y1)), __dmul_rn(Rm[2], y2)), tv[0]);
-          const double x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
-          const double x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
+          double x0, x1, x2;
+          h2(y0, y1, y2, x0, x1, x2);
           // H3 (O3): valid iff -b <= x'_a <= b on every axis (false for NaN)
           const bool inb = fabs(x0) <= a.b && fabs(x1) <= a.b && fabs(x2) <= a.b;
           bad = bad || (act && !inb);
@@ -1043,9 +1162,13 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               ldg_pair_p(a.t.nb_ent + beg, true, pf0, pf1);
             } else {
               RS_DCHECK(qfc < kNQ);
+#if RS_QCOMPACT
+              nq.cb[qfc][lane] = make_int4(lc, beg, beg + cnt, 0);
+#else
               nq.x01[qfc][lane] = make_double2(x0, x1);
               nq.x2z[qfc][lane] = make_double2(x2, z);
               nq.cb[qfc][lane] = make_int4(i0 | (i1 << 16), i2, beg, beg + cnt);
+#endif
               ++qfc;
             }
           }
@@ -1092,6 +1215,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           const double zg = go ? z : 0.0;
           dd_add_prod(hi, lo, zg, phi);
         }
+        // after the last atom, walk until every lane is done: the pose's R and t are dead here,
+        // so a drain round takes two entry pairs (both loaded a round ahead) against one record
+        // latency, where the atom-step rounds take one
         // H7: merge the S lanes of each pose (xor butterfly within aligned groups of S lanes;
         // TwoSum is exact, so partners agree); min d^2 and the invalid flag likewise
         for (int off = S >> 1; off > 0; off >>= 1) {

@@ -407,6 +407,9 @@ int main(void) {
   rs_free(h);
   p.grid_n = 31;
   if (rs_build_protein(q, xyz, 3, 8.0, &p) != NULL) return 5;
+  /* a list entry holds a 19-bit atom index: larger proteins are refused up front */
+  p.grid_n = 32;
+  if (rs_build_protein(q, xyz, 524289, 8.0, &p) != NULL) return 6;
   printf("ok %d %.3e\n", info.R, F1[0]);
   free(F1);
   return 0;
