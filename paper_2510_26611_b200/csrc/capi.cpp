@@ -316,6 +316,17 @@ rs::ScoreArgs base_args(const rs_handle* h) {
     // |x_l - x_m| >= (|D| - sqrt 3) h for cells D apart; +2 cells of margin for snap rounding
     const double t = h->prm.dmin_cap / h->h + std::sqrt(3.0) + 2.0;
     a.vdw_cells2 = (unsigned)std::min(std::ceil(t * t), 4294967295.0);
+    // the kernel's running bounds without a square root: (sqrt(x) c1 + c2)^2 <=
+    // (1 + e) c1^2 x + (1 + 1/e) c2^2 for any e > 0 (AM-GM on the cross term), e = 1/4, each
+    // coefficient rounded up to binary32 plus a relative 1e-6 (the kernel adds 2 after its
+    // rounded-up evaluation)
+    const double c2 = std::sqrt(3.0) + 2.0;
+    const double up = 1.0 + 1e-6;
+    a.thr_a = std::nextafter((float)(1.25 * h->inv_h * h->inv_h * up), INFINITY);
+    a.thr_b = std::nextafter((float)(5.0 * c2 * c2 * up), INFINITY);
+    const double kc = double((1 << h->cg.shift) - 1) * std::sqrt(3.0);
+    a.stop_a = std::nextafter((float)(5.0 * up), INFINITY);   // (2 sqrt T + kc)^2 <= 5 T + 5 kc^2
+    a.stop_b = std::nextafter((float)(5.0 * kc * kc * up), INFINITY);
   }
   a.rmax_hint = -1.0;
   return a;

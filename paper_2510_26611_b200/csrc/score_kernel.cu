@@ -509,11 +509,9 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
   const double t2 = __dmul_rn(t, t);
   return t2 < (double)a.vdw_cells2 ? (unsigned)ceil(t2) + 1u : a.vdw_cells2;
 #else
-  // every binary32 step rounded up: t >= sqrt(best) inv_h + sqrt 3 + 2, so the bound stays
-  // conservative (the 2-cell margin is far above binary32 rounding anyway)
-  const float bf = __double2float_ru(best);
-  const float t = __fadd_ru(__fmul_ru(__fsqrt_ru(bf), __double2float_ru(a.inv_h)), 3.7320509f);
-  const float t2 = __fmul_ru(t, t);
+  // (sqrt(best) inv_h + sqrt 3 + 2)^2 <= thr_a best + thr_b (host: AM-GM, rounded up), in
+  // binary32 with every step rounded up: no square root on the hot path
+  const float t2 = __fadd_ru(__fmul_ru(__double2float_ru(best), a.thr_a), a.thr_b);
   return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
 #endif
 }
@@ -524,13 +522,10 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
 // Early end of a candidate walk.  Every list is sorted by key = |2 i_m - C|^2 (half cells, C
 // the coarse cell's centre; rs_build_protein).  The atom's cell a lies within (2^s - 1) sqrt 3
 // half cells of C, so an entry the walk still needs (|i_m - a|^2 <= max(ns2, vthr)) has
-// key <= (2 sqrt(max(ns2, vthr)) + (2^s - 1) sqrt 3)^2: the first entry above that bound ends
-// the walk (binary32, every step rounded up, plus 2).
+// key <= (2 sqrt(max(ns2, vthr)) + (2^s - 1) sqrt 3)^2 <= stop_a max(ns2, vthr) + stop_b
+// (host: AM-GM, rounded up): the first entry above that bound ends the walk.
 __device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) {
-  const float T = (float)max(a.ns2, vthr);
-  const float r = __fadd_ru(__fmul_ru(2.0f, __fsqrt_ru(T)),
-                            __fmul_ru((float)((1 << a.nb_shift) - 1), 1.7320509f));
-  const float r2 = __fmul_ru(r, r);
+  const float r2 = __fadd_ru(__fmul_ru((float)max(a.ns2, vthr), a.stop_a), a.stop_b);
   return r2 < 4.0e9f ? (unsigned)r2 + 2u : 0xffffffffu;
 }
 // the key of entry en for an atom in cell (c0, c1, c2) whose offsets to the entry are e
@@ -543,6 +538,20 @@ __device__ __forceinline__ unsigned entry_key(const ScoreArgs& a, int c0, int c1
   return (unsigned)(k0 * k0) + (unsigned)(k1 * k1) + (unsigned)(k2 * k2);
 }
 
+#ifndef RS_DEFER_BALL
+#define RS_DEFER_BALL 0
+#endif
+// O5 terms of a round whose memo values are still in flight: added one round later
+struct BallPending {
+  double q0, q1, sv0, sv1, z;
+  int f;   // bit 0 / 1: entry 0 / 1 is inside the n_sigma ball
+};
+__device__ __forceinline__ void ball_flush(BallPending& pd, double& hi, double& lo) {
+  if (pd.f & 1) dd_add_prod(hi, lo, pd.z, __dmul_rn(pd.q0, pd.sv0));
+  if (pd.f & 2) dd_add_prod(hi, lo, pd.z, __dmul_rn(pd.q1, pd.sv1));
+  pd.f = 0;
+}
+
 // H5 + H6 for two candidate list entries of one ligand atom (cell c0..c2, coordinates
 // x0..x2, charge z); a0/a1: the entries are real candidates.  The integer prefilter on the
 // cell offset decides whether the memo value (O5 replica term inside the n_sigma ball, with
@@ -551,7 +560,8 @@ __device__ __forceinline__ unsigned entry_key(const ScoreArgs& a, int c0, int c1
 __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x1, double x2,
                                          double z, int c0, int c1, int c2, const int4 en0,
                                          const int4 en1, bool a0, bool a1, double& hi, double& lo,
-                                         double& best, unsigned vthr, unsigned stopk, bool& end) {
+                                         double& best, unsigned vthr, unsigned stopk, bool& end,
+                                         BallPending& pd) {
   int e00, e01, e02, e10, e11, e12;
   unsigned dd0 = entry_dd(c0, c1, c2, en0, e00, e01, e02);
   unsigned dd1 = entry_dd(c0, c1, c2, en1, e10, e11, e12);
@@ -572,8 +582,14 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   const double sv1 = short_value(a, e10, e11, e12, sr1);
   pair_hit(x0, x1, x2, rc0, v0, best);
   pair_hit(x0, x1, x2, rc1, v1, best);
+#if RS_DEFER_BALL
+  // the O5 terms wait for the next round (their memo values land behind the atom step)
+  pd.q0 = entry_q(en0); pd.q1 = entry_q(en1); pd.sv0 = sv0; pd.sv1 = sv1; pd.z = z;
+  pd.f = (sr0 ? 1 : 0) | (sr1 ? 2 : 0);
+#else
   if (sr0) dd_add_prod(hi, lo, z, __dmul_rn(entry_q(en0), sv0));
   if (sr1) dd_add_prod(hi, lo, z, __dmul_rn(entry_q(en1), sv1));
+#endif
 }
 
 #ifndef RS_NQ
@@ -1036,6 +1052,8 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         unsigned vthr = a.vdw_cells2;
         unsigned stopk = stop_key(a, vthr);
         double bthr = INFINITY;   // the minimum the bounds were computed from
+        BallPending bp;
+        bp.f = 0;
         const int nsteps = (L + S - 1) >> lgS;
         // H5 + H6 as a per-lane queue: a lane walks the candidate list of one atom at a time, two
         // entries per atom step, while later atoms with candidates wait on its stack; the entry
@@ -1077,8 +1095,11 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             }
 #endif
             bool end;
+#if RS_DEFER_BALL
+            ball_flush(bp, hi, lo);
+#endif
             nbr_pair(a, q0, q1, q2, qz, qc01 & 0xffff, (int)((unsigned)qc01 >> 16), qc2, pf0, pf1, act,
-                     qpos + 1 < qend, hi, lo, best, vthr, stopk, end);
+                     qpos + 1 < qend, hi, lo, best, vthr, stopk, end, bp);
             qpos = end ? qend : qpos + 2;
             if (act && qpos >= qend && qfc > 0) {
               --qfc;
@@ -1218,6 +1239,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         // after the last atom, walk until every lane is done: the pose's R and t are dead here,
         // so a drain round takes two entry pairs (both loaded a round ahead) against one record
         // latency, where the atom-step rounds take one
+#if RS_DEFER_BALL
+        ball_flush(bp, hi, lo);
+#endif
         // H7: merge the S lanes of each pose (xor butterfly within aligned groups of S lanes;
         // TwoSum is exact, so partners agree); min d^2 and the invalid flag likewise
         for (int off = S >> 1; off > 0; off >>= 1) {
