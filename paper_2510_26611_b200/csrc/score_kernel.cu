@@ -73,7 +73,7 @@ constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 #define RS_TAIL_DIV 8
 #endif
 #ifndef RS_TAIL_CHUNK
-#define RS_TAIL_CHUNK 128
+#define RS_TAIL_CHUNK 256
 #endif
 constexpr int kTailChunk = RS_TAIL_CHUNK;  // chunk size over the last 1/RS_TAIL_DIV of the poses
 constexpr unsigned kFull = 0xffffffffu;
@@ -508,6 +508,20 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
   const double t = __dadd_rn(__dmul_rn(__dsqrt_rn(best), a.inv_h), 3.7320508075688772);
   const double t2 = __dmul_rn(t, t);
   return t2 < (double)a.vdw_cells2 ? (unsigned)ceil(t2) + 1u : a.vdw_cells2;
+#elif RS_DYN_THR == 4
+  // as 3 with the hardware's approximate square root (relative error <= 2^-22, covered by the
+  // factor 1 + 2^-20 and the roundings up)
+  float sq;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(__double2float_ru(best)));
+  const float t = __fadd_ru(__fmul_ru(__fmul_ru(sq, 1.00000095367431640625f), a.thr_s), a.thr_c);
+  const float t2 = __fmul_ru(t, t);
+  return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
+#elif RS_DYN_THR == 3
+  // (sqrt(best) inv_h + sqrt 3 + 2)^2 in binary32, every step rounded up (thr_s = inv_h and
+  // thr_c = sqrt 3 + 2 rounded up on the host); evaluated only when the minimum moved
+  const float t = __fadd_ru(__fmul_ru(__fsqrt_ru(__double2float_ru(best)), a.thr_s), a.thr_c);
+  const float t2 = __fmul_ru(t, t);
+  return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
 #else
   // (sqrt(best) inv_h + sqrt 3 + 2)^2 <= thr_a best + thr_b (host: AM-GM, rounded up), in
   // binary32 with every step rounded up: no square root on the hot path
@@ -524,7 +538,19 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
 // half cells of C, so an entry the walk still needs (|i_m - a|^2 <= max(ns2, vthr)) has
 // key <= (2 sqrt(max(ns2, vthr)) + (2^s - 1) sqrt 3)^2 <= stop_a max(ns2, vthr) + stop_b
 // (host: AM-GM, rounded up): the first entry above that bound ends the walk.
+#ifndef RS_STOP_EXACT
+#define RS_STOP_EXACT 1
+#endif
+// RS_STOP_EXACT: the bound with the atom's own offset from the centre instead of the worst
+// case.  With rho^2 = max(ns2, vthr), A = 2 a - C (|A_r| <= 2^s - 1) and delta = |A|, a needed
+// entry has key <= (2 rho + delta)^2, i.e. the walk ends at the first entry with
+// key - 4 rho^2 - delta^2 > 4 rho delta, tested exactly in integers (both sides squared);
+// stop_key returns 4 rho^2 (saturated: no early end when it does not fit 32 bits).
 __device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) {
+#if RS_STOP_EXACT
+  const unsigned m = max(a.ns2, vthr);
+  return m < 0x40000000u ? 4u * m : 0xffffffffu;
+#endif
   const float r2 = __fadd_ru(__fmul_ru((float)max(a.ns2, vthr), a.stop_a), a.stop_b);
   return r2 < 4.0e9f ? (unsigned)r2 + 2u : 0xffffffffu;
 }
@@ -540,6 +566,18 @@ __device__ __forceinline__ unsigned entry_key(const ScoreArgs& a, int c0, int c1
 
 #ifndef RS_DEFER_BALL
 #define RS_DEFER_BALL 0
+#endif
+#ifndef RS_PF_POSES
+#define RS_PF_POSES 0   // 1: bulk L2 prefetch of the next tile's poses
+#endif
+#ifndef RS_VOTE_MASK
+#define RS_VOTE_MASK 0
+#endif
+#ifndef RS_HIT_VOTE
+#define RS_HIT_VOTE 0   // 1: the O7 distances of a round only when some lane's prefilter passed
+#endif
+#ifndef RS_LIG_CALL
+#define RS_LIG_CALL 1   // 1: ligand atoms beyond the staged ones through an out-of-line load
 #endif
 // O5 terms of a round whose memo values are still in flight: added one round later
 struct BallPending {
@@ -565,7 +603,18 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   int e00, e01, e02, e10, e11, e12;
   unsigned dd0 = entry_dd(c0, c1, c2, en0, e00, e01, e02);
   unsigned dd1 = entry_dd(c0, c1, c2, en1, e10, e11, e12);
-#if RS_EARLY_STOP
+#if RS_EARLY_STOP && RS_STOP_EXACT
+  {
+    const int msk = (1 << a.nb_shift) - 1;
+    const int A0 = 2 * (c0 & msk) - msk, A1 = 2 * (c1 & msk) - msk, A2 = 2 * (c2 & msk) - msk;
+    const int k0 = A0 - 2 * e10, k1 = A1 - 2 * e11, k2 = A2 - 2 * e12;   // 2 i_m - C
+    const unsigned key = (unsigned)(k0 * k0) + (unsigned)(k1 * k1) + (unsigned)(k2 * k2);
+    const unsigned d2 = (unsigned)(A0 * A0) + (unsigned)(A1 * A1) + (unsigned)(A2 * A2);
+    const unsigned t = key - stopk, u = t - d2;
+    end = a1 && key > stopk && t > d2 &&
+          (unsigned long long)u * u > (((unsigned long long)stopk * d2) << 2);
+  }
+#elif RS_EARLY_STOP
   end = a1 && entry_key(a, c0, c1, c2, e10, e11, e12) > stopk;
 #else
   end = false;
@@ -580,8 +629,15 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   const double4 rc1 = ldg_d4_p(a.t.prec + entry_k(en1), v1);
   const double sv0 = short_value(a, e00, e01, e02, sr0);
   const double sv1 = short_value(a, e10, e11, e12, sr1);
+#if RS_HIT_VOTE
+  if (__any_sync(kFull, v0 || v1)) {
+    pair_hit(x0, x1, x2, rc0, v0, best);
+    pair_hit(x0, x1, x2, rc1, v1, best);
+  }
+#else
   pair_hit(x0, x1, x2, rc0, v0, best);
   pair_hit(x0, x1, x2, rc1, v1, best);
+#endif
 #if RS_DEFER_BALL
   // the O5 terms wait for the next round (their memo values land behind the atom step)
   pd.q0 = entry_q(en0); pd.q1 = entry_q(en1); pd.sv0 = sv0; pd.sv1 = sv1; pd.z = z;
@@ -620,6 +676,14 @@ struct __align__(16) NbrQueue {
 
 
 constexpr size_t kQueueBytes = sizeof(NbrQueue) * kWarps;   // dynamic shared memory
+
+// ligand atom lc from global memory (atoms beyond the shared-memory staging): out of line, so the
+// staged case pays one branch instead of the predicated-off loads
+__device__ __noinline__ double4 lig_atom_global(const double* __restrict__ yl,
+                                                const double* __restrict__ zl, int lc) {
+  return make_double4(__ldg(yl + 3 * (int64_t)lc), __ldg(yl + 3 * (int64_t)lc + 1),
+                      __ldg(yl + 3 * (int64_t)lc + 2), __ldg(zl + lc));
+}
 
 __device__ __forceinline__ int pow2_floor(int v) {   // v >= 1
   return 1 << (31 - __clz(v));
@@ -993,6 +1057,17 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         mbar_wait(&s_bar, phase);
         phase ^= 1;
       }
+#if RS_PF_POSES
+      // the next tile's poses towards L2 while this tile computes (one bulk prefetch; only inside
+      // the chunk, whose poses have landed)
+      if (tid == 32) {
+        const int64_t e = p + T + kTile < p_end ? p + T + kTile : p_end;
+        const uintptr_t b0 = (reinterpret_cast<uintptr_t>(a.poses + 7 * (p + T)) + 15u) & ~(uintptr_t)15u;
+        const uintptr_t b1 = reinterpret_cast<uintptr_t>(a.poses + 7 * e) & ~(uintptr_t)15u;
+        if (b1 > b0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0)) : "memory");
+      }
+#endif
       const bool use_win = window_mode && fits;
       // per-lane window row bases (shared addresses, with the lane's XOR offset in bits 4..)
       unsigned wb0, wb1, wb2;
@@ -1069,10 +1144,15 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
             y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
           } else {
+#if RS_LIG_CALL
+            const double4 v = lig_atom_global(a.yl, a.zl, lc);
+            y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
+#else
             y0 = __ldg(a.yl + 3 * (int64_t)lc);
             y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
             y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
             z = __ldg(a.zl + lc);
+#endif
           }
         };
         // H2 (O2): x' = R y + t, the pose's R and t in registers
@@ -1081,9 +1161,17 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           x1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[3], y0), __dmul_rn(Rm[4], y1)), __dmul_rn(Rm[5], y2)), tv[1]);
           x2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(Rm[6], y0), __dmul_rn(Rm[7], y1)), __dmul_rn(Rm[8], y2)), tv[2]);
         };
+#if RS_VOTE_MASK
+        unsigned am = 0;   // lanes with a walk in progress (kept across the loop: one ballot per
+                           // round and per atom step instead of a vote before every decision)
+#endif
         auto nbr_step = [&]() {
           const bool act = qpos < qend;
+#if RS_VOTE_MASK
+          if (am) {
+#else
           if (__any_sync(kFull, act)) {
+#endif
 #if RS_DYN_THR
             // the bounds follow the lane's minimum lazily: it may have moved in the previous
             // round, whose record loads have landed behind the atom step since (a branch on this
@@ -1120,18 +1208,31 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             }
             const bool more = qpos < qend;
             RS_DCHECK(!more || (qpos >= 0 && qpos + 2 <= a.n_ent));
+#if RS_VOTE_MASK
+            am = __ballot_sync(kFull, more);
+            if (am) ldg_pair_p(a.t.nb_ent + qpos, more, pf0, pf1);
+#else
             if (__any_sync(kFull, more)) ldg_pair_p(a.t.nb_ent + qpos, more, pf0, pf1);
+#endif
           }
         };
         // one candidate round per pass; an atom step only when every lane can take its atom
         // (idle, or room on its stack); after the last atom, walk until every lane is done
         for (int it = 0;;) {
           nbr_step();
+#if RS_VOTE_MASK
+          if (am && __any_sync(kFull, qfc == kNQ && qpos < qend)) continue;
+          if (it >= nsteps) {
+            if (am) continue;
+            break;
+          }
+#else
           if (__any_sync(kFull, qfc == kNQ && qpos < qend)) continue;
           if (it >= nsteps) {
             if (__any_sync(kFull, qpos < qend)) continue;
             break;
           }
+#endif
           const int l = (it++ << lgS) + sub;
           const bool act = live && l < L;
           const int lc = l < L ? l : L - 1;
@@ -1193,6 +1294,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
               ++qfc;
             }
           }
+#if RS_VOTE_MASK
+          am = __ballot_sync(kFull, qpos < qend);
+#endif
           // H4 (O4)
           double phi = 0.0;
           if constexpr (RT > 0) {
