@@ -324,11 +324,6 @@ rs::ScoreArgs base_args(const rs_handle* h) {
     const double up = 1.0 + 1e-6;
     a.thr_a = std::nextafter((float)(1.25 * h->inv_h * h->inv_h * up), INFINITY);
     a.thr_b = std::nextafter((float)(5.0 * c2 * c2 * up), INFINITY);
-    a.thr_s = std::nextafter((float)(h->inv_h * up), INFINITY);
-    a.thr_c = std::nextafter((float)(c2 * up), INFINITY);
-    const double kc = double((1 << h->cg.shift) - 1) * std::sqrt(3.0);
-    a.stop_a = std::nextafter((float)(5.0 * up), INFINITY);   // (2 sqrt T + kc)^2 <= 5 T + 5 kc^2
-    a.stop_b = std::nextafter((float)(5.0 * kc * kc * up), INFINITY);
   }
   a.rmax_hint = -1.0;
   return a;

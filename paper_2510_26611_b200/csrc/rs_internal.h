@@ -184,8 +184,6 @@ struct ScoreArgs {               // one launch of the scoring kernel
   int64_t n_ent = 0, n_prot = 0;  // list entries and protein records (bounds for checked builds)
   unsigned vdw_cells2;           // keep a candidate for H6 iff |D|^2 < vdw_cells2 (conservative)
   float thr_a, thr_b;            // running H6 bound: |D|^2 < thr_a best + thr_b (AM-GM, rounded up)
-  float thr_s, thr_c;            // binary32 inv_h and sqrt 3 + 2, rounded up (RS_DYN_THR == 3)
-  float stop_a, stop_b;          // early end of a walk: key > stop_a max(ns2, bound) + stop_b
   unsigned ns2;                  // n_sigma^2: H5 iff |D|^2 <= ns2
   int f32;                       // long-range part from the binary32 factors (A21)
   int tk = 0;                    // long-range part from the Tucker form (N5, reading A26)

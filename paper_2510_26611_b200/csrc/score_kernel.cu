@@ -508,20 +508,6 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
   const double t = __dadd_rn(__dmul_rn(__dsqrt_rn(best), a.inv_h), 3.7320508075688772);
   const double t2 = __dmul_rn(t, t);
   return t2 < (double)a.vdw_cells2 ? (unsigned)ceil(t2) + 1u : a.vdw_cells2;
-#elif RS_DYN_THR == 4
-  // as 3 with the hardware's approximate square root (relative error <= 2^-22, covered by the
-  // factor 1 + 2^-20 and the roundings up)
-  float sq;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(__double2float_ru(best)));
-  const float t = __fadd_ru(__fmul_ru(__fmul_ru(sq, 1.00000095367431640625f), a.thr_s), a.thr_c);
-  const float t2 = __fmul_ru(t, t);
-  return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
-#elif RS_DYN_THR == 3
-  // (sqrt(best) inv_h + sqrt 3 + 2)^2 in binary32, every step rounded up (thr_s = inv_h and
-  // thr_c = sqrt 3 + 2 rounded up on the host); evaluated only when the minimum moved
-  const float t = __fadd_ru(__fmul_ru(__fsqrt_ru(__double2float_ru(best)), a.thr_s), a.thr_c);
-  const float t2 = __fmul_ru(t, t);
-  return t2 < (float)a.vdw_cells2 ? (unsigned)t2 + 2u : a.vdw_cells2;
 #else
   // (sqrt(best) inv_h + sqrt 3 + 2)^2 <= thr_a best + thr_b (host: AM-GM, rounded up), in
   // binary32 with every step rounded up: no square root on the hot path
@@ -534,47 +520,31 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
 #define RS_EARLY_STOP 1
 #endif
 // Early end of a candidate walk.  Every list is sorted by key = |2 i_m - C|^2 (half cells, C
-// the coarse cell's centre; rs_build_protein).  The atom's cell a lies within (2^s - 1) sqrt 3
-// half cells of C, so an entry the walk still needs (|i_m - a|^2 <= max(ns2, vthr)) has
-// key <= (2 sqrt(max(ns2, vthr)) + (2^s - 1) sqrt 3)^2 <= stop_a max(ns2, vthr) + stop_b
-// (host: AM-GM, rounded up): the first entry above that bound ends the walk.
-#ifndef RS_STOP_EXACT
-#define RS_STOP_EXACT 1
-#endif
-// RS_STOP_EXACT: the bound with the atom's own offset from the centre instead of the worst
-// case.  With rho^2 = max(ns2, vthr), A = 2 a - C (|A_r| <= 2^s - 1) and delta = |A|, a needed
-// entry has key <= (2 rho + delta)^2, i.e. the walk ends at the first entry with
-// key - 4 rho^2 - delta^2 > 4 rho delta, tested exactly in integers (both sides squared);
-// stop_key returns 4 rho^2 (saturated: no early end when it does not fit 32 bits).
+// the coarse cell's centre; rs_build_protein).  With rho^2 = max(ns2, vthr), A = 2 a - C for
+// the atom's cell a (|A_r| <= 2^s - 1) and delta = |A|, an entry the walk still needs
+// (|i_m - a| <= rho) has key <= (2 rho + delta)^2: the walk ends at the first entry with
+// key - 4 rho^2 - delta^2 > 4 rho delta, tested exactly in integers (both sides squared).  The
+// atom's own offset from the centre instead of the worst case (2^s - 1) sqrt 3 cuts the walked
+// entries by about a third at C3.  stop_key returns 4 rho^2 (saturated: no early end when it
+// does not fit 32 bits).
 __device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) {
-#if RS_STOP_EXACT
   const unsigned m = max(a.ns2, vthr);
-  return m < 0x40000000u ? 4u * m : 0xffffffffu;
-#endif
-  const float r2 = __fadd_ru(__fmul_ru((float)max(a.ns2, vthr), a.stop_a), a.stop_b);
-  return r2 < 4.0e9f ? (unsigned)r2 + 2u : 0xffffffffu;
-}
-// the key of entry en for an atom in cell (c0, c1, c2) whose offsets to the entry are e
-__device__ __forceinline__ unsigned entry_key(const ScoreArgs& a, int c0, int c1, int c2, int e0, int e1,
-                                              int e2) {
-  const int s = a.nb_shift, off = (1 << s) - 1;
-  const int k0 = 2 * (c0 - e0) - ((c0 >> s) * (2 << s) + off);
-  const int k1 = 2 * (c1 - e1) - ((c1 >> s) * (2 << s) + off);
-  const int k2 = 2 * (c2 - e2) - ((c2 >> s) * (2 << s) + off);
-  return (unsigned)(k0 * k0) + (unsigned)(k1 * k1) + (unsigned)(k2 * k2);
+  // (coarse cells of more than 2^12 cells would overflow the 64-bit product of the test)
+  return (m < 0x40000000u && a.nb_shift <= 12) ? 4u * m : 0xffffffffu;
 }
 
 #ifndef RS_DEFER_BALL
 #define RS_DEFER_BALL 0
 #endif
-#ifndef RS_PF_POSES
-#define RS_PF_POSES 0   // 1: bulk L2 prefetch of the next tile's poses
-#endif
 #ifndef RS_VOTE_MASK
-#define RS_VOTE_MASK 0
+#define RS_VOTE_MASK 1
 #endif
-#ifndef RS_HIT_VOTE
-#define RS_HIT_VOTE 0   // 1: the O7 distances of a round only when some lane's prefilter passed
+#ifndef RS_MIN_UNIT
+#define RS_MIN_UNIT 4   // smallest unit of a tile's tail (poses); smaller units pay more per pose
+#endif                  // in H1 and the drain of their candidate walks than they gain in balance
+constexpr int kMinUnit = RS_MIN_UNIT;
+#ifndef RS_TILE_OVERLAP
+#define RS_TILE_OVERLAP 1
 #endif
 #ifndef RS_LIG_CALL
 #define RS_LIG_CALL 1   // 1: ligand atoms beyond the staged ones through an out-of-line load
@@ -603,7 +573,7 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   int e00, e01, e02, e10, e11, e12;
   unsigned dd0 = entry_dd(c0, c1, c2, en0, e00, e01, e02);
   unsigned dd1 = entry_dd(c0, c1, c2, en1, e10, e11, e12);
-#if RS_EARLY_STOP && RS_STOP_EXACT
+#if RS_EARLY_STOP
   {
     const int msk = (1 << a.nb_shift) - 1;
     const int A0 = 2 * (c0 & msk) - msk, A1 = 2 * (c1 & msk) - msk, A2 = 2 * (c2 & msk) - msk;
@@ -614,8 +584,6 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
     end = a1 && key > stopk && t > d2 &&
           (unsigned long long)u * u > (((unsigned long long)stopk * d2) << 2);
   }
-#elif RS_EARLY_STOP
-  end = a1 && entry_key(a, c0, c1, c2, e10, e11, e12) > stopk;
 #else
   end = false;
 #endif
@@ -629,15 +597,8 @@ __device__ __forceinline__ void nbr_pair(const ScoreArgs& a, double x0, double x
   const double4 rc1 = ldg_d4_p(a.t.prec + entry_k(en1), v1);
   const double sv0 = short_value(a, e00, e01, e02, sr0);
   const double sv1 = short_value(a, e10, e11, e12, sr1);
-#if RS_HIT_VOTE
-  if (__any_sync(kFull, v0 || v1)) {
-    pair_hit(x0, x1, x2, rc0, v0, best);
-    pair_hit(x0, x1, x2, rc1, v1, best);
-  }
-#else
   pair_hit(x0, x1, x2, rc0, v0, best);
   pair_hit(x0, x1, x2, rc1, v1, best);
-#endif
 #if RS_DEFER_BALL
   // the O5 terms wait for the next round (their memo values land behind the atom step)
   pd.q0 = entry_q(en0); pd.q1 = entry_q(en1); pd.sv0 = sv0; pd.sv1 = sv1; pd.z = z;
@@ -1057,17 +1018,6 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         mbar_wait(&s_bar, phase);
         phase ^= 1;
       }
-#if RS_PF_POSES
-      // the next tile's poses towards L2 while this tile computes (one bulk prefetch; only inside
-      // the chunk, whose poses have landed)
-      if (tid == 32) {
-        const int64_t e = p + T + kTile < p_end ? p + T + kTile : p_end;
-        const uintptr_t b0 = (reinterpret_cast<uintptr_t>(a.poses + 7 * (p + T)) + 15u) & ~(uintptr_t)15u;
-        const uintptr_t b1 = reinterpret_cast<uintptr_t>(a.poses + 7 * e) & ~(uintptr_t)15u;
-        if (b1 > b0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((unsigned)(b1 - b0)) : "memory");
-      }
-#endif
       const bool use_win = window_mode && fits;
       // per-lane window row bases (shared addresses, with the lane's XOR offset in bits 4..)
       unsigned wb0, wb1, wb2;
@@ -1093,7 +1043,9 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         int s = 0, g = 32;
         if (lane == 0) {
           const int r = T - *(volatile int*)&s_next;       // a hint only: ranges come from the atomic
-          if (r < 32 * kWarps) g = min(32, pow2_floor(max(1, r / kWarps)));
+          // the tile's last units shrink (a power of two >= kMinUnit poses, S lanes per pose) so
+          // that the warps finish together
+          if (r < 32 * kWarps) g = min(32, pow2_floor(max(kMinUnit, r / kWarps)));
           s = atomicAdd(&s_next, g);
         }
         s = __shfl_sync(kFull, s, 0);
@@ -1365,7 +1317,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
           if (bad && a.invalid) atomicAdd(a.invalid, 1ull);
         }
       }
+#if RS_TILE_OVERLAP
+      // inside a chunk of a window launch the next tile's scan starts with per-warp work (pose
+      // loads, warp scans) that touches nothing the units use; its first barrier ends this tile,
+      // so warps that finish early overlap that work with the slower warps' last units
+      if (!(window_mode && !a.done && p + T < p_end)) __syncthreads();
+#else
       __syncthreads();
+#endif
       if (a.done) {
         // release the tile's outputs to the copy stream that waits on done[chunk]
         __threadfence();

@@ -16,7 +16,7 @@ tail -c 400 $OUT/bench.json
 if [ "$NCU" = "1" ]; then
   CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench"
   timeout 300 $CMD > $OUT/plain.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_kernel -s 2 -c 1 \
     -o $OUT/score_full -f $CMD > $OUT/ncu_full.log 2>&1
