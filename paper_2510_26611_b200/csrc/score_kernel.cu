@@ -1318,10 +1318,14 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         }
       }
 #if RS_TILE_OVERLAP
-      // inside a chunk of a window launch the next tile's scan starts with per-warp work (pose
-      // loads, warp scans) that touches nothing the units use; its first barrier ends this tile,
-      // so warps that finish early overlap that work with the slower warps' last units
-      if (!(window_mode && !a.done && p + T < p_end)) __syncthreads();
+      // No barrier of its own at the end of a tile: the next barrier every warp meets ends it --
+      // the first barrier of the next tile's scan (window launches: the scan starts with
+      // per-warp work, pose loads and warp scans, that touches nothing the units use, so warps
+      // that finish early overlap it with the slower warps' last units), or at the end of a chunk
+      // the barrier behind the next chunk's claim.  Nothing the units read is written before
+      // that barrier.  Kept where the next tile's set-up follows without one (interior tiles of
+      // L2 launches) and in streamed launches (the completion counters below).
+      if (a.done || (!window_mode && p + T < p_end)) __syncthreads();
 #else
       __syncthreads();
 #endif
