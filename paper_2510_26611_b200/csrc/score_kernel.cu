@@ -75,6 +75,7 @@ constexpr int kChunk = RS_CHUNK;         // poses per unit of dynamic CTA work
 #ifndef RS_TAIL_CHUNK
 #define RS_TAIL_CHUNK 256
 #endif
+constexpr int kMinBig = 128;               // smallest big chunk (small batches: C5's 10^5 poses)
 constexpr int kTailChunk = RS_TAIL_CHUNK;  // chunk size over the last 1/RS_TAIL_DIV of the poses
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -1096,15 +1097,18 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
             const double2 v0 = s_lig[lc], v1 = s_lig[lig_smem_n + lc];
             y0 = v0.x; y1 = v0.y; y2 = v1.x; z = v1.y;
           } else {
-#if RS_LIG_CALL
-            const double4 v = lig_atom_global(a.yl, a.zl, lc);
-            y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
-#else
-            y0 = __ldg(a.yl + 3 * (int64_t)lc);
-            y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
-            y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
-            z = __ldg(a.zl + lc);
-#endif
+            // window launches stage up to 256 atoms, so this is their rare case: out of line
+            // (one branch instead of predicated-off loads in every atom step); L2 launches
+            // with a ligand beyond shared memory (C5's 5,000-atom partner) take it every step
+            if constexpr (WIN && RS_LIG_CALL) {
+              const double4 v = lig_atom_global(a.yl, a.zl, lc);
+              y0 = v.x; y1 = v.y; y2 = v.z; z = v.w;
+            } else {
+              y0 = __ldg(a.yl + 3 * (int64_t)lc);
+              y1 = __ldg(a.yl + 3 * (int64_t)lc + 1);
+              y2 = __ldg(a.yl + 3 * (int64_t)lc + 2);
+              z = __ldg(a.zl + lc);
+            }
           }
         };
         // H2 (O2): x' = R y + t, the pose's R and t in registers
@@ -1469,7 +1473,7 @@ int launch_t(const ScoreArgs& a, cudaStream_t st, int dev, int slot, bool plan_o
   // at most kTailChunk poses, small enough that every SM gets work when P is small
   // (big chunks also shrink with P: at least ~4 per SM, so one chunk never dominates a launch)
   ChunkPlan cp;
-  cp.big = (int)std::max<int64_t>(kTailChunk, std::min<int64_t>(kChunk, a.P / (4 * (int64_t)dc.sms)));
+  cp.big = (int)std::max<int64_t>(kMinBig, std::min<int64_t>(kChunk, a.P / (4 * (int64_t)dc.sms)));
   cp.nbig = (a.P - a.P / RS_TAIL_DIV) / cp.big;
   const int64_t rest = a.P - cp.nbig * cp.big;
   cp.tail = (int)std::max<int64_t>(1, std::min<int64_t>(kTailChunk, (rest + 2 * dc.sms - 1) / (2 * dc.sms)));

@@ -20,6 +20,8 @@ KEYS = {
     "global_ld_sectors": ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 1.0),
     "l1tex_data_pipe_wavefronts_pct": ("l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed", 1.0),
     "smem_ld_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", 1.0),
+    "smem_wavefronts_all_ops": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1.0),
+    "l1tex_data_pipe_wavefronts_per_sm": ("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg", 1.0),
     "smem_ld_bank_conflicts": ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", 1.0),
     "smem_wavefront_pct_of_peak": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 1.0),
     "fp64_pipe_pct_active": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
