@@ -540,10 +540,6 @@ __device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) 
 #ifndef RS_VOTE_MASK
 #define RS_VOTE_MASK 1
 #endif
-#ifndef RS_MIN_UNIT
-#define RS_MIN_UNIT 4   // smallest unit of a tile's tail (poses); smaller units pay more per pose
-#endif                  // in H1 and the drain of their candidate walks than they gain in balance
-constexpr int kMinUnit = RS_MIN_UNIT;
 #ifndef RS_TILE_OVERLAP
 #define RS_TILE_OVERLAP 1
 #endif
@@ -743,6 +739,11 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
   const bool window_mode = WIN && RT > 0 && cap_rows > 0;
   const int L = (int)a.L;
   const bool lig_all_smem = L <= lig_smem_n;
+  // smallest unit of a tile's tail: at most ~L/6 lanes per pose, so a lane keeps >= ~6 atoms
+  // (C3's 60 and C2's 50 atoms: units of >= 4 poses; C5's 5,000-atom partner: down to single
+  // poses).  Smaller units lose more in H1 and the drain of their walks than idle warps cost:
+  // lowering the floor for tiles too small to give every warp a unit measured +2.4 % at C3
+  const int min_unit = 32 / pow2_floor(max(1, min(32, L / 6)));
   const int nm1 = a.n - 1;
   const unsigned rho16 = (unsigned)(lane & 7) << 4;
   unsigned phase = 0;
@@ -1044,9 +1045,10 @@ __global__ void __launch_bounds__(kThreads, 1) score_kernel(const ScoreArgs a, i
         int s = 0, g = 32;
         if (lane == 0) {
           const int r = T - *(volatile int*)&s_next;       // a hint only: ranges come from the atomic
-          // the tile's last units shrink (a power of two >= kMinUnit poses, S lanes per pose) so
-          // that the warps finish together
-          if (r < 32 * kWarps) g = min(32, pow2_floor(max(kMinUnit, r / kWarps)));
+          // the tile's last units shrink (a power of two >= min_unit poses, S lanes per pose) so
+          // that the warps finish together; smaller units pay more per pose in H1 and the drain
+          // of their candidate walks than they gain in balance
+          if (r < 32 * kWarps) g = min(32, pow2_floor(max(min_unit, r / kWarps)));
           s = atomicAdd(&s_next, g);
         }
         s = __shfl_sync(kFull, s, 0);

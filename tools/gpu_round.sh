@@ -11,7 +11,7 @@ if [ "$TESTS" = "1" ]; then
   timeout 1800 python -m pytest tests -m gpu -x -q > $OUT/gpu_tests.log 2>&1; echo "tests_rc=$?" >> $OUT/gpu_tests.log
   tail -3 $OUT/gpu_tests.log
 fi
-timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench_rc=$?"
+timeout 600 python bench.py --config $CFG > $OUT/bench.json 2> $OUT/bench.err; echo "bench_rc=$?"
 tail -c 400 $OUT/bench.json
 if [ "$NCU" = "1" ]; then
   CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench"
