@@ -1,10 +1,7 @@
 #!/bin/bash
-# scratch gpurun command: spot bench of several configs
-OUT=gpurun_out/s4o; mkdir -p $OUT
-run() { name=$1; shift; timeout 900 python bench.py "$@" > $OUT/$name.json 2> $OUT/$name.err; echo "$name rc=$? $(python -c "import json; d=json.loads(open('$OUT/$name.json').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],4), d['roofline']['frac'], (d.get('e2e') or {}).get('value'))" 2>&1 | tail -1)"; }
-run C3a --config C3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench
-run C5_R16_s1 --config C5 --c5-rank 16 --c5-sigma-mult 1 --steps 10 --warmup 3 --no-cpu-baseline
-run C5_R8_s3 --config C5 --c5-rank 8 --c5-sigma-mult 3 --steps 10 --warmup 3 --no-cpu-baseline
-run C2 --config C2 --steps 20 --warmup 3 --no-cpu-baseline
-run C4 --config C4 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e
-run C3b --config C3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-microbench
+# scratch gpurun command: A/B + parity of one variant
+ROUNDS=2 STEPS=20 bash tools/abi.sh s4p C3 base pfs
+RSDOCK_LIB=$PWD/build/variants/librsdock_pfs.so timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s4p/tests_pfs.log 2>&1; echo "tests pfs: $(tail -1 gpurun_out/s4p/tests_pfs.log)"
+for c in "C4:--config C4 --steps 5" "C5:--config C5 --c5-rank 16 --c5-sigma-mult 1 --steps 10" "C2:--config C2 --steps 20"; do n=${c%%:*}; a=${c#*:};
+ for L in base pfs; do if [ $L = base ]; then LIB=$PWD/paper_2510_26611_b200/librsdock.so; else LIB=$PWD/build/variants/librsdock_$L.so; fi
+  RSDOCK_LIB=$LIB timeout 600 python bench.py $a --warmup 3 --no-cpu-baseline --no-e2e --no-microbench > gpurun_out/s4p/${n}_$L.json 2>/dev/null; echo "$n $L $(python -c "import json; d=json.loads(open('gpurun_out/s4p/${n}_$L.json').read().strip().splitlines()[-1]); print(round(d['ms_per_step'],4))")"; done; done
