@@ -526,7 +526,7 @@ __device__ __forceinline__ unsigned vdw_thr(const ScoreArgs& a, double best) {
 // (|i_m - a| <= rho) has key <= (2 rho + delta)^2: the walk ends at the first entry with
 // key - 4 rho^2 - delta^2 > 4 rho delta, tested exactly in integers (both sides squared).  The
 // atom's own offset from the centre instead of the worst case (2^s - 1) sqrt 3 cuts the walked
-// entries by about a third at C3.  stop_key returns 4 rho^2 (saturated: no early end when it
+// entries by about a fifth at C3.  stop_key returns 4 rho^2 (saturated: no early end when it
 // does not fit 32 bits).
 __device__ __forceinline__ unsigned stop_key(const ScoreArgs& a, unsigned vthr) {
   const unsigned m = max(a.ns2, vthr);
